@@ -1,0 +1,202 @@
+/* libpermatrace_b200 -- C ABI of the B200-native (sm_100a) manifold-tracing / refinement /
+ * collision-checking hot path.  This is the drop-in boundary: plain pointers and sizes, no
+ * exceptions, no torch types.  Every data pointer may be HOST or DEVICE memory (classified with
+ * cudaPointerGetAttributes); results are written to the memory space of the output pointer.
+ *
+ * Each entry point names the reference interface it replaces (paths relative to
+ * /root/reference/pkg/src/permatrace/).  Return value: PT_OK (0) or a negative PT_E_* code;
+ * pt_last_error() returns the message of the calling thread's last failure.
+ */
+#ifndef PERMATRACE_B200_H
+#define PERMATRACE_B200_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PT_OK 0
+#define PT_E_INVALID (-1)    /* bad argument (maps to ValueError) */
+#define PT_E_CUDA (-2)       /* CUDA runtime failure (maps to RuntimeError) */
+#define PT_E_RANGE (-3)      /* lattice window exceeds the packed-key range */
+#define PT_E_LIMIT (-4)      /* configuration outside joint limits (maps to LimitError) */
+#define PT_E_NOMEM (-5)      /* device memory exhausted */
+#define PT_E_STATE (-6)      /* call sequence error */
+
+typedef struct pt_ctx pt_ctx;
+typedef struct pt_field pt_field;       /* an implicit manifold resident on the device */
+typedef struct pt_checker pt_checker;   /* robot + scene resident on the device */
+typedef struct pt_trace pt_trace;       /* one BFS trace (visited table, sign table, frontier) */
+typedef struct pt_cells pt_cells;       /* sorted, deduplicated full-dimensional cells */
+typedef struct pt_refine pt_refine;     /* result of one batch refinement */
+
+/* ---- context ------------------------------------------------------------------------------ */
+const char* pt_last_error(void);
+int pt_version(void);
+int pt_ctx_create(int device, pt_ctx** out);
+void pt_ctx_destroy(pt_ctx* ctx);
+/* run all work of this context on an existing CUDA stream (e.g. torch's current stream) */
+int pt_ctx_set_stream(pt_ctx* ctx, void* cuda_stream);
+int pt_ctx_synchronize(pt_ctx* ctx);
+/* per-kernel CUDA-event profiler (events on the launching stream) */
+int pt_ctx_profile_enable(pt_ctx* ctx, int on);
+int pt_ctx_profile_reset(pt_ctx* ctx);
+/* writes "name,launches,total_ms\n" lines; returns bytes needed (call with cap=0 to size) */
+long long pt_ctx_profile_dump(pt_ctx* ctx, char* buf, long long cap);
+long long pt_ctx_launch_count(pt_ctx* ctx);
+
+/* ---- B1: the reference's kernel plugin seam (backend.py:30-33, _kernels.pyx) ---------------- */
+/* _kernels.pyx:18-40 rbf_values(points[m,n], support[S,n], weights[S], gamma, bias) -> out[m] */
+int pt_rbf_values(pt_ctx* ctx, const double* points, long long m, int n, const double* support,
+                  long long S, const double* weights, double gamma, double bias, double* out);
+/* _kernels.pyx:43-76 sphere_box_hits(centers[m,3], radii[m], lx, ly, lz) -> out[m] (uint8) */
+int pt_sphere_box_hits(pt_ctx* ctx, const double* centers, const double* radii, long long m,
+                       double lx, double ly, double lz, uint8_t* out);
+/* _kernels.pyx:79-104 sphere_cylinder_hits(centers, radii, height, radius) */
+int pt_sphere_cylinder_hits(pt_ctx* ctx, const double* centers, const double* radii, long long m,
+                            double height, double radius, uint8_t* out);
+/* _kernels.pyx:107-122 sphere_sphere_hits(centers, radii, radius) */
+int pt_sphere_sphere_hits(pt_ctx* ctx, const double* centers, const double* radii, long long m,
+                          double radius, uint8_t* out);
+
+/* ---- implicit manifolds (manifold.py:49-217) ------------------------------------------------ */
+#define PT_FIELD_RBF 0        /* KernelClassifierManifold (manifold.py:177-208) */
+#define PT_FIELD_SPHERE 1     /* SphereManifold (manifold.py:75-95) */
+#define PT_FIELD_ELLIPSOID 2  /* EllipsoidManifold (manifold.py:98-120) */
+#define PT_FIELD_PLANE 3      /* PlaneManifold (manifold.py:123-140) */
+/* KernelClassifierManifold(support, weights, gamma, bias, barrier); barrier = NULL or
+ * [scale, gain, lower[n], upper[n]] (BoxBarrier, manifold.py:143-169).  Host pointers. */
+int pt_field_create_rbf(pt_ctx* ctx, int n, long long S, const double* support,
+                        const double* weights, double gamma, double bias, const double* barrier,
+                        pt_field** out);
+/* analytic fields: params = sphere [center[n], radius^2]; ellipsoid [center[n], semi_axes[n]];
+ * plane [normal[n], offset].  Host pointers. */
+int pt_field_create_analytic(pt_ctx* ctx, int kind, int n, const double* params, pt_field** out);
+void pt_field_destroy(pt_field* f);
+/* precision policy: 0 = FP64 everywhere (default); 1 = FP32 screening with an FP64 recheck of
+ * every value whose sign is not certain under the rigorous FP32 error bound */
+int pt_field_set_precision(pt_field* f, int mode);
+/* ImplicitManifold.values / .signs (manifold.py:54-72): out_values (f64) and out_signs (i8, +1/-1)
+ * may each be NULL */
+int pt_field_values(pt_ctx* ctx, const pt_field* f, const double* points, long long m,
+                    double* out_values, int8_t* out_signs);
+/* intersection_points_batch(manifold, a, b, eps, signs_a) (manifold.py:351-383); signs_a NULL ->
+ * evaluated at a */
+int pt_intersection_points(pt_ctx* ctx, const pt_field* f, const double* a, const double* b,
+                           long long m, double eps, const int8_t* signs_a, double* out);
+
+/* ---- collision (collision.py:191-329, pipeline.py:256-270) --------------------------------- */
+/* Robot: joints[nj]: kind (0 revolute, 1 prismatic), axis[3] (unit), origin rotation[9] row-major,
+ * origin translation[3], limits[2]; spheres[ns]: link, offset[3], radius.
+ * Scene: obstacles[no]: type (0 box, 1 cylinder, 2 sphere), rotation[9], translation[3],
+ * dims[3] (box lx,ly,lz | cylinder height,radius,- | sphere radius,-,-).  Host pointers. */
+int pt_checker_create(pt_ctx* ctx, int nj, const int* joint_kind, const double* joint_axis,
+                      const double* joint_rot, const double* joint_trans, const double* joint_limits,
+                      int ns, const int* sphere_link, const double* sphere_offset,
+                      const double* sphere_radius, int no, const int* obs_type,
+                      const double* obs_rot, const double* obs_trans, const double* obs_dims,
+                      pt_checker** out);
+void pt_checker_destroy(pt_checker* ck);
+/* fk_batch (collision.py:204-225): centers out[m, ns, 3] */
+int pt_fk_batch(pt_ctx* ctx, const pt_checker* ck, const double* configs, long long m,
+                double* out_centers);
+#define PT_LIMIT_ERROR 0   /* batch_check(on_limit="error"): PT_E_LIMIT, *first_bad = row */
+#define PT_LIMIT_UNFREE 1  /* batch_check(on_limit="unfree") == _not_free_checker */
+#define PT_LIMIT_IGNORE 2  /* _batch_hits: no limit test */
+/* batch_check (collision.py:306-329): out[m] uint8 in-collision mask */
+int pt_batch_check(pt_ctx* ctx, const pt_checker* ck, const double* configs, long long m,
+                   int on_limit, uint8_t* out, long long* first_bad);
+
+/* ---- tracer (tracer.py:152-452) ------------------------------------------------------------- */
+typedef struct pt_trace_stats {
+    long long levels, seeds, visited_edges, field_evaluations, dropped_out_of_box;
+    long long candidates;        /* sum of (edge, coface) records expanded */
+    long long frontier;          /* current frontier size */
+    int complete, closure_ok;
+    long long table_capacity, sign_table_capacity;
+    long long n_stages;          /* StageStat rows available through pt_trace_stages */
+} pt_trace_stats;
+
+/* TraceConfig(lattice=LatticeConfig(n, scale, offset), box, max_edges, eps) (tracer.py:43-59).
+ * box_lo/box_hi NULL -> no clamp.  window_center: lattice-unit centre of the packed-key window
+ * when no box is given (NULL -> centred on the first seed). */
+int pt_trace_create(pt_ctx* ctx, const pt_field* field, int n, double scale, const double* offset,
+                    const double* box_lo, const double* box_hi, long long max_edges, double eps,
+                    pt_trace** out);
+void pt_trace_destroy(pt_trace* t);
+/* _Tracer.locate + admit_frontier (tracer.py:256-306) */
+int pt_trace_locate(pt_trace* t, const double* seeds, long long m);
+/* _Tracer.expand (tracer.py:322-380): one BFS wave; *frontier_out = new frontier size */
+int pt_trace_expand(pt_trace* t, long long* frontier_out);
+/* trace() (tracer.py:436-452): locate, then expand until the frontier empties or the cap hits */
+int pt_trace_run(pt_trace* t, const double* seeds, long long m);
+/* seed the visited set + frontier directly from canonical edges (expand_frontier, tracer.py:418-433):
+ * base[m,n] int32, mask[m] uint32; the first n_visited rows are "visited", the rest the frontier
+ * (rows already present are skipped). */
+int pt_trace_seed_edges(pt_trace* t, const int32_t* base, const uint32_t* mask, long long n_visited,
+                        long long n_frontier);
+int pt_trace_get_stats(pt_trace* t, pt_trace_stats* out);
+/* StageStat rows (tracer.py:74-80): out[rows,5] = kind (0 locate_cells,1 cell_edges,2 edge_cofaces,
+ * 3 coface_partner), level, items, capacity, produced */
+int pt_trace_stages(pt_trace* t, long long* out, long long rows);
+/* edges in admission order: base[E,n] int32, mask[E] uint32 (bit d set <=> label d in p1),
+ * sign_a[E] int8 (sign at the base vertex); any pointer may be NULL.  Rows [first, first+count). */
+int pt_trace_edges(pt_trace* t, long long first, long long count, int32_t* base, uint32_t* mask,
+                   int8_t* sign_a);
+/* frontier rows (indices into the edge list) of the current frontier */
+int pt_trace_frontier(pt_trace* t, long long* first, long long* count);
+/* _Tracer.result (tracer.py:384-395): one bisection point per edge, out[E,n] */
+int pt_trace_points(pt_trace* t, double* out);
+/* sorted unique adjacency pairs (tracer.py:249-251,398): returns count; pairs[count,2] int64 when
+ * pairs != NULL (call once with NULL to size) */
+long long pt_trace_adjacency(pt_trace* t, long long* pairs, long long cap);
+
+/* ---- coarse cells (subdivision.py:132-141, lattice.py:245-266) ------------------------------ */
+int pt_cells_from_trace(pt_trace* t, pt_cells** out);
+/* same from canonical edges given on the host: base[E,n] int32, mask[E] uint32 */
+int pt_cells_from_edges(pt_ctx* ctx, int n, const int32_t* base, const uint32_t* mask, long long count,
+                        pt_cells** out);
+/* cells given by the caller in processing order: base[C,n] int32, perm[C,n] uint8 */
+int pt_cells_from_host(pt_ctx* ctx, int n, const int32_t* base, const uint8_t* perm, long long count,
+                       pt_cells** out);
+void pt_cells_destroy(pt_cells* c);
+long long pt_cells_count(const pt_cells* c);
+int pt_cells_get(const pt_cells* c, long long first, long long count, int32_t* base, uint8_t* perm);
+
+/* ---- refine (subdivision.py:220-301) -------------------------------------------------------- */
+typedef struct pt_refine_stats {
+    long long cells, fine_vertices, crossing_edges, unique_fine_vertices, unique_fine_edges,
+        points, in_collision, free_points, dedup_rounds, field_evaluations;
+} pt_refine_stats;
+/* template: tv[V,n] int32 vertices (lex sorted), te[E,2] int32 edges; k subdivision factor;
+ * lattice (n, scale, offset) is the COARSE lattice of the cells; checker NULL -> labels all 0 and
+ * the caller labels the points itself.  batch_bounds[nb+1] (cell index boundaries, may be NULL)
+ * only shapes the per-batch statistics: results never depend on it. */
+int pt_refine_run(pt_ctx* ctx, const pt_field* field, const pt_cells* cells, int n, double scale,
+                  const double* offset, int k, int V, const int32_t* tv, int E, const int32_t* te,
+                  double eps, double eps_dedup, const pt_checker* checker,
+                  const long long* batch_bounds, int nb, pt_refine** out);
+void pt_refine_destroy(pt_refine* r);
+int pt_refine_get_stats(const pt_refine* r, pt_refine_stats* out);
+/* points[P,n] f64, labels[P] uint8 (1 = not free), first_tag[P] int64 (global crossing index of the
+ * point's first occurrence); any may be NULL */
+int pt_refine_points(const pt_refine* r, double* points, uint8_t* labels, long long* first_tag);
+/* per-batch rows out[nb,2] = crossing_edges, new_points */
+int pt_refine_batch_stats(const pt_refine* r, long long* out, int nb);
+/* overwrite labels (used when the checker is an arbitrary host callable) */
+int pt_refine_set_labels(pt_refine* r, const uint8_t* labels);
+
+/* ---- host-executable mirrors of the device lattice arithmetic (tests, no GPU needed) -------- */
+/* expansion plan of edge type `mask` in dimension n (tracer.py:123-149): rows of 10 int32:
+ * c_plus,c_minus, bc_bplus,bc_bminus,bc_mask,bc_shared, ac_bplus,ac_bminus,ac_mask,ac_shared */
+int pt_host_expansion_plan(int n, uint32_t mask, int32_t* out, int cap);
+/* cell cofaces of edge type `mask` (lattice.py:245-258): rows of (1+n) int32: y_mask, perm[n] */
+int pt_host_cellcofaces(int n, uint32_t mask, int32_t* out, int cap);
+int pt_host_perm_rank(int n, const uint8_t* perm);
+int pt_host_perm_unrank(int n, int rank, uint8_t* perm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

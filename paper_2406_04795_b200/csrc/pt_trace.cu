@@ -1,0 +1,956 @@
+// Batched BFS manifold tracing on the Freudenthal-Kuhn lattice (tracer.py:152-452).
+//
+// One wave (= _Tracer.expand, tracer.py:322-380) over a chunk of frontier edges:
+//   pt_wave_probe_kernel    warp per frontier edge enumerates its 2-simplex cofaces, inserts the third
+//                           vertices into the vertex-sign table, queues the unknown ones
+//   (field evaluation of the queued vertices -- _ensure_signs, tracer.py:195-209)
+//   pt_wave_partner_kernel  partner rule + box clamp + visited insert with atomicMin(slot id)
+//   pt_wave_count_kernel    winners (first occurrence in slot order) per frontier edge
+//   pt_wave_admit_kernel    admission in slot order: edge index = visited + rank (tracer.py:239-252)
+// Slot id = frontier position * stride + coface ordinal reproduces the reference's admission order.
+#include <cub/cub.cuh>
+#include "pt_trace.cuh"
+#include "pt_field.cuh"
+
+#define PT_NONE32 0xFFFFFFFFu
+
+int pt_bits_for_dim(int n) {
+    int b = (63 - PT_CELL_RANK_BITS) / n;
+    return b > 20 ? 20 : b;
+}
+
+// ---- table management ----------------------------------------------------------------------
+__global__ void pt_rehash_kernel(PtTable src, PtTable dst, unsigned* err) {
+    u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > src.cap_mask) return;
+    u64 key = src.ent[2 * i];
+    if (key == PT_EMPTY) return;
+    bool ins;
+    u64 slot = pt_table_insert(dst, key, ins, err);
+    dst.ent[2 * slot + 1] = src.ent[2 * i + 1];
+}
+
+int pt_table_init(pt_ctx* ctx, PtHashTable& t, u64 capacity) {
+    u64 cap = 1024;
+    while (cap < capacity) cap <<= 1;
+    PT_TRY(t.ent.alloc(ctx, 2 * cap));
+    PT_CUDA(ctx, cudaMemsetAsync(t.ent.p, 0xFF, 2 * cap * sizeof(u64), ctx->stream));
+    t.capacity = cap; t.count = 0;
+    return PT_OK;
+}
+
+int pt_table_reserve(pt_ctx* ctx, PtHashTable& t, u64 extra) {
+    u64 need = 2 * (t.count + extra);
+    if (need <= t.capacity) return PT_OK;
+    u64 cap = t.capacity;
+    while (cap < need) cap <<= 1;
+    if (cap > (1ull << 31)) return pt_fail(ctx, PT_E_NOMEM, "hash table would exceed 2^31 entries");
+    PtBuf<u64> fresh;
+    PT_TRY(fresh.alloc(ctx, 2 * cap));
+    PT_CUDA(ctx, cudaMemsetAsync(fresh.p, 0xFF, 2 * cap * sizeof(u64), ctx->stream));
+    PtTable dst; dst.ent = fresh.p; dst.cap_mask = cap - 1;
+    PtBuf<unsigned> err;
+    PT_TRY(err.alloc(ctx, 1));
+    PT_CUDA(ctx, cudaMemsetAsync(err.p, 0, sizeof(unsigned), ctx->stream));
+    {
+        PT_LAUNCH(ctx, "table_rehash");
+        pt_rehash_kernel<<<pt_grid_for(t.capacity, 256), 256, 0, ctx->stream>>>(t.view(), dst, err.p);
+        PT_TRY(pt_check_launch(ctx, "pt_rehash_kernel"));
+    }
+    // swap storage
+    u64* old = t.ent.p;
+    t.ent.p = fresh.p; t.ent.count = 2 * cap; t.ent.ctx = ctx;
+    fresh.p = old; fresh.count = 2 * t.capacity; fresh.ctx = ctx;
+    t.capacity = cap;
+    return PT_OK;
+}
+
+// ---- small helpers -------------------------------------------------------------------------
+__device__ __forceinline__ void pt_vertex_point(const PtGeom& g, const int* v, double* x) {
+    // numpy: asarray(v, f64) * scale + offset, two roundings (tracer.py:204)
+    for (int d = 0; d < g.n; ++d) x[d] = __dadd_rn(__dmul_rn((double)v[d], g.scale), g.offset[d]);
+}
+
+// warp-aggregated counter bump; returns this lane's position (valid where pred)
+__device__ __forceinline__ unsigned long long pt_warp_append(unsigned long long* counter, bool pred) {
+    unsigned ballot = __ballot_sync(0xffffffffu, pred);
+    if (ballot == 0) return 0;
+    int lane = threadIdx.x & 31;
+    int leader = __ffs(ballot) - 1;
+    unsigned long long base = 0;
+    if (lane == leader) base = atomicAdd(counter, (unsigned long long)__popc(ballot));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    return base + (unsigned long long)__popc(ballot & ((1u << lane) - 1u));
+}
+
+// ---- locate (tracer.py:256-301) ---------------------------------------------------------------
+// locate_point (lattice.py:135-153): base = floor((p - offset)/scale); labels by (-frac, index)
+__global__ void pt_locate_cells_kernel(PtGeom g, const double* __restrict__ seeds, size_t m,
+                                       int* __restrict__ cell_base, uint8_t* __restrict__ cell_perm) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    double frac[PT_NMAX]; uint8_t ord[PT_NMAX];
+    for (int d = 0; d < g.n; ++d) {
+        double y = __ddiv_rn(__dsub_rn(seeds[i * g.n + d], g.offset[d]), g.scale);
+        double b = floor(y);
+        frac[d] = __dsub_rn(y, b);
+        cell_base[i * g.n + d] = (int)b;
+        ord[d] = (uint8_t)d;
+    }
+    // stable insertion sort, descending fraction (ties keep ascending index)
+    for (int a = 1; a < g.n; ++a) {
+        uint8_t key = ord[a]; int b = a - 1;
+        while (b >= 0 && frac[ord[b]] < frac[key]) { ord[b + 1] = ord[b]; --b; }
+        ord[b + 1] = key;
+    }
+    for (int d = 0; d < g.n; ++d) cell_perm[i * g.n + d] = ord[d];
+}
+
+// insert the n+1 vertices of each seed cell into the sign table, queue unknown ones
+__global__ void pt_cell_vertices_kernel(PtGeom g, PtTable sgn, const int* __restrict__ cell_base,
+                                        const uint8_t* __restrict__ cell_perm, size_t m,
+                                        uint32_t* __restrict__ pending, PtCounters* ctr) {
+    size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    size_t i = tid / (g.n + 1);
+    int j = (int)(tid % (g.n + 1));
+    bool live = i < m;
+    bool inserted = false; u64 slot = 0;
+    if (live) {
+        int v[PT_NMAX];
+        for (int d = 0; d < g.n; ++d) v[d] = cell_base[i * g.n + d];
+        for (int a = 0; a < j; ++a) v[cell_perm[i * g.n + a]] += 1;
+        u64 key;
+        if (!pt_pack_vertex(g, v, key)) atomicOr(&ctr->error, PT_ERR_KEY_RANGE);
+        else slot = pt_table_insert(sgn, key, inserted, &ctr->error);
+    }
+    unsigned long long pos = pt_warp_append(&ctr->n_pending, inserted);
+    if (inserted) pending[pos] = (uint32_t)slot;
+}
+
+// cell_edges stage (tracer.py:272-285): sign-changing in-box edges of each seed cell, slot order
+// = (cell, pair ordinal) with pairs (a<b), a outer (lattice.py:182-193)
+__global__ void pt_cell_edges_kernel(PtGeom g, PtTable sgn, PtTable vis, const int* __restrict__ cell_base,
+                                     const uint8_t* __restrict__ cell_perm, size_t m, int bound,
+                                     uint32_t* __restrict__ vis_slot, PtCounters* ctr) {
+    size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    size_t i = tid / bound;
+    int ord = (int)(tid % bound);
+    if (i >= m) return;
+    // ordinal -> (a, b)
+    int a = 0, rem = ord;
+    while (rem >= g.n - a) { rem -= g.n - a; ++a; }
+    int b = a + 1 + rem;
+    int va[PT_NMAX], vb[PT_NMAX];
+    for (int d = 0; d < g.n; ++d) va[d] = cell_base[i * g.n + d];
+    for (int k = 0; k < a; ++k) va[cell_perm[i * g.n + k]] += 1;
+    uint32_t mask = 0;
+    for (int d = 0; d < g.n; ++d) vb[d] = va[d];
+    for (int k = a; k < b; ++k) { int lab = cell_perm[i * g.n + k]; vb[lab] += 1; mask |= 1u << lab; }
+    u64 ka, kb;
+    uint32_t marker = PT_NONE32;
+    if (pt_pack_vertex(g, va, ka) && pt_pack_vertex(g, vb, kb)) {
+        u64 sa_slot, sb_slot;
+        if (pt_table_find(sgn, ka, sa_slot) && pt_table_find(sgn, kb, sb_slot)) {
+            const int sa = pt_ld_cg(&sgn.ent[2 * sa_slot + 1]) ? 1 : -1;
+            const int sb = pt_ld_cg(&sgn.ent[2 * sb_slot + 1]) ? 1 : -1;
+            if (sa != sb) {
+                atomicAdd(&ctr->markers, 1ull);
+                if (pt_in_box(g, va) && pt_in_box(g, vb)) {
+                    bool ins;
+                    u64 slot = pt_table_insert(vis, pt_edge_key(g, ka, mask), ins, &ctr->error);
+                    atomicMin(&vis.ent[2 * slot + 1], PT_VAL_PENDING_BASE + (u64)tid);
+                    marker = (uint32_t)slot | (sa > 0 ? 0x80000000u : 0u);
+                } else {
+                    atomicAdd(&ctr->dropped, 1ull);
+                }
+            }
+        }
+    } else {
+        atomicOr(&ctr->error, PT_ERR_KEY_RANGE);
+    }
+    vis_slot[tid] = marker;
+}
+
+// ---- pending vertex evaluation --------------------------------------------------------------
+__global__ void pt_pending_points_kernel(PtGeom g, PtTable sgn, const uint32_t* __restrict__ pending, size_t count,
+                                         double* __restrict__ pts) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    u64 key = sgn.ent[2 * (u64)pending[i]];
+    int v[PT_NMAX]; double x[PT_NMAX];
+    pt_unpack_vertex(g, key, v);
+    pt_vertex_point(g, v, x);
+    for (int d = 0; d < g.n; ++d) pts[i * g.n + d] = x[d];
+}
+__global__ void pt_pending_store_kernel(PtTable sgn, const uint32_t* __restrict__ pending, size_t count,
+                                        const int8_t* __restrict__ s) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    sgn.ent[2 * (u64)pending[i] + 1] = s[i] > 0 ? 1ull : 0ull;
+}
+
+// ---- wave kernels ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+pt_wave_probe_kernel(PtGeom g, PtTable sgn, const u64* __restrict__ edge_key, const uint32_t* __restrict__ frontier,
+                     size_t fcount, int stride, uint32_t* __restrict__ sgn_slot, uint32_t* __restrict__ pending,
+                     PtCounters* ctr) {
+    const size_t w = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= fcount) return;
+    const u64 ek = edge_key[frontier[w]];
+    const uint32_t s = pt_edge_mask(g, ek);
+    int u[PT_NMAX];
+    pt_unpack_vertex(g, pt_edge_vkey(g, ek), u);
+    const int nc = pt_ncofaces(g.n, s);
+    if (lane == 0) atomicAdd(&ctr->candidates, (unsigned long long)nc);
+    for (int j0 = 0; j0 < nc; j0 += 32) {
+        const int j = j0 + lane;
+        bool inserted = false; u64 slot = 0;
+        if (j < nc) {
+            PtCoface f = pt_coface(g.n, s, j);
+            int c[PT_NMAX];
+            pt_apply_masks(g.n, u, f.c_plus, f.c_minus, c);
+            u64 ck;
+            if (!pt_pack_vertex(g, c, ck)) atomicOr(&ctr->error, PT_ERR_KEY_RANGE);
+            else slot = pt_table_insert(sgn, ck, inserted, &ctr->error);
+            sgn_slot[w * stride + j] = (uint32_t)slot;
+        }
+        unsigned long long pos = pt_warp_append(&ctr->n_pending, inserted);
+        if (inserted) pending[pos] = (uint32_t)slot;
+    }
+}
+
+// new canonical edge produced by coface j of edge (u, s, sa) given sign(c) = sc (tracer.py:340-350)
+struct PtPartner { int base[PT_NMAX]; uint32_t mask; int sign_base; };
+__device__ __forceinline__ PtPartner pt_partner(int n, const int* u, uint32_t s, int sa, int j, int sc) {
+    PtCoface f = pt_coface(n, s, j);
+    PtPartner p;
+    if (sc == sa) {   // (b, c) crosses; shared endpoint b carries -sa
+        pt_apply_masks(n, u, f.bc_bplus, f.bc_bminus, p.base);
+        p.mask = f.bc_mask;
+        p.sign_base = f.bc_shared ? -sa : sc;
+    } else {          // (a, c) crosses; shared endpoint a carries sa
+        pt_apply_masks(n, u, f.ac_bplus, f.ac_bminus, p.base);
+        p.mask = f.ac_mask;
+        p.sign_base = f.ac_shared ? sa : sc;
+    }
+    return p;
+}
+
+__global__ void __launch_bounds__(256)
+pt_wave_partner_kernel(PtGeom g, PtTable sgn, PtTable vis, const u64* __restrict__ edge_key,
+                       const int8_t* __restrict__ edge_sa, const uint32_t* __restrict__ frontier, size_t fcount,
+                       int stride, const uint32_t* __restrict__ sgn_slot, uint32_t* __restrict__ vis_slot,
+                       PtCounters* ctr) {
+    const size_t w = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= fcount) return;
+    const uint32_t e = frontier[w];
+    const u64 ek = edge_key[e];
+    const int sa = edge_sa[e];
+    const uint32_t s = pt_edge_mask(g, ek);
+    int u[PT_NMAX];
+    pt_unpack_vertex(g, pt_edge_vkey(g, ek), u);
+    const int nc = pt_ncofaces(g.n, s);
+    for (int j0 = 0; j0 < stride; j0 += 32) {
+        const int j = j0 + lane;
+        uint32_t marker = PT_NONE32;
+        bool dropped = false;
+        if (j < nc) {
+            const int sc = pt_ld_cg(&sgn.ent[2 * (u64)sgn_slot[w * stride + j] + 1]) ? 1 : -1;
+            PtPartner p = pt_partner(g.n, u, s, sa, j, sc);
+            int other[PT_NMAX];
+            pt_apply_masks(g.n, p.base, p.mask, 0u, other);
+            if (!(pt_in_box(g, p.base) && pt_in_box(g, other))) {
+                dropped = true;
+            } else {
+                u64 bk;
+                if (!pt_pack_vertex(g, p.base, bk)) atomicOr(&ctr->error, PT_ERR_KEY_RANGE);
+                else {
+                    bool ins;
+                    u64 slot = pt_table_insert(vis, pt_edge_key(g, bk, p.mask), ins, &ctr->error);
+                    atomicMin(&vis.ent[2 * slot + 1], PT_VAL_PENDING_BASE + (u64)(w * stride + j));
+                    marker = (uint32_t)slot | (p.sign_base > 0 ? 0x80000000u : 0u);
+                }
+            }
+        }
+        unsigned db = __ballot_sync(0xffffffffu, dropped);
+        if (lane == 0 && db) atomicAdd(&ctr->dropped, (unsigned long long)__popc(db));
+        if (j < stride) vis_slot[w * stride + j] = marker;
+    }
+}
+
+// winners of each item (frontier edge or seed cell): val still equals this slot's pending id
+__global__ void __launch_bounds__(256)
+pt_wave_count_kernel(PtTable vis, size_t items, int stride, const uint32_t* __restrict__ vis_slot,
+                     uint32_t* __restrict__ wcount) {
+    const size_t w = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= items) return;
+    int count = 0;
+    for (int j0 = 0; j0 < stride; j0 += 32) {
+        const int j = j0 + lane;
+        bool win = false;
+        if (j < stride) {
+            uint32_t mk = vis_slot[w * stride + j];
+            if (mk != PT_NONE32)
+                win = pt_ld_cg(&vis.ent[2 * (u64)(mk & 0x7fffffffu) + 1]) == PT_VAL_PENDING_BASE + (u64)(w * stride + j);
+        }
+        count += __popc(__ballot_sync(0xffffffffu, win));
+    }
+    if (lane == 0) wcount[w] = (uint32_t)count;
+}
+
+__global__ void __launch_bounds__(256)
+pt_wave_admit_kernel(PtTable vis, size_t items, int stride, const uint32_t* __restrict__ vis_slot,
+                     const uint32_t* __restrict__ woff, long long n_edges, long long max_edges,
+                     u64* __restrict__ edge_key, int8_t* __restrict__ edge_sa) {
+    const size_t w = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= items) return;
+    long long running = n_edges + (long long)woff[w];
+    for (int j0 = 0; j0 < stride; j0 += 32) {
+        const int j = j0 + lane;
+        bool win = false; uint32_t mk = PT_NONE32;
+        if (j < stride) {
+            mk = vis_slot[w * stride + j];
+            if (mk != PT_NONE32)
+                win = pt_ld_cg(&vis.ent[2 * (u64)(mk & 0x7fffffffu) + 1]) == PT_VAL_PENDING_BASE + (u64)(w * stride + j);
+        }
+        unsigned ballot = __ballot_sync(0xffffffffu, win);
+        if (win) {
+            const long long idx = running + __popc(ballot & ((1u << lane) - 1u));
+            const u64 slot = (u64)(mk & 0x7fffffffu);
+            if (idx < max_edges) {
+                edge_key[idx] = vis.ent[2 * slot];
+                edge_sa[idx] = (mk & 0x80000000u) ? (int8_t)1 : (int8_t)-1;
+                vis.ent[2 * slot + 1] = (u64)idx;
+            } else {
+                vis.ent[2 * slot + 1] = PT_VAL_DEAD;
+            }
+        }
+        running += __popc(ballot);
+    }
+}
+
+__global__ void pt_iota_kernel(uint32_t* out, size_t count, uint32_t first) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) out[i] = first + (uint32_t)i;
+}
+
+// ---- host orchestration ----------------------------------------------------------------------
+int pt_read_counters(pt_trace* t) {
+    pt_ctx* ctx = t->ctx;
+    PT_CUDA(ctx, cudaMemcpyAsync(ctx->pinned, t->counters.p, sizeof(PtCounters), cudaMemcpyDeviceToHost, ctx->stream));
+    PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    memcpy(&t->host_counters, ctx->pinned, sizeof(PtCounters));
+    if (t->host_counters.error & PT_ERR_KEY_RANGE)
+        return pt_fail(ctx, PT_E_RANGE, "lattice coordinates left the packed-key window (%d bits per axis at n=%d)",
+                       t->geom.bits, t->geom.n);
+    if (t->host_counters.error & PT_ERR_TABLE_FULL) return pt_fail(ctx, PT_E_STATE, "hash table overflow (sizing bug)");
+    return PT_OK;
+}
+
+static int pt_reset_pending(pt_trace* t) {
+    // n_pending is the first field of PtCounters
+    PT_CUDA(t->ctx, cudaMemsetAsync(t->counters.p, 0, sizeof(unsigned long long), t->ctx->stream));
+    return PT_OK;
+}
+
+// evaluate the `count` queued vertices (slots in `pending`) and store their signs
+static int pt_eval_pending(pt_trace* t, const uint32_t* pending, size_t count) {
+    if (count == 0) return PT_OK;
+    pt_ctx* ctx = t->ctx;
+    PtBuf<double> pts; PtBuf<int8_t> sg;
+    PT_TRY(pts.alloc(ctx, count * t->geom.n));
+    PT_TRY(sg.alloc(ctx, count));
+    {
+        PT_LAUNCH(ctx, "trace_pending_points");
+        pt_pending_points_kernel<<<pt_grid_for(count, 256), 256, 0, ctx->stream>>>(t->geom, t->signs.view(), pending, count, pts.p);
+        PT_TRY(pt_check_launch(ctx, "pt_pending_points_kernel"));
+    }
+    PT_TRY(pt_field_eval_dev(ctx, t->field, pts.p, count, nullptr, sg.p));
+    {
+        PT_LAUNCH(ctx, "trace_pending_store");
+        pt_pending_store_kernel<<<pt_grid_for(count, 256), 256, 0, ctx->stream>>>(t->signs.view(), pending, count, sg.p);
+        PT_TRY(pt_check_launch(ctx, "pt_pending_store_kernel"));
+    }
+    t->field_evaluations += (long long)count;
+    t->signs.count += count;
+    return PT_OK;
+}
+
+// count winners, scan, admit; returns number admitted (after the cap)
+static int pt_admit_items(pt_trace* t, size_t items, int stride, const uint32_t* vis_slot, long long* admitted,
+                          long long* winners = nullptr) {
+    pt_ctx* ctx = t->ctx;
+    *admitted = 0;
+    if (winners) *winners = 0;
+    if (items == 0) return PT_OK;
+    PtBuf<uint32_t> wcount, woff;
+    PT_TRY(wcount.alloc(ctx, items + 1));
+    PT_TRY(woff.alloc(ctx, items + 1));
+    PT_CUDA(ctx, cudaMemsetAsync(wcount.p + items, 0, sizeof(uint32_t), ctx->stream));
+    {
+        PT_LAUNCH(ctx, "trace_wave_count");
+        pt_wave_count_kernel<<<pt_grid_for(items * 32, 256), 256, 0, ctx->stream>>>(t->visited.view(), items, stride, vis_slot, wcount.p);
+        PT_TRY(pt_check_launch(ctx, "pt_wave_count_kernel"));
+    }
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, wcount.p, woff.p, (int)(items + 1), ctx->stream);
+    PtBuf<uint8_t> tmp;
+    PT_TRY(tmp.alloc(ctx, tmp_bytes));
+    {
+        PT_LAUNCH(ctx, "trace_wave_scan");
+        PT_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp.p, tmp_bytes, wcount.p, woff.p, (int)(items + 1), ctx->stream));
+        ctx->launches++;
+    }
+    uint32_t* h = (uint32_t*)ctx->pinned;
+    PT_CUDA(ctx, cudaMemcpyAsync(h, woff.p + items, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    const long long total = (long long)*h;
+    if (winners) *winners = total;
+    t->visited.count += (u64)total;   // every winner owns a fresh table entry (admitted or dead)
+    if (total == 0) return PT_OK;
+    long long room = t->max_edges - t->n_edges;
+    if (room < 0) room = 0;
+    const long long take = total < room ? total : room;
+    if (take < total) t->complete = false;
+    PT_TRY(t->edge_key.ensure(ctx, (size_t)(t->n_edges + take + 1), (size_t)t->n_edges));
+    PT_TRY(t->edge_sa.ensure(ctx, (size_t)(t->n_edges + take + 1), (size_t)t->n_edges));
+    {
+        PT_LAUNCH(ctx, "trace_wave_admit");
+        pt_wave_admit_kernel<<<pt_grid_for(items * 32, 256), 256, 0, ctx->stream>>>(
+            t->visited.view(), items, stride, vis_slot, woff.p, t->n_edges, t->max_edges, t->edge_key.p, t->edge_sa.p);
+        PT_TRY(pt_check_launch(ctx, "pt_wave_admit_kernel"));
+    }
+    t->n_edges += take;
+    *admitted = take;
+    return PT_OK;
+}
+
+static int pt_set_window(pt_trace* t, const int* first_cell_base) {
+    PtGeom& g = t->geom;
+    if (g.has_box) {
+        for (int d = 0; d < g.n; ++d) {
+            g.origin[d] = g.box_lo[d] - 2;
+            long long span = (long long)g.box_hi[d] + 2 - g.origin[d];
+            if (span >= (1ll << g.bits))
+                return pt_fail(t->ctx, PT_E_RANGE, "clamp box spans %lld lattice units on axis %d; packed keys hold %lld at n=%d",
+                               span, d, (1ll << g.bits), g.n);
+        }
+    } else {
+        for (int d = 0; d < g.n; ++d) g.origin[d] = first_cell_base[d] - (1 << (g.bits - 1));
+    }
+    t->window_set = true;
+    return PT_OK;
+}
+
+static int pt_stride_for(int n) {
+    // max over edge types of (2^m1 - 2) + (2^(n+1-m1) - 2): attained at m1 = 1 or n
+    return (1 << n) - 2;
+}
+
+static int pt_set_range_frontier(pt_trace* t, long long first, long long count) {
+    pt_ctx* ctx = t->ctx;
+    PT_TRY(t->frontier.ensure(ctx, (size_t)(count > 0 ? count : 1), 0));
+    if (count > 0) {
+        pt_iota_kernel<<<pt_grid_for((size_t)count, 256), 256, 0, ctx->stream>>>(t->frontier.p, (size_t)count, (uint32_t)first);
+        PT_TRY(pt_check_launch(ctx, "pt_iota_kernel"));
+    }
+    t->n_frontier = count;
+    t->range_frontier = true;
+    return PT_OK;
+}
+
+static int pt_trace_locate_impl(pt_trace* t, const double* seeds, long long m) {
+    pt_ctx* ctx = t->ctx;
+    PtGeom& g = t->geom;
+    const int n = g.n;
+    if (m <= 0 || !seeds) return pt_fail(ctx, PT_E_INVALID, "seeds must be a non-empty (m, n) array");
+    PtBuf<double> tmp;
+    const double* sdev;
+    PT_TRY(pt_stage_in(ctx, seeds, (size_t)m * n, tmp, &sdev));
+    if (!t->window_set) {
+        double first[PT_NMAX];
+        PT_CUDA(ctx, cudaMemcpyAsync(first, sdev, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        int cb[PT_NMAX];
+        for (int d = 0; d < n; ++d) {
+            double y = (first[d] - g.offset[d]) / g.scale;
+            if (!(y == y) || y > 1e9 || y < -1e9) return pt_fail(ctx, PT_E_INVALID, "point coordinates must be finite");
+            cb[d] = (int)floor(y);
+        }
+        PT_TRY(pt_set_window(t, cb));
+    }
+    t->seeds += m;
+    PtBuf<int> cell_base; PtBuf<uint8_t> cell_perm;
+    PT_TRY(cell_base.alloc(ctx, (size_t)m * n));
+    PT_TRY(cell_perm.alloc(ctx, (size_t)m * n));
+    {
+        PT_LAUNCH(ctx, "trace_locate_cells");
+        pt_locate_cells_kernel<<<pt_grid_for((size_t)m, 128), 128, 0, ctx->stream>>>(g, sdev, (size_t)m, cell_base.p, cell_perm.p);
+        PT_TRY(pt_check_launch(ctx, "pt_locate_cells_kernel"));
+    }
+    t->stages.insert(t->stages.end(), {0, t->levels, m, m, m});
+    const size_t nverts = (size_t)m * (n + 1);
+    PT_TRY(pt_table_reserve(ctx, t->signs, nverts));
+    PtBuf<uint32_t> pending;
+    PT_TRY(pending.alloc(ctx, nverts));
+    PT_TRY(pt_reset_pending(t));
+    {
+        PT_LAUNCH(ctx, "trace_cell_vertices");
+        pt_cell_vertices_kernel<<<pt_grid_for(nverts, 256), 256, 0, ctx->stream>>>(g, t->signs.view(), cell_base.p, cell_perm.p,
+                                                                                     (size_t)m, pending.p, t->counters.p);
+        PT_TRY(pt_check_launch(ctx, "pt_cell_vertices_kernel"));
+    }
+    PT_TRY(pt_read_counters(t));
+    PT_TRY(pt_eval_pending(t, pending.p, (size_t)t->host_counters.n_pending));
+    const int bound = (n + 1) * n / 2;
+    const size_t nslots = (size_t)m * bound;
+    PT_TRY(pt_table_reserve(ctx, t->visited, nslots));
+    PtBuf<uint32_t> vis_slot;
+    PT_TRY(vis_slot.alloc(ctx, nslots));
+    const unsigned long long markers_before = t->host_counters.markers;
+    {
+        PT_LAUNCH(ctx, "trace_cell_edges");
+        pt_cell_edges_kernel<<<pt_grid_for(nslots, 256), 256, 0, ctx->stream>>>(g, t->signs.view(), t->visited.view(), cell_base.p,
+                                                                                  cell_perm.p, (size_t)m, bound, vis_slot.p, t->counters.p);
+        PT_TRY(pt_check_launch(ctx, "pt_cell_edges_kernel"));
+    }
+    const long long before = t->n_edges;
+    long long admitted = 0;
+    PT_TRY(pt_admit_items(t, (size_t)m, bound, vis_slot.p, &admitted));
+    PT_TRY(pt_read_counters(t));
+    t->stages.insert(t->stages.end(), {1, t->levels, m, (long long)nslots, (long long)(t->host_counters.markers - markers_before)});
+    PT_TRY(pt_set_range_frontier(t, before, admitted));
+    return PT_OK;
+}
+
+static int pt_trace_expand_impl(pt_trace* t, long long* frontier_out) {
+    pt_ctx* ctx = t->ctx;
+    PtGeom& g = t->geom;
+    t->levels += 1;
+    const long long F = t->n_frontier;
+    const int stride = pt_stride_for(g.n);
+    const long long before = t->n_edges;
+    const unsigned long long cand_before = t->host_counters.candidates;
+    // chunk the frontier so the per-slot scratch stays bounded (~2^26 slots)
+    size_t chunk_edges = ((size_t)1 << 26) / (size_t)stride;
+    if (chunk_edges < 1024) chunk_edges = 1024;
+    PtBuf<uint32_t> sgn_slot, vis_slot, pending;
+    // the frontier buffer is replaced at the end; chunks read the current one
+    for (long long f0 = 0; f0 < F; f0 += (long long)chunk_edges) {
+        const size_t fc = (size_t)((F - f0) < (long long)chunk_edges ? (F - f0) : (long long)chunk_edges);
+        const size_t nslots = fc * (size_t)stride;
+        PT_TRY(sgn_slot.ensure(ctx, nslots, 0));
+        PT_TRY(vis_slot.ensure(ctx, nslots, 0));
+        PT_TRY(pending.ensure(ctx, nslots, 0));
+        PT_TRY(pt_table_reserve(ctx, t->signs, nslots));
+        PT_TRY(pt_table_reserve(ctx, t->visited, nslots));
+        PT_TRY(pt_reset_pending(t));
+        const uint32_t* fr = t->frontier.p + f0;
+        {
+            PT_LAUNCH(ctx, "trace_wave_probe");
+            pt_wave_probe_kernel<<<pt_grid_for(fc * 32, 256), 256, 0, ctx->stream>>>(g, t->signs.view(), t->edge_key.p, fr, fc, stride,
+                                                                                       sgn_slot.p, pending.p, t->counters.p);
+            PT_TRY(pt_check_launch(ctx, "pt_wave_probe_kernel"));
+        }
+        PT_TRY(pt_read_counters(t));
+        PT_TRY(pt_eval_pending(t, pending.p, (size_t)t->host_counters.n_pending));
+        {
+            PT_LAUNCH(ctx, "trace_wave_partner");
+            pt_wave_partner_kernel<<<pt_grid_for(fc * 32, 256), 256, 0, ctx->stream>>>(g, t->signs.view(), t->visited.view(), t->edge_key.p,
+                                                                                         t->edge_sa.p, fr, fc, stride, sgn_slot.p,
+                                                                                         vis_slot.p, t->counters.p);
+            PT_TRY(pt_check_launch(ctx, "pt_wave_partner_kernel"));
+        }
+        long long admitted = 0;
+        PT_TRY(pt_admit_items(t, fc, stride, vis_slot.p, &admitted));
+    }
+    PT_TRY(pt_read_counters(t));
+    const long long cands = (long long)(t->host_counters.candidates - cand_before);
+    t->stages.insert(t->stages.end(), {2, t->levels, F, cands, cands});
+    t->stages.insert(t->stages.end(), {3, t->levels, cands, cands, cands});
+    if (t->range_frontier) t->expanded_upto = before;   // everything before the new frontier is expanded
+    PT_TRY(pt_set_range_frontier(t, before, t->n_edges - before));
+    t->n_adj = -1;
+    if (frontier_out) *frontier_out = t->n_frontier;
+    return PT_OK;
+}
+
+// ---- result assembly ------------------------------------------------------------------------
+__global__ void pt_edge_endpoints_kernel(PtGeom g, const u64* __restrict__ edge_key, size_t first, size_t count,
+                                         double* __restrict__ a, double* __restrict__ b) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const u64 ek = edge_key[first + i];
+    int u[PT_NMAX], v[PT_NMAX]; double x[PT_NMAX];
+    pt_unpack_vertex(g, pt_edge_vkey(g, ek), u);
+    pt_apply_masks(g.n, u, pt_edge_mask(g, ek), 0u, v);
+    pt_vertex_point(g, u, x);
+    for (int d = 0; d < g.n; ++d) a[i * g.n + d] = x[d];
+    pt_vertex_point(g, v, x);
+    for (int d = 0; d < g.n; ++d) b[i * g.n + d] = x[d];
+}
+
+__global__ void pt_edge_unpack_kernel(PtGeom g, const u64* __restrict__ edge_key, size_t first, size_t count,
+                                      int32_t* __restrict__ base, uint32_t* __restrict__ mask) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const u64 ek = edge_key[first + i];
+    if (base) {
+        int u[PT_NMAX];
+        pt_unpack_vertex(g, pt_edge_vkey(g, ek), u);
+        for (int d = 0; d < g.n; ++d) base[i * g.n + d] = u[d];
+    }
+    if (mask) mask[i] = pt_edge_mask(g, ek);
+}
+
+// adjacency (tracer.py:249-251): pairs (edge, partner) for every coface of every expanded edge
+__global__ void __launch_bounds__(256)
+pt_adjacency_kernel(PtGeom g, PtTable sgn, PtTable vis, const u64* __restrict__ edge_key, const int8_t* __restrict__ edge_sa,
+                    size_t count, int stride, u64* __restrict__ pairs) {
+    const size_t w = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= count) return;
+    const u64 ek = edge_key[w];
+    const int sa = edge_sa[w];
+    const uint32_t s = pt_edge_mask(g, ek);
+    int u[PT_NMAX];
+    pt_unpack_vertex(g, pt_edge_vkey(g, ek), u);
+    const int nc = pt_ncofaces(g.n, s);
+    for (int j = lane; j < stride; j += 32) {
+        u64 out = PT_EMPTY;
+        if (j < nc) {
+            PtCoface f = pt_coface(g.n, s, j);
+            int c[PT_NMAX]; u64 ck, cslot;
+            pt_apply_masks(g.n, u, f.c_plus, f.c_minus, c);
+            if (pt_pack_vertex(g, c, ck) && pt_table_find(sgn, ck, cslot)) {
+                u64 sv = sgn.ent[2 * cslot + 1];
+                if (sv <= 1ull) {
+                    PtPartner p = pt_partner(g.n, u, s, sa, j, sv ? 1 : -1);
+                    u64 bk, eslot;
+                    if (pt_pack_vertex(g, p.base, bk) && pt_table_find(vis, pt_edge_key(g, bk, p.mask), eslot)) {
+                        u64 idx = vis.ent[2 * eslot + 1];
+                        if (idx < PT_VAL_PENDING_BASE && idx != (u64)w) {
+                            u64 lo = idx < (u64)w ? idx : (u64)w, hi = idx < (u64)w ? (u64)w : idx;
+                            out = (lo << 32) | hi;
+                        }
+                    }
+                }
+            }
+        }
+        pairs[w * stride + j] = out;
+    }
+}
+
+// ---- seeding from explicit edges (expand_frontier, tracer.py:418-433) ---------------------------
+__global__ void pt_seed_insert_kernel(PtGeom g, PtTable vis, const int32_t* __restrict__ base, const uint32_t* __restrict__ mask,
+                                      size_t m, uint32_t* __restrict__ vis_slot, PtCounters* ctr) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    int u[PT_NMAX];
+    for (int d = 0; d < g.n; ++d) u[d] = base[i * g.n + d];
+    u64 bk; uint32_t marker = PT_NONE32;
+    if (!pt_pack_vertex(g, u, bk)) atomicOr(&ctr->error, PT_ERR_KEY_RANGE);
+    else {
+        bool ins;
+        u64 slot = pt_table_insert(vis, pt_edge_key(g, bk, mask[i]), ins, &ctr->error);
+        atomicMin(&vis.ent[2 * slot + 1], PT_VAL_PENDING_BASE + (u64)i);
+        marker = (uint32_t)slot;
+    }
+    vis_slot[i] = marker;
+}
+// resolve frontier rows to edge indices and queue their endpoints for sign evaluation
+__global__ void pt_seed_frontier_kernel(PtGeom g, PtTable vis, PtTable sgn, const int32_t* __restrict__ base,
+                                        const uint32_t* __restrict__ mask, size_t count, uint32_t* __restrict__ frontier,
+                                        uint32_t* __restrict__ pending, PtCounters* ctr) {
+    size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    size_t i = tid >> 1; int which = (int)(tid & 1);
+    bool inserted = false; u64 slot = 0;
+    if (i < count) {
+        int u[PT_NMAX], v[PT_NMAX];
+        for (int d = 0; d < g.n; ++d) u[d] = base[i * g.n + d];
+        pt_apply_masks(g.n, u, which ? mask[i] : 0u, 0u, v);
+        u64 vk;
+        if (!pt_pack_vertex(g, v, vk)) atomicOr(&ctr->error, PT_ERR_KEY_RANGE);
+        else {
+            slot = pt_table_insert(sgn, vk, inserted, &ctr->error);
+            if (!which) {
+                u64 es;
+                if (pt_table_find(vis, pt_edge_key(g, vk, mask[i]), es)) frontier[i] = (uint32_t)vis.ent[2 * es + 1];
+                else { frontier[i] = 0; atomicOr(&ctr->error, PT_ERR_TABLE_FULL); }
+            }
+        }
+    }
+    unsigned long long pos = pt_warp_append(&ctr->n_pending, inserted);
+    if (inserted) pending[pos] = (uint32_t)slot;
+}
+__global__ void pt_seed_signs_kernel(PtGeom g, PtTable sgn, const u64* __restrict__ edge_key, const uint32_t* __restrict__ frontier,
+                                     size_t count, int8_t* __restrict__ edge_sa) {
+    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const uint32_t e = frontier[i];
+    u64 slot;
+    if (pt_table_find(sgn, pt_edge_vkey(g, edge_key[e]), slot)) edge_sa[e] = sgn.ent[2 * slot + 1] ? (int8_t)1 : (int8_t)-1;
+}
+
+extern "C" {
+
+int pt_trace_seed_edges(pt_trace* t, const int32_t* base, const uint32_t* mask, long long n_visited, long long n_frontier) {
+    if (!t) return pt_fail(nullptr, PT_E_INVALID, "trace is NULL");
+    pt_ctx* ctx = t->ctx;
+    PtGeom& g = t->geom;
+    const int n = g.n;
+    const long long m = n_visited + n_frontier;
+    if (n_visited < 0 || n_frontier < 0) return pt_fail(ctx, PT_E_INVALID, "negative edge count");
+    if (m == 0) { t->n_frontier = 0; return PT_OK; }
+    if (!base || !mask) return pt_fail(ctx, PT_E_INVALID, "edge arrays are NULL");
+    PtBuf<int32_t> tb; PtBuf<uint32_t> tm;
+    const int32_t* bdev; const uint32_t* mdev;
+    PT_TRY(pt_stage_in(ctx, base, (size_t)m * n, tb, &bdev));
+    PT_TRY(pt_stage_in(ctx, mask, (size_t)m, tm, &mdev));
+    if (!t->window_set) {
+        int32_t first[PT_NMAX];
+        PT_CUDA(ctx, cudaMemcpyAsync(first, bdev, n * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+        PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        int cb[PT_NMAX];
+        for (int d = 0; d < n; ++d) cb[d] = first[d];
+        PT_TRY(pt_set_window(t, cb));
+    }
+    PT_TRY(pt_table_reserve(ctx, t->visited, (u64)m));
+    PtBuf<uint32_t> vis_slot;
+    PT_TRY(vis_slot.alloc(ctx, (size_t)m));
+    {
+        PT_LAUNCH(ctx, "trace_seed_insert");
+        pt_seed_insert_kernel<<<pt_grid_for((size_t)m, 256), 256, 0, ctx->stream>>>(g, t->visited.view(), bdev, mdev, (size_t)m,
+                                                                                      vis_slot.p, t->counters.p);
+        PT_TRY(pt_check_launch(ctx, "pt_seed_insert_kernel"));
+    }
+    long long admitted = 0;
+    PT_TRY(pt_admit_items(t, (size_t)m, 1, vis_slot.p, &admitted));
+    PT_TRY(t->frontier.ensure(ctx, (size_t)(n_frontier > 0 ? n_frontier : 1), 0));
+    t->n_frontier = n_frontier;
+    t->range_frontier = false;
+    if (n_frontier > 0) {
+        PT_TRY(pt_table_reserve(ctx, t->signs, (u64)(2 * n_frontier)));
+        PtBuf<uint32_t> pending;
+        PT_TRY(pending.alloc(ctx, (size_t)(2 * n_frontier)));
+        PT_TRY(pt_reset_pending(t));
+        {
+            PT_LAUNCH(ctx, "trace_seed_frontier");
+            pt_seed_frontier_kernel<<<pt_grid_for((size_t)(2 * n_frontier), 256), 256, 0, ctx->stream>>>(
+                g, t->visited.view(), t->signs.view(), bdev + (size_t)n_visited * n, mdev + n_visited, (size_t)n_frontier,
+                t->frontier.p, pending.p, t->counters.p);
+            PT_TRY(pt_check_launch(ctx, "pt_seed_frontier_kernel"));
+        }
+        PT_TRY(pt_read_counters(t));
+        PT_TRY(pt_eval_pending(t, pending.p, (size_t)t->host_counters.n_pending));
+        {
+            PT_LAUNCH(ctx, "trace_seed_signs");
+            pt_seed_signs_kernel<<<pt_grid_for((size_t)n_frontier, 256), 256, 0, ctx->stream>>>(g, t->signs.view(), t->edge_key.p,
+                                                                                                  t->frontier.p, (size_t)n_frontier, t->edge_sa.p);
+            PT_TRY(pt_check_launch(ctx, "pt_seed_signs_kernel"));
+        }
+    }
+    PT_TRY(pt_read_counters(t));
+    return PT_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int pt_trace_create(pt_ctx* ctx, const pt_field* field, int n, double scale, const double* offset, const double* box_lo,
+                    const double* box_hi, long long max_edges, double eps, pt_trace** out) {
+    if (!ctx || !field || !out) return pt_fail(ctx, PT_E_INVALID, "pt_trace_create: NULL argument");
+    if (n < 2 || n > 7) return pt_fail(ctx, PT_E_INVALID, "lattice dimension %d unsupported (2..7)", n);
+    if (pt_field_dim(field) != n) return pt_fail(ctx, PT_E_INVALID, "manifold and lattice dimension mismatch");
+    if (!(scale > 0.0)) return pt_fail(ctx, PT_E_INVALID, "lattice scale must be positive");
+    if (max_edges < 1) return pt_fail(ctx, PT_E_INVALID, "max_edges must be positive");
+    if (max_edges > (1ll << 31) - 2) return pt_fail(ctx, PT_E_INVALID, "max_edges above 2^31-2 is not supported");
+    if (!(eps > 0.0)) return pt_fail(ctx, PT_E_INVALID, "eps must be positive");
+    if ((box_lo == nullptr) != (box_hi == nullptr)) return pt_fail(ctx, PT_E_INVALID, "box needs both bounds");
+    pt_trace* t = new pt_trace();
+    t->ctx = ctx; t->field = field; t->max_edges = max_edges; t->eps = eps;
+    memset(&t->geom, 0, sizeof(t->geom));
+    memset(&t->host_counters, 0, sizeof(t->host_counters));
+    PtGeom& g = t->geom;
+    g.n = n; g.bits = pt_bits_for_dim(n); g.scale = scale;
+    for (int d = 0; d < n; ++d) g.offset[d] = offset ? offset[d] : 0.0;
+    if (box_lo) {
+        g.has_box = 1;
+        for (int d = 0; d < n; ++d) {
+            if (!(box_lo[d] < box_hi[d])) { delete t; return pt_fail(ctx, PT_E_INVALID, "box must be a (lower, upper) pair with lower < upper"); }
+            // vertex bounds in lattice units (tracer.py:174-175); integer v passes iff lo <= v <= hi
+            double lo = (box_lo[d] - g.offset[d]) / scale, hi = (box_hi[d] - g.offset[d]) / scale;
+            if (lo < -2e9 || hi > 2e9) { delete t; return pt_fail(ctx, PT_E_RANGE, "clamp box too large for 32-bit lattice coordinates"); }
+            g.box_lo[d] = (int)ceil(lo); g.box_hi[d] = (int)floor(hi);
+            t->box_lo_f[d] = lo; t->box_hi_f[d] = hi;
+        }
+        int rc = pt_set_window(t, nullptr);
+        if (rc != PT_OK) { delete t; return rc; }
+    }
+    int rc = t->counters.alloc(ctx, 1);
+    if (rc == PT_OK) { cudaMemsetAsync(t->counters.p, 0, sizeof(PtCounters), ctx->stream); }
+    if (rc == PT_OK) rc = pt_table_init(ctx, t->visited, 1 << 16);
+    if (rc == PT_OK) rc = pt_table_init(ctx, t->signs, 1 << 16);
+    if (rc == PT_OK) rc = t->edge_key.alloc(ctx, 1 << 12);
+    if (rc == PT_OK) rc = t->edge_sa.alloc(ctx, 1 << 12);
+    if (rc != PT_OK) { delete t; return rc; }
+    *out = t;
+    return PT_OK;
+}
+
+void pt_trace_destroy(pt_trace* t) { delete t; }
+
+int pt_trace_locate(pt_trace* t, const double* seeds, long long m) {
+    if (!t) return pt_fail(nullptr, PT_E_INVALID, "trace is NULL");
+    return pt_trace_locate_impl(t, seeds, m);
+}
+
+int pt_trace_expand(pt_trace* t, long long* frontier_out) {
+    if (!t) return pt_fail(nullptr, PT_E_INVALID, "trace is NULL");
+    if (!t->window_set) return pt_fail(t->ctx, PT_E_STATE, "expand before locate/seed");
+    return pt_trace_expand_impl(t, frontier_out);
+}
+
+int pt_trace_run(pt_trace* t, const double* seeds, long long m) {
+    if (!t) return pt_fail(nullptr, PT_E_INVALID, "trace is NULL");
+    PT_TRY(pt_trace_locate_impl(t, seeds, m));
+    while (t->n_frontier > 0 && t->complete) PT_TRY(pt_trace_expand_impl(t, nullptr));
+    if (t->n_frontier == 0) t->expanded_upto = t->n_edges;
+    return PT_OK;
+}
+
+int pt_trace_get_stats(pt_trace* t, pt_trace_stats* out) {
+    if (!t || !out) return pt_fail(nullptr, PT_E_INVALID, "pt_trace_get_stats: NULL argument");
+    PT_TRY(pt_read_counters(t));
+    out->levels = t->levels; out->seeds = t->seeds; out->visited_edges = t->n_edges;
+    out->field_evaluations = t->field_evaluations;
+    out->dropped_out_of_box = (long long)t->host_counters.dropped;
+    out->candidates = (long long)t->host_counters.candidates;
+    out->frontier = t->n_frontier;
+    out->complete = t->complete ? 1 : 0;
+    out->closure_ok = (t->n_edges > 0 && t->complete && t->host_counters.dropped == 0) ? 1 : 0;
+    out->table_capacity = (long long)t->visited.capacity;
+    out->sign_table_capacity = (long long)t->signs.capacity;
+    out->n_stages = (long long)(t->stages.size() / 5);
+    return PT_OK;
+}
+
+int pt_trace_stages(pt_trace* t, long long* out, long long rows) {
+    if (!t || !out) return pt_fail(nullptr, PT_E_INVALID, "pt_trace_stages: NULL argument");
+    long long have = (long long)(t->stages.size() / 5);
+    if (rows > have) rows = have;
+    memcpy(out, t->stages.data(), (size_t)rows * 5 * sizeof(long long));
+    return PT_OK;
+}
+
+int pt_trace_edges(pt_trace* t, long long first, long long count, int32_t* base, uint32_t* mask, int8_t* sign_a) {
+    if (!t) return pt_fail(nullptr, PT_E_INVALID, "trace is NULL");
+    pt_ctx* ctx = t->ctx;
+    if (first < 0 || count < 0 || first + count > t->n_edges) return pt_fail(ctx, PT_E_INVALID, "edge range out of bounds");
+    if (count == 0) return PT_OK;
+    const int n = t->geom.n;
+    PtBuf<int32_t> tb; PtBuf<uint32_t> tm;
+    int32_t* bdev = nullptr; uint32_t* mdev = nullptr;
+    if (base) { if (pt_is_device_ptr(base)) bdev = base; else { PT_TRY(tb.alloc(ctx, (size_t)count * n)); bdev = tb.p; } }
+    if (mask) { if (pt_is_device_ptr(mask)) mdev = mask; else { PT_TRY(tm.alloc(ctx, (size_t)count)); mdev = tm.p; } }
+    if (bdev || mdev) {
+        pt_edge_unpack_kernel<<<pt_grid_for((size_t)count, 256), 256, 0, ctx->stream>>>(t->geom, t->edge_key.p, (size_t)first,
+                                                                                          (size_t)count, bdev, mdev);
+        PT_TRY(pt_check_launch(ctx, "pt_edge_unpack_kernel"));
+    }
+    if (base && bdev != base) PT_TRY(pt_copy_out(ctx, base, bdev, (size_t)count * n, false));
+    if (mask && mdev != mask) PT_TRY(pt_copy_out(ctx, mask, mdev, (size_t)count, false));
+    if (sign_a) PT_TRY(pt_copy_out(ctx, sign_a, t->edge_sa.p + first, (size_t)count, false));
+    PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return PT_OK;
+}
+
+int pt_trace_frontier(pt_trace* t, long long* first, long long* count) {
+    if (!t) return pt_fail(nullptr, PT_E_INVALID, "trace is NULL");
+    if (!t->range_frontier) return pt_fail(t->ctx, PT_E_STATE, "frontier is not an index range");
+    if (first) *first = t->n_edges - t->n_frontier;
+    if (count) *count = t->n_frontier;
+    return PT_OK;
+}
+
+int pt_trace_points(pt_trace* t, double* out) {
+    if (!t) return pt_fail(nullptr, PT_E_INVALID, "trace is NULL");
+    pt_ctx* ctx = t->ctx;
+    const size_t E = (size_t)t->n_edges;
+    if (E == 0) return PT_OK;
+    if (!out) return pt_fail(ctx, PT_E_INVALID, "points output is NULL");
+    const int n = t->geom.n;
+    PtBuf<double> a, b, o;
+    PT_TRY(a.alloc(ctx, E * n));
+    PT_TRY(b.alloc(ctx, E * n));
+    double* odev = out;
+    if (!pt_is_device_ptr(out)) { PT_TRY(o.alloc(ctx, E * n)); odev = o.p; }
+    {
+        PT_LAUNCH(ctx, "trace_edge_endpoints");
+        pt_edge_endpoints_kernel<<<pt_grid_for(E, 256), 256, 0, ctx->stream>>>(t->geom, t->edge_key.p, 0, E, a.p, b.p);
+        PT_TRY(pt_check_launch(ctx, "pt_edge_endpoints_kernel"));
+    }
+    PT_TRY(pt_field_bisect_dev(ctx, t->field, a.p, b.p, t->edge_sa.p, E, t->eps, odev));
+    if (odev != out) PT_TRY(pt_copy_out(ctx, out, odev, E * n, false));
+    PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return PT_OK;
+}
+
+long long pt_trace_adjacency(pt_trace* t, long long* pairs, long long cap) {
+    if (!t) { pt_fail(nullptr, PT_E_INVALID, "trace is NULL"); return PT_E_INVALID; }
+    pt_ctx* ctx = t->ctx;
+    if (t->n_adj < 0) {
+        const size_t count = (size_t)t->expanded_upto;
+        t->n_adj = 0;
+        if (count > 0) {
+            const int stride = pt_stride_for(t->geom.n);
+            const size_t total = count * (size_t)stride;
+            PtBuf<u64> raw, sorted;
+            if (raw.alloc(ctx, total) != PT_OK || sorted.alloc(ctx, total) != PT_OK) return PT_E_NOMEM;
+            {
+                PT_LAUNCH(ctx, "trace_adjacency");
+                pt_adjacency_kernel<<<pt_grid_for(count * 32, 256), 256, 0, ctx->stream>>>(t->geom, t->signs.view(), t->visited.view(),
+                                                                                             t->edge_key.p, t->edge_sa.p, count, stride, raw.p);
+                if (pt_check_launch(ctx, "pt_adjacency_kernel") != PT_OK) return PT_E_CUDA;
+            }
+            size_t tb = 0, tb2 = 0;
+            cub::DeviceRadixSort::SortKeys(nullptr, tb, raw.p, sorted.p, (long long)total, 0, 64, ctx->stream);
+            PtBuf<long long> nsel;
+            if (nsel.alloc(ctx, 1) != PT_OK) return PT_E_NOMEM;
+            cub::DeviceSelect::Unique(nullptr, tb2, sorted.p, raw.p, nsel.p, (long long)total, ctx->stream);
+            PtBuf<uint8_t> tmp;
+            if (tmp.alloc(ctx, tb > tb2 ? tb : tb2) != PT_OK) return PT_E_NOMEM;
+            cub::DeviceRadixSort::SortKeys(tmp.p, tb, raw.p, sorted.p, (long long)total, 0, 64, ctx->stream);
+            cub::DeviceSelect::Unique(tmp.p, tb2, sorted.p, raw.p, nsel.p, (long long)total, ctx->stream);
+            ctx->launches += 2;
+            long long* h = (long long*)ctx->pinned;
+            cudaMemcpyAsync(h, nsel.p, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream);
+            if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) { pt_fail(ctx, PT_E_CUDA, "adjacency sort failed"); return PT_E_CUDA; }
+            long long uniq = *h;
+            // the EMPTY sentinel (all ones) sorts last; drop it if present
+            if (uniq > 0) {
+                u64 last;
+                cudaMemcpy(&last, raw.p + (uniq - 1), sizeof(u64), cudaMemcpyDeviceToHost);
+                if (last == PT_EMPTY) uniq -= 1;
+            }
+            if (t->adj.alloc(ctx, (size_t)(uniq > 0 ? uniq : 1)) != PT_OK) return PT_E_NOMEM;
+            cudaMemcpyAsync(t->adj.p, raw.p, (size_t)uniq * sizeof(u64), cudaMemcpyDeviceToDevice, ctx->stream);
+            cudaStreamSynchronize(ctx->stream);
+            t->n_adj = uniq;
+        }
+    }
+    if (pairs) {
+        long long take = t->n_adj < cap ? t->n_adj : cap;
+        std::vector<u64> h((size_t)take);
+        if (take > 0) cudaMemcpy(h.data(), t->adj.p, (size_t)take * sizeof(u64), cudaMemcpyDeviceToHost);
+        for (long long i = 0; i < take; ++i) { pairs[2 * i] = (long long)(h[(size_t)i] >> 32); pairs[2 * i + 1] = (long long)(h[(size_t)i] & 0xffffffffull); }
+    }
+    return t->n_adj;
+}
+
+}  // extern "C"
