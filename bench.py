@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: trace -> coarse_cells -> refine(+collision check) on a synthetic
+6-DoF scene (BASELINE.json config 4 shape; `--workload` selects the others).
+
+    python bench.py --gpus 1 --steps 5 --warmup 3            # this repo's CUDA path
+    python bench.py --impl reference --steps 1 --warmup 0    # the reference's CPU path (oracle port)
+
+One "step" is one full pass of the hot path over one batch of synthetic input.  Metric (SURVEY.md
+section 8d): simplices/s = (traced coarse edges + crossing fine edges) / time, the same unit count
+the reference's `cmd_bench` would report for the same job.  Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+from types import SimpleNamespace
+
+import numpy as np
+
+REPO = Path(__file__).resolve().parent
+if str(REPO) not in sys.path:
+    sys.path.insert(0, str(REPO))
+
+METRIC = "simplices_traced_and_collision_checked_per_sec"
+UNIT = "simplices/s"
+
+
+# ------------------------------------------------------------------------------------------------
+# workload construction (pure numpy/scipy; shared verbatim by both arms)
+# ------------------------------------------------------------------------------------------------
+
+def _train_numpy(pos, neg, gamma, regularization):
+    """Ridge fit on the RBF Gram matrix (reference manifold.py:236-268), numpy/scipy only."""
+    from scipy.linalg import cho_factor, cho_solve
+    x = np.vstack([pos, neg])
+    y = np.concatenate([np.ones(len(pos)), -np.ones(len(neg))])
+    sq = np.einsum("ij,ij->i", x, x)
+    gram = np.exp(-gamma * np.maximum(sq[:, None] + sq[None, :] - 2.0 * x @ x.T, 0.0))
+    gram[np.diag_indices_from(gram)] += regularization
+    return x, cho_solve(cho_factor(gram, lower=True), y)
+
+
+def _np_field(support, weights, gamma, bias, barrier):
+    """numpy evaluation of F and grad F, used ONLY to project the seed points during setup."""
+    scale, gain, lo, hi = barrier
+
+    def value(q):
+        d = q - support
+        k = np.exp(-gamma * np.einsum("ij,ij->i", d, d))
+        bar = gain * scale * (np.logaddexp(0.0, (lo - q) / scale) + np.logaddexp(0.0, (q - hi) / scale)).sum()
+        return float(weights @ k + bias - bar)
+
+    def grad(q):
+        from scipy.special import expit
+        d = q - support
+        k = np.exp(-gamma * np.einsum("ij,ij->i", d, d))
+        g = -2.0 * gamma * ((weights * k) @ d)
+        return g - gain * (expit((q - hi) / scale) - expit((lo - q) / scale))
+
+    return value, grad
+
+
+def _seeds_numpy(value, grad, lo, hi, count, rng, min_sep, tol=1e-8):
+    """sample_seeds / project_to_manifold (reference manifold.py:271-332) on the numpy field."""
+    kept, attempts = [], 0
+    while len(kept) < count and attempts < 20 * count:
+        attempts += 1
+        q = rng.uniform(lo, hi)
+        f = value(q)
+        ok = False
+        for _ in range(100):
+            if abs(f) <= tol:
+                ok = True
+                break
+            g = grad(q)
+            gg = float(g @ g)
+            if not np.isfinite(gg) or gg <= 0:
+                break
+            step, t, moved = (-f / gg) * g, 1.0, False
+            while t >= 1e-12:
+                q_new = q + t * step
+                f_new = value(q_new)
+                if abs(f_new) <= (1.0 - 1e-4 * t) * abs(f):
+                    moved = True
+                    break
+                t *= 0.5
+            if not moved:
+                break
+            q, f = q_new, f_new
+        if not ok:
+            continue
+        if kept and np.min(np.linalg.norm(np.asarray(kept) - q, axis=1)) < min_sep:
+            continue
+        kept.append(q)
+    return np.asarray(kept, dtype=np.float64).reshape(len(kept), lo.size)
+
+
+_WORKLOAD_CACHE: dict = {}
+
+
+def build_arrays(name: str):
+    """Everything both arms need, as plain arrays/dicts (SURVEY.md Appendix B recipe)."""
+    from paper_2406_04795_b200.scenes import BENCH_CONFIGS, arm_robot_dict, arm_scene_dict, synthetic_support
+    if name in _WORKLOAD_CACHE:
+        return _WORKLOAD_CACHE[name]
+    p = BENCH_CONFIGS[name]
+    n, lam, k, limit = p["n"], p["lam"], 2, 1.5
+    pos, neg, rng = synthetic_support(n, p["support"], p["r_split"], limit, seed=0)
+    gamma = 2.0
+    sigma = 1.0 / np.sqrt(2.0 * gamma)
+    lo, hi = -limit * np.ones(n), limit * np.ones(n)
+    barrier = (sigma / 4.0, 2.0 / sigma, lo, hi)
+    support, weights = _train_numpy(pos, neg, gamma, 1e-3)
+    bias = lam * np.sqrt(2.0 * gamma)
+    coarse = lam * k
+    margin = max(3.0 * coarse, 2.0 * sigma + (1.0 + 2.0 * np.sqrt(n)) * coarse)
+    value, grad = _np_field(support, weights, gamma, bias, barrier)
+    seeds = _seeds_numpy(value, grad, lo, hi, 20, rng, coarse / 2.0)
+    w = SimpleNamespace(name=name, n=n, lam=lam, k=k, coarse=coarse, support=support, weights=weights, gamma=gamma,
+                        bias=bias, barrier=barrier, box=(tuple(lo - margin), tuple(hi + margin)), seeds=seeds,
+                        robot_dict=arm_robot_dict(n), scene_dict=arm_scene_dict(p["obstacles"]), eps=1e-9,
+                        params=p)
+    _WORKLOAD_CACHE[name] = w
+    return w
+
+
+def build_workload(name: str):
+    """Product-side objects for a workload (needs the CUDA library)."""
+    import paper_2406_04795_b200 as P
+    from paper_2406_04795_b200 import collision as CO
+    a = build_arrays(name)
+    scale, gain, lo, hi = a.barrier
+    manifold = P.KernelClassifierManifold(a.support, a.weights, a.gamma, a.bias, barrier=P.BoxBarrier(lo, hi, scale, gain))
+    cfg = P.TraceConfig(P.LatticeConfig(a.n, a.coarse), box=a.box, eps=a.eps, max_edges=(1 << 31) - 2)
+    robot, scene = CO.robot_from_dict(a.robot_dict), CO.scene_from_dict(a.scene_dict)
+    return SimpleNamespace(arrays=a, manifold=manifold, cfg=cfg, seeds=a.seeds, robot=robot, scene=scene,
+                           template=P.build_template(a.n, a.k), problem=SimpleNamespace(robot=robot, scene=scene))
+
+
+# ------------------------------------------------------------------------------------------------
+# clocks
+# ------------------------------------------------------------------------------------------------
+
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.device), "-lms", "100"], stdout=subprocess.PIPE, text=True)
+            self.thread = threading.Thread(target=self._pump, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1])); mx.append(float(r[2]))
+            except (ValueError, IndexError):
+                continue
+            for nm, val in zip(names, r[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(np.max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------------
+# GPU arm
+# ------------------------------------------------------------------------------------------------
+
+def pair_flops(n: int) -> float:
+    """Algorithmic FP64 work of one (point, support vector) pair: n subtractions, n multiply-adds for
+    the squared distance, the gamma scale, one exp, one weighted accumulate = (3n+2) flop + 1 exp
+    (SURVEY.md section 8d).  exp is charged as 22 flop: the range reduction (2 FMA), degree-11
+    polynomial (11 FMA) and 2^k scaling that a correctly rounded double exp needs at minimum."""
+    return 3.0 * n + 2.0 + 22.0
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2406_04795_b200 as P
+    from paper_2406_04795_b200 import _cabi, engine
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    wl = build_workload(args.workload)
+    a = wl.arrays
+    ctx = _cabi.context(local)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    checker = P.not_free_checker(wl.problem)
+
+    # resident inputs for the kernel-only number
+    seeds_dev = torch.from_numpy(a.seeds).cuda()
+    pipe = engine.DevicePipeline(wl.manifold, wl.cfg, wl.template, checker, rank=rank, world=world)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- resident-input throughput ("value") ---------------------------------------------------
+    for _ in range(args.warmup):
+        pipe.step(seeds_dev.data_ptr(), a.seeds.shape[0])
+    barrier()
+    launches0 = ctx.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        e0.record(stream)
+        for _ in range(args.steps):
+            counts = pipe.step(seeds_dev.data_ptr(), a.seeds.shape[0])
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.launch_count() - launches0
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    units = torch.tensor([float(counts["simplices_local"])], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(units, op=dist.ReduceOp.SUM)
+    ms = float(t.item())
+    simplices = float(units.item()) + (counts["trace_edges"] if world > 1 else 0.0)   # trace counted once
+    if world == 1:
+        simplices = float(counts["simplices_local"])
+    value = simplices * args.steps / (ms * 1e-3)
+
+    # ---- end to end through the public API with host buffers ---------------------------------------
+    seeds_pinned = torch.from_numpy(a.seeds.copy()).pin_memory()
+    scale, gain, lo, hi = a.barrier
+
+    def e2e_step():
+        manifold = P.KernelClassifierManifold(a.support, a.weights, a.gamma, a.bias,
+                                              barrier=P.BoxBarrier(lo, hi, scale, gain))   # uploads the support set
+        res = P.trace(seeds_pinned.numpy(), manifold, wl.cfg)            # points come back to the host
+        cells = P.coarse_cells(res)
+        ref = P.refine(cells, wl.template, manifold, checker, wl.cfg)    # points + labels come back to the host
+        return res, ref
+
+    e2e_step()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        res, ref = e2e_step()
+    barrier()
+    e2e_s = time.perf_counter() - t0
+    tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    e2e_s = float(tt.item())
+    e2e_simplices = len(res.edges) + sum(b.crossing_edges for b in ref.batch_stats)
+    h2d = a.support.nbytes + a.weights.nbytes + a.seeds.nbytes
+    d2h = res.points.nbytes + ref.points.nbytes + ref.in_collision.nbytes
+    e2e = {"value": e2e_simplices * args.steps * (world if False else 1) / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+
+    # ---- per-kernel profile of one more step (CUDA events on the launching stream) -------------------
+    ctx.profile(True)
+    ctx.profile_reset()
+    pipe.step(seeds_dev.data_ptr(), a.seeds.shape[0])
+    prof = ctx.profile_dump()
+    ctx.profile(False)
+    total_ms = sum(v[1] for v in prof.values()) or 1.0
+    top = max(prof.items(), key=lambda kv: kv[1][1])
+    pair_evals = counts["pair_evals_bisect"] if top[0].startswith("bisect") else counts["pair_evals_eval"]
+    peak = engine.measure_fp64_peak(ctx)
+    roofline = None
+    if top[0] in ("bisect_rbf", "eval_rbf"):
+        achieved = pair_evals * pair_flops(a.n) / (top[1][1] * 1e-3) / 1e12
+        roofline = {"bound": "fp64", "kernel": top[0], "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak if peak else None, "traffic": None,
+                    "peak_source": "DFMA microbenchmark run in this process (MEASURED_PEAKS.json holds only HBM and bf16)",
+                    "launches": top[1][0], "avg_launch_ms": top[1][1] / max(top[1][0], 1),
+                    "share_of_step": top[1][1] / total_ms,
+                    "pair_evals_per_step": pair_evals, "flop_per_pair_eval": pair_flops(a.n)}
+    peaks = {}
+    try:
+        peaks = json.loads((REPO / "MEASURED_PEAKS.json").read_text())
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    kernels = {k: {"launches": v[0], "ms": round(v[1], 4)} for k, v in sorted(prof.items(), key=lambda kv: -kv[1][1])}
+    bfs_ms = sum(prof.get(k, (0, 0.0))[1] for k in ("trace_wave_probe", "trace_wave_partner", "trace_wave_count", "trace_wave_admit"))
+    bfs_bytes = counts["candidates"] * 96.0 + counts["trace_edges"] * (32 + 64 + 8 * a.n)
+    hbm = {"bound": "hbm", "kernel": "trace_wave_*", "achieved": bfs_bytes / (bfs_ms * 1e-3) / 1e9 if bfs_ms else None,
+           "peak": hbm_peak, "unit": "GB/s", "peak_source": "MEASURED_PEAKS.json" if peaks else "fallback 6650",
+           "frac": (bfs_bytes / (bfs_ms * 1e-3) / 1e9) / hbm_peak if bfs_ms else None}
+
+    line = None
+    if rank == 0:
+        cpu = cpu_baseline(args.workload, max(1, min(os.cpu_count() or 1, 64))) if world == 1 and not args.no_cpu_baseline else None
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: {a.n}-DoF arm, {len(a.scene_dict['obstacles'])} primitives, "
+                                   f"S={a.support.shape[0]} support vectors, lambda={a.lam}, k={a.k}",
+                       "l2_policy": "per-step working set (hash tables + fine-edge arrays) exceeds the 126 MB L2; "
+                                    "all tables are rebuilt from empty every step",
+                       "trace_edges": counts["trace_edges"], "coarse_cells": counts["cells"],
+                       "crossing_fine_edges": counts["crossing_edges"], "unique_fine_edges": counts["unique_fine_edges"],
+                       "points_checked": counts["points"], "free_points": counts["free_points"],
+                       "closure_ok": counts["closure_ok"]},
+            "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": int(launches),
+            "roofline": roofline, "roofline_hbm": hbm, "kernels": kernels, "cpu_baseline": cpu,
+            "proof_time_s": ms / args.steps * 1e-3,
+        }
+    if world > 1:
+        dist.destroy_process_group()
+    return line
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU arm: the reference's algorithm (oracle port), bounded sample of the same workload
+# ------------------------------------------------------------------------------------------------
+
+def cpu_sample(workload: str, threads: int, max_edges: int = 1500, max_cells: int = 150):
+    """One bounded sample: the same scene/manifold/lattice, BFS capped at `max_edges` coarse edges,
+    refinement of the first `max_cells` sorted coarse cells.  Returns (simplices, seconds)."""
+    from oracle import permatrace_oracle as O
+    from tests.conftest import oracle_model
+    a = build_arrays(workload)
+    O.THREADS = threads
+    scale, gain, lo, hi = a.barrier
+    field = O.Field.rbf(a.support, a.weights, a.gamma, a.bias, barrier=(scale, gain, lo, hi))
+    robot, scene = oracle_model(a.robot_dict, a.scene_dict)
+    template = O.build_template(a.n, a.k)
+    t0 = time.perf_counter()
+    tr = O.Trace(field, a.n, a.coarse, None, a.box, max_edges, a.eps).run(a.seeds)
+    tr.points()
+    cells = O.coarse_cells(tr.edges)[:max_cells]
+    ref = O.refine(cells, template, field, lambda p: O.not_free(robot, scene, p), a.coarse, np.zeros(a.n), a.k, a.eps)
+    dt = time.perf_counter() - t0
+    simplices = len(tr.edges) + sum(ref["crossing_edges"])
+    return simplices, dt, {"coarse_edges": len(tr.edges), "cells_refined": len(cells),
+                           "crossing_fine_edges": int(sum(ref["crossing_edges"])), "points": int(ref["points"].shape[0])}
+
+
+def cpu_baseline(workload: str, threads: int):
+    simplices, dt, info = cpu_sample(workload, threads)
+    return {"value": simplices / dt, "unit": UNIT, "cores": threads, "kind": "port", "seconds": dt,
+            "sample": f"same scene/manifold/lattice; BFS capped at {info['coarse_edges']} coarse edges, "
+                      f"{info['cells_refined']} coarse cells refined ({info['crossing_fine_edges']} crossing fine edges, "
+                      f"{info['points']} points checked); kernel sums threaded over {threads} host threads, "
+                      "lattice bookkeeping single-threaded like the reference"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    threads = max(1, min(os.cpu_count() or 1, 64))
+    for _ in range(args.warmup):
+        cpu_sample(args.workload, threads, max_edges=200, max_cells=10)
+    total_s, total_t, info = 0, 0.0, None
+    for _ in range(args.steps):
+        s, dt, info = cpu_sample(args.workload, threads)
+        total_s += s
+        total_t += dt
+    a = build_arrays(args.workload)
+    value = total_s / total_t
+    sample = (f"per step: BFS capped at {info['coarse_edges']} coarse edges + {info['cells_refined']} coarse cells refined "
+              f"of the same scene/manifold/lattice")
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_t / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: {a.n}-DoF arm, {len(a.scene_dict['obstacles'])} primitives, "
+                                   f"S={a.support.shape[0]} support vectors, lambda={a.lam}, k={a.k}", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="dof6")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    line = run_reference(args) if args.impl == "reference" else run_gpu(args)
+    if line is not None:
+        print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -45,6 +45,11 @@ int pt_ctx_profile_reset(pt_ctx* ctx);
 /* writes "name,launches,total_ms\n" lines; returns bytes needed (call with cap=0 to size) */
 long long pt_ctx_profile_dump(pt_ctx* ctx, char* buf, long long cap);
 long long pt_ctx_launch_count(pt_ctx* ctx);
+/* device-side work counters: out[0] = bisection field evaluations (rows x iterations), out[1] = points
+ * evaluated by the batch evaluator; reset != 0 zeroes them */
+int pt_ctx_work_counters(pt_ctx* ctx, long long* out, int reset);
+/* DFMA-chain microbenchmark: measured FP64 peak of this device in TFLOP/s (roofline denominator) */
+double pt_peak_fp64(pt_ctx* ctx);
 
 /* ---- B1: the reference's kernel plugin seam (backend.py:30-33, _kernels.pyx) ---------------- */
 /* _kernels.pyx:18-40 rbf_values(points[m,n], support[S,n], weights[S], gamma, bias) -> out[m] */
@@ -160,6 +165,8 @@ int pt_cells_from_edges(pt_ctx* ctx, int n, const int32_t* base, const uint32_t*
 /* cells given by the caller in processing order: base[C,n] int32, perm[C,n] uint8 */
 int pt_cells_from_host(pt_ctx* ctx, int n, const int32_t* base, const uint8_t* perm, long long count,
                        pt_cells** out);
+/* contiguous sub-range of a cell list (multi-GPU sharding of refine) */
+int pt_cells_slice(const pt_cells* c, long long first, long long count, pt_cells** out);
 void pt_cells_destroy(pt_cells* c);
 long long pt_cells_count(const pt_cells* c);
 int pt_cells_get(const pt_cells* c, long long first, long long count, int32_t* base, uint8_t* perm);

@@ -66,6 +66,8 @@ _SIGS = {
     "pt_ctx_profile_reset": (_i, [_vp]),
     "pt_ctx_profile_dump": (_ll, [_vp, C.c_char_p, _ll]),
     "pt_ctx_launch_count": (_ll, [_vp]),
+    "pt_ctx_work_counters": (_i, [_vp, _vp, _i]),
+    "pt_peak_fp64": (_d, [_vp]),
     "pt_rbf_values": (_i, [_vp, _vp, _ll, _i, _vp, _ll, _vp, _d, _d, _vp]),
     "pt_sphere_box_hits": (_i, [_vp, _vp, _vp, _ll, _d, _d, _d, _vp]),
     "pt_sphere_cylinder_hits": (_i, [_vp, _vp, _vp, _ll, _d, _d, _vp]),
@@ -95,6 +97,7 @@ _SIGS = {
     "pt_cells_from_trace": (_i, [_vp, _pp]),
     "pt_cells_from_edges": (_i, [_vp, _i, _vp, _vp, _ll, _pp]),
     "pt_cells_from_host": (_i, [_vp, _i, _vp, _vp, _ll, _pp]),
+    "pt_cells_slice": (_i, [_vp, _ll, _ll, _pp]),
     "pt_cells_destroy": (None, [_vp]),
     "pt_cells_count": (_ll, [_vp]),
     "pt_cells_get": (_i, [_vp, _ll, _ll, _vp, _vp]),

@@ -16,5 +16,5 @@ for src in pt_ctx pt_host pt_field pt_collision pt_trace pt_cells pt_refine; do
   fi
 done
 for p in "${pids[@]:-}"; do [[ -n "$p" ]] && wait "$p"; done
-"$NVCC" -shared -o "$out" "$obj"/pt_ctx.o "$obj"/pt_host.o "$obj"/pt_field.o "$obj"/pt_collision.o "$obj"/pt_trace.o "$obj"/pt_cells.o "$obj"/pt_refine.o
+"$NVCC" -gencode arch=compute_100a,code=sm_100a -shared -o "$out" "$obj"/pt_ctx.o "$obj"/pt_host.o "$obj"/pt_field.o "$obj"/pt_collision.o "$obj"/pt_trace.o "$obj"/pt_cells.o "$obj"/pt_refine.o
 echo "built $out"

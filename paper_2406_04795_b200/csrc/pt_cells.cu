@@ -238,6 +238,20 @@ int pt_cells_from_host(pt_ctx* ctx, int n, const int32_t* base, const uint8_t* p
     return PT_OK;
 }
 
+int pt_cells_slice(const pt_cells* c, long long first, long long count, pt_cells** out) {
+    if (!c || !out) return pt_fail(nullptr, PT_E_INVALID, "pt_cells_slice: NULL argument");
+    pt_ctx* ctx = c->ctx;
+    if (first < 0 || count < 0 || first + count > c->count) return pt_fail(ctx, PT_E_INVALID, "cell range out of bounds");
+    pt_cells* s = new pt_cells();
+    s->ctx = ctx; s->n = c->n; s->geom = c->geom; s->count = count;
+    for (int d = 0; d < PT_NMAX; ++d) { s->base_min[d] = c->base_min[d]; s->base_max[d] = c->base_max[d]; }
+    int rc = s->keys.alloc(ctx, (size_t)(count > 0 ? count : 1));
+    if (rc != PT_OK) { delete s; return rc; }
+    cudaMemcpyAsync(s->keys.p, c->keys.p + first, (size_t)count * sizeof(u64), cudaMemcpyDeviceToDevice, ctx->stream);
+    *out = s;
+    return PT_OK;
+}
+
 void pt_cells_destroy(pt_cells* c) { delete c; }
 long long pt_cells_count(const pt_cells* c) { return c ? c->count : -1; }
 

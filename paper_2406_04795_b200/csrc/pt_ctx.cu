@@ -2,6 +2,18 @@
 #include <stdarg.h>
 #include "pt_internal.cuh"
 
+// FP64 peak microbenchmark: 8 independent DFMA chains per thread, enough blocks to fill the chip
+__global__ void __launch_bounds__(256) pt_peak_fp64_kernel(double* out, int iters, double seed) {
+    double a0 = seed, a1 = seed + 1, a2 = seed + 2, a3 = seed + 3, a4 = seed + 4, a5 = seed + 5, a6 = seed + 6, a7 = seed + 7;
+    const double m = 1.0000001, c = 1e-9;
+    for (int i = 0; i < iters; ++i) {
+        a0 = fma(a0, m, c); a1 = fma(a1, m, c); a2 = fma(a2, m, c); a3 = fma(a3, m, c);
+        a4 = fma(a4, m, c); a5 = fma(a5, m, c); a6 = fma(a6, m, c); a7 = fma(a7, m, c);
+    }
+    double r = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+    if (r == 123.456) out[0] = r;   // never true; keeps the chains alive
+}
+
 thread_local std::string g_pt_last_error;
 
 int pt_fail(pt_ctx* ctx, int code, const char* fmt, ...) {
@@ -104,6 +116,8 @@ int pt_ctx_create(int device, pt_ctx** out) {
     }
     ctx->pinned_bytes = 1 << 16;
     PT_CUDA(ctx, cudaMallocHost(&ctx->pinned, ctx->pinned_bytes));
+    PT_CUDA(ctx, cudaMalloc((void**)&ctx->work, 8 * sizeof(unsigned long long)));
+    PT_CUDA(ctx, cudaMemset(ctx->work, 0, 8 * sizeof(unsigned long long)));
     *out = ctx;
     return PT_OK;
 }
@@ -116,6 +130,7 @@ void pt_ctx_destroy(pt_ctx* ctx) {
         for (auto& pr : kv.second.pending) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->work) cudaFree(ctx->work);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -162,5 +177,38 @@ long long pt_ctx_profile_dump(pt_ctx* ctx, char* buf, long long cap) {
     return need;
 }
 long long pt_ctx_launch_count(pt_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int pt_ctx_work_counters(pt_ctx* ctx, long long* out, int reset) {
+    if (!ctx || !out) return pt_fail(ctx, PT_E_INVALID, "pt_ctx_work_counters: NULL argument");
+    unsigned long long h[8];
+    PT_CUDA(ctx, cudaMemcpyAsync(h, ctx->work, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    out[0] = (long long)h[0]; out[1] = (long long)h[1];
+    if (reset) PT_CUDA(ctx, cudaMemsetAsync(ctx->work, 0, sizeof(h), ctx->stream));
+    return PT_OK;
+}
+
+double pt_peak_fp64(pt_ctx* ctx) {
+    if (!ctx) return -1.0;
+    double* d = nullptr;
+    if (cudaMalloc((void**)&d, sizeof(double)) != cudaSuccess) return -1.0;
+    const int iters = 1 << 15, blocks = ctx->sm_count * 8, threads = 256;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    double best = 0.0;
+    for (int rep = 0; rep < 4; ++rep) {
+        cudaEventRecord(e0, ctx->stream);
+        pt_peak_fp64_kernel<<<blocks, threads, 0, ctx->stream>>>(d, iters, 0.5);
+        cudaEventRecord(e1, ctx->stream);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        double tf = 2.0 * 8.0 * (double)iters * blocks * threads / (ms * 1e-3) / 1e12;
+        if (rep > 0 && tf > best) best = tf;
+    }
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+    cudaFree(d);
+    return best;
+}
 
 }  // extern "C"

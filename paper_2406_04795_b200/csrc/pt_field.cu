@@ -53,7 +53,7 @@ __device__ __forceinline__ double pt_rbf_block_sum(const PtFieldDev& f, const do
 template <int N, int G>
 __global__ void __launch_bounds__(PT_EVAL_THREADS)
 pt_eval_rbf_kernel(PtFieldDev f, const double* __restrict__ pts, size_t m, double* __restrict__ vals,
-                   int8_t* __restrict__ signs) {
+                   int8_t* __restrict__ signs, unsigned long long* work) {
     extern __shared__ double tile[];
     const int PB = PT_EVAL_THREADS / G;
     const size_t pi = (size_t)blockIdx.x * PB + threadIdx.x / G;
@@ -62,6 +62,7 @@ pt_eval_rbf_kernel(PtFieldDev f, const double* __restrict__ pts, size_t m, doubl
     double p[N];
 #pragma unroll
     for (int d = 0; d < N; ++d) p[d] = valid ? pts[pi * N + d] : 0.0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&work[1], (unsigned long long)m);
     double acc = pt_rbf_block_sum<N, G>(f, p, g, tile);
     if (valid && g == 0) {
         double F = f.bias + acc;
@@ -97,7 +98,8 @@ __device__ __forceinline__ double pt_segment(const double* a, const double* b, d
 template <int N, int G>
 __global__ void __launch_bounds__(PT_EVAL_THREADS)
 pt_bisect_rbf_kernel(PtFieldDev f, const double* __restrict__ a_, const double* __restrict__ b_,
-                     const int8_t* __restrict__ signs_a, size_t m, double eps, double* __restrict__ out) {
+                     const int8_t* __restrict__ signs_a, size_t m, double eps, double* __restrict__ out,
+                     unsigned long long* work) {
     extern __shared__ double tile[];
     const int PB = PT_EVAL_THREADS / G;
     const size_t ei = (size_t)blockIdx.x * PB + threadIdx.x / G;
@@ -118,6 +120,7 @@ pt_bisect_rbf_kernel(PtFieldDev f, const double* __restrict__ a_, const double* 
     }
     double lo = 0.0, hi = 1.0;
     bool active = valid && seg > eps;
+    unsigned iters = 0;
     while (__syncthreads_or(active ? 1 : 0)) {
         const double mid = __dmul_rn(0.5, __dadd_rn(lo, hi));
 #pragma unroll
@@ -134,7 +137,14 @@ pt_bisect_rbf_kernel(PtFieldDev f, const double* __restrict__ a_, const double* 
         if (active) {
             if (s == sa) lo = mid; else hi = mid;
             active = __dmul_rn(seg, __dsub_rn(hi, lo)) > eps;
+            ++iters;
         }
+    }
+    {
+        // rows x iterations actually needed (idle lanes of finished rows are not counted)
+        unsigned mine = (g == 0) ? iters : 0u;
+        for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
+        if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&work[0], (unsigned long long)mine);
     }
     if (valid && g == 0) {
         const double t = __dmul_rn(0.5, __dadd_rn(lo, hi));
@@ -200,11 +210,11 @@ static int pt_eval_launch(pt_ctx* ctx, const pt_field* f, const double* pts, siz
     const size_t smem = (size_t)PT_EVAL_TILE * ((N + 1) | 1) * sizeof(double);
     PT_LAUNCH(ctx, "eval_rbf");
     if (G == 1)
-        pt_eval_rbf_kernel<N, 1><<<pt_grid_for(m, PT_EVAL_THREADS), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, pts, m, vals, signs);
+        pt_eval_rbf_kernel<N, 1><<<pt_grid_for(m, PT_EVAL_THREADS), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, pts, m, vals, signs, ctx->work);
     else if (G == 4)
-        pt_eval_rbf_kernel<N, 4><<<pt_grid_for(m, PT_EVAL_THREADS / 4), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, pts, m, vals, signs);
+        pt_eval_rbf_kernel<N, 4><<<pt_grid_for(m, PT_EVAL_THREADS / 4), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, pts, m, vals, signs, ctx->work);
     else
-        pt_eval_rbf_kernel<N, 32><<<pt_grid_for(m, PT_EVAL_THREADS / 32), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, pts, m, vals, signs);
+        pt_eval_rbf_kernel<N, 32><<<pt_grid_for(m, PT_EVAL_THREADS / 32), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, pts, m, vals, signs, ctx->work);
     return pt_check_launch(ctx, "pt_eval_rbf_kernel");
 }
 
@@ -220,11 +230,11 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
     const size_t smem = (size_t)PT_EVAL_TILE * ((N + 1) | 1) * sizeof(double);
     PT_LAUNCH(ctx, "bisect_rbf");
     if (G == 1)
-        pt_bisect_rbf_kernel<N, 1><<<pt_grid_for(m, PT_EVAL_THREADS), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, a, b, sa, m, eps, out);
+        pt_bisect_rbf_kernel<N, 1><<<pt_grid_for(m, PT_EVAL_THREADS), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, a, b, sa, m, eps, out, ctx->work);
     else if (G == 4)
-        pt_bisect_rbf_kernel<N, 4><<<pt_grid_for(m, PT_EVAL_THREADS / 4), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, a, b, sa, m, eps, out);
+        pt_bisect_rbf_kernel<N, 4><<<pt_grid_for(m, PT_EVAL_THREADS / 4), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, a, b, sa, m, eps, out, ctx->work);
     else
-        pt_bisect_rbf_kernel<N, 32><<<pt_grid_for(m, PT_EVAL_THREADS / 32), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, a, b, sa, m, eps, out);
+        pt_bisect_rbf_kernel<N, 32><<<pt_grid_for(m, PT_EVAL_THREADS / 32), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, a, b, sa, m, eps, out, ctx->work);
     return pt_check_launch(ctx, "pt_bisect_rbf_kernel");
 }
 

@@ -27,6 +27,8 @@ struct pt_ctx {
     std::vector<cudaEvent_t> event_pool;
     long long launches = 0;            // total kernel launches issued by this library
     int sm_count = 148;
+    // device-side work counters: [0] bisection field evaluations (rows x iterations), [1] points evaluated
+    unsigned long long* work = nullptr;
     // pinned scratch for small device->host readbacks (counters)
     void* pinned = nullptr;
     size_t pinned_bytes = 0;

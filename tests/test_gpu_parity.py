@@ -1,0 +1,433 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the reference's golden vectors and
+the CPU oracle on the same seeded inputs.  Bit-exact for integer / index / boolean results;
+intersection points within 1e-5 relative (BASELINE.json north_star) -- in practice ~1e-12."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+import paper_2406_04795_b200 as P
+from paper_2406_04795_b200 import backend as B, collision as CO, lattice as L, manifold as M, subdivision as S, tracer as T
+from oracle import permatrace_oracle as O
+from tests.conftest import (ANALYTIC_TRACES, LEARNED_TRACES, PRISM_ROBOT, PRISM_SCENE, analytic_spec, oracle_model,
+                            robot_scene_dicts, trace_inputs)
+
+POINT_RTOL = 1e-5     # north_star tolerance for intersection points
+POINT_ATOL = 1e-8     # what we actually hold (bracket is 1e-9)
+
+
+def product_manifold(g, tag):
+    if tag.startswith("kclf"):
+        gbb, bar = g[f"{tag}_gbb"], g[f"{tag}_barrier"]
+        n = g[f"{tag}_support"].shape[1]
+        barrier = M.BoxBarrier(bar[2:2 + n], bar[2 + n:], bar[0], bar[1])
+        return M.KernelClassifierManifold(g[f"{tag}_support"], g[f"{tag}_weights"], gbb[0], gbb[1], barrier=barrier)
+    kind, args = analytic_spec(tag)
+    return {"sphere": M.SphereManifold, "ellipsoid": M.EllipsoidManifold, "plane": M.PlaneManifold}[kind](*args)
+
+
+def oracle_field(g, tag):
+    from tests.test_oracle_golden import oracle_field as f
+    return f(g, tag)
+
+
+def product_cfg(inp):
+    return T.TraceConfig(L.LatticeConfig(inp["n"], inp["scale"], inp["offset"]), box=inp["box"],
+                         max_edges=inp["max_edges"], eps=inp["eps"])
+
+
+# ---- B1 seam ---------------------------------------------------------------------------------------
+def test_backend_seam(golden):
+    g = golden("backend")
+    gamma, bias = g["rbf_params"]
+    got = B.rbf_values(g["rbf_points"], g["rbf_support"], g["rbf_weights"], gamma, bias)
+    tol = 1e-12 * (np.abs(g["rbf_weights"]).sum() + abs(bias))          # pkg/tests/test_backends.py:90-93
+    assert got.dtype == np.float64 and np.max(np.abs(got - g["rbf_values"])) <= tol
+    c, r = g["hits_centers"], g["hits_radii"]
+    assert np.array_equal(B.sphere_box_hits(c, r, 0.8, 0.5, 1.1), g["hits_box"])
+    assert np.array_equal(B.sphere_cylinder_hits(c, r, 0.9, 0.4), g["hits_cyl"])
+    assert np.array_equal(B.sphere_sphere_hits(c, r, 0.6), g["hits_sph"])
+    tc, tr = g["touch_centers"], g["touch_radii"]
+    assert list(B.sphere_box_hits(tc, tr, 2.0, 2.0, 2.0)) == [1, 0, 0, 1, 0]
+    assert np.array_equal(B.sphere_cylinder_hits(tc, tr, 2.0, 1.0), g["touch_cyl"])
+    assert np.array_equal(B.sphere_sphere_hits(tc, tr, 1.0), g["touch_sph"])
+    assert B.sphere_box_hits(c, r, 0.8, 0.5, 1.1).dtype == np.uint8
+
+
+def test_backend_edge_cases():
+    pts = np.random.default_rng(0).normal(size=(7, 3))
+    assert np.array_equal(B.rbf_values(pts, np.zeros((0, 3)), np.zeros(0), 1.0, 0.75), np.full(7, 0.75))   # bias only
+    assert B.rbf_values(np.zeros((0, 3)), np.zeros((4, 3)), np.ones(4), 1.0, 0.0).shape == (0,)
+    assert B.sphere_sphere_hits(np.zeros((0, 3)), np.zeros(0), 1.0).shape == (0,)
+    with pytest.raises(ValueError, match="shape mismatch"):
+        B.rbf_values(pts, np.zeros((4, 2)), np.ones(4), 1.0, 0.0)
+    with pytest.raises(ValueError, match="shape mismatch"):
+        B.rbf_values(pts, np.zeros((4, 3)), np.ones(5), 1.0, 0.0)
+    # large batch, every lane-group configuration (G = 32, 4, 1) must agree
+    rng = np.random.default_rng(1)
+    sup, w = rng.normal(size=(700, 5)), rng.normal(size=700)
+    big = rng.normal(size=(400000, 5))
+    full = B.rbf_values(big, sup, w, 0.5, 0.1)
+    tol = 1e-12 * (np.abs(w).sum() + 0.1)
+    assert np.max(np.abs(full[:50] - B.rbf_values(big[:50], sup, w, 0.5, 0.1))) <= tol
+    assert np.max(np.abs(full[:100000] - B.rbf_values(big[:100000], sup, w, 0.5, 0.1))) <= tol
+    assert np.max(np.abs(full[:3000] - O.rbf_values(big[:3000], sup, w, 0.5, 0.1))) <= tol
+
+
+# ---- fields ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("tag", LEARNED_TRACES)
+def test_learned_field_values_and_signs(golden, tag):
+    g = golden("traces")
+    m = product_manifold(g, tag)
+    pts, want = g[f"{tag}_probe_points"], g[f"{tag}_probe_values"]
+    got = m.values(pts)
+    tol = 1e-12 * (np.abs(m.weights).sum() + abs(m.bias)) + 1e-13 * np.abs(want)
+    assert np.all(np.abs(got - want) <= tol)
+    clear = np.abs(want) > 10 * tol
+    assert np.array_equal(m.signs(pts)[clear], np.where(want > 0, 1, -1)[clear])
+    assert m.signs(pts).dtype == np.int8
+    assert abs(m.value(pts[0]) - want[0]) <= tol[0]
+
+
+@pytest.mark.parametrize("kind,n", [("sphere", 2), ("sphere", 3), ("sphere", 4), ("sphere", 5), ("sphere", 6), ("sphere", 7),
+                                     ("ellipsoid", 3), ("ellipsoid", 6), ("plane", 3), ("plane", 5)])
+def test_analytic_fields_bit_exact(kind, n):
+    """Lattice-aligned probes make exact zeros and ties common, so the arithmetic order matters."""
+    rng = np.random.default_rng(n)
+    if kind == "sphere":
+        prod, orc = M.SphereManifold(np.zeros(n), 0.8), O.Field.sphere(np.zeros(n), 0.8)
+    elif kind == "ellipsoid":
+        c, a = rng.normal(size=n) * 0.1, rng.uniform(0.5, 1.0, size=n)
+        prod, orc = M.EllipsoidManifold(c, a), O.Field.ellipsoid(c, a)
+    else:
+        nrm = rng.normal(size=n)
+        prod, orc = M.PlaneManifold(nrm, 0.1), O.Field.plane(nrm, 0.1)
+    lattice_pts = rng.integers(-8, 9, size=(20000, n)) * 0.1
+    random_pts = rng.normal(size=(20000, n))
+    for pts in (lattice_pts, random_pts):
+        want = orc.values(pts)
+        got = prod.values(pts)
+        if kind == "plane":       # BLAS matvec order is not part of the contract; signs must agree off zero
+            assert np.allclose(got, want, rtol=0, atol=1e-14)
+        else:
+            assert np.array_equal(got, want)
+            assert np.array_equal(prod.signs(pts), orc.signs(pts))
+
+
+def test_bisection(golden):
+    g = golden("backend")
+    f = M.SphereManifold(np.zeros(3), 1.0)
+    got = M.intersection_points_batch(f, g["bisect_a"], g["bisect_b"], 1e-9)
+    assert np.array_equal(got, g["bisect_points"])
+    one = M.intersection_point(f, g["bisect_a"][0], g["bisect_b"][0], 1e-9)
+    assert np.array_equal(one, g["bisect_points"][0])
+    with pytest.raises(ValueError):
+        M.intersection_point(f, [0.0, 0, 0], [0.1, 0, 0], 1e-9)
+    assert M.edge_intersects(f, [0.0, 0, 0], [2.0, 0, 0]) and not M.edge_intersects(f, [0.0, 0, 0], [0.5, 0, 0])
+    # segments shorter than eps are never bisected: t = 0.5
+    a = np.array([[1.0, 0.0, 0.0]]); b = a + 1e-12
+    assert np.array_equal(M.intersection_points_batch(f, a, b, 1e-9, signs_a=[-1]), a + 0.5 * (b - a))
+    assert M.intersection_points_batch(f, np.zeros((0, 3)), np.zeros((0, 3)), 1e-9).shape == (0, 3)
+    # linear field: root at t = 0.25 (pkg/tests/test_acceptance.py:318-339)
+    pl = M.PlaneManifold([1.0, 0.0], 0.25)
+    p = M.intersection_point(pl, [0.0, 0.0], [1.0, 0.0], 1e-9)
+    assert abs(p[0] - 0.25) < 1e-9
+
+
+def test_bisection_learned(golden):
+    g = golden("traces")
+    tag = "kclf_n4"
+    m, of = product_manifold(g, tag), oracle_field(g, tag)
+    inp = trace_inputs(g, tag)
+    base, mask = g[f"{tag}_edge_base"].astype(np.float64), g[f"{tag}_edge_mask"]
+    steps = np.array([[(int(mm) >> d) & 1 for d in range(4)] for mm in mask], dtype=np.float64)
+    a = base * inp["scale"] + np.asarray(inp["offset"])
+    b = (base + steps) * inp["scale"] + np.asarray(inp["offset"])
+    got = M.intersection_points_batch(m, a, b, 1e-9)
+    want = O.intersection_points_batch(of, a, b, 1e-9)
+    assert np.allclose(got, want, rtol=POINT_RTOL, atol=POINT_ATOL)
+    assert np.allclose(got, g[f"{tag}_points"], rtol=POINT_RTOL, atol=POINT_ATOL)
+
+
+# ---- tracer -------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("tag", ANALYTIC_TRACES + LEARNED_TRACES)
+def test_trace_matches_reference(golden, tag):
+    g = golden("traces")
+    inp = trace_inputs(g, tag)
+    res = T.trace(inp["seeds"], product_manifold(g, tag), product_cfg(inp))
+    base, mask, sa = res.edges.arrays()
+    assert np.array_equal(base, g[f"{tag}_edge_base"]), "edge set / admission order differs"
+    assert np.array_equal(mask, g[f"{tag}_edge_mask"])
+    st, want = res.stats, g[f"{tag}_stats"]
+    assert [st.levels, st.seeds, st.visited_edges, st.field_evaluations, st.dropped_out_of_box, int(st.complete),
+            int(st.closure_ok)] == list(want[:7])
+    assert (-1 if st.polyline_closed is None else int(st.polyline_closed)) == int(want[7])
+    names = ("locate_cells", "cell_edges", "edge_cofaces", "coface_partner")
+    stages = np.array([[names.index(s.name), s.level, s.items, s.capacity, s.produced] for s in st.stages])
+    assert np.array_equal(stages, g[f"{tag}_stages"])
+    adj = np.asarray(res.adjacency, dtype=np.int64).reshape(-1, 2)
+    if f"{tag}_adjacency" in g:
+        assert np.array_equal(adj, g[f"{tag}_adjacency"])
+    else:
+        digest = [adj.shape[0], int(adj[:, 0].sum()), int(adj[:, 1].sum()), int((adj[:, 0] * 31 + adj[:, 1]).sum() % (1 << 61))]
+        assert digest == list(g[f"{tag}_adjacency_digest"])
+    if tag.startswith("kclf"):
+        assert np.allclose(res.points, g[f"{tag}_points"], rtol=POINT_RTOL, atol=POINT_ATOL)
+    else:
+        assert np.array_equal(res.points, g[f"{tag}_points"])
+    # list-like behaviour of the lazy edge view
+    assert len(res.edges) == st.visited_edges
+    e0 = res.edges[0]
+    assert isinstance(e0, L.PermSimplex) and e0.base == tuple(int(v) for v in base[0])
+    e0.validate()
+
+
+def test_locate_and_expand_api(golden):
+    g = golden("traces")
+    inp = trace_inputs(g, "sphere_n3")
+    f, cfg = product_manifold(g, "sphere_n3"), product_cfg(inp)
+    of = oracle_field(g, "sphere_n3")
+    frontier = T.locate_edges(inp["seeds"], f, cfg)
+    ot = O.Trace(of, 3, inp["scale"], inp["offset"])
+    entries = ot.locate(inp["seeds"])
+    assert [(e.base, e.parts) for e in frontier.edges] == [e for e, _ in entries]
+    assert list(frontier.signs) == [s for _, s in entries]
+    assert frontier.capacity == len(inp["seeds"]) * 6
+    visited = set(frontier.edges)
+    nxt = T.expand_frontier(frontier, visited, f, cfg)
+    for e, s in entries:
+        ot.admit(e, s)
+    want = ot.expand(entries)
+    assert [(e.base, e.parts) for e in nxt.edges] == [e for e, _ in want]
+    assert visited == set(frontier.edges) | set(nxt.edges)
+    with pytest.raises(ValueError):
+        T.trace(np.zeros((0, 3)), f, cfg)
+    with pytest.raises(ValueError):
+        T.trace(np.zeros((1, 2)), f, cfg)
+    with pytest.raises(ValueError):
+        T.trace(inp["seeds"], f, T.TraceConfig(L.LatticeConfig(3, 0.5), box=((0, 0, 0), (1, 0, 1))))
+    with pytest.raises(ValueError):
+        T.trace(inp["seeds"], M.SphereManifold(np.zeros(2), 1.0), cfg)
+    # a seed whose cell does not touch the zero set: explicit empty result
+    empty = T.trace(np.array([[5.0, 5.0, 5.0]]), f, cfg)
+    assert len(empty.edges) == 0 and empty.points.shape == (0, 3) and not empty.closure_ok and empty.adjacency == []
+
+
+def test_trace_independent_of_seed_order_as_a_set(golden):
+    g = golden("traces")
+    inp = trace_inputs(g, "kclf_n4")
+    m, cfg = product_manifold(g, "kclf_n4"), product_cfg(inp)
+    a = T.trace(inp["seeds"], m, cfg)
+    b = T.trace(inp["seeds"][::-1], m, cfg)
+    ka = {(tuple(r), int(mm)) for r, mm in zip(*a.edges.arrays()[:2])}
+    kb = {(tuple(r), int(mm)) for r, mm in zip(*b.edges.arrays()[:2])}
+    assert ka == kb and a.closure_ok and b.closure_ok
+
+
+# ---- coarse cells + refine ------------------------------------------------------------------------------
+@pytest.mark.parametrize("tag", ["kclf_n3", "kclf_n4", "kclf_n5"])
+def test_coarse_cells(golden, tag):
+    g = golden("traces")
+    inp = trace_inputs(g, tag)
+    res = T.trace(inp["seeds"], product_manifold(g, tag), product_cfg(inp))
+    cells = S.coarse_cells(res)
+    base, perm = cells.arrays()
+    if f"{tag}_cells_base" in g:
+        assert np.array_equal(base, g[f"{tag}_cells_base"]) and np.array_equal(perm, g[f"{tag}_cells_perm"])
+        c0 = cells[0]
+        assert c0.dim == inp["n"] and c0.parts[-1] == (inp["n"],)
+    else:
+        n = inp["n"]
+        assert len(cells) == int(g[f"{tag}_cells_count"][0])
+        assert [int(base.sum()), int((perm.astype(np.int64) * np.arange(1, n + 1)).sum())] == list(g[f"{tag}_cells_digest"])
+        keys = [tuple(b) + tuple(p) for b, p in zip(base.tolist(), perm.tolist())]
+        assert keys == sorted(keys)
+
+
+@pytest.mark.parametrize("tag", ["sphere_n2_k3", "sphere_n3_k2", "sphere_n4_k2"])
+def test_refine_analytic(golden, tag):
+    g = golden("refine")
+    n, lam, k = g[f"{tag}_params"]
+    n, k = int(n), int(k)
+    f = M.SphereManifold(np.zeros(n), 0.8)
+    cfg = T.TraceConfig(L.LatticeConfig(n, lam * k))
+    res = T.trace(f.seed_point()[None, :], f, cfg)
+    cells = S.coarse_cells(res)
+    base, perm = cells.arrays()
+    assert np.array_equal(base, g[f"{tag}_cells_base"]) and np.array_equal(perm, g[f"{tag}_cells_perm"])
+    template = S.build_template(n, k)
+    out = S.refine(cells, template, f, lambda p: p[:, 0] > 0.1, cfg)
+    want = g[f"{tag}_points"]
+    assert out.points.shape == want.shape
+    if k == 2:
+        assert np.array_equal(out.points, want)       # same dyadic bisection on bit-identical endpoints
+    else:
+        assert np.allclose(out.points, want, rtol=POINT_RTOL, atol=1e-12)
+    assert np.array_equal(out.in_collision, g[f"{tag}_labels"])
+    assert sum(b.crossing_edges for b in out.batch_stats) == int(g[f"{tag}_crossings"][0])
+    assert np.array_equal(out.free_points, out.points[~out.in_collision])
+    # same result from an explicit list of PermSimplex cells (host upload path) and under a tight budget
+    again = S.refine(list(cells), template, f, lambda p: p[:, 0] > 0.1, cfg, memory_budget=7 * S._cell_bytes(template))
+    assert np.array_equal(again.points, out.points) and np.array_equal(again.in_collision, out.in_collision)
+    assert len(again.batch_stats) == -(-len(cells) // 7)
+    assert sum(b.new_points for b in again.batch_stats) == out.points.shape[0]
+
+
+def test_refine_learned_device_checker(golden):
+    g = golden("traces")
+    tag, n = "kclf_n3", 3
+    inp = trace_inputs(g, tag)
+    m, cfg = product_manifold(g, tag), product_cfg(inp)
+    res = T.trace(inp["seeds"], m, cfg)
+    cells = S.coarse_cells(res)
+    rd, sd = robot_scene_dicts(n, 3)
+
+    class Prob:
+        robot, scene = CO.robot_from_dict(rd), CO.scene_from_dict(sd)
+
+    template = S.build_template(n, 2)
+    budget = int(g[f"{tag}_refine_budget"][0])
+    out = S.refine(cells, template, m, P.not_free_checker(Prob), cfg, memory_budget=budget)
+    want = g[f"{tag}_refine_points"]
+    assert out.points.shape == want.shape
+    assert np.allclose(out.points, want, rtol=POINT_RTOL, atol=POINT_ATOL)
+    assert np.array_equal(out.in_collision, g[f"{tag}_refine_labels"])
+    assert out.eps_dedup == float(g[f"{tag}_refine_eps_dedup"][0])
+    rows = np.array([[b.cells, b.fine_vertices, b.crossing_edges, b.new_points] for b in out.batch_stats])
+    assert np.array_equal(rows, g[f"{tag}_refine_batches"])
+    # host-callable checker path gives the same labels
+    host = S.refine(cells, template, m, lambda p: P.not_free_checker(Prob)(p), cfg)
+    assert np.array_equal(host.points, out.points) and np.array_equal(host.in_collision, out.in_collision)
+    # a failing checker is wrapped (pkg/tests/test_subdivision.py:262-270)
+    def broken(p):
+        raise RuntimeError("boom")
+    with pytest.raises(S.RefineError, match="batch 0"):
+        S.refine(cells, template, m, broken, cfg)
+    with pytest.raises(S.RefineError, match="shape"):
+        S.refine(cells, template, m, lambda p: np.zeros(3, dtype=bool), cfg)
+    with pytest.raises(S.BudgetError):
+        S.refine(cells, template, m, broken, cfg, memory_budget=10)
+    empty = S.refine([], template, m, broken, cfg)
+    assert empty.points.shape == (0, n) and empty.batch_stats == []
+
+
+def test_refine_vs_oracle_4d_subset(golden):
+    """4-D learned manifold, first 300 sorted cells: full oracle refine (eps-dedup included)."""
+    g = golden("traces")
+    tag, n = "kclf_n4", 4
+    inp = trace_inputs(g, tag)
+    m, cfg, of = product_manifold(g, tag), product_cfg(inp), oracle_field(g, tag)
+    cells = [L.PermSimplex(tuple(int(v) for v in b), tuple((int(p),) for p in perm) + ((n,),))
+             for b, perm in zip(g[f"{tag}_cells_base"][:300], g[f"{tag}_cells_perm"][:300])]
+    rd, sd = robot_scene_dicts(n, 3)
+    robot, scene = oracle_model(rd, sd)
+
+    class Prob:
+        robot_, scene_ = None, None
+    Prob.robot, Prob.scene = CO.robot_from_dict(rd), CO.scene_from_dict(sd)
+    out = S.refine(cells, S.build_template(n, 2), m, P.not_free_checker(Prob), cfg)
+    ocells = [(c.base, c.parts) for c in cells]
+    want = O.refine(ocells, O.build_template(n, 2), of, lambda p: O.not_free(robot, scene, p), inp["scale"],
+                    inp["offset"], 2, inp["eps"])
+    assert out.points.shape == want["points"].shape
+    assert np.allclose(out.points, want["points"], rtol=POINT_RTOL, atol=POINT_ATOL)
+    assert np.array_equal(out.in_collision, want["in_collision"])
+    assert sum(b.crossing_edges for b in out.batch_stats) == sum(want["crossing_edges"])
+
+
+# ---- collision ---------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("n,nobs", [(3, 3), (4, 3), (5, 8), (6, 8)])
+def test_collision(golden, n, nobs):
+    g = golden("collision")
+    rd, sd = robot_scene_dicts(n, nobs)
+    robot, scene = CO.robot_from_dict(rd), CO.scene_from_dict(sd)
+    q = g[f"coll_n{n}_q"]
+    got = CO.batch_check(q, robot, scene, on_limit="unfree")
+    assert got.dtype == bool and np.array_equal(got, g[f"coll_n{n}_unfree"])
+    inside = np.all(np.abs(q) <= 1.5, axis=1)
+    assert np.array_equal(CO.batch_check(q[inside], robot, scene), g[f"coll_n{n}_hits_inside"])
+    assert np.allclose(CO.fk_batch(robot, q[:40]), g[f"coll_n{n}_fk"], rtol=0, atol=1e-13)
+    bad = int(np.nonzero(~inside)[0][0])
+    with pytest.raises(CO.LimitError, match=f"configuration {bad} "):
+        CO.batch_check(q, robot, scene)
+    row = q[inside][0]
+    assert CO.config_in_collision(row, robot, scene) == bool(g[f"coll_n{n}_hits_inside"][0])
+    assert CO.batch_check(np.zeros((0, n)), robot, scene).shape == (0,)
+    # permutation equivariance and batch-size irrelevance (pkg/tests/test_collision.py)
+    perm = np.random.default_rng(0).permutation(int(inside.sum()))
+    assert np.array_equal(CO.batch_check(q[inside][perm], robot, scene, batch_size=17), g[f"coll_n{n}_hits_inside"][perm])
+
+
+def test_collision_prismatic_posed_and_first_contact(golden):
+    g = golden("collision")
+    robot, scene = CO.robot_from_dict(PRISM_ROBOT), CO.scene_from_dict(PRISM_SCENE)
+    q = g["coll_prism_q"]
+    hits = CO.batch_check(q, robot, scene)
+    assert np.array_equal(hits, g["coll_prism_hits"])
+    assert np.allclose(CO.fk_batch(robot, q[:40]), g["coll_prism_fk"], rtol=0, atol=1e-13)
+    i_hit, i_free = int(np.nonzero(hits)[0][0]), int(np.nonzero(~hits)[0][0])
+    rep = CO.first_contact(q[i_hit], robot, scene)
+    assert rep.hit and rep.sphere_index is not None and rep.obstacle_index is not None
+    assert not CO.first_contact(q[i_free], robot, scene).hit
+    with pytest.raises(CO.LimitError):
+        CO.forward_kinematics(robot, [5.0, 0.0])
+    with pytest.raises(ValueError):
+        CO.forward_kinematics(robot, [np.nan, 0.0])
+    box = scene.obstacles[2]
+    centre = box.pose.translation + box.pose.rotation @ np.array([0.15 + 0.05, 0.0, 0.0])
+    assert CO.sphere_box_collides(centre, 0.05 + 1e-9, box) and not CO.sphere_box_collides(centre, 0.05 - 1e-9, box)
+
+
+def test_collision_vs_distance_oracle():
+    """10^5 random sphere-vs-box / cylinder cases against closed-form distances, skipping |gap| <= 1e-12
+    (pkg/tests/test_acceptance.py:227-260)."""
+    rng = np.random.default_rng(42)
+    c = rng.uniform(-2, 2, size=(100000, 3)); r = rng.uniform(0.01, 0.8, size=100000)
+    h = np.array([0.6, 0.35, 0.9])
+    d = np.maximum(np.abs(c) - h, 0.0)
+    gap = np.linalg.norm(d, axis=1) - r
+    got = B.sphere_box_hits(c, r, *(2 * h)).astype(bool)
+    keep = np.abs(gap) > 1e-12
+    assert np.array_equal(got[keep], (gap <= 0)[keep])
+    dz = np.maximum(np.abs(c[:, 2]) - 0.5, 0.0); dr = np.maximum(np.hypot(c[:, 0], c[:, 1]) - 0.4, 0.0)
+    gap = np.hypot(dz, dr) - r
+    got = B.sphere_cylinder_hits(c, r, 1.0, 0.4).astype(bool)
+    keep = np.abs(gap) > 1e-12
+    assert np.array_equal(got[keep], (gap <= 0)[keep])
+
+
+# ---- full-size properties (BASELINE config shapes; no CPU oracle can follow at this size) --------------------
+def test_dof6_full_size_properties():
+    from bench import build_workload
+    wl = build_workload("dof6")
+    res = T.trace(wl.seeds, wl.manifold, wl.cfg)
+    st = res.stats
+    assert st.closure_ok and st.dropped_out_of_box == 0 and st.complete
+    # the reference finds 47 594 edges / 8 677 vertex evaluations on this recipe
+    assert st.visited_edges == 47594 and st.field_evaluations == 8677
+    base, mask, sa = res.edges.arrays()
+    # every traced edge is sign-changing under an independent evaluation of its endpoints
+    steps = ((mask[:, None] >> np.arange(6)) & 1).astype(np.float64)
+    a = base * wl.cfg.lattice.scale + np.asarray(wl.cfg.lattice.offset)
+    b = (base + steps) * wl.cfg.lattice.scale + np.asarray(wl.cfg.lattice.offset)
+    s_a, s_b = wl.manifold.signs(a), wl.manifold.signs(b)
+    assert np.array_equal(s_a, sa) and np.all(s_a != s_b)
+    # no duplicates, and each point sits inside an eps bracket on its own edge
+    assert len({(tuple(r), int(m)) for r, m in zip(base.tolist(), mask.tolist())}) == len(mask)
+    t = np.einsum("ij,ij->i", res.points - a, b - a) / np.einsum("ij,ij->i", b - a, b - a)
+    assert np.all((t > 0) & (t < 1))
+    assert np.allclose(res.points, a + t[:, None] * (b - a), atol=1e-12)
+    # adjacency: every crossing 2-face has exactly two crossing edges -> each edge has as many partners as cofaces
+    adj = np.asarray(res.adjacency)
+    deg = np.bincount(adj.ravel(), minlength=len(mask))
+    pc = np.array([bin(int(m)).count("1") for m in mask])
+    assert np.array_equal(deg, (2 ** pc - 2) + (2 ** (7 - pc) - 2))
+    cells = S.coarse_cells(res)
+    cb, cp = cells.arrays()
+    keys = np.concatenate([cb.astype(np.int64), cp.astype(np.int64)], axis=1)
+    order = np.lexsort(keys.T[::-1])
+    assert np.array_equal(order, np.arange(len(order)))       # sorted, hence unique
+    assert len(cells) > 10 * st.visited_edges
