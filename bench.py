@@ -270,6 +270,10 @@ def run_gpu(args):
         ref = P.refine(cells, wl.template, manifold, checker, wl.cfg)    # points + labels come back to the host
         return res, ref
 
+    if args.kernel_only:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": value, "unit": UNIT, "ms_per_step": ms / args.steps, "kernel_only": True}))
+        return None
     e2e_step()
     barrier()
     t0 = time.perf_counter()
@@ -295,10 +299,11 @@ def run_gpu(args):
     ctx.profile(False)
     total_ms = sum(v[1] for v in prof.values()) or 1.0
     top = max(prof.items(), key=lambda kv: kv[1][1])
-    pair_evals = counts["pair_evals_bisect"] if top[0].startswith("bisect") else counts["pair_evals_eval"]
+    pair_evals = {"bisect_rbf": counts["pair_evals_bisect"], "bisect_fp64_finish": counts["pair_evals_bisect"],
+                  "eval_rbf": counts["pair_evals_eval"]}.get(top[0], 0)
     peak = engine.measure_fp64_peak(ctx)
     roofline = None
-    if top[0] in ("bisect_rbf", "eval_rbf"):
+    if top[0] in ("bisect_rbf", "bisect_fp64_finish", "eval_rbf"):
         achieved = pair_evals * pair_flops(a.n) / (top[1][1] * 1e-3) / 1e12
         roofline = {"bound": "fp64", "kernel": top[0], "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": achieved / peak if peak else None, "traffic": None,
@@ -333,7 +338,8 @@ def run_gpu(args):
                        "trace_edges": counts["trace_edges"], "coarse_cells": counts["cells"],
                        "crossing_fine_edges": counts["crossing_edges"], "unique_fine_edges": counts["unique_fine_edges"],
                        "points_checked": counts["points"], "free_points": counts["free_points"],
-                       "closure_ok": counts["closure_ok"]},
+                       "closure_ok": counts["closure_ok"], "fp32_screened_pair_evals": counts["pair_evals_fp32"],
+                       "fp64_root_solve_pair_evals": counts["pair_evals_bisect"], "bisect_fallbacks": counts["bisect_fallbacks"]},
             "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": int(launches),
             "roofline": roofline, "roofline_hbm": hbm, "kernels": kernels, "cpu_baseline": cpu,
             "proof_time_s": ms / args.steps * 1e-3,
@@ -347,7 +353,7 @@ def run_gpu(args):
 # CPU arm: the reference's algorithm (oracle port), bounded sample of the same workload
 # ------------------------------------------------------------------------------------------------
 
-def cpu_sample(workload: str, threads: int, max_edges: int = 1500, max_cells: int = 150):
+def cpu_sample(workload: str, threads: int, max_edges: int = 4000, max_cells: int = 600):
     """One bounded sample: the same scene/manifold/lattice, BFS capped at `max_edges` coarse edges,
     refinement of the first `max_cells` sorted coarse cells.  Returns (simplices, seconds)."""
     from oracle import permatrace_oracle as O
@@ -411,6 +417,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="dof6")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kernel-only", action="store_true", help="skip the e2e and CPU legs (for ncu captures)")
     args = ap.parse_args()
     line = run_reference(args) if args.impl == "reference" else run_gpu(args)
     if line is not None:

@@ -45,8 +45,9 @@ int pt_ctx_profile_reset(pt_ctx* ctx);
 /* writes "name,launches,total_ms\n" lines; returns bytes needed (call with cap=0 to size) */
 long long pt_ctx_profile_dump(pt_ctx* ctx, char* buf, long long cap);
 long long pt_ctx_launch_count(pt_ctx* ctx);
-/* device-side work counters: out[0] = bisection field evaluations (rows x iterations), out[1] = points
- * evaluated by the batch evaluator; reset != 0 zeroes them */
+/* device-side work counters, out[4]: [0] fp64 field evaluations spent in root solves, [1] points
+ * evaluated by the batch evaluator, [2] fp32-screened bisection evaluations, [3] root solves that fell
+ * back to plain fp64 bisection; reset != 0 zeroes them */
 int pt_ctx_work_counters(pt_ctx* ctx, long long* out, int reset);
 /* DFMA-chain microbenchmark: measured FP64 peak of this device in TFLOP/s (roofline denominator) */
 double pt_peak_fp64(pt_ctx* ctx);

@@ -11,7 +11,9 @@ struct PtFieldDev {
     long long S;           // support vectors
     int row;               // doubles per packed support row (odd, >= n+1): coords, weight, pad
     const double* sv;      // [S][row]
-    const float* sv32;     // [S][row32] fp32 screening copy (row32 = n+2: coords*c, |s|^2 term, w)
+    const float* sv32;     // [S][row32] fp32 screening copy: coords, -gamma*log2(e)*|s|^2, weight, pad
+    int row32;             // floats per fp32 row (multiple of 4)
+    double smax;           // max_j |s_j| (enters the fp32 error bound)
     double gamma, bias;
     int has_barrier;
     double b_scale, b_gain;
@@ -19,10 +21,14 @@ struct PtFieldDev {
     double p0[PT_NMAX];    // sphere/ellipsoid centre, plane normal
     double p1[PT_NMAX];    // ellipsoid semi-axes
     double c0;             // sphere radius^2, plane offset
-    double err32;          // rigorous bound on |F32 - F64| excluding the barrier (screening mode)
 };
 
 static inline int pt_sv_row(int n) { int r = n + 1; return (r & 1) ? r : r + 1; }
+static inline int pt_sv_row32(int n) { return (n + 2 + 3) & ~3; }
+
+#define PT_L2E 1.4426950408889634
+#define PT_LN2 0.6931471805599453
+#define PT_U32 5.9604644775390625e-08   /* 2^-24, unit roundoff of binary32 */
 
 #ifdef __CUDACC__
 // numpy.logaddexp(0, v) branch structure (npy_logaddexp): max + log1p(exp(-|diff|))
@@ -40,6 +46,36 @@ __device__ __forceinline__ double pt_barrier_value(const PtFieldDev& f, const do
     for (int d = 0; d < N; ++d) {
         double lo = pt_softplus(__ddiv_rn(__dsub_rn(f.b_lo[d], p[d]), f.b_scale));
         double hi = pt_softplus(__ddiv_rn(__dsub_rn(p[d], f.b_hi[d]), f.b_scale));
+        acc = __dadd_rn(acc, __dadd_rn(lo, hi));
+    }
+    return __dmul_rn(__dmul_rn(f.b_gain, f.b_scale), acc);
+}
+
+// Same value as pt_barrier_value, with the 2N softplus terms spread over the G lanes that share a
+// point (lane g of the group computes terms g, g+G, ...); the sum is formed in the reference order on
+// every lane.  All G lanes of the group must call it.
+template <int N, int G>
+__device__ __forceinline__ double pt_barrier_group(const PtFieldDev& f, const double* p, int g) {
+    if (G == 1) return pt_barrier_value<N>(f, p);
+    double mine[(2 * N + G - 1) / G];
+#pragma unroll
+    for (int k = 0; k < (2 * N + G - 1) / G; ++k) {
+        const int i = g + k * G;
+        double v = 0.0;
+        if (i < 2 * N) {
+            const int d = i >> 1;
+            v = (i & 1) ? pt_softplus(__ddiv_rn(__dsub_rn(p[d], f.b_hi[d]), f.b_scale))
+                        : pt_softplus(__ddiv_rn(__dsub_rn(f.b_lo[d], p[d]), f.b_scale));
+        }
+        mine[k] = v;
+    }
+    const int lane0 = (threadIdx.x & 31) & ~(G - 1);
+    double acc = 0.0;
+#pragma unroll
+    for (int d = 0; d < N; ++d) {
+        const int il = 2 * d, ih = 2 * d + 1;
+        const double lo = __shfl_sync(0xffffffffu, mine[il / G], lane0 + (il % G));
+        const double hi = __shfl_sync(0xffffffffu, mine[ih / G], lane0 + (ih % G));
         acc = __dadd_rn(acc, __dadd_rn(lo, hi));
     }
     return __dmul_rn(__dmul_rn(f.b_gain, f.b_scale), acc);

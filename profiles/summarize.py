@@ -1,0 +1,63 @@
+"""Turn ncu CSV exports into the small text summaries committed under profiles/.
+
+    python profiles/summarize.py launches gpurun_out/launches_v0.csv > profiles/r1_v0_launches.txt
+    python profiles/summarize.py raw gpurun_out/prof_bisect_v0.ncu-rep > profiles/r1_v0_bisect_full.txt
+"""
+import csv
+import subprocess
+import sys
+from collections import defaultdict
+
+KEEP = [
+    "gpu__time_duration.sum", "launch__grid_size", "launch__block_size", "launch__registers_per_thread",
+    "launch__shared_mem_per_block_dynamic", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__warps_active.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active", "l1tex__t_sector_hit_rate.pct", "lts__t_sector_hit_rate.pct",
+    "smsp__warp_issue_stalled_barrier_per_warp_active.pct", "smsp__warp_issue_stalled_math_pipe_throttle_per_warp_active.pct",
+    "smsp__warp_issue_stalled_long_scoreboard_per_warp_active.pct", "smsp__warp_issue_stalled_short_scoreboard_per_warp_active.pct",
+    "smsp__warp_issue_stalled_wait_per_warp_active.pct",
+]
+
+
+def launches(path):
+    rows = [r for r in csv.reader(open(path, errors="replace")) if r and not r[0].startswith("==")]
+    hdr = rows[0]
+    kn, mv, mn = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Name")
+    unit = hdr.index("Metric Unit")
+    agg = defaultdict(lambda: [0, 0.0])
+    for r in rows[1:]:
+        if len(r) <= mv or r[mn] != "gpu__time_duration.sum":
+            continue
+        v = float(r[mv].replace(",", ""))
+        if r[unit] in ("ns", "nsecond"):
+            v /= 1e6
+        elif r[unit] in ("us", "usecond"):
+            v /= 1e3
+        name = r[kn].split("(")[0]
+        agg[name][0] += 1
+        agg[name][1] += v
+    total = sum(v[1] for v in agg.values())
+    print(f"# {path}: {sum(v[0] for v in agg.values())} launches, {total:.3f} ms under ncu (cold-cache, serialised: compare shares)")
+    print(f"{'kernel':90s} {'launches':>8s} {'ms':>10s} {'share':>7s}")
+    for name, (n, ms) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        print(f"{name[:90]:90s} {n:8d} {ms:10.3f} {100 * ms / total:6.2f}%")
+
+
+def raw(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    hdr, units = rows[0], rows[1]
+    idx = {h: i for i, h in enumerate(hdr)}
+    for r in rows[2:]:
+        print("kernel:", r[idx["Kernel Name"]].split("(")[0])
+        for k in KEEP:
+            if k in idx:
+                print(f"  {k:75s} {r[idx[k]]:>14s} {units[idx[k]]}")
+        print()
+
+
+if __name__ == "__main__":
+    {"launches": launches, "raw": raw}[sys.argv[1]](sys.argv[2])
