@@ -7,7 +7,7 @@ obj="$here/build"
 mkdir -p "$obj"
 NVCC="${NVCC:-nvcc}"
 FLAGS=(-gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -std=c++17 -Xcompiler -fPIC -Xcompiler -O3
-       -Xcudafe --diag_suppress=177 --expt-relaxed-constexpr)
+       -Xcudafe --diag_suppress=177 -Xcudafe --diag_suppress=128 --expt-relaxed-constexpr)
 pids=()
 for src in pt_ctx pt_host pt_field pt_collision pt_trace pt_cells pt_refine; do
   if [[ ! -f "$obj/$src.o" || "$here/$src.cu" -nt "$obj/$src.o" || -n "$(find "$here" -maxdepth 1 \( -name '*.cuh' -o -name '*.h' \) -newer "$obj/$src.o" 2>/dev/null)" || "$here/../../include/permatrace_b200.h" -nt "$obj/$src.o" ]]; then

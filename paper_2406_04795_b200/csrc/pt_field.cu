@@ -23,20 +23,67 @@ int pt_field_dim(const pt_field* f) { return f->d.n; }
 #define PT_EVAL_THREADS 256
 #define PT_EVAL_TILE 256
 
+#define PT_ROW64(N) (((N) + 2) | 1)
+#define PT_SMEM64(N) ((size_t)(PT_EVAL_TILE * PT_ROW64(N) + 32) * sizeof(double))
+
+// 2^x for x <= ~0 in fp64: x = (32k + i)/32 + r, |r| <= 1/64; 2^r by a degree-6 Taylor polynomial
+// (truncation 3e-18), 2^(i/32) from a 32-entry shared-memory table, 2^k by an exponent-field add.
+// Arguments below -1000 are clamped (the term is < 1e-300 of its weight).  Branch-free on purpose so
+// independent rows interleave; non-finite points are handled once per point (PtPoint64::poison).
+__device__ __forceinline__ double pt_exp2_neg(double x, const double* __restrict__ tab) {
+    x = fmax(x, -1000.0);
+    const double MAGIC = 6755399441055744.0;   // 1.5 * 2^52: the low word of x*32 + MAGIC is round(32 x)
+    const double t = fma(x, 32.0, MAGIC);
+    const int mi = __double2loint(t);
+    const double r = fma(t - MAGIC, -0.03125, x);
+    double p = 0.00015403530393381606;
+    p = fma(p, r, 0.0013333558146428441);
+    p = fma(p, r, 0.009618129107628477);
+    p = fma(p, r, 0.055504108664821576);
+    p = fma(p, r, 0.2402265069591007);
+    p = fma(p, r, 0.6931471805599453);
+    p = fma(p, r, 1.0);
+    const double v = tab[mi & 31] * p;
+    return __hiloint2double(__double2hiint(v) + ((mi >> 5) << 20), __double2loint(v));
+}
+
+// per-point constants of the expanded exponent: -gamma*log2(e)*|p - s|^2 = c_s + c_p + sum_d q_d s_d
 template <int N>
-__device__ __forceinline__ double pt_rbf_term(const double* __restrict__ row, const double* p, double neg_gamma) {
-    double d2 = 0.0;
+struct PtPoint64 {
+    double q[N];
+    double cp;
+    double poison;   // 0 for a finite point, NaN otherwise (added to every sum so F is NaN like the reference's)
+    __device__ __forceinline__ void set(const double* p, double gl) {
+        double p2 = 0.0;
 #pragma unroll
-    for (int d = 0; d < N; ++d) { double df = p[d] - row[d]; d2 = fma(df, df, d2); }
-    return row[N] * exp(neg_gamma * d2);
+        for (int d = 0; d < N; ++d) { q[d] = 2.0 * gl * p[d]; p2 = fma(p[d], p[d], p2); }
+        cp = -gl * p2;
+        poison = p2 - p2;
+    }
+};
+
+template <int N>
+__device__ __forceinline__ double pt_rbf_term(const double* __restrict__ row, const PtPoint64<N>& pp,
+                                              const double* __restrict__ tab) {
+    double arg = row[N + 1] + pp.cp;
+#pragma unroll
+    for (int d = 0; d < N; ++d) arg = fma(pp.q[d], row[d], arg);
+    return row[N] * pt_exp2_neg(arg, tab);
+}
+
+__device__ __forceinline__ void pt_exp_table_init(double* tab) {
+    if (threadIdx.x < 32) tab[threadIdx.x] = exp2((double)threadIdx.x * 0.03125);
 }
 
 // accumulate this lane's share of sum_j w_j k(p, s_j); all threads of the block must call it
+// (tile holds PT_EVAL_TILE rows followed by the 32-entry 2^(i/32) table, see pt_exp_table_init)
 template <int N, int G>
 __device__ __forceinline__ double pt_rbf_block_sum(const PtFieldDev& f, const double* p, int g, double* tile) {
-    const int ROW = (N + 1) | 1;
+    const int ROW = PT_ROW64(N);
+    const double* tab = tile + PT_EVAL_TILE * ROW;
+    PtPoint64<N> pp;
+    pp.set(p, f.gamma * PT_L2E);
     double acc = 0.0;
-    const double ng = -f.gamma;
     for (long long t0 = 0; t0 < f.S; t0 += PT_EVAL_TILE) {
         long long rem = f.S - t0;
         int cnt = rem < PT_EVAL_TILE ? (int)rem : PT_EVAL_TILE;
@@ -44,8 +91,19 @@ __device__ __forceinline__ double pt_rbf_block_sum(const PtFieldDev& f, const do
         const double* src = f.sv + t0 * ROW;
         for (int i = threadIdx.x; i < cnt * ROW; i += PT_EVAL_THREADS) tile[i] = src[i];
         __syncthreads();
-        for (int j = g; j < cnt; j += G) acc += pt_rbf_term<N>(tile + j * ROW, p, ng);
+        // four independent accumulators: the serial exponent/polynomial chains of neighbouring rows overlap
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int j = g;
+        for (; j + 3 * G < cnt; j += 4 * G) {
+            s0 += pt_rbf_term<N>(tile + j * ROW, pp, tab);
+            s1 += pt_rbf_term<N>(tile + (j + G) * ROW, pp, tab);
+            s2 += pt_rbf_term<N>(tile + (j + 2 * G) * ROW, pp, tab);
+            s3 += pt_rbf_term<N>(tile + (j + 3 * G) * ROW, pp, tab);
+        }
+        for (; j < cnt; j += G) s0 += pt_rbf_term<N>(tile + j * ROW, pp, tab);
+        acc += (s0 + s1) + (s2 + s3);
     }
+    acc += pp.poison;
 #pragma unroll
     for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
     return acc;
@@ -56,6 +114,7 @@ __global__ void __launch_bounds__(PT_EVAL_THREADS)
 pt_eval_rbf_kernel(PtFieldDev f, const double* __restrict__ pts, size_t m, double* __restrict__ vals,
                    int8_t* __restrict__ signs, unsigned long long* work) {
     extern __shared__ double tile[];
+    pt_exp_table_init(tile + PT_EVAL_TILE * PT_ROW64(N));
     const int PB = PT_EVAL_THREADS / G;
     const size_t pi = (size_t)blockIdx.x * PB + threadIdx.x / G;
     const int g = threadIdx.x % G;
@@ -102,6 +161,7 @@ pt_bisect_rbf_kernel(PtFieldDev f, const double* __restrict__ a_, const double* 
                      const int8_t* __restrict__ signs_a, size_t m, double eps, double* __restrict__ out,
                      unsigned long long* work) {
     extern __shared__ double tile[];
+    pt_exp_table_init(tile + PT_EVAL_TILE * PT_ROW64(N));
     const int PB = PT_EVAL_THREADS / G;
     const size_t ei = (size_t)blockIdx.x * PB + threadIdx.x / G;
     const int g = threadIdx.x % G;
@@ -177,16 +237,25 @@ __global__ void pt_bisect_analytic_kernel(PtFieldDev f, const double* __restrict
 }
 
 
-// ==== fast root solve: fp32-screened bisection + fp64 secant endgame ================================
-// Phase 1 (pt_bisect32_kernel) replays the reference's bisection with the field evaluated in fp32; a
-// step is taken only when |F32| exceeds a rigorous bound on |F32 - F| (so the decision equals the
-// fp64 one), otherwise the row stops with its current dyadic bracket.
-// Phase 2 (pt_bisect_finish_kernel) finds the root inside that bracket by two fp64 secant steps,
-// maps it to the depth-I dyadic cell the reference's bisection would end in, and VERIFIES the cell
-// by evaluating the field at its two ends with exactly the midpoints' arithmetic (sign(a side) ==
-// signs_a, other side differs).  A failed verification falls back to plain fp64 bisection from the
-// phase-1 bracket, so the returned point is always the reference's a + (lo+hi)/2 * (b-a).
+// ==== fast root solve ===================================================================================
+// The reference bisects every crossing edge ~30 times in fp64.  The fast path returns the SAME dyadic
+// bracket midpoint with ~6 fp64 evaluations per edge:
+//   K1 pt_bisect32_kernel     replays the bisection with the field evaluated in fp32; a step is taken only
+//                             when |F32| exceeds a rigorous bound on |F32 - F| (the decision then equals the
+//                             fp64 one); otherwise the row stops with its current dyadic bracket.
+//   K2 pt_bisect_resolve      rows that stopped while the bracket is still wide take ONE true fp64 bisection
+//                             step and go back to K1 (compacted row lists, so nobody waits for them).
+//   K3 pt_bisect_newton       for a bracket [lo,hi] of width w: evaluates F, F', F'' at the next midpoint
+//                             (a true bisection step), then proves F monotone on the bracket from
+//                             |F'(m)| > w|F''(m)| + w^2 M3/2 (M3 = global bound on the third derivative along
+//                             the edge).  A monotone bracket holds exactly one root, so the reference's final
+//                             depth-I cell is the one containing it: Newton + secant steps locate the root, and
+//                             the cell is VERIFIED by evaluating F at its two ends with the midpoints' own
+//                             arithmetic (a side has signs_a, the other does not).
+//   K4 pt_bisect_rbf_kernel   rows whose proof or verification failed finish by plain fp64 bisection from
+//                             their (always true) bisection bracket.
 #define PT_TILE32 512
+#define PT_HANDOFF_WIDTH 0.0078125   /* 2^-7: brackets wider than this never enter K3 */
 
 template <int N> struct PtRow32 { static const int value = (N + 2 + 3) & ~3; };
 
@@ -195,6 +264,10 @@ __device__ __forceinline__ float pt_ex2(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+
+// optional row indirection: kernels walk either all m rows or a compacted list whose length lives on the device
+struct PtRows { const uint32_t* list; const unsigned long long* count; size_t m; };
+__device__ __forceinline__ size_t pt_rows_total(const PtRows& r) { return r.list ? (size_t)*r.count : r.m; }
 
 // lane share of sum_j w_j 2^(c_s + c_p + q.s_j) and of the same sum with |w_j|; fp32 chunks of <= 64
 // terms are flushed into fp64 accumulators; all threads of the block must call it
@@ -235,18 +308,74 @@ __device__ __forceinline__ void pt_rbf32_block_sum(const PtFieldDev& f, const fl
     acc_out = acc; abs_out = ab;
 }
 
+// F, dF/dt, d2F/dt2 of the kernel sum along p(t) = a + t*diff at the point p
+template <int N, int G>
+__device__ __forceinline__ void pt_rbf_block_sum_d(const PtFieldDev& f, const double* p, const double* diff, double seg2,
+                                                   int g, double* tile, double& F, double& D1, double& D2) {
+    const int ROW = PT_ROW64(N);
+    const double* tab = tile + PT_EVAL_TILE * ROW;
+    PtPoint64<N> pp;
+    pp.set(p, f.gamma * PT_L2E);
+    double pd = 0.0;
+#pragma unroll
+    for (int d = 0; d < N; ++d) pd = fma(p[d], diff[d], pd);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    const double ng2 = -2.0 * f.gamma, c2 = 2.0 * f.gamma * seg2;
+    for (long long t0 = 0; t0 < f.S; t0 += PT_EVAL_TILE) {
+        long long rem = f.S - t0;
+        const int cnt = rem < PT_EVAL_TILE ? (int)rem : PT_EVAL_TILE;
+        __syncthreads();
+        const double* src = f.sv + t0 * ROW;
+        for (int i = threadIdx.x; i < cnt * ROW; i += PT_EVAL_THREADS) tile[i] = src[i];
+        __syncthreads();
+        for (int j = g; j < cnt; j += G) {
+            const double* row = tile + j * ROW;
+            double x = pd;                           // (p - s) . diff
+#pragma unroll
+            for (int d = 0; d < N; ++d) x = fma(-diff[d], row[d], x);
+            const double e = pt_rbf_term<N>(row, pp, tab);
+            const double gx = ng2 * x;
+            a0 += e; a1 = fma(e, gx, a1); a2 = fma(e, fma(gx, gx, -c2), a2);
+        }
+    }
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) {
+        a0 += __shfl_xor_sync(0xffffffffu, a0, off);
+        a1 += __shfl_xor_sync(0xffffffffu, a1, off);
+        a2 += __shfl_xor_sync(0xffffffffu, a2, off);
+    }
+    F = a0 + pp.poison; D1 = a1; D2 = a2;
+}
+
+// first and second t-derivatives of the box barrier along p(t) = a + t*diff
+template <int N>
+__device__ __forceinline__ void pt_barrier_derivs(const PtFieldDev& f, const double* p, const double* diff, double& B1, double& B2) {
+    double b1 = 0.0, b2 = 0.0;
+#pragma unroll
+    for (int d = 0; d < N; ++d) {
+        const double sl = 1.0 / (1.0 + exp(-(f.b_lo[d] - p[d]) / f.b_scale));
+        const double sh = 1.0 / (1.0 + exp(-(p[d] - f.b_hi[d]) / f.b_scale));
+        b1 = fma(diff[d], sh - sl, b1);
+        b2 = fma(diff[d] * diff[d], sh * (1.0 - sh) + sl * (1.0 - sl), b2);
+    }
+    B1 = f.b_gain * b1; B2 = f.b_gain / f.b_scale * b2;
+}
+
 template <int N, int G>
 __global__ void __launch_bounds__(PT_EVAL_THREADS)
-pt_bisect32_kernel(PtFieldDev f, const double* __restrict__ a_, const double* __restrict__ b_,
-                   const int8_t* __restrict__ signs_a, size_t m, double eps, double* __restrict__ lo_out,
-                   double* __restrict__ hi_out, unsigned long long* work) {
+pt_bisect32_kernel(PtFieldDev f, PtRows rows, const double* __restrict__ a_, const double* __restrict__ b_,
+                   const int8_t* __restrict__ signs_a, double eps, int fresh, double* __restrict__ lo_io,
+                   double* __restrict__ hi_io, unsigned long long* work) {
     extern __shared__ float tile32[];
     const int PB = PT_EVAL_THREADS / G;
-    const size_t ei = (size_t)blockIdx.x * PB + threadIdx.x / G;
+    const size_t total = pt_rows_total(rows);
+    if ((size_t)blockIdx.x * PB >= total) return;
+    const size_t idx = (size_t)blockIdx.x * PB + threadIdx.x / G;
     const int g = threadIdx.x % G;
-    const bool valid = ei < m;
+    const bool valid = idx < total;
+    const size_t ei = valid ? (rows.list ? (size_t)rows.list[idx] : idx) : 0;
     double a[N], diff[N], p[N];
-    double seg = 0.0;
+    double seg = 0.0, lo = 0.0, hi = 1.0;
     int sa = 1;
     if (valid) {
         double b[N];
@@ -254,13 +383,13 @@ pt_bisect32_kernel(PtFieldDev f, const double* __restrict__ a_, const double* __
         for (int d = 0; d < N; ++d) { a[d] = a_[ei * N + d]; b[d] = b_[ei * N + d]; }
         seg = pt_segment<N>(a, b, diff);
         sa = signs_a[ei];
+        if (!fresh) { lo = lo_io[ei]; hi = hi_io[ei]; }
     } else {
 #pragma unroll
         for (int d = 0; d < N; ++d) { a[d] = 0.0; diff[d] = 0.0; }
     }
     const double gl = f.gamma * PT_L2E;
-    double lo = 0.0, hi = 1.0;
-    bool active = valid && seg > eps;
+    bool active = valid && __dmul_rn(seg, __dsub_rn(hi, lo)) > eps;
     unsigned iters = 0;
     while (__syncthreads_or(active ? 1 : 0)) {
         const double mid = __dmul_rn(0.5, __dadd_rn(lo, hi));
@@ -273,7 +402,7 @@ pt_bisect32_kernel(PtFieldDev f, const double* __restrict__ a_, const double* __
             q[d] = (float)(2.0 * gl * p[d]);
         }
         const float cp = (float)(-gl * p2);
-        // |arg32 - arg| <= (N+4) u T with T = gamma*log2(e) (|p| + max|s|)^2 (input roundings + fma chain);
+        // |arg32 - arg| <= (N+3) u T with T = gamma*log2(e) (|p| + max|s|)^2 (input roundings + fma chain);
         // ex2.approx, weight rounding, products and the <=64-term fp32 chunks add < 80 u relative
         const double pn = sqrt(p2) + f.smax;
         const double rel = 1.01 * ((double)(N + 4) * PT_U32 * gl * pn * pn * PT_LN2) + 80.0 * PT_U32;
@@ -288,7 +417,7 @@ pt_bisect32_kernel(PtFieldDev f, const double* __restrict__ a_, const double* __
                 ++iters;
                 active = __dmul_rn(seg, __dsub_rn(hi, lo)) > eps;
             } else {
-                active = false;   // sign not certain in fp32 (or NaN): hand the bracket to phase 2
+                active = false;   // sign not certain in fp32 (or NaN): stop with the current bracket
             }
         }
     }
@@ -297,16 +426,99 @@ pt_bisect32_kernel(PtFieldDev f, const double* __restrict__ a_, const double* __
         for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
         if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&work[2], (unsigned long long)mine);
     }
-    if (valid && g == 0) { lo_out[ei] = lo; hi_out[ei] = hi; }
+    if (valid && g == 0) { lo_io[ei] = lo; hi_io[ei] = hi; }
 }
 
+// rows still active whose bracket is wider than the hand-off width -> compacted list
+template <int N>
+__global__ void pt_select_shallow_kernel(PtRows rows, const double* __restrict__ a_, const double* __restrict__ b_,
+                                         const double* __restrict__ lo_, const double* __restrict__ hi_, double eps,
+                                         uint32_t* __restrict__ list_out, unsigned long long* count_out) {
+    const size_t total = pt_rows_total(rows);
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool take = false; size_t ei = 0;
+    if (idx < total) {
+        ei = rows.list ? (size_t)rows.list[idx] : idx;
+        double a[N], b[N], diff[N];
+#pragma unroll
+        for (int d = 0; d < N; ++d) { a[d] = a_[ei * N + d]; b[d] = b_[ei * N + d]; }
+        const double seg = pt_segment<N>(a, b, diff);
+        const double w = hi_[ei] - lo_[ei];
+        take = (w > PT_HANDOFF_WIDTH) && (__dmul_rn(seg, w) > eps);
+    }
+    const unsigned ballot = __ballot_sync(0xffffffffu, take);
+    if (ballot) {
+        const int lane = threadIdx.x & 31, leader = __ffs(ballot) - 1;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(count_out, (unsigned long long)__popc(ballot));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (take) list_out[base + __popc(ballot & ((1u << lane) - 1u))] = (uint32_t)ei;
+    }
+}
+
+__global__ void pt_select_flag_kernel(const uint8_t* __restrict__ flag, size_t m, uint32_t* __restrict__ list_out,
+                                      unsigned long long* count_out) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool take = i < m && flag[i] != 0;
+    const unsigned ballot = __ballot_sync(0xffffffffu, take);
+    if (ballot) {
+        const int lane = threadIdx.x & 31, leader = __ffs(ballot) - 1;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(count_out, (unsigned long long)__popc(ballot));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (take) list_out[base + __popc(ballot & ((1u << lane) - 1u))] = (uint32_t)i;
+    }
+}
+
+// K2: one true fp64 bisection step for the listed rows
 template <int N, int G>
 __global__ void __launch_bounds__(PT_EVAL_THREADS)
-pt_bisect_finish_kernel(PtFieldDev f, const double* __restrict__ a_, const double* __restrict__ b_,
-                        const int8_t* __restrict__ signs_a, const double* __restrict__ lo_in,
-                        const double* __restrict__ hi_in, size_t m, double eps, double* __restrict__ out,
+pt_bisect_resolve_kernel(PtFieldDev f, PtRows rows, const double* __restrict__ a_, const double* __restrict__ b_,
+                         const int8_t* __restrict__ signs_a, double* __restrict__ lo_io, double* __restrict__ hi_io,
+                         unsigned long long* work) {
+    extern __shared__ double tile[];
+    pt_exp_table_init(tile + PT_EVAL_TILE * PT_ROW64(N));
+    const int PB = PT_EVAL_THREADS / G;
+    const size_t total = pt_rows_total(rows);
+    if ((size_t)blockIdx.x * PB >= total) return;
+    const size_t idx = (size_t)blockIdx.x * PB + threadIdx.x / G;
+    const int g = threadIdx.x % G;
+    const bool valid = idx < total;
+    const size_t ei = valid ? (rows.list ? (size_t)rows.list[idx] : idx) : 0;
+    double p[N];
+    double lo = 0.0, hi = 1.0;
+    int sa = 1;
+#pragma unroll
+    for (int d = 0; d < N; ++d) p[d] = 0.0;
+    if (valid) {
+        lo = lo_io[ei]; hi = hi_io[ei]; sa = signs_a[ei];
+        const double mid = __dmul_rn(0.5, __dadd_rn(lo, hi));
+#pragma unroll
+        for (int d = 0; d < N; ++d) {
+            const double av = a_[ei * N + d];
+            p[d] = __dadd_rn(av, __dmul_rn(mid, __dsub_rn(b_[ei * N + d], av)));
+        }
+    }
+    double F = f.bias + pt_rbf_block_sum<N, G>(f, p, g, tile);
+    if (f.has_barrier) F -= pt_barrier_group<N, G>(f, p, g);
+    if (valid && g == 0) {
+        const double mid = __dmul_rn(0.5, __dadd_rn(lo, hi));
+        if ((F > 0.0 ? 1 : -1) == sa) lo_io[ei] = mid; else hi_io[ei] = mid;
+    }
+    unsigned mine = (valid && g == 0) ? 1u : 0u;
+    for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&work[0], (unsigned long long)mine);
+}
+
+// K3: monotonicity proof + Newton/secant + verified final cell (see the block comment above)
+template <int N, int G>
+__global__ void __launch_bounds__(PT_EVAL_THREADS)
+pt_bisect_newton_kernel(PtFieldDev f, double sum_abs_w, const double* __restrict__ a_, const double* __restrict__ b_,
+                        const int8_t* __restrict__ signs_a, double* __restrict__ lo_io, double* __restrict__ hi_io,
+                        size_t m, double eps, double* __restrict__ out, uint8_t* __restrict__ slow,
                         unsigned long long* work) {
     extern __shared__ double tile[];
+    pt_exp_table_init(tile + PT_EVAL_TILE * PT_ROW64(N));
     const int PB = PT_EVAL_THREADS / G;
     const size_t ei = (size_t)blockIdx.x * PB + threadIdx.x / G;
     const int g = threadIdx.x % G;
@@ -320,16 +532,18 @@ pt_bisect_finish_kernel(PtFieldDev f, const double* __restrict__ a_, const doubl
         for (int d = 0; d < N; ++d) { a[d] = a_[ei * N + d]; b[d] = b_[ei * N + d]; }
         seg = pt_segment<N>(a, b, diff);
         sa = signs_a[ei];
-        lo = lo_in[ei]; hi = hi_in[ei];
+        lo = lo_io[ei]; hi = hi_io[ei];
     } else {
 #pragma unroll
         for (int d = 0; d < N; ++d) { a[d] = 0.0; diff[d] = 0.0; }
     }
     unsigned evals = 0;
-    // F at parameter t with the reference's point arithmetic; every thread of the block calls it
-    auto eval = [&](double t, bool count) -> double {
+    auto point = [&](double t) {
 #pragma unroll
         for (int d = 0; d < N; ++d) p[d] = __dadd_rn(a[d], __dmul_rn(t, diff[d]));
+    };
+    auto eval = [&](double t, bool count) -> double {
+        point(t);
         double F = f.bias + pt_rbf_block_sum<N, G>(f, p, g, tile);
         if (f.has_barrier) F -= pt_barrier_group<N, G>(f, p, g);
         if (count) ++evals;
@@ -339,37 +553,67 @@ pt_bisect_finish_kernel(PtFieldDev f, const double* __restrict__ a_, const doubl
     // depth of the reference's final bracket: smallest I with seg * 2^-I <= eps
     double delta = 1.0;
     if (valid) while (__dmul_rn(seg, delta) > eps) delta *= 0.5;
-    const double width = hi - lo;
-    const bool need = valid && width > delta;       // phase 1 did not reach the final depth
+    double width = hi - lo;
+    const bool finished0 = valid && !(__dmul_rn(seg, width) > eps);
+    const bool shallow = valid && !finished0 && width > PT_HANDOFF_WIDTH;
+    bool need = valid && !finished0 && !shallow;
+    bool to_slow = shallow;
     double t_final = __dmul_rn(0.5, __dadd_rn(lo, hi));
-    bool fallback = false;
     if (__syncthreads_or(need ? 1 : 0)) {
-        const double F_lo = eval(lo, need);
-        const double F_hi = eval(hi, need);
-        const bool ok = need && sgn(F_lo) == sa && sgn(F_hi) != sa;
-        // safeguarded secant on (x0,f0),(x1,f1); [blo,bhi] is the sign bracket.  The next iterate is
-        // used WITHOUT being evaluated once its predicted error 10*e_cur*e_prev (e = |f / slope|, the
-        // secant's error recursion with a generous curvature constant) is far below the cell width.
-        double x0 = lo, f0 = F_lo, x1 = hi, f1 = F_hi, blo = lo, bhi = hi;
-        const double slope = fabs((F_hi - F_lo) / width) + 1e-300;
-        double e_prev = width, e_cur = width;
-        double x2 = lo + 0.5 * width;
-        bool searching = ok;
+        // true bisection step at the midpoint, with derivatives along the edge
+        const double mid = __dmul_rn(0.5, __dadd_rn(lo, hi));
+        point(mid);
+        const double seg2 = seg * seg;
+        double F0, D1, D2;
+        pt_rbf_block_sum_d<N, G>(f, p, diff, seg2, g, tile, F0, D1, D2);
+        F0 += f.bias;
+        if (f.has_barrier) {
+            F0 -= pt_barrier_group<N, G>(f, p, g);
+            double B1, B2;
+            pt_barrier_derivs<N>(f, p, diff, B1, B2);
+            D1 -= B1; D2 -= B2;
+        }
+        if (need) {
+            ++evals;
+            if (sgn(F0) == sa) lo = mid; else hi = mid;
+            width = hi - lo;
+            if (!(__dmul_rn(seg, width) > eps)) { need = false; t_final = __dmul_rn(0.5, __dadd_rn(lo, hi)); }
+        }
+        // third-derivative bound along the edge: kernel sum + barrier (1.5x safety)
+        double m3 = 4.0 * f.gamma * sqrt(f.gamma) * sum_abs_w * seg2 * seg;
+        if (f.has_barrier) {
+            double s3 = 0.0;
+#pragma unroll
+            for (int d = 0; d < N; ++d) { const double r = fabs(diff[d]) / f.b_scale; s3 += r * r * r; }
+            m3 += 0.2 * f.b_gain * f.b_scale * s3;
+        }
+        m3 *= 1.5;
+        const bool monotone = need && fabs(D1) > width * fabs(D2) + 0.5 * width * width * m3;
+        if (need && !monotone) { to_slow = true; need = false; }
+        // Newton from the midpoint, then secant on the last two evaluated points; an iterate is used
+        // without being evaluated once its predicted error is far below the final cell width
+        const double slope = fabs(D1) + 1e-300;
+        double x0 = mid, f0 = F0, x1 = mid, f1 = F0, x2 = mid;
+        double e_prev = width, e_cur = fabs(F0) / slope;
+        bool searching = need;
+        bool first = true;
         for (int it = 0; it < 8; ++it) {
             if (searching) {
-                const double den = f1 - f0;
-                x2 = (den != 0.0) ? x1 - f1 * ((x1 - x0) / den) : 0.5 * (blo + bhi);
-                if (!(x2 > blo && x2 < bhi)) x2 = 0.5 * (blo + bhi);
-                if (10.0 * e_cur * e_prev < 0.0625 * delta) searching = false;
+                if (first) x2 = mid - F0 / D1;
+                else { const double den = f1 - f0; x2 = (den != 0.0) ? x1 - f1 * ((x1 - x0) / den) : 0.5 * (lo + hi); }
+                if (!(x2 > lo && x2 < hi)) x2 = 0.5 * (lo + hi);
+                const double predicted = first ? 10.0 * e_cur * e_cur : 10.0 * e_cur * e_prev;
+                if (predicted < 0.0625 * delta) searching = false;
             }
             if (!__syncthreads_or(searching ? 1 : 0)) break;
             const double f2 = eval(x2, searching);
             if (searching) {
-                if (sgn(f2) == sa) blo = x2; else bhi = x2;
                 x0 = x1; f0 = f1; x1 = x2; f1 = f2;
                 e_prev = e_cur; e_cur = fabs(f2) / slope;
+                first = false;
             }
         }
+        if (searching) { to_slow = true; need = false; }   // did not converge in 8 evaluations
         const double nsub = width / delta;            // exact: both are powers of two
         double j = floor((x2 - lo) / delta);
         if (!(j >= 0.0)) j = 0.0;
@@ -377,10 +621,9 @@ pt_bisect_finish_kernel(PtFieldDev f, const double* __restrict__ a_, const doubl
         double c = lo + j * delta;                    // exact dyadic arithmetic
         const int sc = sgn(eval(c, need));
         const int sd = sgn(eval(c + delta, need));
-        bool accepted = ok && sc == sa && sd != sa;
-        // one neighbouring cell when the secant landed within rounding of a cell boundary
-        const bool try_left = ok && !accepted && sc != sa && j > 0.0;
-        const bool try_right = ok && !accepted && sc == sa && sd == sa && j < nsub - 1.0;
+        bool accepted = need && sc == sa && sd != sa;
+        const bool try_left = need && !accepted && sc != sa && j > 0.0;
+        const bool try_right = need && !accepted && sc == sa && sd == sa && j < nsub - 1.0;
         if (__syncthreads_or((try_left || try_right) ? 1 : 0)) {
             const double tq = try_left ? c - delta : c + 2.0 * delta;
             const int sq = sgn(eval(tq, try_left || try_right));
@@ -389,42 +632,85 @@ pt_bisect_finish_kernel(PtFieldDev f, const double* __restrict__ a_, const doubl
         }
         if (need) {
             if (accepted) t_final = c + 0.5 * delta;
-            else {
-                fallback = true;
-                // a bracket whose ends do not show the expected signs cannot be trusted: replay from [0,1]
-                if (!ok) { lo = 0.0; hi = 1.0; }
-            }
-        }
-    }
-    // plain fp64 bisection from the phase-1 bracket for the rows that could not be verified
-    bool active = fallback;
-    while (__syncthreads_or(active ? 1 : 0)) {
-        const double mid = __dmul_rn(0.5, __dadd_rn(lo, hi));
-        const int s = sgn(eval(mid, active));
-        if (active) {
-            if (s == sa) lo = mid; else hi = mid;
-            active = __dmul_rn(seg, __dsub_rn(hi, lo)) > eps;
-            if (!active) t_final = __dmul_rn(0.5, __dadd_rn(lo, hi));
+            else to_slow = true;
         }
     }
     {
         unsigned mine = (g == 0) ? evals : 0u;
-        unsigned fb = (g == 0 && fallback) ? 1u : 0u;
-        for (int off = 16; off > 0; off >>= 1) { mine += __shfl_xor_sync(0xffffffffu, mine, off); fb += __shfl_xor_sync(0xffffffffu, fb, off); }
+        unsigned sl = (g == 0 && to_slow) ? 1u : 0u;
+        for (int off = 16; off > 0; off >>= 1) { mine += __shfl_xor_sync(0xffffffffu, mine, off); sl += __shfl_xor_sync(0xffffffffu, sl, off); }
         if ((threadIdx.x & 31) == 0) {
             if (mine) atomicAdd(&work[0], (unsigned long long)mine);
-            if (fb) atomicAdd(&work[3], (unsigned long long)fb);
+            if (sl) atomicAdd(&work[3], (unsigned long long)sl);
         }
     }
     if (valid && g == 0) {
+        slow[ei] = to_slow ? 1 : 0;
+        if (to_slow) { lo_io[ei] = lo; hi_io[ei] = hi; }
+        else {
 #pragma unroll
-        for (int d = 0; d < N; ++d) out[ei * N + d] = __dadd_rn(a[d], __dmul_rn(t_final, diff[d]));
+            for (int d = 0; d < N; ++d) out[ei * N + d] = __dadd_rn(a[d], __dmul_rn(t_final, diff[d]));
+        }
+    }
+}
+
+// K4: plain fp64 bisection of the listed rows from their stored brackets
+template <int N, int G>
+__global__ void __launch_bounds__(PT_EVAL_THREADS)
+pt_bisect_rest_kernel(PtFieldDev f, PtRows rows, const double* __restrict__ a_, const double* __restrict__ b_,
+                      const int8_t* __restrict__ signs_a, const double* __restrict__ lo_in, const double* __restrict__ hi_in,
+                      double eps, double* __restrict__ out, unsigned long long* work) {
+    extern __shared__ double tile[];
+    pt_exp_table_init(tile + PT_EVAL_TILE * PT_ROW64(N));
+    const int PB = PT_EVAL_THREADS / G;
+    const size_t total = pt_rows_total(rows);
+    if ((size_t)blockIdx.x * PB >= total) return;
+    const size_t idx = (size_t)blockIdx.x * PB + threadIdx.x / G;
+    const int g = threadIdx.x % G;
+    const bool valid = idx < total;
+    const size_t ei = valid ? (rows.list ? (size_t)rows.list[idx] : idx) : 0;
+    double a[N], diff[N], p[N];
+    double seg = 0.0, lo = 0.0, hi = 1.0;
+    int sa = 1;
+    if (valid) {
+        double b[N];
+#pragma unroll
+        for (int d = 0; d < N; ++d) { a[d] = a_[ei * N + d]; b[d] = b_[ei * N + d]; }
+        seg = pt_segment<N>(a, b, diff);
+        sa = signs_a[ei]; lo = lo_in[ei]; hi = hi_in[ei];
+    } else {
+#pragma unroll
+        for (int d = 0; d < N; ++d) { a[d] = 0.0; diff[d] = 0.0; }
+    }
+    bool active = valid && __dmul_rn(seg, __dsub_rn(hi, lo)) > eps;
+    unsigned iters = 0;
+    while (__syncthreads_or(active ? 1 : 0)) {
+        const double mid = __dmul_rn(0.5, __dadd_rn(lo, hi));
+#pragma unroll
+        for (int d = 0; d < N; ++d) p[d] = __dadd_rn(a[d], __dmul_rn(mid, diff[d]));
+        double F = f.bias + pt_rbf_block_sum<N, G>(f, p, g, tile);
+        if (f.has_barrier) F -= pt_barrier_group<N, G>(f, p, g);
+        if (active) {
+            if ((F > 0.0 ? 1 : -1) == sa) lo = mid; else hi = mid;
+            active = __dmul_rn(seg, __dsub_rn(hi, lo)) > eps;
+            ++iters;
+        }
+    }
+    {
+        unsigned mine = (g == 0) ? iters : 0u;
+        for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
+        if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&work[0], (unsigned long long)mine);
+    }
+    if (valid && g == 0) {
+        const double t = __dmul_rn(0.5, __dadd_rn(lo, hi));
+#pragma unroll
+        for (int d = 0; d < N; ++d) out[ei * N + d] = __dadd_rn(a[d], __dmul_rn(t, diff[d]));
     }
 }
 
 // pack the fp32 screening copy and record max |s_j|
 __global__ void pt_pack_sv32_kernel(const double* __restrict__ sv, long long S, int n, int row, int row32, double gl,
-                                    float* __restrict__ sv32, unsigned long long* rmax_bits) {
+                                    float* __restrict__ sv32, unsigned long long* rmax_bits, double* sum_abs_w) {
     long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= S) return;
     double s2 = 0.0;
@@ -433,16 +719,19 @@ __global__ void pt_pack_sv32_kernel(const double* __restrict__ sv, long long S, 
     sv32[j * row32 + n + 1] = (float)sv[j * row + n];
     for (int d = n + 2; d < row32; ++d) sv32[j * row32 + d] = 0.f;
     atomicMax(rmax_bits, (unsigned long long)__double_as_longlong(sqrt(s2)));
+    atomicAdd(sum_abs_w, fabs(sv[j * row + n]));
 }
 
 // pack raw (support[S][n], weights[S]) into the padded row layout
 __global__ void pt_pack_sv_kernel(const double* __restrict__ support, const double* __restrict__ weights,
-                                  long long S, int n, int row, double* __restrict__ sv) {
+                                  long long S, int n, int row, double gl, double* __restrict__ sv) {
     long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= S) return;
-    for (int d = 0; d < n; ++d) sv[j * row + d] = support[j * n + d];
+    double s2 = 0.0;
+    for (int d = 0; d < n; ++d) { const double v = support[j * n + d]; sv[j * row + d] = v; s2 = fma(v, v, s2); }
     sv[j * row + n] = weights[j];
-    for (int d = n + 1; d < row; ++d) sv[j * row + d] = 0.0;
+    sv[j * row + n + 1] = -gl * s2;
+    for (int d = n + 2; d < row; ++d) sv[j * row + d] = 0.0;
 }
 
 // lanes per item so that small batches still fill the machine
@@ -462,7 +751,7 @@ static int pt_eval_launch(pt_ctx* ctx, const pt_field* f, const double* pts, siz
         return pt_check_launch(ctx, "pt_eval_analytic_kernel");
     }
     const int G = pt_pick_group(ctx, m, f->d.S);
-    const size_t smem = (size_t)PT_EVAL_TILE * ((N + 1) | 1) * sizeof(double);
+    const size_t smem = PT_SMEM64(N);
     PT_LAUNCH(ctx, "eval_rbf");
     if (G == 1)
         pt_eval_rbf_kernel<N, 1><<<pt_grid_for(m, PT_EVAL_THREADS), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, pts, m, vals, signs, ctx->work);
@@ -482,7 +771,7 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
         return pt_check_launch(ctx, "pt_bisect_analytic_kernel");
     }
     const int G = pt_pick_group(ctx, m, f->d.S);
-    const size_t smem = (size_t)PT_EVAL_TILE * ((N + 1) | 1) * sizeof(double);
+    const size_t smem = PT_SMEM64(N);
     const unsigned grid = pt_grid_for(m, PT_EVAL_THREADS / G);
     if (f->precision == 0 || f->d.S == 0) {
         PT_LAUNCH(ctx, "bisect_rbf");
@@ -491,24 +780,60 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
         else pt_bisect_rbf_kernel<N, 32><<<grid, PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, a, b, sa, m, eps, out, ctx->work);
         return pt_check_launch(ctx, "pt_bisect_rbf_kernel");
     }
-    PtBuf<double> lo, hi;
+    PtBuf<double> lo, hi; PtBuf<uint32_t> list; PtBuf<unsigned long long> cnt; PtBuf<uint8_t> slow;
     PT_TRY(lo.alloc(ctx, m));
     PT_TRY(hi.alloc(ctx, m));
+    PT_TRY(list.alloc(ctx, m));
+    PT_TRY(slow.alloc(ctx, m));
+    PT_TRY(cnt.alloc(ctx, 4));
+    PT_CUDA(ctx, cudaMemsetAsync(cnt.p, 0, 4 * sizeof(unsigned long long), ctx->stream));
     const size_t smem32 = (size_t)PT_TILE32 * PtRow32<N>::value * sizeof(float);
+    const PtRows all{nullptr, nullptr, m};
+#define PT_G_LAUNCH(KERNEL, SMEM, ...)                                                            \
+    do {                                                                                            \
+        if (G == 1) KERNEL<N, 1><<<grid, PT_EVAL_THREADS, SMEM, ctx->stream>>>(__VA_ARGS__);        \
+        else if (G == 4) KERNEL<N, 4><<<grid, PT_EVAL_THREADS, SMEM, ctx->stream>>>(__VA_ARGS__);   \
+        else KERNEL<N, 32><<<grid, PT_EVAL_THREADS, SMEM, ctx->stream>>>(__VA_ARGS__);              \
+        PT_TRY(pt_check_launch(ctx, #KERNEL));                                                      \
+    } while (0)
     {
         PT_LAUNCH(ctx, "bisect_fp32_screen");
-        if (G == 1) pt_bisect32_kernel<N, 1><<<grid, PT_EVAL_THREADS, smem32, ctx->stream>>>(f->d, a, b, sa, m, eps, lo.p, hi.p, ctx->work);
-        else if (G == 4) pt_bisect32_kernel<N, 4><<<grid, PT_EVAL_THREADS, smem32, ctx->stream>>>(f->d, a, b, sa, m, eps, lo.p, hi.p, ctx->work);
-        else pt_bisect32_kernel<N, 32><<<grid, PT_EVAL_THREADS, smem32, ctx->stream>>>(f->d, a, b, sa, m, eps, lo.p, hi.p, ctx->work);
-        PT_TRY(pt_check_launch(ctx, "pt_bisect32_kernel"));
+        PT_G_LAUNCH(pt_bisect32_kernel, smem32, f->d, all, a, b, sa, eps, 1, lo.p, hi.p, ctx->work);
+    }
+    // rows that stopped while their bracket is still wide: one true fp64 step, then back to fp32
+    for (int round = 0; round < 2; ++round) {
+        unsigned long long* c = cnt.p + round;
+        const PtRows sub{list.p, c, m};
+        {
+            PT_LAUNCH(ctx, "bisect_select");
+            pt_select_shallow_kernel<N><<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>(all, a, b, lo.p, hi.p, eps, list.p, c);
+            PT_TRY(pt_check_launch(ctx, "pt_select_shallow_kernel"));
+        }
+        {
+            PT_LAUNCH(ctx, "bisect_fp64_resolve");
+            PT_G_LAUNCH(pt_bisect_resolve_kernel, smem, f->d, sub, a, b, sa, lo.p, hi.p, ctx->work);
+        }
+        {
+            PT_LAUNCH(ctx, "bisect_fp32_screen");
+            PT_G_LAUNCH(pt_bisect32_kernel, smem32, f->d, sub, a, b, sa, eps, 0, lo.p, hi.p, ctx->work);
+        }
     }
     {
-        PT_LAUNCH(ctx, "bisect_fp64_finish");
-        if (G == 1) pt_bisect_finish_kernel<N, 1><<<grid, PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, a, b, sa, lo.p, hi.p, m, eps, out, ctx->work);
-        else if (G == 4) pt_bisect_finish_kernel<N, 4><<<grid, PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, a, b, sa, lo.p, hi.p, m, eps, out, ctx->work);
-        else pt_bisect_finish_kernel<N, 32><<<grid, PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, a, b, sa, lo.p, hi.p, m, eps, out, ctx->work);
-        PT_TRY(pt_check_launch(ctx, "pt_bisect_finish_kernel"));
+        PT_LAUNCH(ctx, "bisect_fp64_newton");
+        PT_G_LAUNCH(pt_bisect_newton_kernel, smem, f->d, f->sum_abs_w, a, b, sa, lo.p, hi.p, m, eps, out, slow.p, ctx->work);
     }
+    {
+        unsigned long long* c = cnt.p + 2;
+        const PtRows sub{list.p, c, m};
+        {
+            PT_LAUNCH(ctx, "bisect_select");
+            pt_select_flag_kernel<<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>(slow.p, m, list.p, c);
+            PT_TRY(pt_check_launch(ctx, "pt_select_flag_kernel"));
+        }
+        PT_LAUNCH(ctx, "bisect_fp64_rest");
+        PT_G_LAUNCH(pt_bisect_rest_kernel, smem, f->d, sub, a, b, sa, lo.p, hi.p, eps, out, ctx->work);
+    }
+#undef PT_G_LAUNCH
     return PT_OK;
 }
 
@@ -549,7 +874,7 @@ static int pt_field_build_rbf(pt_ctx* ctx, int n, long long S, const double* sup
     f->d.kind = PT_FIELD_RBF; f->d.n = n; f->d.S = S; f->d.row = pt_sv_row(n);
     {
         const char* env = getenv("PERMATRACE_B200_PRECISION");
-        f->precision = (env && env[0] == '1') ? 1 : 0;
+        f->precision = (env && env[0] == '0') ? 0 : 1;
     }
     f->d.gamma = gamma; f->d.bias = bias;
     if (barrier_host) {
@@ -565,23 +890,24 @@ static int pt_field_build_rbf(pt_ctx* ctx, int n, long long S, const double* sup
         rc = pt_stage_in(ctx, support, (size_t)S * n, tmp_s, &sdev);
         if (rc == PT_OK) rc = pt_stage_in(ctx, weights, (size_t)S, tmp_w, &wdev);
         if (rc != PT_OK) { delete f; return rc; }
-        pt_pack_sv_kernel<<<pt_grid_for((size_t)S, 256), 256, 0, ctx->stream>>>(sdev, wdev, S, n, f->d.row, f->sv.p);
+        pt_pack_sv_kernel<<<pt_grid_for((size_t)S, 256), 256, 0, ctx->stream>>>(sdev, wdev, S, n, f->d.row, gamma * PT_L2E, f->sv.p);
         rc = pt_check_launch(ctx, "pt_pack_sv_kernel");
         if (rc != PT_OK) { delete f; return rc; }
         f->d.row32 = pt_sv_row32(n);
         rc = f->sv32.alloc(ctx, (size_t)S * f->d.row32);
         PtBuf<unsigned long long> rmax;
-        if (rc == PT_OK) rc = rmax.alloc(ctx, 1);
+        if (rc == PT_OK) rc = rmax.alloc(ctx, 2);
         if (rc != PT_OK) { delete f; return rc; }
-        cudaMemsetAsync(rmax.p, 0, sizeof(unsigned long long), ctx->stream);
+        cudaMemsetAsync(rmax.p, 0, 2 * sizeof(unsigned long long), ctx->stream);
         pt_pack_sv32_kernel<<<pt_grid_for((size_t)S, 256), 256, 0, ctx->stream>>>(f->sv.p, S, n, f->d.row, f->d.row32,
-                                                                                gamma * PT_L2E, f->sv32.p, rmax.p);
+                                                                                gamma * PT_L2E, f->sv32.p, rmax.p, (double*)(rmax.p + 1));
         rc = pt_check_launch(ctx, "pt_pack_sv32_kernel");
         if (rc != PT_OK) { delete f; return rc; }
-        unsigned long long bits = 0;
-        cudaMemcpyAsync(&bits, rmax.p, sizeof(bits), cudaMemcpyDeviceToHost, ctx->stream);
+        unsigned long long bits[2] = {0, 0};
+        cudaMemcpyAsync(bits, rmax.p, sizeof(bits), cudaMemcpyDeviceToHost, ctx->stream);
         cudaStreamSynchronize(ctx->stream);
-        memcpy(&f->d.smax, &bits, sizeof(double));
+        memcpy(&f->d.smax, &bits[0], sizeof(double));
+        memcpy(&f->sum_abs_w, &bits[1], sizeof(double));
         f->d.sv32 = f->sv32.p;
     }
     f->d.sv = f->sv.p;

@@ -9,7 +9,7 @@ struct PtFieldDev {
     int kind;              // PT_FIELD_*
     int n;
     long long S;           // support vectors
-    int row;               // doubles per packed support row (odd, >= n+1): coords, weight, pad
+    int row;               // doubles per packed support row (odd, >= n+2): coords, weight, -gamma*log2(e)*|s|^2, pad
     const double* sv;      // [S][row]
     const float* sv32;     // [S][row32] fp32 screening copy: coords, -gamma*log2(e)*|s|^2, weight, pad
     int row32;             // floats per fp32 row (multiple of 4)
@@ -23,7 +23,7 @@ struct PtFieldDev {
     double c0;             // sphere radius^2, plane offset
 };
 
-static inline int pt_sv_row(int n) { int r = n + 1; return (r & 1) ? r : r + 1; }
+static inline int pt_sv_row(int n) { return (n + 2) | 1; }
 static inline int pt_sv_row32(int n) { return (n + 2 + 3) & ~3; }
 
 #define PT_L2E 1.4426950408889634

@@ -15,6 +15,17 @@ from oracle import permatrace_oracle as O
 from tests.conftest import (ANALYTIC_TRACES, LEARNED_TRACES, PRISM_ROBOT, PRISM_SCENE, analytic_spec, oracle_model,
                             robot_scene_dicts, trace_inputs)
 
+import os
+
+
+@pytest.fixture(autouse=True, params=["fp64", "fast"])
+def precision_mode(request, monkeypatch):
+    """Every parity test runs twice: plain fp64 bisection and the fp32-screened / Newton fast path.
+    Both must return the reference's dyadic bracket midpoints."""
+    monkeypatch.setenv("PERMATRACE_B200_PRECISION", "1" if request.param == "fast" else "0")
+    return request.param
+
+
 POINT_RTOL = 1e-5     # north_star tolerance for intersection points
 POINT_ATOL = 1e-8     # what we actually hold (bracket is 1e-9)
 
