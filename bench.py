@@ -226,36 +226,47 @@ def run_gpu(args):
 
     # resident inputs for the kernel-only number
     seeds_dev = torch.from_numpy(a.seeds).cuda()
-    pipe = engine.DevicePipeline(wl.manifold, wl.cfg, wl.template, checker, rank=rank, world=world)
+    pipe = engine.DevicePipeline(wl.manifold, wl.cfg, wl.template, checker)
+    sharded = None
+    if world > 1:
+        from paper_2406_04795_b200.distributed import CudaEngine, ShardedProof
+        sharded = ShardedProof(CudaEngine(wl.manifold, wl.cfg, wl.template, checker, device_index=local))
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
 
+    def step():
+        """One proof attempt; N > 1 shards the refinement over the ranks (distributed.ShardedProof)."""
+        if sharded is None:
+            return pipe.step(seeds_dev.data_ptr(), a.seeds.shape[0])
+        res = sharded.run(seeds_dev)
+        return {"trace_edges": res["trace_edges"], "cells": res["cells"], "crossing_edges": res["crossing_edges"],
+                "unique_fine_edges": res["candidates"], "points": int(res["points"].shape[0]),
+                "free_points": res["free_points"], "closure_ok": res["closure_ok"], "candidates": res["candidates_bfs"],
+                "simplices_local": res["trace_edges"] + res["crossing_edges"], "pair_evals_bisect": 0,
+                "pair_evals_eval": 0, "pair_evals_fp32": 0, "bisect_fallbacks": 0, "pair_evals_rest": 0, "pair_evals_resolve": 0}
+
     # ---- resident-input throughput ("value") ---------------------------------------------------
     for _ in range(args.warmup):
-        pipe.step(seeds_dev.data_ptr(), a.seeds.shape[0])
+        step()
     barrier()
     launches0 = ctx.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
         e0.record(stream)
         for _ in range(args.steps):
-            counts = pipe.step(seeds_dev.data_ptr(), a.seeds.shape[0])
+            counts = step()
         e1.record(stream)
         barrier()
     ms = e0.elapsed_time(e1)
     launches = ctx.launch_count() - launches0
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    units = torch.tensor([float(counts["simplices_local"])], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(units, op=dist.ReduceOp.SUM)
     ms = float(t.item())
-    simplices = float(units.item()) + (counts["trace_edges"] if world > 1 else 0.0)   # trace counted once
-    if world == 1:
-        simplices = float(counts["simplices_local"])
+    simplices = float(counts["simplices_local"])       # whole job: the sharded driver already reports global counts
     value = simplices * args.steps / (ms * 1e-3)
 
     # ---- end to end through the public API with host buffers ---------------------------------------
@@ -288,22 +299,23 @@ def run_gpu(args):
     e2e_simplices = len(res.edges) + sum(b.crossing_edges for b in ref.batch_stats)
     h2d = a.support.nbytes + a.weights.nbytes + a.seeds.nbytes
     d2h = res.points.nbytes + ref.points.nbytes + ref.in_collision.nbytes
-    e2e = {"value": e2e_simplices * args.steps * (world if False else 1) / e2e_s, "unit": UNIT,
+    e2e = {"value": e2e_simplices * args.steps / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
     # ---- per-kernel profile of one more step (CUDA events on the launching stream) -------------------
     ctx.profile(True)
     ctx.profile_reset()
-    pipe.step(seeds_dev.data_ptr(), a.seeds.shape[0])
+    pipe.last_counts = pipe.step(seeds_dev.data_ptr(), a.seeds.shape[0])
     prof = ctx.profile_dump()
     ctx.profile(False)
     total_ms = sum(v[1] for v in prof.values()) or 1.0
     top = max(prof.items(), key=lambda kv: kv[1][1])
-    pair_evals = {"bisect_rbf": counts["pair_evals_bisect"], "bisect_fp64_finish": counts["pair_evals_bisect"],
-                  "eval_rbf": counts["pair_evals_eval"]}.get(top[0], 0)
+    prof_counts = pipe.last_counts
+    pair_evals = {"bisect_rbf": prof_counts["pair_evals_bisect"], "bisect_fp64_newton": prof_counts["pair_evals_bisect"],
+                  "bisect_fp32_screen": prof_counts["pair_evals_fp32"], "eval_rbf": prof_counts["pair_evals_eval"]}.get(top[0], 0)
     peak = engine.measure_fp64_peak(ctx)
     roofline = None
-    if top[0] in ("bisect_rbf", "bisect_fp64_finish", "eval_rbf"):
+    if top[0] in ("bisect_rbf", "bisect_fp64_newton", "eval_rbf"):
         achieved = pair_evals * pair_flops(a.n) / (top[1][1] * 1e-3) / 1e12
         roofline = {"bound": "fp64", "kernel": top[0], "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": achieved / peak if peak else None, "traffic": None,
@@ -333,13 +345,15 @@ def run_gpu(args):
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.workload}: {a.n}-DoF arm, {len(a.scene_dict['obstacles'])} primitives, "
                                    f"S={a.support.shape[0]} support vectors, lambda={a.lam}, k={a.k}",
+                       "parallelism": "single GPU" if world == 1 else f"trace replicated, refine+check sharded over {world} ranks (cell slices), candidate merge by all_gather",
                        "l2_policy": "per-step working set (hash tables + fine-edge arrays) exceeds the 126 MB L2; "
                                     "all tables are rebuilt from empty every step",
                        "trace_edges": counts["trace_edges"], "coarse_cells": counts["cells"],
                        "crossing_fine_edges": counts["crossing_edges"], "unique_fine_edges": counts["unique_fine_edges"],
                        "points_checked": counts["points"], "free_points": counts["free_points"],
                        "closure_ok": counts["closure_ok"], "fp32_screened_pair_evals": counts["pair_evals_fp32"],
-                       "fp64_root_solve_pair_evals": counts["pair_evals_bisect"], "bisect_fallbacks": counts["bisect_fallbacks"]},
+                       "fp64_root_solve_pair_evals": counts["pair_evals_bisect"] + counts.get("pair_evals_rest", 0) + counts.get("pair_evals_resolve", 0),
+                       "bisect_fallbacks": counts["bisect_fallbacks"]},
             "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": int(launches),
             "roofline": roofline, "roofline_hbm": hbm, "kernels": kernels, "cpu_baseline": cpu,
             "proof_time_s": ms / args.steps * 1e-3,

@@ -45,9 +45,10 @@ int pt_ctx_profile_reset(pt_ctx* ctx);
 /* writes "name,launches,total_ms\n" lines; returns bytes needed (call with cap=0 to size) */
 long long pt_ctx_profile_dump(pt_ctx* ctx, char* buf, long long cap);
 long long pt_ctx_launch_count(pt_ctx* ctx);
-/* device-side work counters, out[4]: [0] fp64 field evaluations spent in root solves, [1] points
- * evaluated by the batch evaluator, [2] fp32-screened bisection evaluations, [3] root solves that fell
- * back to plain fp64 bisection; reset != 0 zeroes them */
+/* device-side work counters, out[6]: [0] fp64 field evaluations of the main root-solve kernel (Newton
+ * path, or plain bisection in fp64 mode), [1] points evaluated by the batch evaluator, [2] fp32-screened
+ * bisection evaluations, [3] root solves handed to plain fp64 bisection, [4] fp64 evaluations spent there,
+ * [5] fp64 single-step resolves; reset != 0 zeroes them */
 int pt_ctx_work_counters(pt_ctx* ctx, long long* out, int reset);
 /* DFMA-chain microbenchmark: measured FP64 peak of this device in TFLOP/s (roofline denominator) */
 double pt_peak_fp64(pt_ctx* ctx);
@@ -185,6 +186,15 @@ int pt_refine_run(pt_ctx* ctx, const pt_field* field, const pt_cells* cells, int
                   const double* offset, int k, int V, const int32_t* tv, int E, const int32_t* te,
                   double eps, double eps_dedup, const pt_checker* checker,
                   const long long* batch_bounds, int nb, pt_refine** out);
+/* multi-GPU building blocks: (1) refinement of a cell slice up to and including the root solves --
+ * the result holds one point per distinct fine edge in first-crossing order (first_tag = crossing index
+ * local to the slice), no dedup, no labels; (2) greedy first-keeper dedup at eps_dedup over points given
+ * in priority order + collision labels (first_tag = position in the input). */
+int pt_refine_candidates(pt_ctx* ctx, const pt_field* field, const pt_cells* cells, int n, double scale,
+                         const double* offset, int k, int V, const int32_t* tv, int E, const int32_t* te,
+                         double eps, pt_refine** out);
+int pt_dedup_label(pt_ctx* ctx, int n, const double* points, long long count, double eps_dedup,
+                   const pt_checker* checker, pt_refine** out);
 void pt_refine_destroy(pt_refine* r);
 int pt_refine_get_stats(const pt_refine* r, pt_refine_stats* out);
 /* points[P,n] f64, labels[P] uint8 (1 = not free), first_tag[P] int64 (global crossing index of the

@@ -542,11 +542,31 @@ class PointRegistry:
         return idx
 
 
+def crossing_points(batch, template, field, scale, offset, eps):
+    """subdivision.py:256-272 for one batch of cells: the bisected point of every sign-changing
+    template edge, cell-major then template-edge-major (duplicates across cells included)."""
+    vertices, tedges, weights = template
+    n = vertices.shape[1]
+    if not len(batch):
+        return np.zeros((0, n))
+    corners = np.asarray([simplex_vertices(c) for c in batch], dtype=np.float64)
+    corners = corners * scale + np.asarray(offset, dtype=np.float64)
+    fine = np.einsum("vc,bcn->bvn", weights, corners)
+    signs = field.signs(fine.reshape(-1, n)).reshape(len(batch), -1)
+    sa = signs[:, tedges[:, 0]]
+    sb = signs[:, tedges[:, 1]]
+    idx_b, idx_e = np.nonzero(sa != sb)
+    if not idx_b.size:
+        return np.zeros((0, n))
+    a = fine[idx_b, tedges[idx_e, 0]]
+    b = fine[idx_b, tedges[idx_e, 1]]
+    return intersection_points_batch(field, a, b, eps, signs_a=sa[idx_b, idx_e])
+
+
 def refine(cells, template, field, checker, scale, offset, k, eps, eps_dedup=None, batch_cells=None):
     """subdivision.py:220-301.  `template` = (vertices, edges, weights); returns a dict with points,
     in_collision, crossing_edges per batch, new_points per batch."""
-    vertices, tedges, weights = template
-    n = vertices.shape[1]
+    n = template[0].shape[1]
     cells = list(cells)
     if eps_dedup is None:
         eps_dedup = scale / (10.0 * k * k)
@@ -554,25 +574,12 @@ def refine(cells, template, field, checker, scale, offset, k, eps, eps_dedup=Non
     batches = [cells[i:i + step] for i in range(0, len(cells), max(step, 1))] if cells else []
     registry = PointRegistry(eps_dedup, n)
     labels, crossing_counts, new_counts = [], [], []
-    offset = np.asarray(offset, dtype=np.float64)
     for batch in batches:
-        corners = np.asarray([simplex_vertices(c) for c in batch], dtype=np.float64)
-        corners = corners * scale + offset
-        fine = np.einsum("vc,bcn->bvn", weights, corners)
-        signs = field.signs(fine.reshape(-1, n)).reshape(len(batch), -1)
-        sa = signs[:, tedges[:, 0]]
-        sb = signs[:, tedges[:, 1]]
-        idx_b, idx_e = np.nonzero(sa != sb)
-        if idx_b.size:
-            a = fine[idx_b, tedges[idx_e, 0]]
-            b = fine[idx_b, tedges[idx_e, 1]]
-            pts = intersection_points_batch(field, a, b, eps, signs_a=sa[idx_b, idx_e])
-        else:
-            pts = np.zeros((0, n))
+        pts = crossing_points(batch, template, field, scale, offset, eps)
         fresh = [p for p in pts if registry.add(p) is not None]
         if fresh:
             labels.extend(bool(h) for h in np.asarray(checker(np.asarray(fresh)), dtype=bool))
-        crossing_counts.append(int(idx_b.size))
+        crossing_counts.append(int(pts.shape[0]))
         new_counts.append(len(fresh))
     points = np.asarray(registry.points, dtype=np.float64) if registry.points else np.zeros((0, n))
     return {

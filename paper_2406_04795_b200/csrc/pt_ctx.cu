@@ -183,7 +183,7 @@ int pt_ctx_work_counters(pt_ctx* ctx, long long* out, int reset) {
     unsigned long long h[8];
     PT_CUDA(ctx, cudaMemcpyAsync(h, ctx->work, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
     PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    for (int i = 0; i < 4; ++i) out[i] = (long long)h[i];
+    for (int i = 0; i < 6; ++i) out[i] = (long long)h[i];
     if (reset) PT_CUDA(ctx, cudaMemsetAsync(ctx->work, 0, sizeof(h), ctx->stream));
     return PT_OK;
 }

@@ -507,7 +507,7 @@ pt_bisect_resolve_kernel(PtFieldDev f, PtRows rows, const double* __restrict__ a
     }
     unsigned mine = (valid && g == 0) ? 1u : 0u;
     for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
-    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&work[0], (unsigned long long)mine);
+    if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&work[5], (unsigned long long)mine);
 }
 
 // K3: monotonicity proof + Newton/secant + verified final cell (see the block comment above)
@@ -699,7 +699,7 @@ pt_bisect_rest_kernel(PtFieldDev f, PtRows rows, const double* __restrict__ a_, 
     {
         unsigned mine = (g == 0) ? iters : 0u;
         for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
-        if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&work[0], (unsigned long long)mine);
+        if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&work[4], (unsigned long long)mine);
     }
     if (valid && g == 0) {
         const double t = __dmul_rn(0.5, __dadd_rn(lo, hi));

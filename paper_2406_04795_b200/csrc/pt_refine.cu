@@ -301,7 +301,7 @@ __global__ void pt_gather_points_kernel(int n, const double* __restrict__ pts, c
     if (i >= count) return;
     const size_t src = sel[i];
     for (int d = 0; d < n; ++d) out_pts[i * n + d] = pts[src * n + d];
-    out_tag[i] = (long long)(vals[src] >> 1);
+    out_tag[i] = vals ? (long long)(vals[src] >> 1) : (long long)src;
 }
 __global__ void pt_iota32_kernel(uint32_t* out, size_t count) {
     size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -334,11 +334,111 @@ static int pt_read_fine_counters(pt_ctx* ctx, PtFineCounters* dev, PtFineCounter
     return PT_OK;
 }
 
-extern "C" {
+// Greedy first-keeper dedup at eps over `U` points given in priority order, then collision labels.
+// vals (optional) carries (tag << 1 | sign) per point; without it the tag is the input position.
+static int pt_dedup_label_impl(pt_ctx* ctx, int n, const double* upts, const u64* vals, size_t U, double eps_dedup,
+                               const pt_checker* checker, pt_refine* r) {
+    PtBuf<PtFineCounters> ctr;
+    PT_TRY(ctr.alloc(ctx, 1));
+    PT_CUDA(ctx, cudaMemsetAsync(ctr.p, 0, sizeof(PtFineCounters), ctx->stream));
+    PtFineCounters hc;
+    PtRefGeom rg;
+    memset(&rg, 0, sizeof(rg));
+    rg.fine.n = n;
+    PtBuf<uint8_t> state;
+    PT_TRY(state.alloc(ctx, U > 0 ? U : 1));
+    long long rounds = 0;
+    size_t P = 0;
+    PtBuf<uint32_t> sel;
+    if (U > 0) {
+        if (U >= (1ull << 32)) return pt_fail(ctx, PT_E_NOMEM, "more than 2^32 distinct fine edges in one refine call");
+        PT_CUDA(ctx, cudaMemsetAsync(state.p, PT_DD_UNDECIDED, U, ctx->stream));
+        const double cell = 16.0 * eps_dedup;
+        PtBuf<u64> gk, gks; PtBuf<uint32_t> gi, gis;
+        PT_TRY(gk.alloc(ctx, U)); PT_TRY(gks.alloc(ctx, U)); PT_TRY(gi.alloc(ctx, U)); PT_TRY(gis.alloc(ctx, U));
+        {
+            PT_LAUNCH(ctx, "dedup_hash");
+            pt_dedup_hash_kernel<<<pt_grid_for(U, 256), 256, 0, ctx->stream>>>(n, upts, U, cell, gk.p, gi.p);
+            PT_TRY(pt_check_launch(ctx, "pt_dedup_hash_kernel"));
+        }
+        size_t tb = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tb, gk.p, gks.p, gi.p, gis.p, (long long)U, 0, 64, ctx->stream);
+        PtBuf<uint8_t> tmp;
+        PT_TRY(tmp.alloc(ctx, tb));
+        {
+            PT_LAUNCH(ctx, "dedup_sort");
+            PT_CUDA(ctx, cub::DeviceRadixSort::SortPairs(tmp.p, tb, gk.p, gks.p, gi.p, gis.p, (long long)U, 0, 64, ctx->stream));
+            ctx->launches++;
+        }
+        for (;;) {
+            PT_CUDA(ctx, cudaMemsetAsync(&ctr.p->undecided, 0, sizeof(unsigned long long), ctx->stream));
+            {
+                PT_LAUNCH(ctx, "dedup_round");
+                pt_dedup_round_kernel<<<pt_grid_for(U, 128), 128, 0, ctx->stream>>>(n, upts, U, cell, eps_dedup, gks.p, gis.p, state.p, ctr.p);
+                PT_TRY(pt_check_launch(ctx, "pt_dedup_round_kernel"));
+            }
+            ++rounds;
+            PT_TRY(pt_read_fine_counters(ctx, ctr.p, &hc, rg));
+            if (hc.undecided == 0) break;
+            if (rounds > 100000) return pt_fail(ctx, PT_E_STATE, "eps-dedup did not converge");
+        }
+        // compact the kept points, order preserved
+        PtBuf<uint8_t> flag; PtBuf<uint32_t> iota; PtBuf<long long> nsel;
+        PT_TRY(flag.alloc(ctx, U)); PT_TRY(iota.alloc(ctx, U)); PT_TRY(sel.alloc(ctx, U)); PT_TRY(nsel.alloc(ctx, 1));
+        pt_flag_kept_kernel<<<pt_grid_for(U, 256), 256, 0, ctx->stream>>>(state.p, U, flag.p);
+        PT_TRY(pt_check_launch(ctx, "pt_flag_kept_kernel"));
+        pt_iota32_kernel<<<pt_grid_for(U, 256), 256, 0, ctx->stream>>>(iota.p, U);
+        PT_TRY(pt_check_launch(ctx, "pt_iota32_kernel"));
+        size_t tb2 = 0;
+        cub::DeviceSelect::Flagged(nullptr, tb2, iota.p, flag.p, sel.p, nsel.p, (long long)U, ctx->stream);
+        PT_TRY(tmp.alloc(ctx, tb2));
+        {
+            PT_LAUNCH(ctx, "dedup_compact");
+            PT_CUDA(ctx, cub::DeviceSelect::Flagged(tmp.p, tb2, iota.p, flag.p, sel.p, nsel.p, (long long)U, ctx->stream));
+            ctx->launches++;
+        }
+        long long* h = (long long*)ctx->pinned;
+        PT_CUDA(ctx, cudaMemcpyAsync(h, nsel.p, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+        PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        P = (size_t)*h;
+    }
+    r->stats.dedup_rounds = rounds;
+    r->n_points = (long long)P;
+    r->stats.points = (long long)P;
+    PT_TRY(r->points.alloc(ctx, (P > 0 ? P : 1) * n));
+    PT_TRY(r->labels.alloc(ctx, P > 0 ? P : 1));
+    PT_TRY(r->first_tag.alloc(ctx, P > 0 ? P : 1));
+    if (P > 0) {
+        PT_LAUNCH(ctx, "refine_gather");
+        pt_gather_points_kernel<<<pt_grid_for(P, 256), 256, 0, ctx->stream>>>(n, upts, vals, sel.p, P, r->points.p, r->first_tag.p);
+        PT_TRY(pt_check_launch(ctx, "pt_gather_points_kernel"));
+    }
 
-int pt_refine_run(pt_ctx* ctx, const pt_field* field, const pt_cells* cells, int n, double scale, const double* offset, int k,
-                  int V, const int32_t* tv_host, int E, const int32_t* te_host, double eps, double eps_dedup,
-                  const pt_checker* checker, const long long* batch_bounds, int nb, pt_refine** out) {
+    // ---- R6: labels --------------------------------------------------------------------------
+    PT_CUDA(ctx, cudaMemsetAsync(r->labels.p, 0, P > 0 ? P : 1, ctx->stream));
+    if (checker && P > 0) {
+        PT_TRY(pt_checker_run_dev(ctx, checker, r->points.p, P, PT_LIMIT_UNFREE, r->labels.p, nullptr));
+        PtBuf<unsigned long long> nh;
+        PT_TRY(nh.alloc(ctx, 1));
+        PT_CUDA(ctx, cudaMemsetAsync(nh.p, 0, sizeof(unsigned long long), ctx->stream));
+        pt_count_labels_kernel<<<pt_grid_for(P, 256), 256, 0, ctx->stream>>>(r->labels.p, P, nh.p);
+        PT_TRY(pt_check_launch(ctx, "pt_count_labels_kernel"));
+        unsigned long long* h = (unsigned long long*)ctx->pinned;
+        PT_CUDA(ctx, cudaMemcpyAsync(h, nh.p, sizeof(*h), cudaMemcpyDeviceToHost, ctx->stream));
+        PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        r->stats.in_collision = (long long)*h;
+        r->stats.free_points = (long long)P - r->stats.in_collision;
+    } else {
+        r->stats.free_points = (long long)P;
+    }
+
+    return PT_OK;
+}
+
+static int pt_refine_impl(pt_ctx* ctx, const pt_field* field, const pt_cells* cells, int n, double scale, const double* offset, int k,
+                          int V, const int32_t* tv_host, int E, const int32_t* te_host, double eps, double eps_dedup,
+                          const pt_checker* checker, const long long* batch_bounds, int nb, bool candidates_only,
+                          pt_refine** out) {
     if (!ctx || !field || !cells || !out) return pt_fail(ctx, PT_E_INVALID, "pt_refine_run: NULL argument");
     if (cells->n != n || pt_field_dim(field) != n) return pt_fail(ctx, PT_E_INVALID, "template and lattice dimension mismatch");
     if (k < 1 || k > 64) return pt_fail(ctx, PT_E_INVALID, "subdivision factor must be in 1..64");
@@ -536,92 +636,25 @@ int pt_refine_run(pt_ctx* ctx, const pt_field* field, const pt_cells* cells, int
         }
     }
 
-    // ---- R5: greedy eps-dedup in first-occurrence order ---------------------------------------
-    PtBuf<uint8_t> state;
-    PT_TRY(state.alloc(ctx, U > 0 ? U : 1));
-    long long rounds = 0;
-    size_t P = 0;
-    PtBuf<uint32_t> sel;
-    if (U > 0) {
-        if (U >= (1ull << 32)) return pt_fail(ctx, PT_E_NOMEM, "more than 2^32 distinct fine edges in one refine call");
-        PT_CUDA(ctx, cudaMemsetAsync(state.p, PT_DD_UNDECIDED, U, ctx->stream));
-        const double cell = 16.0 * eps_dedup;
-        PtBuf<u64> gk, gks; PtBuf<uint32_t> gi, gis;
-        PT_TRY(gk.alloc(ctx, U)); PT_TRY(gks.alloc(ctx, U)); PT_TRY(gi.alloc(ctx, U)); PT_TRY(gis.alloc(ctx, U));
-        {
-            PT_LAUNCH(ctx, "dedup_hash");
-            pt_dedup_hash_kernel<<<pt_grid_for(U, 256), 256, 0, ctx->stream>>>(n, upts.p, U, cell, gk.p, gi.p);
-            PT_TRY(pt_check_launch(ctx, "pt_dedup_hash_kernel"));
+    // ---- R5 + R6: greedy eps-dedup in first-occurrence order, labels --------------------------------
+    if (candidates_only) {
+        // hand back the root-solved points of the distinct fine edges (multi-GPU merge happens upstream)
+        r->n_points = (long long)U;
+        r->stats.points = (long long)U;
+        PT_TRY(r->points.alloc(ctx, (U > 0 ? U : 1) * n));
+        PT_TRY(r->labels.alloc(ctx, U > 0 ? U : 1));
+        PT_TRY(r->first_tag.alloc(ctx, U > 0 ? U : 1));
+        PT_CUDA(ctx, cudaMemsetAsync(r->labels.p, 0, U > 0 ? U : 1, ctx->stream));
+        if (U > 0) {
+            PtBuf<uint32_t> iota;
+            PT_TRY(iota.alloc(ctx, U));
+            pt_iota32_kernel<<<pt_grid_for(U, 256), 256, 0, ctx->stream>>>(iota.p, U);
+            PT_TRY(pt_check_launch(ctx, "pt_iota32_kernel"));
+            pt_gather_points_kernel<<<pt_grid_for(U, 256), 256, 0, ctx->stream>>>(n, upts.p, vals.p, iota.p, U, r->points.p, r->first_tag.p);
+            PT_TRY(pt_check_launch(ctx, "pt_gather_points_kernel"));
         }
-        size_t tb = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, tb, gk.p, gks.p, gi.p, gis.p, (long long)U, 0, 64, ctx->stream);
-        PtBuf<uint8_t> tmp;
-        PT_TRY(tmp.alloc(ctx, tb));
-        {
-            PT_LAUNCH(ctx, "dedup_sort");
-            PT_CUDA(ctx, cub::DeviceRadixSort::SortPairs(tmp.p, tb, gk.p, gks.p, gi.p, gis.p, (long long)U, 0, 64, ctx->stream));
-            ctx->launches++;
-        }
-        for (;;) {
-            PT_CUDA(ctx, cudaMemsetAsync(&ctr.p->undecided, 0, sizeof(unsigned long long), ctx->stream));
-            {
-                PT_LAUNCH(ctx, "dedup_round");
-                pt_dedup_round_kernel<<<pt_grid_for(U, 128), 128, 0, ctx->stream>>>(n, upts.p, U, cell, eps_dedup, gks.p, gis.p, state.p, ctr.p);
-                PT_TRY(pt_check_launch(ctx, "pt_dedup_round_kernel"));
-            }
-            ++rounds;
-            PT_TRY(pt_read_fine_counters(ctx, ctr.p, &hc, rg));
-            if (hc.undecided == 0) break;
-            if (rounds > 100000) return pt_fail(ctx, PT_E_STATE, "eps-dedup did not converge");
-        }
-        // compact the kept points, order preserved
-        PtBuf<uint8_t> flag; PtBuf<uint32_t> iota; PtBuf<long long> nsel;
-        PT_TRY(flag.alloc(ctx, U)); PT_TRY(iota.alloc(ctx, U)); PT_TRY(sel.alloc(ctx, U)); PT_TRY(nsel.alloc(ctx, 1));
-        pt_flag_kept_kernel<<<pt_grid_for(U, 256), 256, 0, ctx->stream>>>(state.p, U, flag.p);
-        PT_TRY(pt_check_launch(ctx, "pt_flag_kept_kernel"));
-        pt_iota32_kernel<<<pt_grid_for(U, 256), 256, 0, ctx->stream>>>(iota.p, U);
-        PT_TRY(pt_check_launch(ctx, "pt_iota32_kernel"));
-        size_t tb2 = 0;
-        cub::DeviceSelect::Flagged(nullptr, tb2, iota.p, flag.p, sel.p, nsel.p, (long long)U, ctx->stream);
-        PT_TRY(tmp.alloc(ctx, tb2));
-        {
-            PT_LAUNCH(ctx, "dedup_compact");
-            PT_CUDA(ctx, cub::DeviceSelect::Flagged(tmp.p, tb2, iota.p, flag.p, sel.p, nsel.p, (long long)U, ctx->stream));
-            ctx->launches++;
-        }
-        long long* h = (long long*)ctx->pinned;
-        PT_CUDA(ctx, cudaMemcpyAsync(h, nsel.p, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
-        PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-        P = (size_t)*h;
-    }
-    r->stats.dedup_rounds = rounds;
-    r->n_points = (long long)P;
-    r->stats.points = (long long)P;
-    PT_TRY(r->points.alloc(ctx, (P > 0 ? P : 1) * n));
-    PT_TRY(r->labels.alloc(ctx, P > 0 ? P : 1));
-    PT_TRY(r->first_tag.alloc(ctx, P > 0 ? P : 1));
-    if (P > 0) {
-        PT_LAUNCH(ctx, "refine_gather");
-        pt_gather_points_kernel<<<pt_grid_for(P, 256), 256, 0, ctx->stream>>>(n, upts.p, vals.p, sel.p, P, r->points.p, r->first_tag.p);
-        PT_TRY(pt_check_launch(ctx, "pt_gather_points_kernel"));
-    }
-
-    // ---- R6: labels --------------------------------------------------------------------------
-    PT_CUDA(ctx, cudaMemsetAsync(r->labels.p, 0, P > 0 ? P : 1, ctx->stream));
-    if (checker && P > 0) {
-        PT_TRY(pt_checker_run_dev(ctx, checker, r->points.p, P, PT_LIMIT_UNFREE, r->labels.p, nullptr));
-        PtBuf<unsigned long long> nh;
-        PT_TRY(nh.alloc(ctx, 1));
-        PT_CUDA(ctx, cudaMemsetAsync(nh.p, 0, sizeof(unsigned long long), ctx->stream));
-        pt_count_labels_kernel<<<pt_grid_for(P, 256), 256, 0, ctx->stream>>>(r->labels.p, P, nh.p);
-        PT_TRY(pt_check_launch(ctx, "pt_count_labels_kernel"));
-        unsigned long long* h = (unsigned long long*)ctx->pinned;
-        PT_CUDA(ctx, cudaMemcpyAsync(h, nh.p, sizeof(*h), cudaMemcpyDeviceToHost, ctx->stream));
-        PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-        r->stats.in_collision = (long long)*h;
-        r->stats.free_points = (long long)P - r->stats.in_collision;
     } else {
-        r->stats.free_points = (long long)P;
+        PT_TRY(pt_dedup_label_impl(ctx, n, upts.p, vals.p, U, eps_dedup, checker, r));
     }
 
     // ---- per-batch statistics ------------------------------------------------------------------
@@ -634,6 +667,7 @@ int pt_refine_run(pt_ctx* ctx, const pt_field* field, const pt_cells* cells, int
         }
         PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
         std::vector<unsigned long long> bins((size_t)nb, 0);
+        const size_t P = (size_t)r->n_points;
         if (P > 0) {
             PtBuf<unsigned long long> db, dbins;
             PT_TRY(db.alloc(ctx, (size_t)nb + 1));
@@ -652,6 +686,40 @@ int pt_refine_run(pt_ctx* ctx, const pt_field* field, const pt_cells* cells, int
     }
     PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     guard.keep = true;
+    *out = r;
+    return PT_OK;
+}
+
+extern "C" {
+
+int pt_refine_run(pt_ctx* ctx, const pt_field* field, const pt_cells* cells, int n, double scale, const double* offset, int k,
+                  int V, const int32_t* tv_host, int E, const int32_t* te_host, double eps, double eps_dedup,
+                  const pt_checker* checker, const long long* batch_bounds, int nb, pt_refine** out) {
+    return pt_refine_impl(ctx, field, cells, n, scale, offset, k, V, tv_host, E, te_host, eps, eps_dedup, checker,
+                          batch_bounds, nb, false, out);
+}
+
+int pt_refine_candidates(pt_ctx* ctx, const pt_field* field, const pt_cells* cells, int n, double scale, const double* offset,
+                         int k, int V, const int32_t* tv_host, int E, const int32_t* te_host, double eps, pt_refine** out) {
+    return pt_refine_impl(ctx, field, cells, n, scale, offset, k, V, tv_host, E, te_host, eps, 1.0, nullptr, nullptr, 0, true, out);
+}
+
+int pt_dedup_label(pt_ctx* ctx, int n, const double* points, long long count, double eps_dedup, const pt_checker* checker,
+                   pt_refine** out) {
+    if (!ctx || !out) return pt_fail(ctx, PT_E_INVALID, "pt_dedup_label: NULL argument");
+    if (n < 2 || n > 7) return pt_fail(ctx, PT_E_INVALID, "dimension %d unsupported (2..7)", n);
+    if (count < 0) return pt_fail(ctx, PT_E_INVALID, "negative point count");
+    if (!(eps_dedup > 0.0)) return pt_fail(ctx, PT_E_INVALID, "eps_dedup must be positive");
+    if (count > 0 && !points) return pt_fail(ctx, PT_E_INVALID, "points is NULL");
+    pt_refine* r = new pt_refine();
+    r->ctx = ctx; r->n = n;
+    memset(&r->stats, 0, sizeof(r->stats));
+    PtBuf<double> tmp;
+    const double* pdev;
+    int rc = pt_stage_in(ctx, points, (size_t)count * n, tmp, &pdev);
+    if (rc == PT_OK) rc = pt_dedup_label_impl(ctx, n, pdev, nullptr, (size_t)count, eps_dedup, checker, r);
+    if (rc == PT_OK) rc = (cudaStreamSynchronize(ctx->stream) == cudaSuccess) ? PT_OK : pt_fail(ctx, PT_E_CUDA, "dedup failed");
+    if (rc != PT_OK) { delete r; return rc; }
     *out = r;
     return PT_OK;
 }

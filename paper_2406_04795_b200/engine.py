@@ -48,7 +48,7 @@ class DevicePipeline:
 
     def step(self, seeds_ptr: int, m: int) -> dict:
         lib, ctx, n = _cabi.lib, self.ctx, self.n
-        work = np.zeros(4, dtype=np.int64)
+        work = np.zeros(6, dtype=np.int64)
         _cabi.check(lib.pt_ctx_work_counters(ctx.handle, work.ctypes.data, 1))
         trace = C.c_void_p()
         _cabi.check(lib.pt_trace_create(
@@ -94,6 +94,7 @@ class DevicePipeline:
                 "simplices_local": (edges if self.world == 1 else 0) + int(rs.crossing_edges),
                 "pair_evals_bisect": int(work[0]) * self.support, "pair_evals_eval": int(work[1]) * self.support,
                 "pair_evals_fp32": int(work[2]) * self.support, "bisect_fallbacks": int(work[3]),
+                "pair_evals_rest": int(work[4]) * self.support, "pair_evals_resolve": int(work[5]) * self.support,
             }
         finally:
             if ref:

@@ -1,0 +1,139 @@
+"""world_size-2 (and 3) gloo tests of the multi-GPU exchange logic on the CPU.
+
+The driver `distributed.ShardedProof` is the product code; the rank-local compute is supplied by an
+oracle-backed engine (test infrastructure) so the test needs no GPU.  What is checked: the slices
+tile the cell list, crossing offsets are the exclusive scan over ranks, the merged candidate list is
+in global first-crossing order, and the final point set / labels equal the single-process reference
+result (golden vectors of the real reference)."""
+
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from tests.conftest import Golden, oracle_model, robot_scene_dicts, trace_inputs
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+class OracleEngine:
+    """Engine protocol of distributed.ShardedProof on top of the CPU oracle."""
+
+    tensor_device = torch.device("cpu")
+
+    def __init__(self, tag="kclf_n3"):
+        from oracle import permatrace_oracle as O
+        from tests.test_oracle_golden import oracle_field
+        self.O = O
+        g = Golden("traces")
+        self.g, self.tag = g, tag
+        self.inp = trace_inputs(g, tag)
+        self.n = self.inp["n"]
+        self.field = oracle_field(g, tag)
+        self.template = O.build_template(self.n, 2)
+        self.robot, self.scene = oracle_model(*robot_scene_dicts(self.n, 3))
+        self.eps_dedup = self.inp["scale"] / 40.0
+
+    def trace(self, seeds):
+        O, inp = self.O, self.inp
+        t = O.Trace(self.field, self.n, inp["scale"], inp["offset"], inp["box"], inp["max_edges"], inp["eps"]).run(seeds)
+        self.cells = O.coarse_cells(t.edges)
+        return dict(trace_edges=len(t.edges), cells=len(self.cells), closure_ok=t.closure_ok)
+
+    def candidates(self, first, count):
+        pts = self.O.crossing_points(self.cells[first:first + count], self.template, self.field, self.inp["scale"],
+                                     self.inp["offset"], self.inp["eps"])
+        return torch.from_numpy(np.ascontiguousarray(pts)), int(pts.shape[0])
+
+    def dedup_label(self, points):
+        reg = self.O.PointRegistry(self.eps_dedup, self.n)
+        kept = [i for i, p in enumerate(points.numpy()) if reg.add(p) is not None]
+        kept_pts = points.numpy()[kept] if kept else np.zeros((0, self.n))
+        labels = self.O.not_free(self.robot, self.scene, kept_pts) if kept else np.zeros(0, dtype=bool)
+        return torch.tensor(kept, dtype=torch.int64), torch.from_numpy(labels.astype(np.uint8))
+
+
+def _worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2406_04795_b200.distributed import ShardedProof
+        eng = OracleEngine()
+        res = ShardedProof(eng).run(eng.inp["seeds"])
+        out[rank] = dict(points=res["points"].numpy(), labels=res["in_collision"].numpy(), crossing=res["crossing_edges"],
+                         local=res["crossing_edges_local"], offsets=list(res["crossing_offsets"]), slice=res["slice"],
+                         cells=res["cells"], edges=res["trace_edges"], candidates=res["candidates"])
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_refine_equals_single_process_reference(world):
+    g = Golden("traces")
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    want_pts, want_lab = g["kclf_n3_refine_points"], g["kclf_n3_refine_labels"]
+    total = int(g["kclf_n3_refine_batches"][:, 2].sum())
+    covered = 0
+    for r in range(world):
+        res = out[r]
+        assert res["points"].shape == want_pts.shape
+        assert np.allclose(res["points"], want_pts, rtol=0, atol=1e-8)        # every rank ends with the same answer
+        assert np.array_equal(res["labels"], want_lab)
+        assert res["crossing"] == total and res["edges"] == 324
+        assert res["offsets"][r] == sum(out[q]["local"] for q in range(r))     # exclusive scan over ranks
+        first, count = res["slice"]
+        assert first == covered
+        covered += count
+    assert covered == out[0]["cells"]
+    assert sum(out[r]["local"] for r in range(world)) == total
+
+
+def test_cell_slices_tile_and_owner_hash_is_balanced():
+    from paper_2406_04795_b200.distributed import cell_slice, owner_of_cell
+    for total in (0, 1, 7, 1000, 1298072):
+        for world in (1, 2, 3, 8):
+            at = 0
+            for r in range(world):
+                first, count = cell_slice(total, r, world)
+                assert first == at and count >= 0
+                at += count
+            assert at == total
+            sizes = [cell_slice(total, r, world)[1] for r in range(world)]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        cell_slice(10, 2, 2)
+    rng = np.random.default_rng(0)
+    base = rng.integers(-40, 40, size=(20000, 6))
+    own = owner_of_cell(base, 8)
+    assert own.min() == 0 and own.max() == 7
+    assert np.bincount(own, minlength=8).min() > 2000           # 2500 expected per rank
+    assert np.array_equal(own, owner_of_cell(base, 8))          # deterministic
+
+
+def test_single_process_driver_matches_reference():
+    """world = 1 path of the same driver (no process group)."""
+    from paper_2406_04795_b200.distributed import ShardedProof
+    g = Golden("traces")
+    eng = OracleEngine()
+    res = ShardedProof(eng).run(eng.inp["seeds"])
+    assert np.allclose(res["points"].numpy(), g["kclf_n3_refine_points"], rtol=0, atol=1e-8)
+    assert np.array_equal(res["in_collision"].numpy(), g["kclf_n3_refine_labels"])

@@ -443,3 +443,42 @@ def test_dof6_full_size_properties():
     order = np.lexsort(keys.T[::-1])
     assert np.array_equal(order, np.arange(len(order)))       # sorted, hence unique
     assert len(cells) > 10 * st.visited_edges
+
+
+# ---- device pipeline and the sharded driver on one GPU -----------------------------------------------------
+def test_device_pipeline_and_sharded_driver_agree_with_public_api(golden):
+    from paper_2406_04795_b200 import engine
+    from paper_2406_04795_b200.distributed import CudaEngine, ShardedProof
+    import torch
+    g = golden("traces")
+    tag, n = "kclf_n4", 4
+    inp = trace_inputs(g, tag)
+    m, cfg = product_manifold(g, tag), product_cfg(inp)
+    rd, sd = robot_scene_dicts(n, 3)
+
+    class Prob:
+        robot, scene = CO.robot_from_dict(rd), CO.scene_from_dict(sd)
+
+    checker = P.not_free_checker(Prob)
+    template = S.build_template(n, 2)
+    res = T.trace(inp["seeds"], m, cfg)
+    ref = S.refine(S.coarse_cells(res), template, m, checker, cfg)
+    seeds = torch.from_numpy(inp["seeds"]).cuda()
+    counts = engine.DevicePipeline(m, cfg, template, checker).step(seeds.data_ptr(), seeds.shape[0])
+    assert counts["trace_edges"] == len(res.edges) and counts["points"] == ref.points.shape[0]
+    assert counts["crossing_edges"] == sum(b.crossing_edges for b in ref.batch_stats)
+    assert counts["free_points"] == int((~ref.in_collision).sum())
+    out = ShardedProof(CudaEngine(m, cfg, template, checker)).run(seeds)
+    assert np.array_equal(out["points"].cpu().numpy(), ref.points)
+    assert np.array_equal(out["in_collision"].cpu().numpy(), ref.in_collision)
+    assert out["crossing_edges"] == counts["crossing_edges"] and out["cells"] == counts["cells"]
+    # two "virtual ranks" on one device: slices merged by hand reproduce the same result
+    eng = CudaEngine(m, cfg, template, checker)
+    info = eng.trace(seeds)
+    from paper_2406_04795_b200.distributed import cell_slice
+    parts = [eng.candidates(*cell_slice(info["cells"], r, 3)) for r in range(3)]
+    merged = torch.cat([p for p, _ in parts], dim=0)
+    kept, labels = eng.dedup_label(merged)
+    assert np.array_equal(merged[kept].cpu().numpy(), ref.points)
+    assert np.array_equal(labels.cpu().numpy().astype(bool), ref.in_collision)
+    assert sum(c for _, c in parts) == counts["crossing_edges"]
