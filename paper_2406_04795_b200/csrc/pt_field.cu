@@ -256,6 +256,7 @@ __global__ void pt_bisect_analytic_kernel(PtFieldDev f, const double* __restrict
 //                             their (always true) bisection bracket.
 #define PT_TILE32 512
 #define PT_HANDOFF_WIDTH 0.0078125   /* 2^-7: brackets wider than this never enter K3 */
+#define PT_FP32_STOP_WIDTH 0.001953125 /* 2^-9: fp32 screening stops here; deeper levels are mostly uncertain anyway */
 
 template <int N> struct PtRow32 { static const int value = (N + 2 + 3) & ~3; };
 
@@ -415,7 +416,8 @@ pt_bisect32_kernel(PtFieldDev f, PtRows rows, const double* __restrict__ a_, con
             if (fabs(F) > E) {
                 if ((F > 0.0 ? 1 : -1) == sa) lo = mid; else hi = mid;
                 ++iters;
-                active = __dmul_rn(seg, __dsub_rn(hi, lo)) > eps;
+                const double w = __dsub_rn(hi, lo);
+                active = __dmul_rn(seg, w) > eps && w > PT_FP32_STOP_WIDTH;
             } else {
                 active = false;   // sign not certain in fp32 (or NaN): stop with the current bracket
             }

@@ -40,7 +40,10 @@ int pt_table_init(pt_ctx* ctx, PtHashTable& t, u64 capacity) {
 }
 
 int pt_table_reserve(pt_ctx* ctx, PtHashTable& t, u64 extra) {
-    u64 need = 2 * (t.count + extra);
+    // worst case every one of `extra` probes inserts a new key: the table must never fill up
+    // (count + extra <= capacity); the usual case inserts far fewer, keep the load at <= 1/2 for it
+    u64 need = t.count + extra + (t.count + extra) / 8;
+    if (need < 2 * t.count + 1024) need = 2 * t.count + 1024;
     if (need <= t.capacity) return PT_OK;
     u64 cap = t.capacity;
     while (cap < need) cap <<= 1;
@@ -158,8 +161,8 @@ __global__ void pt_cell_edges_kernel(PtGeom g, PtTable sgn, PtTable vis, const i
                 if (pt_in_box(g, va) && pt_in_box(g, vb)) {
                     bool ins;
                     u64 slot = pt_table_insert(vis, pt_edge_key(g, ka, mask), ins, &ctr->error);
-                    atomicMin(&vis.ent[2 * slot + 1], PT_VAL_PENDING_BASE + (u64)tid);
-                    marker = (uint32_t)slot | (sa > 0 ? 0x80000000u : 0u);
+                    const u64 mine = PT_VAL_PENDING_BASE + (u64)tid;
+                    if (atomicMin(&vis.ent[2 * slot + 1], mine) > mine) marker = (uint32_t)slot | (sa > 0 ? 0x80000000u : 0u);
                 } else {
                     atomicAdd(&ctr->dropped, 1ull);
                 }
@@ -269,8 +272,11 @@ pt_wave_partner_kernel(PtGeom g, PtTable sgn, PtTable vis, const u64* __restrict
                 else {
                     bool ins;
                     u64 slot = pt_table_insert(vis, pt_edge_key(g, bk, p.mask), ins, &ctr->error);
-                    atomicMin(&vis.ent[2 * slot + 1], PT_VAL_PENDING_BASE + (u64)(w * stride + j));
-                    marker = (uint32_t)slot | (p.sign_base > 0 ? 0x80000000u : 0u);
+                    const u64 mine = PT_VAL_PENDING_BASE + (u64)(w * stride + j);
+                    const u64 old = atomicMin(&vis.ent[2 * slot + 1], mine);
+                    // an already admitted edge or a smaller pending slot beats this candidate for good:
+                    // only candidates that lowered the value stay in the winner scan
+                    if (old > mine) marker = (uint32_t)slot | (p.sign_base > 0 ? 0x80000000u : 0u);
                 }
             }
         }
@@ -535,8 +541,8 @@ static int pt_trace_expand_impl(pt_trace* t, long long* frontier_out) {
     const int stride = pt_stride_for(g.n);
     const long long before = t->n_edges;
     const unsigned long long cand_before = t->host_counters.candidates;
-    // chunk the frontier so the per-slot scratch stays bounded (~2^26 slots)
-    size_t chunk_edges = ((size_t)1 << 26) / (size_t)stride;
+    // chunk the frontier: bounds the per-slot scratch and the worst-case table growth per chunk (~2^24 slots)
+    size_t chunk_edges = ((size_t)1 << 24) / (size_t)stride;
     if (chunk_edges < 1024) chunk_edges = 1024;
     PtBuf<uint32_t> sgn_slot, vis_slot, pending;
     // the frontier buffer is replaced at the end; chunks read the current one

@@ -237,16 +237,27 @@ class BatchStat:
     check_seconds: float
 
 
-@dataclass
 class RefinedResult:
-    """Deduplicated fine intersection points with in-collision labels."""
+    """Deduplicated fine intersection points with in-collision labels (reference
+    subdivision.py:184-192).  `free_points` is materialised on first access."""
 
-    points: np.ndarray
-    in_collision: np.ndarray
-    free_points: np.ndarray
-    eps_dedup: float
-    batch_stats: list[BatchStat]
-    device_stats: dict | None = None
+    def __init__(self, points, in_collision, free_points=None, eps_dedup=0.0, batch_stats=None, device_stats=None):
+        self.points = points
+        self.in_collision = in_collision
+        self._free_points = free_points
+        self.eps_dedup = eps_dedup
+        self.batch_stats = batch_stats if batch_stats is not None else []
+        self.device_stats = device_stats
+
+    @property
+    def free_points(self) -> np.ndarray:
+        if self._free_points is None:
+            self._free_points = self.points[~self.in_collision] if self.points.size else self.points.copy()
+        return self._free_points
+
+    def __repr__(self):
+        return (f"RefinedResult(points={self.points.shape}, in_collision={int(self.in_collision.sum())}, "
+                f"eps_dedup={self.eps_dedup!r}, batches={len(self.batch_stats)})")
 
 
 class _RefineHandle:
@@ -310,11 +321,10 @@ def refine(cells, template: SubdivisionTemplate, manifold, checker, cfg: TraceCo
     st = _cabi.RefineStats()
     _cabi.check(_cabi.lib.pt_refine_get_stats(res.handle, C.byref(st)))
     total = int(st.points)
-    points = np.zeros((total, n), dtype=np.float64)
-    labels = np.zeros(total, dtype=np.uint8)
-    tags = np.zeros(total, dtype=np.int64)
+    points = np.empty((total, n), dtype=np.float64)
+    labels = np.empty(total, dtype=np.uint8)
     if total:
-        _cabi.check(_cabi.lib.pt_refine_points(res.handle, points.ctypes.data, labels.ctypes.data, tags.ctypes.data))
+        _cabi.check(_cabi.lib.pt_refine_points(res.handle, points.ctypes.data, labels.ctypes.data, None))
     rows = np.zeros((max(nb, 1), 2), dtype=np.int64)
     if nb:
         _cabi.check(_cabi.lib.pt_refine_batch_stats(res.handle, rows.ctypes.data, nb))
@@ -337,12 +347,11 @@ def refine(cells, template: SubdivisionTemplate, manifold, checker, cfg: TraceCo
                     raise RefineError(f"checker returned shape {hit.shape} in batch {bi}")
                 labels[at:at + fresh] = hit
             at += fresh
-    in_collision = labels.astype(bool)
+    in_collision = labels.view(np.bool_) if labels.dtype == np.uint8 else labels.astype(bool)
     stats = [
         BatchStat(bi, bounds[bi + 1] - bounds[bi], (bounds[bi + 1] - bounds[bi]) * tv.shape[0],
                   int(rows[bi, 0]), int(rows[bi, 1]), seconds[bi])
         for bi in range(nb)
     ]
-    free_points = points[~in_collision] if points.size else points.copy()
     device_stats = {name: int(getattr(st, name)) for name, _ in _cabi.RefineStats._fields_}
-    return RefinedResult(points, in_collision, free_points, float(eps_dedup), stats, device_stats)
+    return RefinedResult(points, in_collision, None, float(eps_dedup), stats, device_stats)
