@@ -149,48 +149,82 @@ def build_workload(name: str):
 # ------------------------------------------------------------------------------------------------
 
 class ClockSampler:
+    """SM clock / throttle-reason samples DURING the timed region (NVML in-process, 50 ms period;
+    falls back to one `nvidia-smi -lms 200` child if NVML is unavailable)."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
     QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device: int):
-        self.device, self.rows, self.proc = device, [], None
+        self.device, self.sm, self.mx, self.reasons, self.power = device, [], [], set(), []
+        self.stop = threading.Event()
+        self.thread = self.proc = None
 
-    def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
-                                          "-i", str(self.device), "-lms", "100"], stdout=subprocess.PIPE, text=True)
-            self.thread = threading.Thread(target=self._pump, daemon=True)
-            self.thread.start()
-        except OSError:
-            self.proc = None
-        return self
-
-    def _pump(self):
-        for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
-
-    def __exit__(self, *exc):
-        if self.proc is not None:
-            time.sleep(0.15)
-            self.proc.terminate()
-            self.thread.join(timeout=2)
-
-    def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
+    def _nvml_loop(self, nvml, handle):
+        while not self.stop.is_set():
             try:
-                sm.append(float(r[1])); mx.append(float(r[2]))
+                self.sm.append(float(nvml.nvmlDeviceGetClockInfo(handle, nvml.NVML_CLOCK_SM)))
+                self.mx.append(float(nvml.nvmlDeviceGetMaxClockInfo(handle, nvml.NVML_CLOCK_SM)))
+                self.power.append(nvml.nvmlDeviceGetPowerUsage(handle) / 1000.0)
+                mask = nvml.nvmlDeviceGetCurrentClocksThrottleReasons(handle)
+                for bit, name in self.REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self.stop.wait(0.05)
+
+    def _smi_loop(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.proc.stdout:
+            r = [c.strip() for c in line.split(",")]
+            try:
+                self.sm.append(float(r[1])); self.mx.append(float(r[2]))
             except (ValueError, IndexError):
                 continue
             for nm, val in zip(names, r[5:9]):
                 if val.lower().startswith("active"):
-                    reasons.add(nm)
-        if not sm:
+                    self.reasons.add(nm)
+
+    def __enter__(self):
+        try:
+            import pynvml as nvml
+            nvml.nvmlInit()
+            uuid_index = self.device
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis:
+                uuid_index = int(vis.split(",")[self.device]) if vis.split(",")[self.device].isdigit() else self.device
+            handle = nvml.nvmlDeviceGetHandleByIndex(uuid_index)
+            self.thread = threading.Thread(target=self._nvml_loop, args=(nvml, handle), daemon=True)
+            self.thread.start()
+        except Exception:
+            try:
+                self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                                              "-i", str(self.device), "-lms", "200"], stdout=subprocess.PIPE, text=True)
+                self.thread = threading.Thread(target=self._smi_loop, daemon=True)
+                self.thread.start()
+            except OSError:
+                self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.stop.set()
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(np.max(mx)), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        out = {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": float(np.max(self.mx)), "reasons": sorted(self.reasons),
+               "samples": len(self.sm)}
+        if self.power:
+            out["power_w_max"] = float(np.max(self.power))
+        return out
 
 
 # ------------------------------------------------------------------------------------------------

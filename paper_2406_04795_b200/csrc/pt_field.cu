@@ -592,19 +592,35 @@ pt_bisect_newton_kernel(PtFieldDev f, double sum_abs_w, const double* __restrict
         m3 *= 1.5;
         const bool monotone = need && fabs(D1) > width * fabs(D2) + 0.5 * width * width * m3;
         if (need && !monotone) { to_slow = true; need = false; }
-        // Newton from the midpoint, then secant on the last two evaluated points; an iterate is used
-        // without being evaluated once its predicted error is far below the final cell width
+        // Root location: a Halley step from the midpoint (uses F''), a Newton step with the extrapolated
+        // derivative F'(m) + F''(m)(x - m), then plain secant if ever needed.  An iterate is used WITHOUT
+        // being evaluated once its predicted error is far below the final cell width.
         const double slope = fabs(D1) + 1e-300;
+        const double e0 = fabs(F0) / slope;                       // ~ distance from the midpoint to the root
+        const double curv = fabs(D2) / slope;
+        const double c3 = m3 / (6.0 * slope) + 0.5 * curv * curv;  // cubic error constant of the Halley step
         double x0 = mid, f0 = F0, x1 = mid, f1 = F0, x2 = mid;
-        double e_prev = width, e_cur = fabs(F0) / slope;
+        double e_prev = width, e_cur = e0;
         bool searching = need;
-        bool first = true;
+        int stage = 0;
         for (int it = 0; it < 8; ++it) {
             if (searching) {
-                if (first) x2 = mid - F0 / D1;
-                else { const double den = f1 - f0; x2 = (den != 0.0) ? x1 - f1 * ((x1 - x0) / den) : 0.5 * (lo + hi); }
-                if (!(x2 > lo && x2 < hi)) x2 = 0.5 * (lo + hi);
-                const double predicted = first ? 10.0 * e_cur * e_cur : 10.0 * e_cur * e_prev;
+                double predicted;
+                if (stage == 0) {
+                    const double nt = F0 / D1;
+                    x2 = mid - nt * (1.0 + 0.5 * nt * (D2 / D1));
+                    predicted = 4.0 * c3 * e0 * e0 * e0;
+                } else if (stage == 1) {
+                    const double dest = D1 + D2 * (x1 - mid);
+                    x2 = x1 - f1 / dest;
+                    // derivative estimate is off by <= m3 w^2 / 2 relative to slope; Newton's own term is quadratic
+                    predicted = 4.0 * e_cur * (0.5 * m3 * width * width / slope + curv * e_cur);
+                } else {
+                    const double den = f1 - f0;
+                    x2 = (den != 0.0) ? x1 - f1 * ((x1 - x0) / den) : 0.5 * (lo + hi);
+                    predicted = 10.0 * e_cur * e_prev;
+                }
+                if (!(x2 > lo && x2 < hi)) { x2 = 0.5 * (lo + hi); predicted = width; }
                 if (predicted < 0.0625 * delta) searching = false;
             }
             if (!__syncthreads_or(searching ? 1 : 0)) break;
@@ -612,7 +628,7 @@ pt_bisect_newton_kernel(PtFieldDev f, double sum_abs_w, const double* __restrict
             if (searching) {
                 x0 = x1; f0 = f1; x1 = x2; f1 = f2;
                 e_prev = e_cur; e_cur = fabs(f2) / slope;
-                first = false;
+                ++stage;
             }
         }
         if (searching) { to_slow = true; need = false; }   // did not converge in 8 evaluations
@@ -666,9 +682,9 @@ pt_bisect_rest_kernel(PtFieldDev f, PtRows rows, const double* __restrict__ a_, 
     pt_exp_table_init(tile + PT_EVAL_TILE * PT_ROW64(N));
     const int PB = PT_EVAL_THREADS / G;
     const size_t total = pt_rows_total(rows);
-    if ((size_t)blockIdx.x * PB >= total) return;
-    const size_t idx = (size_t)blockIdx.x * PB + threadIdx.x / G;
     const int g = threadIdx.x % G;
+    for (size_t blk = blockIdx.x; blk * PB < total; blk += gridDim.x) {
+    const size_t idx = blk * PB + threadIdx.x / G;
     const bool valid = idx < total;
     const size_t ei = valid ? (rows.list ? (size_t)rows.list[idx] : idx) : 0;
     double a[N], diff[N], p[N];
@@ -708,6 +724,7 @@ pt_bisect_rest_kernel(PtFieldDev f, PtRows rows, const double* __restrict__ a_, 
 #pragma unroll
         for (int d = 0; d < N; ++d) out[ei * N + d] = __dadd_rn(a[d], __dmul_rn(t, diff[d]));
     }
+    }   // block-stride loop over the list
 }
 
 // pack the fp32 screening copy and record max |s_j|
@@ -833,7 +850,11 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
             PT_TRY(pt_check_launch(ctx, "pt_select_flag_kernel"));
         }
         PT_LAUNCH(ctx, "bisect_fp64_rest");
-        PT_G_LAUNCH(pt_bisect_rest_kernel, smem, f->d, sub, a, b, sa, lo.p, hi.p, eps, out, ctx->work);
+        // the list is short (<1 % of the rows): 32 lanes per row keep all SMs busy; blocks beyond the
+        // device-side count exit at once
+        const unsigned grid32 = pt_grid_for(m, PT_EVAL_THREADS / 32, 1u << 16);
+        pt_bisect_rest_kernel<N, 32><<<grid32, PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, sub, a, b, sa, lo.p, hi.p, eps, out, ctx->work);
+        PT_TRY(pt_check_launch(ctx, "pt_bisect_rest_kernel"));
     }
 #undef PT_G_LAUNCH
     return PT_OK;
