@@ -31,7 +31,7 @@ int pt_field_dim(const pt_field* f) { return f->d.n; }
 // Arguments below -1000 are clamped (the term is < 1e-300 of its weight).  Branch-free on purpose so
 // independent rows interleave; non-finite points are handled once per point (PtPoint64::poison).
 __device__ __forceinline__ double pt_exp2_neg(double x, const double* __restrict__ tab) {
-    x = fmax(x, -1000.0);
+    if ((unsigned)__double2hiint(x) > 0xC08F4000u) x = -1000.0;   // x < -1000 (integer compare: keeps the FP64 pipe free)
     const double MAGIC = 6755399441055744.0;   // 1.5 * 2^52: the low word of x*32 + MAGIC is round(32 x)
     const double t = fma(x, 32.0, MAGIC);
     const int mi = __double2loint(t);
@@ -47,7 +47,8 @@ __device__ __forceinline__ double pt_exp2_neg(double x, const double* __restrict
     return __hiloint2double(__double2hiint(v) + ((mi >> 5) << 20), __double2loint(v));
 }
 
-// per-point constants of the expanded exponent: -gamma*log2(e)*|p - s|^2 = c_s + c_p + sum_d q_d s_d
+// per-point constants of the expanded exponent: -gamma*log2(e)*|p - s|^2 = c_s + c_p + sum_d p_d s'_d with
+// s'_d = 2*gamma*log2(e)*s_d stored in the packed support rows (so the point itself is the only per-point vector)
 template <int N>
 struct PtPoint64 {
     double q[N];
@@ -56,7 +57,7 @@ struct PtPoint64 {
     __device__ __forceinline__ void set(const double* p, double gl) {
         double p2 = 0.0;
 #pragma unroll
-        for (int d = 0; d < N; ++d) { q[d] = 2.0 * gl * p[d]; p2 = fma(p[d], p[d], p2); }
+        for (int d = 0; d < N; ++d) { q[d] = p[d]; p2 = fma(p[d], p[d], p2); }
         cp = -gl * p2;
         poison = p2 - p2;
     }
@@ -312,15 +313,16 @@ __device__ __forceinline__ void pt_rbf32_block_sum(const PtFieldDev& f, const fl
 // F, dF/dt, d2F/dt2 of the kernel sum along p(t) = a + t*diff at the point p
 template <int N, int G>
 __device__ __forceinline__ void pt_rbf_block_sum_d(const PtFieldDev& f, const double* p, const double* diff, double seg2,
-                                                   int g, double* tile, double& F, double& D1, double& D2) {
+                                                   int g, double* tile, double& F, double& D1, double& D2, double& AB) {
     const int ROW = PT_ROW64(N);
     const double* tab = tile + PT_EVAL_TILE * ROW;
     PtPoint64<N> pp;
     pp.set(p, f.gamma * PT_L2E);
-    double pd = 0.0;
+    double pd = 0.0, dd[N];
+    const double inv2gl = 1.0 / (2.0 * f.gamma * PT_L2E);   // rows hold 2*gamma*log2e*s_d
 #pragma unroll
-    for (int d = 0; d < N; ++d) pd = fma(p[d], diff[d], pd);
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int d = 0; d < N; ++d) { pd = fma(p[d], diff[d], pd); dd[d] = diff[d] * inv2gl; }
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     const double ng2 = -2.0 * f.gamma, c2 = 2.0 * f.gamma * seg2;
     for (long long t0 = 0; t0 < f.S; t0 += PT_EVAL_TILE) {
         long long rem = f.S - t0;
@@ -333,10 +335,10 @@ __device__ __forceinline__ void pt_rbf_block_sum_d(const PtFieldDev& f, const do
             const double* row = tile + j * ROW;
             double x = pd;                           // (p - s) . diff
 #pragma unroll
-            for (int d = 0; d < N; ++d) x = fma(-diff[d], row[d], x);
+            for (int d = 0; d < N; ++d) x = fma(-dd[d], row[d], x);
             const double e = pt_rbf_term<N>(row, pp, tab);
             const double gx = ng2 * x;
-            a0 += e; a1 = fma(e, gx, a1); a2 = fma(e, fma(gx, gx, -c2), a2);
+            a0 += e; a1 = fma(e, gx, a1); a2 = fma(e, fma(gx, gx, -c2), a2); a3 += fabs(e);
         }
     }
 #pragma unroll
@@ -344,8 +346,9 @@ __device__ __forceinline__ void pt_rbf_block_sum_d(const PtFieldDev& f, const do
         a0 += __shfl_xor_sync(0xffffffffu, a0, off);
         a1 += __shfl_xor_sync(0xffffffffu, a1, off);
         a2 += __shfl_xor_sync(0xffffffffu, a2, off);
+        a3 += __shfl_xor_sync(0xffffffffu, a3, off);
     }
-    F = a0 + pp.poison; D1 = a1; D2 = a2;
+    F = a0 + pp.poison; D1 = a1; D2 = a2; AB = a3;
 }
 
 // first and second t-derivatives of the box barrier along p(t) = a + t*diff
@@ -458,10 +461,10 @@ __global__ void pt_select_shallow_kernel(PtRows rows, const double* __restrict__
     }
 }
 
-__global__ void pt_select_flag_kernel(const uint8_t* __restrict__ flag, size_t m, uint32_t* __restrict__ list_out,
+__global__ void pt_select_flag_kernel(const uint8_t* __restrict__ flag, uint8_t want, size_t m, uint32_t* __restrict__ list_out,
                                       unsigned long long* count_out) {
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool take = i < m && flag[i] != 0;
+    const bool take = i < m && flag[i] == want;
     const unsigned ballot = __ballot_sync(0xffffffffu, take);
     if (ballot) {
         const int lane = threadIdx.x & 31, leader = __ffs(ballot) - 1;
@@ -469,6 +472,22 @@ __global__ void pt_select_flag_kernel(const uint8_t* __restrict__ flag, size_t m
         if (lane == leader) base = atomicAdd(count_out, (unsigned long long)__popc(ballot));
         base = __shfl_sync(0xffffffffu, base, leader);
         if (take) list_out[base + __popc(ballot & ((1u << lane) - 1u))] = (uint32_t)i;
+    }
+}
+
+// rows whose bracket is final: out = a + mid * (b - a)
+template <int N>
+__global__ void pt_bisect_finalize_kernel(PtRows rows, const double* __restrict__ a_, const double* __restrict__ b_,
+                                          const double* __restrict__ lo_, const double* __restrict__ hi_, double* __restrict__ out) {
+    const size_t total = pt_rows_total(rows);
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= total) return;
+    const size_t ei = rows.list ? (size_t)rows.list[idx] : idx;
+    const double t = __dmul_rn(0.5, __dadd_rn(lo_[ei], hi_[ei]));
+#pragma unroll
+    for (int d = 0; d < N; ++d) {
+        const double av = a_[ei * N + d];
+        out[ei * N + d] = __dadd_rn(av, __dmul_rn(t, __dsub_rn(b_[ei * N + d], av)));
     }
 }
 
@@ -512,164 +531,267 @@ pt_bisect_resolve_kernel(PtFieldDev f, PtRows rows, const double* __restrict__ a
     if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&work[5], (unsigned long long)mine);
 }
 
-// K3: monotonicity proof + Newton/secant + verified final cell (see the block comment above)
+// K3: monotonicity proof + Halley/Newton root location with a rigorous enclosure (see the block comment above).
+// Exactly two block-wide evaluation passes, no data-dependent loops:
+//   pass 1  F, F', F'' and A = sum|w_j|k_j at the bracket midpoint (a true bisection step);
+//           s_min = |F'| - w|F''| - w^2 M3/2 - noise > 0 proves F monotone on the halved bracket (one root r)
+//   pass 2  F at the Halley iterate x_h; x2 = x_h - F/(F'(m) + F''(m)(x_h - m)) and
+//           |x2 - r| <= [eta + (|F|+eta) Delta/s_min] / |D|  (mean-value form of the Newton error),
+//           eta = bound on the fp64 evaluation noise of BOTH this kernel and the reference loop.
+//   The reference's final cell is the depth-I dyadic cell containing r; it is accepted only when the enclosure
+//   of r stays eta/s_min away from both cell ends (there every sign the reference bisection can see is certain).
+//   Everything else (<1 % of the rows) is flagged for the plain fp64 bisection kernel.
+#define PT_U64 1.1102230246251565e-16   /* 2^-53 */
+
+// two points per thread, each lane walks all support rows (G = 1): the row loads and the loop overhead are shared
+// by four independent chains (2 rows x 2 points), so the FP64 pipe rather than the issue slot is the limiter
+template <int N, int THREADS, bool DERIV>
+__device__ __forceinline__ void pt_rbf_block_sum_x2(const PtFieldDev& f, const double (&p)[2][N], const double (&diff)[2][N],
+                                                    const double (&seg2)[2], double* tile, double (&F)[2], double (&D1)[2],
+                                                    double (&D2)[2], double (&AB)[2]) {
+    const int ROW = PT_ROW64(N);
+    const double* tab = tile + PT_EVAL_TILE * ROW;
+    PtPoint64<N> pp[2];
+    double pd[2], c2[2], dd[2][N];
+    const double ng2 = -2.0 * f.gamma;
+    const double inv2gl = 1.0 / (2.0 * f.gamma * PT_L2E);   // rows hold 2*gamma*log2e*s_d
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        pp[k].set(p[k], f.gamma * PT_L2E);
+        double t = 0.0;
+#pragma unroll
+        for (int d = 0; d < N; ++d) { t = fma(p[k][d], diff[k][d], t); if (DERIV) dd[k][d] = diff[k][d] * inv2gl; }
+        pd[k] = t; c2[k] = 2.0 * f.gamma * seg2[k];
+    }
+    double a0[2] = {0.0, 0.0}, b0[2] = {0.0, 0.0}, a1[2] = {0.0, 0.0}, a2[2] = {0.0, 0.0}, ab[2] = {0.0, 0.0};
+    for (long long t0 = 0; t0 < f.S; t0 += PT_EVAL_TILE) {
+        long long rem = f.S - t0;
+        const int cnt = rem < PT_EVAL_TILE ? (int)rem : PT_EVAL_TILE;
+        __syncthreads();
+        const double* src = f.sv + t0 * ROW;
+        for (int i = threadIdx.x; i < cnt * ROW; i += THREADS) tile[i] = src[i];
+        if ((cnt & 1) && threadIdx.x < ROW) tile[cnt * ROW + threadIdx.x] = 0.0;   // zero-weight pad row
+        __syncthreads();
+        for (int j = 0; j < cnt; j += 2) {
+            const double* r0 = tile + j * ROW;
+            const double* r1 = r0 + ROW;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                const double e0 = pt_rbf_term<N>(r0, pp[k], tab);
+                const double e1 = pt_rbf_term<N>(r1, pp[k], tab);
+                a0[k] += e0; b0[k] += e1;
+                if (DERIV) {
+                    double x0 = pd[k], x1 = pd[k];
+#pragma unroll
+                    for (int d = 0; d < N; ++d) { x0 = fma(-dd[k][d], r0[d], x0); x1 = fma(-dd[k][d], r1[d], x1); }
+                    const double g0 = ng2 * x0, g1 = ng2 * x1;
+                    a1[k] = fma(e0, g0, a1[k]); a1[k] = fma(e1, g1, a1[k]);
+                    a2[k] = fma(e0, fma(g0, g0, -c2[k]), a2[k]); a2[k] = fma(e1, fma(g1, g1, -c2[k]), a2[k]);
+                    ab[k] += fabs(e0) + fabs(e1);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) { F[k] = (a0[k] + b0[k]) + pp[k].poison; D1[k] = a1[k]; D2[k] = a2[k]; AB[k] = ab[k]; }
+}
+
 template <int N, int G>
-__global__ void __launch_bounds__(PT_EVAL_THREADS)
+__global__ void __launch_bounds__(G == 1 ? 128 : PT_EVAL_THREADS, G == 1 ? 3 : 1)
 pt_bisect_newton_kernel(PtFieldDev f, double sum_abs_w, const double* __restrict__ a_, const double* __restrict__ b_,
                         const int8_t* __restrict__ signs_a, double* __restrict__ lo_io, double* __restrict__ hi_io,
                         size_t m, double eps, double* __restrict__ out, uint8_t* __restrict__ slow,
                         unsigned long long* work) {
+    constexpr int PPT = (G == 1) ? 2 : 1;
+    constexpr int THREADS = (G == 1) ? 128 : PT_EVAL_THREADS;
+    constexpr int GROUPS = THREADS / G;
     extern __shared__ double tile[];
     pt_exp_table_init(tile + PT_EVAL_TILE * PT_ROW64(N));
-    const int PB = PT_EVAL_THREADS / G;
-    const size_t ei = (size_t)blockIdx.x * PB + threadIdx.x / G;
     const int g = threadIdx.x % G;
-    const bool valid = ei < m;
-    double a[N], diff[N], p[N];
-    double seg = 0.0, lo = 0.0, hi = 1.0;
-    int sa = 1;
-    if (valid) {
-        double b[N];
+    size_t ei[PPT];
+    bool valid[PPT];
+    double p[PPT][N], diff[PPT][N], seg[PPT], seg2[PPT], lo[PPT], hi[PPT], mid[PPT];
+    int sa[PPT];
 #pragma unroll
-        for (int d = 0; d < N; ++d) { a[d] = a_[ei * N + d]; b[d] = b_[ei * N + d]; }
-        seg = pt_segment<N>(a, b, diff);
-        sa = signs_a[ei];
-        lo = lo_io[ei]; hi = hi_io[ei];
-    } else {
+    for (int k = 0; k < PPT; ++k) {
+        ei[k] = (size_t)blockIdx.x * (GROUPS * PPT) + (size_t)k * GROUPS + threadIdx.x / G;
+        valid[k] = ei[k] < m;
+        seg[k] = 0.0; lo[k] = 0.0; hi[k] = 1.0; sa[k] = 1;
+        if (valid[k]) {
+            double a[N], b[N];
 #pragma unroll
-        for (int d = 0; d < N; ++d) { a[d] = 0.0; diff[d] = 0.0; }
+            for (int d = 0; d < N; ++d) { a[d] = a_[ei[k] * N + d]; b[d] = b_[ei[k] * N + d]; }
+            seg[k] = pt_segment<N>(a, b, diff[k]);
+            sa[k] = signs_a[ei[k]];
+            lo[k] = lo_io[ei[k]]; hi[k] = hi_io[ei[k]];
+            mid[k] = __dmul_rn(0.5, __dadd_rn(lo[k], hi[k]));
+#pragma unroll
+            for (int d = 0; d < N; ++d) p[k][d] = __dadd_rn(a[d], __dmul_rn(mid[k], diff[k][d]));
+        } else {
+            mid[k] = 0.5;
+#pragma unroll
+            for (int d = 0; d < N; ++d) { p[k][d] = 0.0; diff[k][d] = 0.0; }
+        }
+        seg2[k] = seg[k] * seg[k];
     }
+    // ---- pass 1: F, F', F'', sum|w|k at the midpoint ---------------------------------------------------------
+    double F0[PPT], D1[PPT], D2[PPT], AB[PPT];
+    if constexpr (G == 1) {
+        pt_rbf_block_sum_x2<N, THREADS, true>(f, p, diff, seg2, tile, F0, D1, D2, AB);
+    } else {
+        pt_rbf_block_sum_d<N, G>(f, p[0], diff[0], seg2[0], g, tile, F0[0], D1[0], D2[0], AB[0]);
+    }
+    // per-row state that must survive pass 2 lives in shared memory (keeps the evaluation loop's registers free)
+    double* st = tile + PT_EVAL_TILE * PT_ROW64(N) + 32;
+#define PT_ST(field, k) st[((field) * PPT + (k)) * THREADS + threadIdx.x]
+    enum { ST_LO, ST_W, ST_DL, ST_SMIN, ST_ETA, ST_AD2, ST_K, ST_DT, ST_XH, ST_TF, ST_FIELDS };
+    bool need[PPT], to_slow[PPT], one_step[PPT];
     unsigned evals = 0;
-    auto point = [&](double t) {
 #pragma unroll
-        for (int d = 0; d < N; ++d) p[d] = __dadd_rn(a[d], __dmul_rn(t, diff[d]));
-    };
-    auto eval = [&](double t, bool count) -> double {
-        point(t);
-        double F = f.bias + pt_rbf_block_sum<N, G>(f, p, g, tile);
-        if (f.has_barrier) F -= pt_barrier_group<N, G>(f, p, g);
-        if (count) ++evals;
-        return F;
-    };
-    auto sgn = [](double F) -> int { return F > 0.0 ? 1 : -1; };
-    // depth of the reference's final bracket: smallest I with seg * 2^-I <= eps
-    double delta = 1.0;
-    if (valid) while (__dmul_rn(seg, delta) > eps) delta *= 0.5;
-    double width = hi - lo;
-    const bool finished0 = valid && !(__dmul_rn(seg, width) > eps);
-    const bool shallow = valid && !finished0 && width > PT_HANDOFF_WIDTH;
-    bool need = valid && !finished0 && !shallow;
-    bool to_slow = shallow;
-    double t_final = __dmul_rn(0.5, __dadd_rn(lo, hi));
-    if (__syncthreads_or(need ? 1 : 0)) {
-        // true bisection step at the midpoint, with derivatives along the edge
-        const double mid = __dmul_rn(0.5, __dadd_rn(lo, hi));
-        point(mid);
-        const double seg2 = seg * seg;
-        double F0, D1, D2;
-        pt_rbf_block_sum_d<N, G>(f, p, diff, seg2, g, tile, F0, D1, D2);
-        F0 += f.bias;
+    for (int k = 0; k < PPT; ++k) {
+        one_step[k] = false;
+        double B0 = 0.0;
+        F0[k] += f.bias;
         if (f.has_barrier) {
-            F0 -= pt_barrier_group<N, G>(f, p, g);
+            B0 = pt_barrier_group<N, G>(f, p[k], g);
+            F0[k] -= B0;
             double B1, B2;
-            pt_barrier_derivs<N>(f, p, diff, B1, B2);
-            D1 -= B1; D2 -= B2;
+            pt_barrier_derivs<N>(f, p[k], diff[k], B1, B2);
+            D1[k] -= B1; D2[k] -= B2;
         }
-        if (need) {
+        // depth of the reference's final bracket: smallest I with seg * 2^-I <= eps
+        double dl = 1.0;
+        if (valid[k]) while (__dmul_rn(seg[k], dl) > eps) dl *= 0.5;
+        double w = hi[k] - lo[k];
+        const bool finished0 = valid[k] && !(__dmul_rn(seg[k], w) > eps);
+        const bool shallow = valid[k] && !finished0 && w > PT_HANDOFF_WIDTH;
+        need[k] = valid[k] && !finished0 && !shallow;
+        to_slow[k] = shallow;
+        double tf = mid[k], x = mid[k], smin = 1.0, eta = 0.0, ad2 = 0.0, K = 0.0, Dt = 1.0;
+        if (need[k]) {
             ++evals;
-            if (sgn(F0) == sa) lo = mid; else hi = mid;
-            width = hi - lo;
-            if (!(__dmul_rn(seg, width) > eps)) { need = false; t_final = __dmul_rn(0.5, __dadd_rn(lo, hi)); }
-        }
-        // third-derivative bound along the edge: kernel sum + barrier (1.5x safety)
-        double m3 = 4.0 * f.gamma * sqrt(f.gamma) * sum_abs_w * seg2 * seg;
-        if (f.has_barrier) {
-            double s3 = 0.0;
+            if ((F0[k] > 0.0 ? 1 : -1) == sa[k]) lo[k] = mid[k]; else hi[k] = mid[k];
+            w = hi[k] - lo[k];
+            if (!(__dmul_rn(seg[k], w) > eps)) { need[k] = false; tf = __dmul_rn(0.5, __dadd_rn(lo[k], hi[k])); }
+            // third-derivative bound along the edge: kernel sum (max |H3| exp < 4 gamma^1.5) + barrier, 1.5x safety
+            double t3 = 4.0 * f.gamma * sqrt(f.gamma) * sum_abs_w * seg2[k] * seg[k];
+            if (f.has_barrier) {
+                double s3 = 0.0;
 #pragma unroll
-            for (int d = 0; d < N; ++d) { const double r = fabs(diff[d]) / f.b_scale; s3 += r * r * r; }
-            m3 += 0.2 * f.b_gain * f.b_scale * s3;
+                for (int d = 0; d < N; ++d) { const double r = fabs(diff[k][d]) / f.b_scale; s3 += r * r * r; }
+                t3 += 0.2 * f.b_gain * f.b_scale * s3;
+            }
+            const double m3 = 1.5 * t3;
+            // evaluation noise anywhere in the bracket: this kernel's expanded exponent (cancellation at scale
+            // T = gamma log2e (|p|+max|s|)^2) plus the reference's sequential sum, relative to A = sum|w|k
+            double p2 = 0.0;
+#pragma unroll
+            for (int d = 0; d < N; ++d) p2 = fma(p[k][d], p[k][d], p2);
+            const double pn = sqrt(p2) + f.smax + w * seg[k];
+            const double T = f.gamma * PT_L2E * pn * pn;
+            const double ceta = PT_U64 * (1.01 * (double)(4 * N + 3) * T * PT_LN2 + 1.25 * (double)f.S + 400.0);
+            const double A = 1.25 * AB[k];   // sum|w|k varies by < 7 % across a bracket of width 2^-7
+            eta = ceta * A + 64.0 * PT_U64 * (1.1 * fabs(B0) + fabs(f.bias)) + 1e-290;
+            const double gmax = 2.0 * f.gamma * pn * seg[k];
+            const double etaD = (ceta + 16.0 * PT_U64) * gmax * A;
+            const double etaD2 = (ceta + 32.0 * PT_U64) * (gmax * gmax + 2.0 * f.gamma * seg2[k]) * A;
+            ad2 = fabs(D2[k]) + etaD2;
+            K = 0.5 * m3 * w * w + etaD + etaD2 * w;
+            smin = fabs(D1[k]) - etaD - w * ad2 - 0.5 * w * w * m3;
+            if (need[k] && !(smin > 0.0)) { to_slow[k] = true; need[k] = false; }
+            if (need[k]) {
+                const double nt = F0[k] / D1[k];
+                x = mid[k] - nt * (1.0 + 0.5 * nt * (D2[k] / D1[k]));   // Halley step from the midpoint
+                if (!(x > lo[k] && x < hi[k])) x = 0.5 * (lo[k] + hi[k]);
+                Dt = D1[k] + D2[k] * (x - mid[k]);                       // extrapolated slope at the iterate
+            }
         }
-        m3 *= 1.5;
-        const bool monotone = need && fabs(D1) > width * fabs(D2) + 0.5 * width * width * m3;
-        if (need && !monotone) { to_slow = true; need = false; }
-        // Root location: a Halley step from the midpoint (uses F''), a Newton step with the extrapolated
-        // derivative F'(m) + F''(m)(x - m), then plain secant if ever needed.  An iterate is used WITHOUT
-        // being evaluated once its predicted error is far below the final cell width.
-        const double slope = fabs(D1) + 1e-300;
-        const double e0 = fabs(F0) / slope;                       // ~ distance from the midpoint to the root
-        const double curv = fabs(D2) / slope;
-        const double c3 = m3 / (6.0 * slope) + 0.5 * curv * curv;  // cubic error constant of the Halley step
-        double x0 = mid, f0 = F0, x1 = mid, f1 = F0, x2 = mid;
-        double e_prev = width, e_cur = e0;
-        bool searching = need;
-        int stage = 0;
-        for (int it = 0; it < 8; ++it) {
-            if (searching) {
-                double predicted;
-                if (stage == 0) {
-                    const double nt = F0 / D1;
-                    x2 = mid - nt * (1.0 + 0.5 * nt * (D2 / D1));
-                    predicted = 4.0 * c3 * e0 * e0 * e0;
-                } else if (stage == 1) {
-                    const double dest = D1 + D2 * (x1 - mid);
-                    x2 = x1 - f1 / dest;
-                    // derivative estimate is off by <= m3 w^2 / 2 relative to slope; Newton's own term is quadratic
-                    predicted = 4.0 * e_cur * (0.5 * m3 * width * width / slope + curv * e_cur);
-                } else {
-                    const double den = f1 - f0;
-                    x2 = (den != 0.0) ? x1 - f1 * ((x1 - x0) / den) : 0.5 * (lo + hi);
-                    predicted = 10.0 * e_cur * e_prev;
+        PT_ST(ST_LO, k) = lo[k]; PT_ST(ST_W, k) = w; PT_ST(ST_DL, k) = dl; PT_ST(ST_SMIN, k) = smin; PT_ST(ST_ETA, k) = eta;
+        PT_ST(ST_AD2, k) = ad2; PT_ST(ST_K, k) = K; PT_ST(ST_DT, k) = Dt; PT_ST(ST_XH, k) = x; PT_ST(ST_TF, k) = tf;
+        // the point of pass 2
+#pragma unroll
+        for (int d = 0; d < N; ++d) {
+            const double av = valid[k] ? a_[ei[k] * N + d] : 0.0;
+            p[k][d] = __dadd_rn(av, __dmul_rn(x, diff[k][d]));
+        }
+    }
+    // ---- pass 2: F at the Halley iterate ------------------------------------------------------------------
+    bool any = false;
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) any = any || need[k];
+    if (__syncthreads_or(any ? 1 : 0)) {
+        double F1[PPT];
+        if constexpr (G == 1) {
+            double u1[2], u2[2], u3[2];
+            pt_rbf_block_sum_x2<N, THREADS, false>(f, p, diff, seg2, tile, F1, u1, u2, u3);
+        } else {
+            F1[0] = pt_rbf_block_sum<N, G>(f, p[0], g, tile);
+        }
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+            F1[k] += f.bias;
+            if (f.has_barrier) F1[k] -= pt_barrier_group<N, G>(f, p[k], g);
+            if (need[k]) {
+                ++evals;
+                const double lo_ = PT_ST(ST_LO, k), w = PT_ST(ST_W, k), dl = PT_ST(ST_DL, k), smin = PT_ST(ST_SMIN, k);
+                const double eta = PT_ST(ST_ETA, k), Dt = PT_ST(ST_DT, k), x = PT_ST(ST_XH, k);
+                const double aF = fabs(F1[k]);
+                const double rho = (aF + eta) / smin;                            // |x_h - r| <= rho
+                const double x2 = x - F1[k] / Dt;
+                const double Delta = PT_ST(ST_AD2, k) * rho + PT_ST(ST_K, k);    // >= |F'(xi) - Dt|
+                const double err = 1.01 * (eta + (aF + eta) * Delta / smin) / fabs(Dt) + 4e-16;
+                const double zeta = eta / smin;
+                const double nsub = w / dl;                 // exact: both are powers of two
+                const double j = floor((x2 - lo_) / dl);
+                const double c = lo_ + j * dl;              // exact dyadic arithmetic
+                const bool sane = fabs(Dt) >= smin && j >= 0.0 && j <= nsub - 1.0;
+                // a cell end that is also a bracket end already carries a decided sign
+                const bool lower_ok = (x2 - err - zeta > c) || j == 0.0;
+                const bool upper_ok = (x2 + err + zeta < c + dl) || j == nsub - 1.0;
+                if (sane && lower_ok && upper_ok) PT_ST(ST_TF, k) = c + 0.5 * dl;
+                else {
+                    to_slow[k] = true;
+                    // The enclosure straddles ONE interior grid point b: every other point the bisection visits is
+                    // at least dl away and certain, so only the sign at b is open -- store the bracket [b-dl, b+dl];
+                    // one true fp64 bisection step (pt_bisect_resolve_kernel) then finishes the row.
+                    const bool only_lower = sane && !lower_ok && upper_ok && (x2 - err - zeta > c - dl);
+                    const bool only_upper = sane && lower_ok && !upper_ok && (x2 + err + zeta < c + 2.0 * dl);
+                    if (only_lower || only_upper) {
+                        const double bq = only_lower ? c : c + dl;
+                        PT_ST(ST_LO, k) = bq - dl; PT_ST(ST_W, k) = 2.0 * dl;
+                        one_step[k] = true;
+                    }
                 }
-                if (!(x2 > lo && x2 < hi)) { x2 = 0.5 * (lo + hi); predicted = width; }
-                if (predicted < 0.0625 * delta) searching = false;
             }
-            if (!__syncthreads_or(searching ? 1 : 0)) break;
-            const double f2 = eval(x2, searching);
-            if (searching) {
-                x0 = x1; f0 = f1; x1 = x2; f1 = f2;
-                e_prev = e_cur; e_cur = fabs(f2) / slope;
-                ++stage;
-            }
-        }
-        if (searching) { to_slow = true; need = false; }   // did not converge in 8 evaluations
-        const double nsub = width / delta;            // exact: both are powers of two
-        double j = floor((x2 - lo) / delta);
-        if (!(j >= 0.0)) j = 0.0;
-        if (j > nsub - 1.0) j = nsub - 1.0;
-        double c = lo + j * delta;                    // exact dyadic arithmetic
-        const int sc = sgn(eval(c, need));
-        const int sd = sgn(eval(c + delta, need));
-        bool accepted = need && sc == sa && sd != sa;
-        const bool try_left = need && !accepted && sc != sa && j > 0.0;
-        const bool try_right = need && !accepted && sc == sa && sd == sa && j < nsub - 1.0;
-        if (__syncthreads_or((try_left || try_right) ? 1 : 0)) {
-            const double tq = try_left ? c - delta : c + 2.0 * delta;
-            const int sq = sgn(eval(tq, try_left || try_right));
-            if (try_left && sq == sa) { c = c - delta; accepted = true; }
-            if (try_right && sq != sa) { c = c + delta; accepted = true; }
-        }
-        if (need) {
-            if (accepted) t_final = c + 0.5 * delta;
-            else to_slow = true;
         }
     }
     {
         unsigned mine = (g == 0) ? evals : 0u;
-        unsigned sl = (g == 0 && to_slow) ? 1u : 0u;
+        unsigned sl = 0;
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) sl += (g == 0 && to_slow[k]) ? 1u : 0u;
         for (int off = 16; off > 0; off >>= 1) { mine += __shfl_xor_sync(0xffffffffu, mine, off); sl += __shfl_xor_sync(0xffffffffu, sl, off); }
         if ((threadIdx.x & 31) == 0) {
             if (mine) atomicAdd(&work[0], (unsigned long long)mine);
             if (sl) atomicAdd(&work[3], (unsigned long long)sl);
         }
     }
-    if (valid && g == 0) {
-        slow[ei] = to_slow ? 1 : 0;
-        if (to_slow) { lo_io[ei] = lo; hi_io[ei] = hi; }
-        else {
 #pragma unroll
-            for (int d = 0; d < N; ++d) out[ei * N + d] = __dadd_rn(a[d], __dmul_rn(t_final, diff[d]));
+    for (int k = 0; k < PPT; ++k) {
+        if (valid[k] && g == 0) {
+            slow[ei[k]] = to_slow[k] ? (one_step[k] ? 2 : 1) : 0;
+            if (to_slow[k]) { const double l = PT_ST(ST_LO, k); lo_io[ei[k]] = l; hi_io[ei[k]] = l + PT_ST(ST_W, k); }
+            else {
+                const double tf = PT_ST(ST_TF, k);
+#pragma unroll
+                for (int d = 0; d < N; ++d) {
+                    const double av = a_[ei[k] * N + d];
+                    out[ei[k] * N + d] = __dadd_rn(av, __dmul_rn(tf, __dsub_rn(b_[ei[k] * N + d], av)));
+                }
+            }
         }
     }
+#undef PT_ST
 }
 
 // K4: plain fp64 bisection of the listed rows from their stored brackets
@@ -727,30 +849,29 @@ pt_bisect_rest_kernel(PtFieldDev f, PtRows rows, const double* __restrict__ a_, 
     }   // block-stride loop over the list
 }
 
-// pack the fp32 screening copy and record max |s_j|
-__global__ void pt_pack_sv32_kernel(const double* __restrict__ sv, long long S, int n, int row, int row32, double gl,
-                                    float* __restrict__ sv32, unsigned long long* rmax_bits, double* sum_abs_w) {
-    long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= S) return;
-    double s2 = 0.0;
-    for (int d = 0; d < n; ++d) { double v = sv[j * row + d]; s2 = fma(v, v, s2); sv32[j * row32 + d] = (float)v; }
-    sv32[j * row32 + n] = (float)(-gl * s2);
-    sv32[j * row32 + n + 1] = (float)sv[j * row + n];
-    for (int d = n + 2; d < row32; ++d) sv32[j * row32 + d] = 0.f;
-    atomicMax(rmax_bits, (unsigned long long)__double_as_longlong(sqrt(s2)));
-    atomicAdd(sum_abs_w, fabs(sv[j * row + n]));
-}
-
-// pack raw (support[S][n], weights[S]) into the padded row layout
+// pack raw (support[S][n], weights[S]) into the fp64 row layout [2*gl*s_0.., w, -gl*|s|^2, pad] and the fp32
+// screening copy [s_0.., -gl*|s|^2, w, pad]; record max |s_j| and sum |w_j|
 __global__ void pt_pack_sv_kernel(const double* __restrict__ support, const double* __restrict__ weights,
-                                  long long S, int n, int row, double gl, double* __restrict__ sv) {
+                                  long long S, int n, int row, int row32, double gl, double* __restrict__ sv,
+                                  float* __restrict__ sv32, unsigned long long* rmax_bits, double* sum_abs_w) {
     long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= S) return;
     double s2 = 0.0;
-    for (int d = 0; d < n; ++d) { const double v = support[j * n + d]; sv[j * row + d] = v; s2 = fma(v, v, s2); }
-    sv[j * row + n] = weights[j];
+    for (int d = 0; d < n; ++d) {
+        const double v = support[j * n + d];
+        sv[j * row + d] = (2.0 * gl) * v;
+        sv32[j * row32 + d] = (float)v;
+        s2 = fma(v, v, s2);
+    }
+    const double w = weights[j];
+    sv[j * row + n] = w;
     sv[j * row + n + 1] = -gl * s2;
     for (int d = n + 2; d < row; ++d) sv[j * row + d] = 0.0;
+    sv32[j * row32 + n] = (float)(-gl * s2);
+    sv32[j * row32 + n + 1] = (float)w;
+    for (int d = n + 2; d < row32; ++d) sv32[j * row32 + d] = 0.f;
+    atomicMax(rmax_bits, (unsigned long long)__double_as_longlong(sqrt(s2)));
+    atomicAdd(sum_abs_w, fabs(w));
 }
 
 // lanes per item so that small batches still fill the machine
@@ -839,21 +960,47 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
     }
     {
         PT_LAUNCH(ctx, "bisect_fp64_newton");
-        PT_G_LAUNCH(pt_bisect_newton_kernel, smem, f->d, f->sum_abs_w, a, b, sa, lo.p, hi.p, m, eps, out, slow.p, ctx->work);
+        const size_t smem_nt = smem + 10 * 256 * sizeof(double);   // + per-row state (10 fields x rows per block)
+        if (G == 1) pt_bisect_newton_kernel<N, 1><<<pt_grid_for(m, 256), 128, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, a, b, sa, lo.p, hi.p, m, eps, out, slow.p, ctx->work);
+        else if (G == 4) pt_bisect_newton_kernel<N, 4><<<grid, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, a, b, sa, lo.p, hi.p, m, eps, out, slow.p, ctx->work);
+        else pt_bisect_newton_kernel<N, 32><<<grid, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, a, b, sa, lo.p, hi.p, m, eps, out, slow.p, ctx->work);
+        PT_TRY(pt_check_launch(ctx, "pt_bisect_newton_kernel"));
     }
     {
+        // rows with one open decision: a single true fp64 step, then the bracket midpoint
         unsigned long long* c = cnt.p + 2;
         const PtRows sub{list.p, c, m};
         {
             PT_LAUNCH(ctx, "bisect_select");
-            pt_select_flag_kernel<<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>(slow.p, m, list.p, c);
+            pt_select_flag_kernel<<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>(slow.p, (uint8_t)2, m, list.p, c);
+            PT_TRY(pt_check_launch(ctx, "pt_select_flag_kernel"));
+        }
+        {
+            PT_LAUNCH(ctx, "bisect_fp64_resolve");
+            // a few per cent of the rows: 4 lanes per row keep every SM busy; blocks beyond the device-side count exit
+            pt_bisect_resolve_kernel<N, 4><<<pt_grid_for(m, PT_EVAL_THREADS / 4), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, sub, a, b, sa, lo.p, hi.p, ctx->work);
+            PT_TRY(pt_check_launch(ctx, "pt_bisect_resolve_kernel"));
+        }
+        {
+            PT_LAUNCH(ctx, "bisect_select");
+            pt_bisect_finalize_kernel<N><<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>(sub, a, b, lo.p, hi.p, out);
+            PT_TRY(pt_check_launch(ctx, "pt_bisect_finalize_kernel"));
+        }
+    }
+    {
+        PtBuf<uint32_t> list2;
+        PT_TRY(list2.alloc(ctx, m));
+        unsigned long long* c = cnt.p + 3;
+        const PtRows sub{list2.p, c, m};
+        {
+            PT_LAUNCH(ctx, "bisect_select");
+            pt_select_flag_kernel<<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>(slow.p, (uint8_t)1, m, list2.p, c);
             PT_TRY(pt_check_launch(ctx, "pt_select_flag_kernel"));
         }
         PT_LAUNCH(ctx, "bisect_fp64_rest");
-        // the list is short (<1 % of the rows): 32 lanes per row keep all SMs busy; blocks beyond the
-        // device-side count exit at once
-        const unsigned grid32 = pt_grid_for(m, PT_EVAL_THREADS / 32, 1u << 16);
-        pt_bisect_rest_kernel<N, 32><<<grid32, PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, sub, a, b, sa, lo.p, hi.p, eps, out, ctx->work);
+        // the list is short (~1 % of the rows): 4 lanes per row; the block-stride loop ends at the device-side count
+        const unsigned grid4 = pt_grid_for(m, PT_EVAL_THREADS / 4, 1u << 16);
+        pt_bisect_rest_kernel<N, 4><<<grid4, PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, sub, a, b, sa, lo.p, hi.p, eps, out, ctx->work);
         PT_TRY(pt_check_launch(ctx, "pt_bisect_rest_kernel"));
     }
 #undef PT_G_LAUNCH
@@ -913,18 +1060,15 @@ static int pt_field_build_rbf(pt_ctx* ctx, int n, long long S, const double* sup
         rc = pt_stage_in(ctx, support, (size_t)S * n, tmp_s, &sdev);
         if (rc == PT_OK) rc = pt_stage_in(ctx, weights, (size_t)S, tmp_w, &wdev);
         if (rc != PT_OK) { delete f; return rc; }
-        pt_pack_sv_kernel<<<pt_grid_for((size_t)S, 256), 256, 0, ctx->stream>>>(sdev, wdev, S, n, f->d.row, gamma * PT_L2E, f->sv.p);
-        rc = pt_check_launch(ctx, "pt_pack_sv_kernel");
-        if (rc != PT_OK) { delete f; return rc; }
         f->d.row32 = pt_sv_row32(n);
         rc = f->sv32.alloc(ctx, (size_t)S * f->d.row32);
         PtBuf<unsigned long long> rmax;
         if (rc == PT_OK) rc = rmax.alloc(ctx, 2);
         if (rc != PT_OK) { delete f; return rc; }
         cudaMemsetAsync(rmax.p, 0, 2 * sizeof(unsigned long long), ctx->stream);
-        pt_pack_sv32_kernel<<<pt_grid_for((size_t)S, 256), 256, 0, ctx->stream>>>(f->sv.p, S, n, f->d.row, f->d.row32,
-                                                                                gamma * PT_L2E, f->sv32.p, rmax.p, (double*)(rmax.p + 1));
-        rc = pt_check_launch(ctx, "pt_pack_sv32_kernel");
+        pt_pack_sv_kernel<<<pt_grid_for((size_t)S, 256), 256, 0, ctx->stream>>>(sdev, wdev, S, n, f->d.row, f->d.row32, gamma * PT_L2E,
+                                                                              f->sv.p, f->sv32.p, rmax.p, (double*)(rmax.p + 1));
+        rc = pt_check_launch(ctx, "pt_pack_sv_kernel");
         if (rc != PT_OK) { delete f; return rc; }
         unsigned long long bits[2] = {0, 0};
         cudaMemcpyAsync(bits, rmax.p, sizeof(bits), cudaMemcpyDeviceToHost, ctx->stream);
