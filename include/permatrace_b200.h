@@ -39,6 +39,9 @@ void pt_ctx_destroy(pt_ctx* ctx);
 /* run all work of this context on an existing CUDA stream (e.g. torch's current stream) */
 int pt_ctx_set_stream(pt_ctx* ctx, void* cuda_stream);
 int pt_ctx_synchronize(pt_ctx* ctx);
+/* device blocks freed by the library are cached per context for reuse by the next step; this returns them
+ * to the driver (bytes released, or -1) */
+long long pt_ctx_trim(pt_ctx* ctx);
 /* per-kernel CUDA-event profiler (events on the launching stream) */
 int pt_ctx_profile_enable(pt_ctx* ctx, int on);
 int pt_ctx_profile_reset(pt_ctx* ctx);

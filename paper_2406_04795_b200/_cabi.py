@@ -62,6 +62,7 @@ _SIGS = {
     "pt_ctx_destroy": (None, [_vp]),
     "pt_ctx_set_stream": (_i, [_vp, _vp]),
     "pt_ctx_synchronize": (_i, [_vp]),
+    "pt_ctx_trim": (_ll, [_vp]),
     "pt_ctx_profile_enable": (_i, [_vp, _i]),
     "pt_ctx_profile_reset": (_i, [_vp]),
     "pt_ctx_profile_dump": (_ll, [_vp, C.c_char_p, _ll]),
@@ -175,6 +176,10 @@ class _Context:
 
     def synchronize(self):
         check(lib.pt_ctx_synchronize(self.handle))
+
+    def trim(self) -> int:
+        """Return the context's cached device blocks to the driver; bytes released."""
+        return int(lib.pt_ctx_trim(self.handle))
 
     def profile(self, on: bool):
         check(lib.pt_ctx_profile_enable(self.handle, 1 if on else 0))

@@ -35,18 +35,56 @@ bool pt_is_device_ptr(const void* p) {
     return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
 }
 
+// Allocation sizes are rounded up to 4 significant bits (<= 6.25 % slack) so that the slightly different
+// buffer sizes of successive waves / steps land in the same bucket; blocks above PT_CACHE_MAX_BLOCK bypass
+// the cache (they are the per-proof giants whose size follows the problem, not the step).
+#define PT_CACHE_MAX_BLOCK ((size_t)4 << 30)
+static size_t pt_round_block(size_t bytes) {
+    if (bytes < 512) return 512;
+    int top = 63 - __builtin_clzll((unsigned long long)bytes);
+    const size_t gran = (size_t)1 << (top > 4 ? top - 4 : 0);
+    return (bytes + gran - 1) & ~(gran - 1);
+}
+static void pt_cache_release(pt_ctx* ctx) {
+    for (auto& kv : ctx->free_blocks) cudaFreeAsync(kv.second, ctx->stream);
+    ctx->free_blocks.clear();
+    ctx->cached_bytes = 0;
+}
 int pt_dev_alloc(pt_ctx* ctx, void** p, size_t bytes) {
-    if (bytes == 0) bytes = 16;
-    cudaError_t e = cudaMallocAsync(p, bytes, ctx->stream);
+    const size_t want = pt_round_block(bytes);
+    auto it = ctx->free_blocks.lower_bound(want);
+    if (it != ctx->free_blocks.end() && it->first <= want + want / 4) {
+        *p = it->second;
+        ctx->cached_bytes -= it->first;
+        ctx->live_blocks[*p] = it->first;
+        ctx->free_blocks.erase(it);
+        return PT_OK;
+    }
+    cudaError_t e = cudaMallocAsync(p, want, ctx->stream);
+    if (e == cudaErrorMemoryAllocation && !ctx->free_blocks.empty()) {
+        cudaGetLastError();
+        pt_cache_release(ctx);
+        cudaStreamSynchronize(ctx->stream);
+        e = cudaMallocAsync(p, want, ctx->stream);
+    }
     if (e == cudaErrorMemoryAllocation) {
         cudaGetLastError();
         return pt_fail(ctx, PT_E_NOMEM, "device allocation of %zu bytes failed", bytes);
     }
     if (e != cudaSuccess) return pt_fail(ctx, PT_E_CUDA, "cudaMallocAsync(%zu): %s", bytes, cudaGetErrorString(e));
+    ctx->live_blocks[*p] = want;
     return PT_OK;
 }
 void pt_dev_free(pt_ctx* ctx, void* p) {
-    if (p) cudaFreeAsync(p, ctx ? ctx->stream : nullptr);
+    if (!p) return;
+    if (!ctx) { cudaFreeAsync(p, nullptr); return; }
+    auto it = ctx->live_blocks.find(p);
+    if (it == ctx->live_blocks.end()) { cudaFreeAsync(p, ctx->stream); return; }
+    const size_t size = it->second;
+    ctx->live_blocks.erase(it);
+    if (size > PT_CACHE_MAX_BLOCK) { cudaFreeAsync(p, ctx->stream); return; }
+    ctx->free_blocks.emplace(size, p);
+    ctx->cached_bytes += size;
 }
 
 int pt_check_launch(pt_ctx* ctx, const char* what) {
@@ -129,6 +167,8 @@ void pt_ctx_destroy(pt_ctx* ctx) {
     for (auto& kv : ctx->prof)
         for (auto& pr : kv.second.pending) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
+    pt_cache_release(ctx);
+    cudaStreamSynchronize(ctx->stream);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->work) cudaFree(ctx->work);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -141,6 +181,14 @@ int pt_ctx_set_stream(pt_ctx* ctx, void* cuda_stream) {
     if (ctx->own_stream) { cudaStreamDestroy(ctx->stream); ctx->own_stream = false; }
     ctx->stream = (cudaStream_t)cuda_stream;
     return PT_OK;
+}
+
+long long pt_ctx_trim(pt_ctx* ctx) {
+    if (!ctx) return -1;
+    const long long released = (long long)ctx->cached_bytes;
+    pt_cache_release(ctx);
+    cudaStreamSynchronize(ctx->stream);
+    return released;
 }
 
 int pt_ctx_synchronize(pt_ctx* ctx) {

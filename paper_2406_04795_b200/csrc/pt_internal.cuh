@@ -29,6 +29,11 @@ struct pt_ctx {
     int sm_count = 148;
     // device-side work counters: [0] bisection field evaluations (rows x iterations), [1] points evaluated
     unsigned long long* work = nullptr;
+    // size-bucketed cache of device blocks (all work is ordered on `stream`, so a freed block can be handed
+    // out again at once): after the first step the hot path makes no driver allocation calls at all
+    std::multimap<size_t, void*> free_blocks;
+    std::map<void*, size_t> live_blocks;
+    size_t cached_bytes = 0;
     // pinned scratch for small device->host readbacks (counters)
     void* pinned = nullptr;
     size_t pinned_bytes = 0;
