@@ -96,6 +96,13 @@ int pt_field_values(pt_ctx* ctx, const pt_field* f, const double* points, long l
 int pt_intersection_points(pt_ctx* ctx, const pt_field* f, const double* a, const double* b,
                            long long m, double eps, const int8_t* signs_a, double* out);
 
+/* test hook of the tensor-core (tcgen05) fp32 screen: for the midpoint of each segment a[i]..b[i], out[i] =
+ * max over the support set of |exponent computed on the tensor cores - exponent in fp64|, in units of
+ * 2^-24 * gamma*log2(e)*(|p|+max|s|)^2 (the unit of the screen's error bound).  PT_E_STATE if the field has no
+ * tensor-core operand (support set too large for one CTA's shared memory, n > 6, or PERMATRACE_B200_TC=0). */
+int pt_debug_tc_arg_error(pt_ctx* ctx, const pt_field* f, const double* a, const double* b, long long m,
+                          double* out);
+
 /* ---- collision (collision.py:191-329, pipeline.py:256-270) --------------------------------- */
 /* Robot: joints[nj]: kind (0 revolute, 1 prismatic), axis[3] (unit), origin rotation[9] row-major,
  * origin translation[3], limits[2]; spheres[ns]: link, offset[3], radius.

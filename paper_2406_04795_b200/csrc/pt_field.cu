@@ -16,6 +16,10 @@ struct pt_field {
     PtBuf<float> sv32;
     int precision = 0;
     double sum_abs_w = 0.0;
+    // tensor-core screen (pt_field_tc.cuh): packed tf32 support operand; tc_ok = it fits one CTA's shared memory
+    PtBuf<float> tc_bt, tc_wt;
+    PtTcDev tc;
+    bool tc_ok = false;
 };
 
 int pt_field_dim(const pt_field* f) { return f->d.n; }
@@ -365,6 +369,8 @@ __device__ __forceinline__ void pt_barrier_derivs(const PtFieldDev& f, const dou
     B1 = f.b_gain * b1; B2 = f.b_gain / f.b_scale * b2;
 }
 
+#include "pt_field_tc.cuh"
+
 template <int N, int G>
 __global__ void __launch_bounds__(PT_EVAL_THREADS)
 pt_bisect32_kernel(PtFieldDev f, PtRows rows, const double* __restrict__ a_, const double* __restrict__ b_,
@@ -472,22 +478,6 @@ __global__ void pt_select_flag_kernel(const uint8_t* __restrict__ flag, uint8_t 
         if (lane == leader) base = atomicAdd(count_out, (unsigned long long)__popc(ballot));
         base = __shfl_sync(0xffffffffu, base, leader);
         if (take) list_out[base + __popc(ballot & ((1u << lane) - 1u))] = (uint32_t)i;
-    }
-}
-
-// rows whose bracket is final: out = a + mid * (b - a)
-template <int N>
-__global__ void pt_bisect_finalize_kernel(PtRows rows, const double* __restrict__ a_, const double* __restrict__ b_,
-                                          const double* __restrict__ lo_, const double* __restrict__ hi_, double* __restrict__ out) {
-    const size_t total = pt_rows_total(rows);
-    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= total) return;
-    const size_t ei = rows.list ? (size_t)rows.list[idx] : idx;
-    const double t = __dmul_rn(0.5, __dadd_rn(lo_[ei], hi_[ei]));
-#pragma unroll
-    for (int d = 0; d < N; ++d) {
-        const double av = a_[ei * N + d];
-        out[ei * N + d] = __dadd_rn(av, __dmul_rn(t, __dsub_rn(b_[ei * N + d], av)));
     }
 }
 
@@ -601,7 +591,7 @@ __global__ void __launch_bounds__(G == 1 ? 128 : PT_EVAL_THREADS, G == 1 ? 3 : 1
 pt_bisect_newton_kernel(PtFieldDev f, double sum_abs_w, const double* __restrict__ a_, const double* __restrict__ b_,
                         const int8_t* __restrict__ signs_a, double* __restrict__ lo_io, double* __restrict__ hi_io,
                         size_t m, double eps, double* __restrict__ out, uint8_t* __restrict__ slow,
-                        unsigned long long* work) {
+                        double* __restrict__ jlo_out, double* __restrict__ jhi_out, unsigned long long* work) {
     constexpr int PPT = (G == 1) ? 2 : 1;
     constexpr int THREADS = (G == 1) ? 128 : PT_EVAL_THREADS;
     constexpr int GROUPS = THREADS / G;
@@ -741,26 +731,29 @@ pt_bisect_newton_kernel(PtFieldDev f, double sum_abs_w, const double* __restrict
                 const double Delta = PT_ST(ST_AD2, k) * rho + PT_ST(ST_K, k);    // >= |F'(xi) - Dt|
                 const double err = 1.01 * (eta + (aF + eta) * Delta / smin) / fabs(Dt) + 4e-16;
                 const double zeta = eta / smin;
-                const double nsub = w / dl;                 // exact: both are powers of two
-                const double j = floor((x2 - lo_) / dl);
-                const double c = lo_ + j * dl;              // exact dyadic arithmetic
-                const bool sane = fabs(Dt) >= smin && j >= 0.0 && j <= nsub - 1.0;
-                // a cell end that is also a bracket end already carries a decided sign
-                const bool lower_ok = (x2 - err - zeta > c) || j == 0.0;
-                const bool upper_ok = (x2 + err + zeta < c + dl) || j == nsub - 1.0;
-                if (sane && lower_ok && upper_ok) PT_ST(ST_TF, k) = c + 0.5 * dl;
-                else {
-                    to_slow[k] = true;
-                    // The enclosure straddles ONE interior grid point b: every other point the bisection visits is
-                    // at least dl away and certain, so only the sign at b is open -- store the bracket [b-dl, b+dl];
-                    // one true fp64 bisection step (pt_bisect_resolve_kernel) then finishes the row.
-                    const bool only_lower = sane && !lower_ok && upper_ok && (x2 - err - zeta > c - dl);
-                    const bool only_upper = sane && lower_ok && !upper_ok && (x2 + err + zeta < c + 2.0 * dl);
-                    if (only_lower || only_upper) {
-                        const double bq = only_lower ? c : c + dl;
-                        PT_ST(ST_LO, k) = bq - dl; PT_ST(ST_W, k) = 2.0 * dl;
-                        one_step[k] = true;
+                // Every midpoint the reference bisection visits OUTSIDE the enclosure J = [x2 - err - zeta, x2 + err + zeta]
+                // has a certain sign (F is monotone, the root is in J, and the point is at least zeta = eta/s_min
+                // from it), so the bisection is replayed in exact dyadic arithmetic until a midpoint falls inside J.
+                const bool sane = fabs(Dt) >= smin && x2 > lo_ && x2 < lo_ + w;
+                const double Jlo = x2 - err - zeta, Jhi = x2 + err + zeta;
+                double L = lo_, H = lo_ + w;
+                bool open = false;
+                if (sane) {
+                    while (__dmul_rn(seg[k], __dsub_rn(H, L)) > eps) {
+                        const double mq = __dmul_rn(0.5, __dadd_rn(L, H));
+                        if (mq < Jlo) L = mq;
+                        else if (mq > Jhi) H = mq;
+                        else { open = true; break; }
                     }
+                } else open = true;
+                if (!open) PT_ST(ST_TF, k) = __dmul_rn(0.5, __dadd_rn(L, H));
+                else {
+                    // a midpoint inside J needs a true fp64 evaluation: pt_bisect_rest_kernel continues from [L, H],
+                    // still skipping every midpoint outside J
+                    to_slow[k] = true;
+                    PT_ST(ST_LO, k) = L; PT_ST(ST_W, k) = H - L;
+                    one_step[k] = sane;
+                    if (sane) { PT_ST(ST_AD2, k) = Jlo; PT_ST(ST_K, k) = Jhi; }
                 }
             }
         }
@@ -780,7 +773,12 @@ pt_bisect_newton_kernel(PtFieldDev f, double sum_abs_w, const double* __restrict
     for (int k = 0; k < PPT; ++k) {
         if (valid[k] && g == 0) {
             slow[ei[k]] = to_slow[k] ? (one_step[k] ? 2 : 1) : 0;
-            if (to_slow[k]) { const double l = PT_ST(ST_LO, k); lo_io[ei[k]] = l; hi_io[ei[k]] = l + PT_ST(ST_W, k); }
+            if (to_slow[k]) {
+                const double l = PT_ST(ST_LO, k);
+                lo_io[ei[k]] = l; hi_io[ei[k]] = l + PT_ST(ST_W, k);
+                jlo_out[ei[k]] = one_step[k] ? PT_ST(ST_AD2, k) : -1e300;
+                jhi_out[ei[k]] = one_step[k] ? PT_ST(ST_K, k) : 1e300;
+            }
             else {
                 const double tf = PT_ST(ST_TF, k);
 #pragma unroll
@@ -799,6 +797,7 @@ template <int N, int G>
 __global__ void __launch_bounds__(PT_EVAL_THREADS)
 pt_bisect_rest_kernel(PtFieldDev f, PtRows rows, const double* __restrict__ a_, const double* __restrict__ b_,
                       const int8_t* __restrict__ signs_a, const double* __restrict__ lo_in, const double* __restrict__ hi_in,
+                      const double* __restrict__ jlo_in, const double* __restrict__ jhi_in,
                       double eps, double* __restrict__ out, unsigned long long* work) {
     extern __shared__ double tile[];
     pt_exp_table_init(tile + PT_EVAL_TILE * PT_ROW64(N));
@@ -810,7 +809,7 @@ pt_bisect_rest_kernel(PtFieldDev f, PtRows rows, const double* __restrict__ a_, 
     const bool valid = idx < total;
     const size_t ei = valid ? (rows.list ? (size_t)rows.list[idx] : idx) : 0;
     double a[N], diff[N], p[N];
-    double seg = 0.0, lo = 0.0, hi = 1.0;
+    double seg = 0.0, lo = 0.0, hi = 1.0, jlo = -1e300, jhi = 1e300;
     int sa = 1;
     if (valid) {
         double b[N];
@@ -818,6 +817,7 @@ pt_bisect_rest_kernel(PtFieldDev f, PtRows rows, const double* __restrict__ a_, 
         for (int d = 0; d < N; ++d) { a[d] = a_[ei * N + d]; b[d] = b_[ei * N + d]; }
         seg = pt_segment<N>(a, b, diff);
         sa = signs_a[ei]; lo = lo_in[ei]; hi = hi_in[ei];
+        if (jlo_in) { jlo = jlo_in[ei]; jhi = jhi_in[ei]; }
     } else {
 #pragma unroll
         for (int d = 0; d < N; ++d) { a[d] = 0.0; diff[d] = 0.0; }
@@ -825,6 +825,12 @@ pt_bisect_rest_kernel(PtFieldDev f, PtRows rows, const double* __restrict__ a_, 
     bool active = valid && __dmul_rn(seg, __dsub_rn(hi, lo)) > eps;
     unsigned iters = 0;
     while (__syncthreads_or(active ? 1 : 0)) {
+        // midpoints outside [jlo, jhi] have a proven sign (see pt_bisect_newton_kernel): replay those steps exactly
+        while (active) {
+            const double mq = __dmul_rn(0.5, __dadd_rn(lo, hi));
+            if (mq < jlo) lo = mq; else if (mq > jhi) hi = mq; else break;
+            active = __dmul_rn(seg, __dsub_rn(hi, lo)) > eps;
+        }
         const double mid = __dmul_rn(0.5, __dadd_rn(lo, hi));
 #pragma unroll
         for (int d = 0; d < N; ++d) p[d] = __dadd_rn(a[d], __dmul_rn(mid, diff[d]));
@@ -847,6 +853,84 @@ pt_bisect_rest_kernel(PtFieldDev f, PtRows rows, const double* __restrict__ a_, 
         for (int d = 0; d < N; ++d) out[ei * N + d] = __dadd_rn(a[d], __dmul_rn(t, diff[d]));
     }
     }   // block-stride loop over the list
+}
+
+// K4 with the whole support set resident in shared memory and one WARP per row: rows need very different numbers
+// of true evaluations (0..30), so nothing here is block-synchronous -- a warp takes a row, replays the certain
+// midpoints, evaluates the open ones with its 32 lanes splitting the support set, writes the point, takes the next.
+#define PT_RESTW_THREADS 512
+template <int N>
+__global__ void __launch_bounds__(PT_RESTW_THREADS, 1)
+pt_bisect_rest_warp_kernel(PtFieldDev f, PtRows rows, const double* __restrict__ a_, const double* __restrict__ b_,
+                           const int8_t* __restrict__ signs_a, const double* __restrict__ lo_in, const double* __restrict__ hi_in,
+                           const double* __restrict__ jlo_in, const double* __restrict__ jhi_in,
+                           double eps, double* __restrict__ out, unsigned long long* work) {
+    extern __shared__ double tile[];
+    const int ROW = PT_ROW64(N);
+    const size_t total = pt_rows_total(rows);
+    const int warps_per_block = PT_RESTW_THREADS / 32;
+    if ((size_t)blockIdx.x * warps_per_block >= total) return;
+    double* tab = tile + (size_t)f.S * ROW;
+    for (long long i = threadIdx.x; i < f.S * ROW; i += PT_RESTW_THREADS) tile[i] = f.sv[i];
+    if (threadIdx.x < 32) tab[threadIdx.x] = exp2((double)threadIdx.x * 0.03125);
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const size_t warp0 = (size_t)blockIdx.x * warps_per_block + (threadIdx.x >> 5);
+    const size_t nwarps = (size_t)gridDim.x * warps_per_block;
+    const int S = (int)f.S;
+    unsigned iters = 0;
+    for (size_t idx = warp0; idx < total; idx += nwarps) {
+        const size_t ei = rows.list ? (size_t)rows.list[idx] : idx;
+        double a[N], diff[N], p[N];
+        {
+            double b[N];
+#pragma unroll
+            for (int d = 0; d < N; ++d) { a[d] = a_[ei * N + d]; b[d] = b_[ei * N + d]; }
+        const double seg = pt_segment<N>(a, b, diff);
+        const int sa = signs_a[ei];
+        double lo = lo_in[ei], hi = hi_in[ei];
+        const double jlo = jlo_in ? jlo_in[ei] : -1e300, jhi = jhi_in ? jhi_in[ei] : 1e300;
+        bool active = __dmul_rn(seg, __dsub_rn(hi, lo)) > eps;
+        while (active) {
+            // midpoints outside [jlo, jhi] have a proven sign (see pt_bisect_newton_kernel): replay those steps exactly
+            double mid;
+            while (true) {
+                mid = __dmul_rn(0.5, __dadd_rn(lo, hi));
+                if (mid < jlo) lo = mid; else if (mid > jhi) hi = mid; else break;
+                active = __dmul_rn(seg, __dsub_rn(hi, lo)) > eps;
+                if (!active) break;
+            }
+            if (!active) break;
+#pragma unroll
+            for (int d = 0; d < N; ++d) p[d] = __dadd_rn(a[d], __dmul_rn(mid, diff[d]));
+            PtPoint64<N> pp;
+            pp.set(p, f.gamma * PT_L2E);
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int j = lane;
+            for (; j + 96 < S; j += 128) {
+                s0 += pt_rbf_term<N>(tile + (size_t)j * ROW, pp, tab);
+                s1 += pt_rbf_term<N>(tile + (size_t)(j + 32) * ROW, pp, tab);
+                s2 += pt_rbf_term<N>(tile + (size_t)(j + 64) * ROW, pp, tab);
+                s3 += pt_rbf_term<N>(tile + (size_t)(j + 96) * ROW, pp, tab);
+            }
+            for (; j < S; j += 32) s0 += pt_rbf_term<N>(tile + (size_t)j * ROW, pp, tab);
+            double acc = ((s0 + s1) + (s2 + s3)) + pp.poison;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+            double F = f.bias + acc;
+            if (f.has_barrier) F -= pt_barrier_group<N, 32>(f, p, lane);
+            if ((F > 0.0 ? 1 : -1) == sa) lo = mid; else hi = mid;
+            active = __dmul_rn(seg, __dsub_rn(hi, lo)) > eps;
+            ++iters;
+        }
+        if (lane == 0) {
+            const double t = __dmul_rn(0.5, __dadd_rn(lo, hi));
+#pragma unroll
+            for (int d = 0; d < N; ++d) out[ei * N + d] = __dadd_rn(a[d], __dmul_rn(t, diff[d]));
+        }
+        }
+    }
+    if (lane == 0 && iters) atomicAdd(&work[4], (unsigned long long)iters);
 }
 
 // pack raw (support[S][n], weights[S]) into the fp64 row layout [2*gl*s_0.., w, -gl*|s|^2, pad] and the fp32
@@ -902,6 +986,25 @@ static int pt_eval_launch(pt_ctx* ctx, const pt_field* f, const double* pts, siz
     return pt_check_launch(ctx, "pt_eval_rbf_kernel");
 }
 
+// fp32 screen on the tensor cores: persistent CTAs (one per SM), each walking chunks of 128 rows
+template <int N, int MODE>
+static int pt_screen_tc_launch(pt_ctx* ctx, const pt_field* f, const PtRows& rows, const double* a, const double* b,
+                               const int8_t* sa, double eps, int fresh, double* lo, double* hi) {
+    if constexpr (N > 6) {
+        return pt_fail(ctx, PT_E_STATE, "tensor-core screen is built for n <= 6");
+    } else {
+        const size_t smem = pt_tc_smem_bytes(N, f->d.S);
+        static bool configured = false;
+        if (!configured) {
+            PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect32_tc_kernel<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_TC_SMEM_LIMIT));
+            configured = true;
+        }
+        const unsigned grid = pt_grid_for(rows.m, 2 * PT_TC_M, (unsigned)ctx->sm_count);
+        pt_bisect32_tc_kernel<N, MODE><<<grid, PT_TC_THREADS, smem, ctx->stream>>>(f->d, f->tc, rows, a, b, sa, eps, fresh, lo, hi, ctx->work);
+        return pt_check_launch(ctx, "pt_bisect32_tc_kernel");
+    }
+}
+
 template <int N>
 static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, const double* b, const int8_t* sa,
                             size_t m, double eps, double* out) {
@@ -920,9 +1023,11 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
         else pt_bisect_rbf_kernel<N, 32><<<grid, PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, a, b, sa, m, eps, out, ctx->work);
         return pt_check_launch(ctx, "pt_bisect_rbf_kernel");
     }
-    PtBuf<double> lo, hi; PtBuf<uint32_t> list; PtBuf<unsigned long long> cnt; PtBuf<uint8_t> slow;
+    PtBuf<double> lo, hi, jlo, jhi; PtBuf<uint32_t> list; PtBuf<unsigned long long> cnt; PtBuf<uint8_t> slow;
     PT_TRY(lo.alloc(ctx, m));
     PT_TRY(hi.alloc(ctx, m));
+    PT_TRY(jlo.alloc(ctx, m));
+    PT_TRY(jhi.alloc(ctx, m));
     PT_TRY(list.alloc(ctx, m));
     PT_TRY(slow.alloc(ctx, m));
     PT_TRY(cnt.alloc(ctx, 4));
@@ -936,9 +1041,12 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
         else KERNEL<N, 32><<<grid, PT_EVAL_THREADS, SMEM, ctx->stream>>>(__VA_ARGS__);              \
         PT_TRY(pt_check_launch(ctx, #KERNEL));                                                      \
     } while (0)
+    // batches that fill the machine screen on the tensor cores (tcgen05), small ones on the SIMT kernel
+    const bool use_tc = f->tc_ok && m >= (size_t)PT_TC_M * 32;
     {
-        PT_LAUNCH(ctx, "bisect_fp32_screen");
-        PT_G_LAUNCH(pt_bisect32_kernel, smem32, f->d, all, a, b, sa, eps, 1, lo.p, hi.p, ctx->work);
+        PT_LAUNCH(ctx, use_tc ? "bisect_fp32_screen_tc" : "bisect_fp32_screen");
+        if (use_tc) PT_TRY((pt_screen_tc_launch<N, 0>(ctx, f, all, a, b, sa, eps, 1, lo.p, hi.p)));
+        else PT_G_LAUNCH(pt_bisect32_kernel, smem32, f->d, all, a, b, sa, eps, 1, lo.p, hi.p, ctx->work);
     }
     // rows that stopped while their bracket is still wide: one true fp64 step, then back to fp32
     for (int round = 0; round < 2; ++round) {
@@ -954,56 +1062,58 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
             PT_G_LAUNCH(pt_bisect_resolve_kernel, smem, f->d, sub, a, b, sa, lo.p, hi.p, ctx->work);
         }
         {
-            PT_LAUNCH(ctx, "bisect_fp32_screen");
-            PT_G_LAUNCH(pt_bisect32_kernel, smem32, f->d, sub, a, b, sa, eps, 0, lo.p, hi.p, ctx->work);
+            PT_LAUNCH(ctx, use_tc ? "bisect_fp32_screen_tc" : "bisect_fp32_screen");
+            if (use_tc) PT_TRY((pt_screen_tc_launch<N, 0>(ctx, f, sub, a, b, sa, eps, 0, lo.p, hi.p)));
+            else PT_G_LAUNCH(pt_bisect32_kernel, smem32, f->d, sub, a, b, sa, eps, 0, lo.p, hi.p, ctx->work);
         }
     }
     {
         PT_LAUNCH(ctx, "bisect_fp64_newton");
         const size_t smem_nt = smem + 10 * 256 * sizeof(double);   // + per-row state (10 fields x rows per block)
-        if (G == 1) pt_bisect_newton_kernel<N, 1><<<pt_grid_for(m, 256), 128, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, a, b, sa, lo.p, hi.p, m, eps, out, slow.p, ctx->work);
-        else if (G == 4) pt_bisect_newton_kernel<N, 4><<<grid, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, a, b, sa, lo.p, hi.p, m, eps, out, slow.p, ctx->work);
-        else pt_bisect_newton_kernel<N, 32><<<grid, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, a, b, sa, lo.p, hi.p, m, eps, out, slow.p, ctx->work);
+        if (G == 1) pt_bisect_newton_kernel<N, 1><<<pt_grid_for(m, 256), 128, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, a, b, sa, lo.p, hi.p, m, eps, out, slow.p, jlo.p, jhi.p, ctx->work);
+        else if (G == 4) pt_bisect_newton_kernel<N, 4><<<grid, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, a, b, sa, lo.p, hi.p, m, eps, out, slow.p, jlo.p, jhi.p, ctx->work);
+        else pt_bisect_newton_kernel<N, 32><<<grid, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, a, b, sa, lo.p, hi.p, m, eps, out, slow.p, jlo.p, jhi.p, ctx->work);
         PT_TRY(pt_check_launch(ctx, "pt_bisect_newton_kernel"));
     }
-    {
-        // rows with one open decision: a single true fp64 step, then the bracket midpoint
-        unsigned long long* c = cnt.p + 2;
-        const PtRows sub{list.p, c, m};
+    // open rows: (2) root enclosed, a few midpoints inside the enclosure need a true evaluation; (1) no proof --
+    // plain bisection.  Separate launches so that the short rows do not wait for the long ones.
+    PtBuf<uint32_t> list2;
+    PT_TRY(list2.alloc(ctx, m));
+    for (int kind = 2; kind >= 1; --kind) {
+        unsigned long long* c = cnt.p + (kind == 2 ? 2 : 3);
+        uint32_t* lp = kind == 2 ? list.p : list2.p;
+        const PtRows sub{lp, c, m};
         {
             PT_LAUNCH(ctx, "bisect_select");
-            pt_select_flag_kernel<<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>(slow.p, (uint8_t)2, m, list.p, c);
-            PT_TRY(pt_check_launch(ctx, "pt_select_flag_kernel"));
-        }
-        {
-            PT_LAUNCH(ctx, "bisect_fp64_resolve");
-            // a few per cent of the rows: 4 lanes per row keep every SM busy; blocks beyond the device-side count exit
-            pt_bisect_resolve_kernel<N, 4><<<pt_grid_for(m, PT_EVAL_THREADS / 4), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, sub, a, b, sa, lo.p, hi.p, ctx->work);
-            PT_TRY(pt_check_launch(ctx, "pt_bisect_resolve_kernel"));
-        }
-        {
-            PT_LAUNCH(ctx, "bisect_select");
-            pt_bisect_finalize_kernel<N><<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>(sub, a, b, lo.p, hi.p, out);
-            PT_TRY(pt_check_launch(ctx, "pt_bisect_finalize_kernel"));
-        }
-    }
-    {
-        PtBuf<uint32_t> list2;
-        PT_TRY(list2.alloc(ctx, m));
-        unsigned long long* c = cnt.p + 3;
-        const PtRows sub{list2.p, c, m};
-        {
-            PT_LAUNCH(ctx, "bisect_select");
-            pt_select_flag_kernel<<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>(slow.p, (uint8_t)1, m, list2.p, c);
+            pt_select_flag_kernel<<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>(slow.p, (uint8_t)kind, m, lp, c);
             PT_TRY(pt_check_launch(ctx, "pt_select_flag_kernel"));
         }
         PT_LAUNCH(ctx, "bisect_fp64_rest");
-        // the list is short (~1 % of the rows): 4 lanes per row; the block-stride loop ends at the device-side count
-        const unsigned grid4 = pt_grid_for(m, PT_EVAL_THREADS / 4, 1u << 16);
-        pt_bisect_rest_kernel<N, 4><<<grid4, PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, sub, a, b, sa, lo.p, hi.p, eps, out, ctx->work);
-        PT_TRY(pt_check_launch(ctx, "pt_bisect_rest_kernel"));
+        const size_t smem_w = ((size_t)f->d.S * PT_ROW64(N) + 32) * sizeof(double);
+        if (smem_w <= PT_TC_SMEM_LIMIT) {
+            // support set resident in shared memory, one warp per row, persistent CTAs
+            static bool configured = false;
+            if (!configured) {
+                PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_rest_warp_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_TC_SMEM_LIMIT));
+                configured = true;
+            }
+            const unsigned gridw = pt_grid_for(m, PT_RESTW_THREADS / 32, (unsigned)ctx->sm_count);
+            pt_bisect_rest_warp_kernel<N><<<gridw, PT_RESTW_THREADS, smem_w, ctx->stream>>>(f->d, sub, a, b, sa, lo.p, hi.p, jlo.p, jhi.p, eps, out, ctx->work);
+            PT_TRY(pt_check_launch(ctx, "pt_bisect_rest_warp_kernel"));
+        } else {
+            // larger support sets: tiles through shared memory, 4 lanes per row; the block-stride loop ends at the device-side count
+            const unsigned grid4 = pt_grid_for(m, PT_EVAL_THREADS / 4, 1u << 16);
+            pt_bisect_rest_kernel<N, 4><<<grid4, PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, sub, a, b, sa, lo.p, hi.p, jlo.p, jhi.p, eps, out, ctx->work);
+            PT_TRY(pt_check_launch(ctx, "pt_bisect_rest_kernel"));
+        }
     }
 #undef PT_G_LAUNCH
+    if (getenv("PT_DEBUG_COUNTS")) {
+        unsigned long long h[4];
+        cudaMemcpyAsync(h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream);
+        cudaStreamSynchronize(ctx->stream);
+        fprintf(stderr, "[pt] root solve m=%zu resolve_round1=%llu resolve_round2=%llu enclosed_open=%llu unproven=%llu tc=%d\n", m, h[0], h[1], h[2], h[3], (int)use_tc);
+    }
     return PT_OK;
 }
 
@@ -1076,6 +1186,21 @@ static int pt_field_build_rbf(pt_ctx* ctx, int n, long long S, const double* sup
         memcpy(&f->d.smax, &bits[0], sizeof(double));
         memcpy(&f->sum_abs_w, &bits[1], sizeof(double));
         f->d.sv32 = f->sv32.p;
+        // tensor-core screen operand, when the whole packed support set fits one CTA's shared memory
+        const char* tc_env = getenv("PERMATRACE_B200_TC");
+        if (!(tc_env && tc_env[0] == '0') && n <= 6 && pt_tc_smem_bytes(n, S) <= PT_TC_SMEM_LIMIT) {
+            const int kt = pt_tc_kt(n), spad = (int)pt_tc_spad(S);
+            rc = f->tc_bt.alloc(ctx, (size_t)kt * spad);
+            if (rc == PT_OK) rc = f->tc_wt.alloc(ctx, (size_t)spad);
+            if (rc != PT_OK) { delete f; return rc; }
+            pt_pack_tc_kernel<<<pt_grid_for((size_t)spad, 256), 256, 0, ctx->stream>>>(sdev, wdev, S, n, spad, kt, gamma * PT_L2E,
+                                                                                     f->tc_bt.p, f->tc_wt.p);
+            rc = pt_check_launch(ctx, "pt_pack_tc_kernel");
+            if (rc != PT_OK) { delete f; return rc; }
+            f->tc.bt = f->tc_bt.p; f->tc.wt = f->tc_wt.p; f->tc.spad = spad; f->tc.kt = kt;
+            f->tc_ok = true;
+            cudaStreamSynchronize(ctx->stream);   // sdev/wdev may be staging buffers released on return
+        }
     }
     f->d.sv = f->sv.p;
     *out = f;
@@ -1161,6 +1286,30 @@ int pt_intersection_points(pt_ctx* ctx, const pt_field* f, const double* a, cons
     if (odev != out) PT_TRY(pt_copy_out(ctx, out, odev, (size_t)m * n, false));
     PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return PT_OK;
+}
+
+int pt_debug_tc_arg_error(pt_ctx* ctx, const pt_field* f, const double* a, const double* b, long long m, double* out) {
+    if (!ctx || !f || !a || !b || !out || m <= 0) return pt_fail(ctx, PT_E_INVALID, "pt_debug_tc_arg_error: bad argument");
+    if (f->d.kind != PT_FIELD_RBF || !f->tc_ok) return pt_fail(ctx, PT_E_STATE, "field has no tensor-core operand");
+    const int n = f->d.n;
+    PtBuf<double> ta, tb, lo, hi; PtBuf<int8_t> sa;
+    const double *adev, *bdev;
+    PT_TRY(pt_stage_in(ctx, a, (size_t)m * n, ta, &adev));
+    PT_TRY(pt_stage_in(ctx, b, (size_t)m * n, tb, &bdev));
+    PT_TRY(lo.alloc(ctx, m)); PT_TRY(hi.alloc(ctx, m)); PT_TRY(sa.alloc(ctx, m));
+    PT_CUDA(ctx, cudaMemsetAsync(sa.p, 1, (size_t)m, ctx->stream));
+    const PtRows all{nullptr, nullptr, (size_t)m};
+    int rc;
+    switch (n) {
+        case 2: rc = pt_screen_tc_launch<2, 1>(ctx, f, all, adev, bdev, sa.p, 1e-9, 1, lo.p, hi.p); break;
+        case 3: rc = pt_screen_tc_launch<3, 1>(ctx, f, all, adev, bdev, sa.p, 1e-9, 1, lo.p, hi.p); break;
+        case 4: rc = pt_screen_tc_launch<4, 1>(ctx, f, all, adev, bdev, sa.p, 1e-9, 1, lo.p, hi.p); break;
+        case 5: rc = pt_screen_tc_launch<5, 1>(ctx, f, all, adev, bdev, sa.p, 1e-9, 1, lo.p, hi.p); break;
+        case 6: rc = pt_screen_tc_launch<6, 1>(ctx, f, all, adev, bdev, sa.p, 1e-9, 1, lo.p, hi.p); break;
+        default: return pt_fail(ctx, PT_E_INVALID, "dimension %d unsupported by the tensor-core screen", n);
+    }
+    PT_TRY(rc);
+    return pt_copy_out(ctx, out, hi.p, (size_t)m, true);
 }
 
 int pt_rbf_values(pt_ctx* ctx, const double* points, long long m, int n, const double* support, long long S,

@@ -30,6 +30,30 @@ static inline int pt_sv_row32(int n) { return (n + 2 + 3) & ~3; }
 #define PT_LN2 0.6931471805599453
 #define PT_U32 5.9604644775390625e-08   /* 2^-24, unit roundoff of binary32 */
 
+// ---- tensor-core screen (kernels in pt_field_tc.cuh) ----------------------------------------------------
+#define PT_TC_M 128                 /* points per CTA chunk = UMMA M = TMEM lanes */
+#define PT_TC_N 128                 /* support vectors per UMMA = accumulator columns */
+#define PT_TC_THREADS 256           /* two row groups of 4 warps; warp w and w+4 both sit on TMEM lanes 32(w%4).. */
+#define PT_TC_SMEM_LIMIT 232448     /* 227 KB */
+/* bound, in units of u32*T (T = gamma*log2e*(|p|+max|s|)^2), on |arg_tc - arg|: 1.5 from the tf32 splits plus the
+ * tensor-core accumulation; PTX does not specify the latter, so it is CALIBRATED: tests/test_gpu_parity.py measures
+ * the worst case over millions of pairs (pt_debug_tc_arg_error) and asserts it stays below a quarter of this */
+#define PT_TC_ARG_ULPS 16.0
+
+static inline int pt_tc_kt(int n) { return ((3 * n + 6) + 7) & ~7; }
+static inline long long pt_tc_spad(long long S) { return ((S + PT_TC_N - 1) / PT_TC_N) * PT_TC_N; }
+static inline size_t pt_tc_smem_bytes(int n, long long S) {
+    const size_t kc = (size_t)pt_tc_kt(n) / 4;
+    return kc * (size_t)pt_tc_spad(S) * 16 + 2 * kc * PT_TC_M * 16 + (size_t)pt_tc_spad(S) * 4 + 64;
+}
+
+struct PtTcDev {
+    const float* bt;   // [KT/4][Spad][4] tf32 pieces of the support side, UMMA K-major core-matrix order
+    const float* wt;   // [Spad] fp32 weights (0 for the pad rows)
+    int spad;
+    int kt;
+};
+
 #ifdef __CUDACC__
 // numpy.logaddexp(0, v) branch structure (npy_logaddexp): max + log1p(exp(-|diff|))
 __device__ __forceinline__ double pt_softplus(double v) {

@@ -1,0 +1,367 @@
+// Tensor-core (tcgen05 / TMEM) version of the fp32 bisection screen.
+//
+// The exponent of every (point, support vector) pair,
+//     arg_ij = -gamma*log2(e)*|p_i - s_j|^2 = c_s(j) + c_p(i) + q_i . s_j ,   q = 2*gamma*log2(e)*p ,
+// is a [128 points] x [S support vectors] x [K] contraction.  It runs on the 5th-generation tensor cores as
+// kind::tf32 UMMA instructions (M = 128, N = 128, K = 8) with the fp32 accumulator in tensor memory.  TF32
+// carries 11 significant bits, so both operands are split into tf32 pieces (x = x_h + x_l, residual <= 2^-24|x|)
+// and the contraction is widened to K = 3n + 6 columns
+//     q_h.s_h + c_p,h*1 + 1*c_s,h  |  q_h.s_l + c_p,l*1 + 1*c_s,l  |  q_l.s_h + c_p,ll*1 + 1*c_s,ll
+// (every product of two 11-bit pieces is exact in fp32; the dropped q_l.s_l term and the split residuals are
+// <= 3*2^-24 sum_d |q_d s_d|).  The epilogue reads the accumulator back with tcgen05.ld, one point per thread
+// (TMEM lane = point, column = support vector), and does 2^arg (MUFU ex2) and the weighted fp32 sums exactly
+// like the SIMT screen (pt_bisect32_kernel); the decision rule |F32| > E with E a bound on |F32 - F| is the same.
+//
+// Shared memory (one CTA per SM, persistent over chunks of 128 rows):
+//     B  : the whole packed support set, K-major canonical no-swizzle UMMA layout, loaded once per CTA
+//     A  : the 128 points of the current bisection level, rewritten by the epilogue threads every level
+//     W  : the fp32 weights
+// TMEM: 512 columns = four 128 x 128 fp32 accumulators (two per row group), so the MMAs of tile t+1 overlap the
+// epilogue of tile t.
+#pragma once
+#include "pt_field.cuh"
+
+#ifdef __CUDACC__
+__device__ __forceinline__ float pt_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+}
+// x = h + l (+ ll): tf32 pieces, each exactly representable with 11 significant bits
+__device__ __forceinline__ void pt_tf32_split3(double x, float& h, float& l, float& ll) {
+    h = pt_tf32((float)x);
+    const double r = x - (double)h;
+    l = pt_tf32((float)r);
+    ll = pt_tf32((float)(r - (double)l));
+}
+
+// column k of the widened contraction for the support side (see the header comment)
+__global__ void pt_pack_tc_kernel(const double* __restrict__ support, const double* __restrict__ weights, long long S,
+                                  int n, int spad, int kt, double gl, float* __restrict__ bt, float* __restrict__ wt) {
+    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= spad) return;
+    float col[32];
+    for (int k = 0; k < kt; ++k) col[k] = 0.f;
+    float w = 0.f;
+    if (j < S) {
+        double s2 = 0.0;
+        for (int d = 0; d < n; ++d) {
+            const double v = support[j * n + d];
+            s2 = fma(v, v, s2);
+            float h, l, ll;
+            pt_tf32_split3(v, h, l, ll);
+            col[d] = h;                   // q_h . s_h
+            col[(n + 2) + d] = l;         // q_h . s_l
+            col[2 * (n + 2) + d] = h;     // q_l . s_h
+        }
+        float ch, cl, cll;
+        pt_tf32_split3(-gl * s2, ch, cl, cll);
+        col[n] = 1.f;             col[n + 1] = ch;                 // c_p,h * 1 ; 1 * c_s,h
+        col[(n + 2) + n] = 1.f;   col[(n + 2) + n + 1] = cl;
+        col[2 * (n + 2) + n] = 1.f; col[2 * (n + 2) + n + 1] = cll;
+        w = (float)weights[j];
+    }
+    for (int k = 0; k < kt; ++k) bt[((size_t)(k >> 2) * spad + j) * 4 + (k & 3)] = col[k];
+    wt[j] = w;
+}
+
+// ---- raw PTX wrappers ------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t pt_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void pt_mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void pt_mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "PT_MBAR_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@p bra PT_MBAR_DONE;\n\t"
+        "bra PT_MBAR_WAIT;\n\t"
+        "PT_MBAR_DONE:\n\t}" ::"r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void pt_fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void pt_tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void pt_tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// K-major, no swizzle: core matrix = 8 rows x 16 bytes, contiguous (128 B); lbo = byte distance between the two
+// 16-byte K halves of one instruction, sbo = byte distance between successive 8-row groups
+__device__ __forceinline__ uint64_t pt_umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+// D[tmem] (+)= A[smem] * B[smem]^T, kind::tf32, issued by one thread for the whole CTA
+__device__ __forceinline__ void pt_umma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(accumulate) : "memory");
+}
+__device__ __forceinline__ void pt_umma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void pt_tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void pt_tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// instruction descriptor: D = f32, A = B = tf32, both K-major, N = PT_TC_N, M = 128
+#define PT_TC_IDESC ((1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(PT_TC_N >> 3) << 17) | ((uint32_t)(PT_TC_M >> 4) << 24))
+
+// sync / OR-reduce over the 128 threads of one row group (named barriers 1 and 2; barrier 0 stays __syncthreads)
+__device__ __forceinline__ void pt_group_sync(int group) {
+    asm volatile("bar.sync %0, 128;" ::"r"(group + 1) : "memory");
+}
+__device__ __forceinline__ bool pt_group_or(int group, bool pred) {
+    uint32_t out;
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\t"
+        "setp.ne.u32 q, %1, 0;\n\t"
+        "bar.red.or.pred p, %2, 128, q;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(out) : "r"((uint32_t)pred), "r"(group + 1) : "memory");
+    return out != 0;
+}
+
+// box barrier in fp32 (fast exp/log): value and a bound on its error; the screen only needs F to within E
+template <int N>
+__device__ __forceinline__ double pt_barrier_fast(const PtFieldDev& f, const double* p, double inv_scale, double& err) {
+    float acc = 0.f, mag = 0.f;
+#pragma unroll
+    for (int d = 0; d < N; ++d) {
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+            const float v = (float)((side ? (p[d] - f.b_hi[d]) : (f.b_lo[d] - p[d])) * inv_scale);
+            const float t = __logf(1.f + __expf(-fabsf(v)));     // log1p(exp(-|v|)), absolute error < 3 u32
+            acc += fmaxf(v, 0.f) + t;
+            mag += 1.f + fmaxf(v, 0.f);
+        }
+    }
+    const double gs = f.b_gain * f.b_scale;
+    err = 8.0 * PT_U32 * gs * (double)mag;
+    return gs * (double)acc;
+}
+
+// MODE 0: the bisection screen (same contract as pt_bisect32_kernel).
+// MODE 1: calibration -- one evaluation at t = 0.5 per row; hi_io[row] receives max_j |arg_tc - arg_fp64| / (u32*T).
+//
+// Two independent row groups per CTA (warps 0-3 and 4-7, 128 rows each, one row per thread = one TMEM lane): every
+// bisection level ends in a serial stretch (decide, move the bracket, rewrite A, wait for the first MMA), and while
+// one group is there the other one keeps the MUFU pipe busy.  Each group owns two 128-column accumulators.
+template <int N, int MODE>
+__global__ void __launch_bounds__(PT_TC_THREADS, 1)
+pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __restrict__ a_, const double* __restrict__ b_,
+                      const int8_t* __restrict__ signs_a, double eps, int fresh, double* __restrict__ lo_io,
+                      double* __restrict__ hi_io, unsigned long long* work) {
+    extern __shared__ __align__(1024) unsigned char pt_tc_smem[];
+    constexpr int KT = ((3 * N + 6) + 7) & ~7;
+    constexpr int KC = KT / 4;           // 16-byte K chunks
+    const int spad = tc.spad;
+    const int ntiles = spad / PT_TC_N;
+    float* sB = reinterpret_cast<float*>(pt_tc_smem);
+    float* sA0 = sB + (size_t)KC * spad * 4;                    // A of group 0, then group 1
+    float* sW = sA0 + 2 * (size_t)KC * PT_TC_M * 4;
+    unsigned long long* sBar = reinterpret_cast<unsigned long long*>(sW + spad);
+    uint32_t* sTmem = reinterpret_cast<uint32_t*>(sBar + 4);
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int row = tid & (PT_TC_M - 1), group = tid >> 7;
+    const size_t total = pt_rows_total(rows);
+    if ((size_t)blockIdx.x * (2 * PT_TC_M) >= total) return;
+
+    // ---- one-time setup: barriers, TMEM, the packed support set ---------------------------------------------
+    if (tid == 0) {
+        for (int i = 0; i < 4; ++i) pt_mbar_init(pt_smem_u32(&sBar[i]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(pt_smem_u32(sTmem)), "r"(512u));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
+    }
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(tc.bt);
+        uint4* dst = reinterpret_cast<uint4*>(sB);
+        for (int i = tid; i < KC * spad; i += PT_TC_THREADS) dst[i] = src[i];
+        const uint4* ws = reinterpret_cast<const uint4*>(tc.wt);
+        uint4* wd = reinterpret_cast<uint4*>(sW);
+        for (int i = tid; i < spad / 4; i += PT_TC_THREADS) wd[i] = ws[i];
+    }
+    pt_fence_async_smem();
+    pt_tc_fence_before();
+    __syncthreads();
+    pt_tc_fence_after();
+    const uint32_t tmem_base = *sTmem + (uint32_t)group * (2 * PT_TC_N);
+    float* sA = sA0 + (size_t)group * KC * PT_TC_M * 4;
+    const uint32_t sA_u32 = pt_smem_u32(sA), sB_u32 = pt_smem_u32(sB);
+    const uint32_t bar_u32[2] = {pt_smem_u32(&sBar[group * 2]), pt_smem_u32(&sBar[group * 2 + 1])};
+    uint32_t phase[2] = {0u, 0u};
+    const double gl = f.gamma * PT_L2E;
+    const double inv_scale = f.has_barrier ? 1.0 / f.b_scale : 0.0;
+    const bool leader = row == 0;
+
+    // one MMA tile: accumulator buffer `buf` <- A (128 x KT) * B[tile]^T (KT x PT_TC_N)
+    auto issue_tile = [&](int tile, int buf) {
+#pragma unroll
+        for (int ks = 0; ks < KT / 8; ++ks) {
+            const uint64_t da = pt_umma_desc(sA_u32 + (uint32_t)(2 * ks) * (PT_TC_M * 16), PT_TC_M * 16, 128);
+            const uint64_t db = pt_umma_desc(sB_u32 + (uint32_t)(2 * ks) * (uint32_t)(spad * 16) + (uint32_t)tile * (PT_TC_N * 16),
+                                             (uint32_t)(spad * 16), 128);
+            pt_umma_tf32(tmem_base + (uint32_t)buf * PT_TC_N, da, db, PT_TC_IDESC, ks > 0 ? 1u : 0u);
+        }
+        pt_umma_commit(bar_u32[buf]);
+    };
+
+    for (size_t chunk = (size_t)blockIdx.x * 2 + group; chunk * PT_TC_M < total; chunk += (size_t)gridDim.x * 2) {
+        const size_t idx = chunk * PT_TC_M + row;
+        const bool valid = idx < total;
+        const size_t ei = valid ? (rows.list ? (size_t)rows.list[idx] : idx) : 0;
+        double a[N], diff[N], p[N];
+        double seg = 0.0, lo = 0.0, hi = 1.0;
+        int sa = 1;
+        if (valid) {
+            double b[N];
+#pragma unroll
+            for (int d = 0; d < N; ++d) { a[d] = a_[ei * N + d]; b[d] = b_[ei * N + d]; }
+            seg = pt_segment<N>(a, b, diff);
+            sa = signs_a[ei];
+            if (!fresh && MODE == 0) { lo = lo_io[ei]; hi = hi_io[ei]; }
+        } else {
+#pragma unroll
+            for (int d = 0; d < N; ++d) { a[d] = 0.0; diff[d] = 0.0; }
+        }
+        bool active = valid && (MODE == 1 || __dmul_rn(seg, __dsub_rn(hi, lo)) > eps);
+        unsigned iters = 0;
+        double calib = 0.0;
+        while (pt_group_or(group, active)) {
+            const double mid = __dmul_rn(0.5, __dadd_rn(lo, hi));
+            double p2 = 0.0;
+#pragma unroll
+            for (int d = 0; d < N; ++d) {
+                p[d] = __dadd_rn(a[d], __dmul_rn(mid, diff[d]));
+                p2 = fma(p[d], p[d], p2);
+            }
+            {
+                // this point's row of A: tf32 pieces of q = 2 gl p and of c_p = -gl |p|^2, column order as in pt_pack_tc_kernel
+                float col[KT];
+#pragma unroll
+                for (int k = 0; k < KT; ++k) col[k] = 0.f;
+#pragma unroll
+                for (int d = 0; d < N; ++d) {
+                    float h, l, ll;
+                    pt_tf32_split3(2.0 * gl * p[d], h, l, ll);
+                    col[d] = h; col[(N + 2) + d] = h; col[2 * (N + 2) + d] = l;
+                }
+                float ch, cl, cll;
+                pt_tf32_split3(-gl * p2, ch, cl, cll);
+                col[N] = ch;               col[N + 1] = 1.f;
+                col[(N + 2) + N] = cl;     col[(N + 2) + N + 1] = 1.f;
+                col[2 * (N + 2) + N] = cll; col[2 * (N + 2) + N + 1] = 1.f;
+#pragma unroll
+                for (int c = 0; c < KC; ++c)
+                    *reinterpret_cast<float4*>(sA + ((size_t)c * PT_TC_M + row) * 4) =
+                        make_float4(col[4 * c], col[4 * c + 1], col[4 * c + 2], col[4 * c + 3]);
+            }
+            pt_fence_async_smem();
+            pt_group_sync(group);
+            if (leader) {
+                pt_tc_fence_after();
+                issue_tile(0, 0);
+                if (ntiles > 1) issue_tile(1, 1);
+            }
+            double acc = 0.0, ab = 0.0;
+            const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+            for (int t = 0; t < ntiles; ++t) {
+                const int buf = t & 1;
+                pt_mbar_wait(bar_u32[buf], phase[buf]);
+                phase[buf] ^= 1u;
+                pt_tc_fence_after();
+                const uint32_t taddr = tmem_base + lane_base + (uint32_t)(buf * PT_TC_N);
+                const float* wrow = sW + t * PT_TC_N;
+                uint32_t r0[32], r1[32];
+                pt_tmem_ld32(taddr, r0);
+#pragma unroll
+                for (int blk = 0; blk < PT_TC_N / 32; ++blk) {
+                    pt_tmem_wait_ld();
+                    uint32_t (&cur)[32] = (blk & 1) ? r1 : r0;
+                    uint32_t (&nxt)[32] = (blk & 1) ? r0 : r1;
+                    if (blk + 1 < PT_TC_N / 32) pt_tmem_ld32(taddr + (uint32_t)(blk + 1) * 32, nxt);
+                    if (MODE == 0) {
+                        float fa = 0.f, fb = 0.f;
+#pragma unroll
+                        for (int c4 = 0; c4 < 8; ++c4) {
+                            const float4 w4 = *reinterpret_cast<const float4*>(wrow + blk * 32 + c4 * 4);
+                            const float e0 = pt_ex2(__uint_as_float(cur[c4 * 4 + 0]));
+                            const float e1 = pt_ex2(__uint_as_float(cur[c4 * 4 + 1]));
+                            const float e2 = pt_ex2(__uint_as_float(cur[c4 * 4 + 2]));
+                            const float e3 = pt_ex2(__uint_as_float(cur[c4 * 4 + 3]));
+                            fa = fmaf(w4.x, e0, fa); fb = fmaf(fabsf(w4.x), e0, fb);
+                            fa = fmaf(w4.y, e1, fa); fb = fmaf(fabsf(w4.y), e1, fb);
+                            fa = fmaf(w4.z, e2, fa); fb = fmaf(fabsf(w4.z), e2, fb);
+                            fa = fmaf(w4.w, e3, fa); fb = fmaf(fabsf(w4.w), e3, fb);
+                        }
+                        acc += (double)fa; ab += (double)fb;   // 32-term fp32 chunks
+                    } else {
+                        // calibration: exact exponent from the fp64 rows (row layout: 2 gl s_d, w, -gl |s|^2)
+                        const int ROW = PT_ROW64(N);
+                        for (int c = 0; c < 32; ++c) {
+                            const long long j = (long long)t * PT_TC_N + blk * 32 + c;
+                            if (j < f.S) {
+                                const double* srow = f.sv + j * ROW;
+                                double ex = srow[N + 1] - gl * p2;
+#pragma unroll
+                                for (int d = 0; d < N; ++d) ex = fma(p[d], srow[d], ex);
+                                calib = fmax(calib, fabs((double)__uint_as_float(cur[c]) - ex));
+                            }
+                        }
+                    }
+                }
+                pt_tc_fence_before();
+                if (t + 2 < ntiles) {
+                    pt_group_sync(group);
+                    if (leader) { pt_tc_fence_after(); issue_tile(t + 2, buf); }
+                }
+            }
+            const double pn = sqrt(p2) + f.smax;
+            if (MODE == 1) {
+                calib = calib / (PT_U32 * gl * pn * pn);
+                active = false;
+            } else {
+                double F = f.bias + acc, eb = 0.0;
+                if (f.has_barrier) F -= pt_barrier_fast<N>(f, p, inv_scale, eb);
+                // |arg_tc - arg| <= PT_TC_ARG_ULPS u T (tf32 splits + tensor-core accumulation, calibrated);
+                // ex2.approx, weight rounding, products and the 32-term fp32 chunks add < 80 u relative
+                const double rel = 1.01 * (PT_TC_ARG_ULPS * PT_U32 * gl * pn * pn * PT_LN2) + 80.0 * PT_U32;
+                const double E = 2.0 * rel * ab + eb + 1e-280;
+                if (active) {
+                    if (fabs(F) > E) {
+                        if ((F > 0.0 ? 1 : -1) == sa) lo = mid; else hi = mid;
+                        ++iters;
+                        const double w = __dsub_rn(hi, lo);
+                        active = __dmul_rn(seg, w) > eps && w > PT_FP32_STOP_WIDTH;
+                    } else {
+                        active = false;   // sign not certain in fp32 (or NaN): stop with the current bracket
+                    }
+                }
+            }
+        }
+        if (MODE == 0) {
+            unsigned mine = iters;
+            for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
+            if ((tid & 31) == 0 && mine) atomicAdd(&work[2], (unsigned long long)mine);
+            if (valid) { lo_io[ei] = lo; hi_io[ei] = hi; }
+        } else if (valid) {
+            hi_io[ei] = calib;
+        }
+    }
+    pt_tc_fence_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*sTmem), "r"(512u));
+}
+#endif
