@@ -169,6 +169,28 @@ int pt_trace_points(pt_trace* t, double* out);
  * pairs != NULL (call once with NULL to size) */
 long long pt_trace_adjacency(pt_trace* t, long long* pairs, long long cap);
 
+/* ---- owner-hashed sharded BFS (multi-GPU) ------------------------------------------
+ * Rank r of `world` owns the canonical edges whose base lattice vertex hashes to r.  Per wave the caller runs
+ * candidates -> all_to_all of the 16-byte records -> admit -> rank the winner tags across ranks -> commit.
+ * A record is two 64-bit words (packed edge key, tag); tag = ((global admission index of the parent edge * stride
+ * + coface ordinal) << 1) | (sign at base > 0), i.e. the reference's slot order (tracer.py:359-375), comparable
+ * across ranks.  The trace must have a clamp box (all ranks pack keys in the same window). */
+/* after pt_trace_locate (run identically on every rank): keep the owned edges, remember their global indices */
+int pt_trace_shard(pt_trace* t, int rank, int world);
+/* expand the local frontier; counts[world] = records per owner rank (bucketed in that order) */
+int pt_trace_wave_candidates(pt_trace* t, long long* counts);
+/* the bucketed records of the last pt_trace_wave_candidates: out[sum(counts)][2] (host or device) */
+int pt_trace_wave_fetch(pt_trace* t, long long* out);
+/* owner side: records[count][2] received from all ranks (host or device); *n_winners = new edges owned here */
+int pt_trace_wave_admit(pt_trace* t, const long long* records, long long count, long long* n_winners);
+/* tags of the winners of the last admit, ascending: out[n_winners] */
+int pt_trace_wave_winner_tags(pt_trace* t, long long* out);
+/* gidx[n_winners] = global admission index of each winner (tag order), -1 for winners beyond max_edges (they
+ * must be a suffix); alive = number of non-negative entries; global_total = edges admitted by all ranks so far */
+int pt_trace_wave_commit(pt_trace* t, const long long* gidx, long long alive, long long global_total);
+/* global admission indices of local edges [first, first+count) */
+int pt_trace_gidx(pt_trace* t, long long first, long long count, long long* out);
+
 /* ---- coarse cells (subdivision.py:132-141, lattice.py:245-266) ------------------------------ */
 int pt_cells_from_trace(pt_trace* t, pt_cells** out);
 /* same from canonical edges given on the host: base[E,n] int32, mask[E] uint32 */

@@ -96,6 +96,13 @@ _SIGS = {
     "pt_trace_frontier": (_i, [_vp, C.POINTER(_ll), C.POINTER(_ll)]),
     "pt_trace_points": (_i, [_vp, _vp]),
     "pt_trace_adjacency": (_ll, [_vp, _vp, _ll]),
+    "pt_trace_shard": (_i, [_vp, _i, _i]),
+    "pt_trace_wave_candidates": (_i, [_vp, _vp]),
+    "pt_trace_wave_fetch": (_i, [_vp, _vp]),
+    "pt_trace_wave_admit": (_i, [_vp, _vp, _ll, C.POINTER(_ll)]),
+    "pt_trace_wave_winner_tags": (_i, [_vp, _vp]),
+    "pt_trace_wave_commit": (_i, [_vp, _vp, _ll, _ll]),
+    "pt_trace_gidx": (_i, [_vp, _ll, _ll, _vp]),
     "pt_cells_from_trace": (_i, [_vp, _pp]),
     "pt_cells_from_edges": (_i, [_vp, _i, _vp, _vp, _ll, _pp]),
     "pt_cells_from_host": (_i, [_vp, _i, _vp, _vp, _ll, _pp]),

@@ -532,6 +532,9 @@ pt_bisect_resolve_kernel(PtFieldDev f, PtRows rows, const double* __restrict__ a
 //   of r stays eta/s_min away from both cell ends (there every sign the reference bisection can see is certain).
 //   Everything else (<1 % of the rows) is flagged for the plain fp64 bisection kernel.
 #define PT_U64 1.1102230246251565e-16   /* 2^-53 */
+#ifndef PT_NEWTON_MINB
+#define PT_NEWTON_MINB 4
+#endif
 
 // two points per thread, each lane walks all support rows (G = 1): the row loads and the loop overhead are shared
 // by four independent chains (2 rows x 2 points), so the FP64 pipe rather than the issue slot is the limiter
@@ -587,7 +590,7 @@ __device__ __forceinline__ void pt_rbf_block_sum_x2(const PtFieldDev& f, const d
 }
 
 template <int N, int G>
-__global__ void __launch_bounds__(G == 1 ? 128 : PT_EVAL_THREADS, G == 1 ? 3 : 1)
+__global__ void __launch_bounds__(G == 1 ? 128 : PT_EVAL_THREADS, G == 1 ? PT_NEWTON_MINB : 1)
 pt_bisect_newton_kernel(PtFieldDev f, double sum_abs_w, const double* __restrict__ a_, const double* __restrict__ b_,
                         const int8_t* __restrict__ signs_a, double* __restrict__ lo_io, double* __restrict__ hi_io,
                         size_t m, double eps, double* __restrict__ out, uint8_t* __restrict__ slow,

@@ -285,6 +285,7 @@ pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __res
                 const uint32_t taddr = tmem_base + lane_base + (uint32_t)(buf * PT_TC_N);
                 const float* wrow = sW + t * PT_TC_N;
                 uint32_t r0[32], r1[32];
+                float fa_t[PT_TC_N / 32], fb_t[PT_TC_N / 32];
                 pt_tmem_ld32(taddr, r0);
 #pragma unroll
                 for (int blk = 0; blk < PT_TC_N / 32; ++blk) {
@@ -306,7 +307,7 @@ pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __res
                             fa = fmaf(w4.z, e2, fa); fb = fmaf(fabsf(w4.z), e2, fb);
                             fa = fmaf(w4.w, e3, fa); fb = fmaf(fabsf(w4.w), e3, fb);
                         }
-                        acc += (double)fa; ab += (double)fb;   // 32-term fp32 chunks
+                        fa_t[blk] = fa; fb_t[blk] = fb;        // 32-term fp32 chains
                     } else {
                         // calibration: exact exponent from the fp64 rows (row layout: 2 gl s_d, w, -gl |s|^2)
                         const int ROW = PT_ROW64(N);
@@ -322,6 +323,11 @@ pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __res
                         }
                     }
                 }
+                if (MODE == 0) {
+                    // pairwise fp32 sum of the four chains (34 roundings at most), one conversion per tile
+                    acc += (double)((fa_t[0] + fa_t[1]) + (fa_t[2] + fa_t[3]));
+                    ab += (double)((fb_t[0] + fb_t[1]) + (fb_t[2] + fb_t[3]));
+                }
                 pt_tc_fence_before();
                 if (t + 2 < ntiles) {
                     pt_group_sync(group);
@@ -336,7 +342,7 @@ pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __res
                 double F = f.bias + acc, eb = 0.0;
                 if (f.has_barrier) F -= pt_barrier_fast<N>(f, p, inv_scale, eb);
                 // |arg_tc - arg| <= PT_TC_ARG_ULPS u T (tf32 splits + tensor-core accumulation, calibrated);
-                // ex2.approx, weight rounding, products and the 32-term fp32 chunks add < 80 u relative
+                // ex2.approx, weight rounding, products and the 32-term fp32 chains (+2 pairwise levels) add < 80 u relative
                 const double rel = 1.01 * (PT_TC_ARG_ULPS * PT_U32 * gl * pn * pn * PT_LN2) + 80.0 * PT_U32;
                 const double E = 2.0 * rel * ab + eb + 1e-280;
                 if (active) {

@@ -960,3 +960,383 @@ long long pt_trace_adjacency(pt_trace* t, long long* pairs, long long cap) {
 }
 
 }  // extern "C"
+
+// ==== owner-hashed sharded BFS (multi-GPU) =============================================================
+// Rank r of W owns the canonical edges whose base lattice vertex hashes to r.  One wave:
+//   pt_trace_wave_candidates  expand the local frontier (probe signs, evaluate unknown vertices, partner rule,
+//                             box clamp) and emit one 16-byte record per surviving candidate,
+//                             (edge key, tag) with tag = (parent's GLOBAL admission index * stride + coface ordinal)*2
+//                             + (sign at base > 0), bucketed by owner rank  -> all_to_all by the caller
+//   pt_trace_wave_admit       the owner inserts the records it received into its visited shard with atomicMin(tag):
+//                             the winner of a new edge is its first occurrence in the reference's slot order;
+//                             winners come back sorted by tag
+//   pt_trace_wave_commit      after the caller ranked all ranks' winner tags (global admission indices), the
+//                             winners join the local edge list and form the next local frontier
+// Tags are comparable across ranks, so the union of the ranks' edge lists ordered by global index IS the
+// single-GPU (= reference) admission order.
+PT_HD int pt_owner_of(const PtGeom& g, u64 edge_key, int world) {
+    return (int)(pt_mix(pt_edge_vkey(g, edge_key) * 0x9E3779B97F4A7C15ull + 0x632BE59BD9B4E019ull) % (u64)world);
+}
+
+__global__ void pt_shard_select_kernel(PtGeom g, const u64* __restrict__ edge_key, const int8_t* __restrict__ edge_sa,
+                                       size_t count, int rank, int world, u64* __restrict__ out_gidx,
+                                       u64* __restrict__ out_key, int8_t* __restrict__ out_sa, unsigned long long* counter) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool mine = i < count && pt_owner_of(g, edge_key[i], world) == rank;
+    const unsigned long long pos = pt_warp_append(counter, mine);
+    if (mine) { out_gidx[pos] = (u64)i; out_key[pos] = edge_key[i]; out_sa[pos] = edge_sa[i]; }
+}
+
+__global__ void pt_shard_fill_kernel(PtTable vis, const u64* __restrict__ gidx_sorted, const uint32_t* __restrict__ order,
+                                     const u64* __restrict__ key_in, const int8_t* __restrict__ sa_in, size_t count,
+                                     u64* __restrict__ edge_key, int8_t* __restrict__ edge_sa, u64* __restrict__ edge_gidx,
+                                     unsigned* err) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const uint32_t src = order[i];
+    const u64 key = key_in[src];
+    edge_key[i] = key; edge_sa[i] = sa_in[src]; edge_gidx[i] = gidx_sorted[i];
+    bool ins;
+    const u64 slot = pt_table_insert(vis, key, ins, err);
+    vis.ent[2 * slot + 1] = (u64)i;
+}
+
+// partner stage of a sharded wave: emit (edge key, tag) instead of touching a visited table
+__global__ void __launch_bounds__(256)
+pt_wave_emit_kernel(PtGeom g, PtTable sgn, const u64* __restrict__ edge_key, const int8_t* __restrict__ edge_sa,
+                    const u64* __restrict__ edge_gidx, const uint32_t* __restrict__ frontier, size_t fcount, int stride,
+                    const uint32_t* __restrict__ sgn_slot, u64* __restrict__ cand, unsigned long long* cand_count,
+                    PtCounters* ctr) {
+    const size_t w = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= fcount) return;
+    const uint32_t e = frontier[w];
+    const u64 ek = edge_key[e];
+    const int sa = edge_sa[e];
+    const u64 parent = edge_gidx[e];
+    const uint32_t s = pt_edge_mask(g, ek);
+    int u[PT_NMAX];
+    pt_unpack_vertex(g, pt_edge_vkey(g, ek), u);
+    const int nc = pt_ncofaces(g.n, s);
+    for (int j0 = 0; j0 < nc; j0 += 32) {
+        const int j = j0 + lane;
+        bool emit = false, dropped = false;
+        u64 key = 0, tag = 0;
+        if (j < nc) {
+            const int sc = pt_ld_cg(&sgn.ent[2 * (u64)sgn_slot[w * stride + j] + 1]) ? 1 : -1;
+            PtPartner p = pt_partner(g.n, u, s, sa, j, sc);
+            int other[PT_NMAX];
+            pt_apply_masks(g.n, p.base, p.mask, 0u, other);
+            if (!(pt_in_box(g, p.base) && pt_in_box(g, other))) dropped = true;
+            else {
+                u64 bk;
+                if (!pt_pack_vertex(g, p.base, bk)) atomicOr(&ctr->error, PT_ERR_KEY_RANGE);
+                else {
+                    key = pt_edge_key(g, bk, p.mask);
+                    tag = ((parent * (u64)stride + (u64)j) << 1) | (p.sign_base > 0 ? 1ull : 0ull);
+                    emit = true;
+                }
+            }
+        }
+        const unsigned db = __ballot_sync(0xffffffffu, dropped);
+        if (lane == 0 && db) atomicAdd(&ctr->dropped, (unsigned long long)__popc(db));
+        const unsigned long long pos = pt_warp_append(cand_count, emit);
+        if (emit) { cand[2 * pos] = key; cand[2 * pos + 1] = tag; }
+    }
+}
+
+__global__ void pt_owner_count_kernel(PtGeom g, const u64* __restrict__ cand, size_t count, int world,
+                                      unsigned long long* __restrict__ hist) {
+    __shared__ unsigned int local[64];
+    if (threadIdx.x < 64) local[threadIdx.x] = 0;
+    __syncthreads();
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) atomicAdd(&local[pt_owner_of(g, cand[2 * i], world)], 1u);
+    __syncthreads();
+    if (threadIdx.x < world && local[threadIdx.x]) atomicAdd(&hist[threadIdx.x], (unsigned long long)local[threadIdx.x]);
+}
+
+__global__ void pt_owner_scatter_kernel(PtGeom g, const u64* __restrict__ cand, size_t count, int world,
+                                        unsigned long long* __restrict__ cursor, u64* __restrict__ out) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const u64 key = cand[2 * i], tag = cand[2 * i + 1];
+    const unsigned long long pos = atomicAdd(&cursor[pt_owner_of(g, key, world)], 1ull);
+    out[2 * pos] = key; out[2 * pos + 1] = tag;
+}
+
+// owner side: claim the edge for the smallest tag seen this wave (already admitted edges keep their small index)
+__global__ void pt_shard_insert_kernel(PtTable vis, const u64* __restrict__ rec, size_t count, uint32_t* __restrict__ slot_out,
+                                       unsigned* err) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    bool ins;
+    const u64 slot = pt_table_insert(vis, rec[2 * i], ins, err);
+    atomicMin(&vis.ent[2 * slot + 1], PT_VAL_PENDING_BASE + rec[2 * i + 1]);
+    slot_out[i] = (uint32_t)slot;
+}
+
+__global__ void pt_shard_winners_kernel(PtTable vis, const u64* __restrict__ rec, const uint32_t* __restrict__ slot_in,
+                                        size_t count, u64* __restrict__ win_tag, u64* __restrict__ win_key,
+                                        unsigned long long* counter) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool win = false;
+    if (i < count) win = pt_ld_cg(&vis.ent[2 * (u64)slot_in[i] + 1]) == PT_VAL_PENDING_BASE + rec[2 * i + 1];
+    const unsigned long long pos = pt_warp_append(counter, win);
+    if (win) { win_tag[pos] = rec[2 * i + 1]; win_key[pos] = rec[2 * i]; }
+}
+
+__global__ void pt_shard_commit_kernel(PtTable vis, const u64* __restrict__ win, const long long* __restrict__ gidx,
+                                       size_t count, long long first_local, u64* __restrict__ edge_key,
+                                       int8_t* __restrict__ edge_sa, u64* __restrict__ edge_gidx) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    const u64 tag = win[2 * i], key = win[2 * i + 1];
+    u64 slot;
+    if (!pt_table_find(vis, key, slot)) return;
+    if (gidx[i] >= 0) {
+        const long long idx = first_local + (long long)i;      // dead winners (cap) are a suffix in tag order
+        edge_key[idx] = key; edge_sa[idx] = (tag & 1ull) ? (int8_t)1 : (int8_t)-1; edge_gidx[idx] = (u64)gidx[i];
+        vis.ent[2 * slot + 1] = (u64)idx;
+    } else {
+        vis.ent[2 * slot + 1] = PT_VAL_DEAD;
+    }
+}
+
+__global__ void pt_interleave_kernel(const u64* __restrict__ a, const u64* __restrict__ b, size_t count, u64* __restrict__ out) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) { out[2 * i] = a[i]; out[2 * i + 1] = b[i]; }
+}
+
+extern "C" {
+
+int pt_trace_shard(pt_trace* t, int rank, int world) {
+    if (!t) return pt_fail(nullptr, PT_E_INVALID, "trace is NULL");
+    pt_ctx* ctx = t->ctx;
+    if (world < 1 || world > 64 || rank < 0 || rank >= world) return pt_fail(ctx, PT_E_INVALID, "bad rank/world (%d/%d; at most 64 ranks)", rank, world);
+    if (!t->geom.has_box) return pt_fail(ctx, PT_E_STATE, "the sharded trace needs a clamp box (every rank must pack keys in the same window)");
+    if (t->levels != 0 || !t->range_frontier) return pt_fail(ctx, PT_E_STATE, "pt_trace_shard must follow pt_trace_locate directly");
+    const size_t E = (size_t)t->n_edges;
+    t->rank = rank; t->world = world; t->n_global = (long long)E;
+    PtBuf<u64> gidx, key, gidx_sorted; PtBuf<int8_t> sa; PtBuf<uint32_t> order_in, order; PtBuf<unsigned long long> counter;
+    PT_TRY(gidx.alloc(ctx, E + 1)); PT_TRY(key.alloc(ctx, E + 1)); PT_TRY(sa.alloc(ctx, E + 1));
+    PT_TRY(gidx_sorted.alloc(ctx, E + 1)); PT_TRY(order_in.alloc(ctx, E + 1)); PT_TRY(order.alloc(ctx, E + 1));
+    PT_TRY(counter.alloc(ctx, 1));
+    PT_CUDA(ctx, cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), ctx->stream));
+    size_t mine = 0;
+    if (E) {
+        PT_LAUNCH(ctx, "trace_shard");
+        pt_shard_select_kernel<<<pt_grid_for(E, 256), 256, 0, ctx->stream>>>(t->geom, t->edge_key.p, t->edge_sa.p, E, rank, world,
+                                                                             gidx.p, key.p, sa.p, counter.p);
+        PT_TRY(pt_check_launch(ctx, "pt_shard_select_kernel"));
+        unsigned long long* h = (unsigned long long*)ctx->pinned;
+        PT_CUDA(ctx, cudaMemcpyAsync(h, counter.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+        PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        mine = (size_t)*h;
+    }
+    // restore admission order among the kept edges, rebuild the visited shard from empty
+    PT_CUDA(ctx, cudaMemsetAsync(t->visited.ent.p, 0xFF, (size_t)t->visited.capacity * 2 * sizeof(u64), ctx->stream));
+    t->visited.count = 0;
+    PT_TRY(t->edge_gidx.ensure(ctx, mine + 1, 0));
+    if (mine) {
+        pt_iota_kernel<<<pt_grid_for(mine, 256), 256, 0, ctx->stream>>>(order_in.p, mine, 0u);
+        size_t tmp_bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, gidx.p, gidx_sorted.p, order_in.p, order.p, (int)mine, 0, 64, ctx->stream);
+        PtBuf<uint8_t> tmp;
+        PT_TRY(tmp.alloc(ctx, tmp_bytes));
+        PT_CUDA(ctx, cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, gidx.p, gidx_sorted.p, order_in.p, order.p, (int)mine, 0, 64, ctx->stream));
+        PT_TRY(pt_table_reserve(ctx, t->visited, (u64)mine));
+        pt_shard_fill_kernel<<<pt_grid_for(mine, 256), 256, 0, ctx->stream>>>(t->visited.view(), gidx_sorted.p, order.p, key.p, sa.p, mine,
+                                                                              t->edge_key.p, t->edge_sa.p, t->edge_gidx.p, &t->counters.p->error);
+        PT_TRY(pt_check_launch(ctx, "pt_shard_fill_kernel"));
+        t->visited.count = (u64)mine;
+    }
+    t->n_edges = (long long)mine;
+    PT_TRY(pt_set_range_frontier(t, 0, (long long)mine));
+    t->n_adj = -1;
+    // locate ran identically on every rank: its out-of-box drops are reported by rank 0 only
+    if (rank != 0)
+        PT_CUDA(ctx, cudaMemsetAsync((char*)t->counters.p + offsetof(PtCounters, dropped), 0, sizeof(unsigned long long), ctx->stream));
+    return pt_read_counters(t);
+}
+
+int pt_trace_wave_candidates(pt_trace* t, long long* counts) {
+    if (!t || !counts) return pt_fail(t ? t->ctx : nullptr, PT_E_INVALID, "pt_trace_wave_candidates: NULL argument");
+    pt_ctx* ctx = t->ctx;
+    PtGeom& g = t->geom;
+    const long long F = t->n_frontier;
+    const int stride = pt_stride_for(g.n), world = t->world;
+    const unsigned long long cand_before = t->host_counters.candidates;
+    for (int r = 0; r < world; ++r) counts[r] = 0;
+    t->n_cand = 0;
+    PtBuf<unsigned long long> cc;          // [0] candidate cursor, [1..world] histogram, [1+world..] scatter cursors
+    PT_TRY(cc.alloc(ctx, 2 * (size_t)world + 2));
+    PT_CUDA(ctx, cudaMemsetAsync(cc.p, 0, (2 * (size_t)world + 2) * sizeof(unsigned long long), ctx->stream));
+    PtBuf<u64> raw;
+    size_t chunk_edges = ((size_t)1 << 24) / (size_t)stride;
+    if (chunk_edges < 1024) chunk_edges = 1024;
+    PtBuf<uint32_t> sgn_slot, pending;
+    size_t emitted_bound = 0;
+    for (long long f0 = 0; f0 < F; f0 += (long long)chunk_edges) {
+        const size_t fc = (size_t)((F - f0) < (long long)chunk_edges ? (F - f0) : (long long)chunk_edges);
+        const size_t nslots = fc * (size_t)stride;
+        PT_TRY(sgn_slot.ensure(ctx, nslots, 0));
+        PT_TRY(pending.ensure(ctx, nslots, 0));
+        PT_TRY(pt_table_reserve(ctx, t->signs, nslots));
+        PT_TRY(pt_reset_pending(t));
+        const uint32_t* fr = t->frontier.p + f0;
+        {
+            PT_LAUNCH(ctx, "trace_wave_probe");
+            pt_wave_probe_kernel<<<pt_grid_for(fc * 32, 256), 256, 0, ctx->stream>>>(g, t->signs.view(), t->edge_key.p, fr, fc, stride,
+                                                                                       sgn_slot.p, pending.p, t->counters.p);
+            PT_TRY(pt_check_launch(ctx, "pt_wave_probe_kernel"));
+        }
+        PT_TRY(pt_read_counters(t));
+        PT_TRY(pt_eval_pending(t, pending.p, (size_t)t->host_counters.n_pending));
+        // every candidate of the chunks so far may survive the box clamp
+        emitted_bound = (size_t)(t->host_counters.candidates - cand_before);
+        PT_TRY(raw.ensure(ctx, 2 * emitted_bound + 2, 2 * (size_t)t->n_cand));
+        {
+            PT_LAUNCH(ctx, "trace_wave_emit");
+            pt_wave_emit_kernel<<<pt_grid_for(fc * 32, 256), 256, 0, ctx->stream>>>(g, t->signs.view(), t->edge_key.p, t->edge_sa.p,
+                                                                                      t->edge_gidx.p, fr, fc, stride, sgn_slot.p, raw.p,
+                                                                                      cc.p, t->counters.p);
+            PT_TRY(pt_check_launch(ctx, "pt_wave_emit_kernel"));
+        }
+        unsigned long long* h = (unsigned long long*)ctx->pinned;
+        PT_CUDA(ctx, cudaMemcpyAsync(h, cc.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+        PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        t->n_cand = (long long)*h;
+    }
+    PT_TRY(pt_read_counters(t));
+    const long long cands = (long long)(t->host_counters.candidates - cand_before);
+    t->levels += 1;
+    t->stages.insert(t->stages.end(), {2, t->levels, F, cands, cands});
+    t->stages.insert(t->stages.end(), {3, t->levels, cands, cands, cands});
+    const size_t C = (size_t)t->n_cand;
+    PT_TRY(t->cand.ensure(ctx, 2 * C + 2, 0));
+    if (C) {
+        {
+            PT_LAUNCH(ctx, "trace_owner_bucket");
+            pt_owner_count_kernel<<<pt_grid_for(C, 256), 256, 0, ctx->stream>>>(g, raw.p, C, world, cc.p + 1);
+            PT_TRY(pt_check_launch(ctx, "pt_owner_count_kernel"));
+        }
+        unsigned long long* h = (unsigned long long*)ctx->pinned;
+        PT_CUDA(ctx, cudaMemcpyAsync(h, cc.p + 1, (size_t)world * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+        PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        unsigned long long offs[64], run = 0;
+        for (int r = 0; r < world; ++r) { counts[r] = (long long)h[r]; offs[r] = run; run += h[r]; }
+        PT_CUDA(ctx, cudaMemcpyAsync(cc.p + 1 + world, offs, (size_t)world * sizeof(unsigned long long), cudaMemcpyHostToDevice, ctx->stream));
+        {
+            PT_LAUNCH(ctx, "trace_owner_bucket");
+            pt_owner_scatter_kernel<<<pt_grid_for(C, 256), 256, 0, ctx->stream>>>(g, raw.p, C, world, cc.p + 1 + world, t->cand.p);
+            PT_TRY(pt_check_launch(ctx, "pt_owner_scatter_kernel"));
+        }
+        PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));   // offs lives on this stack frame
+    }
+    return PT_OK;
+}
+
+int pt_trace_wave_fetch(pt_trace* t, long long* out) {
+    if (!t) return pt_fail(nullptr, PT_E_INVALID, "trace is NULL");
+    if (t->n_cand == 0) return PT_OK;
+    if (!out) return pt_fail(t->ctx, PT_E_INVALID, "output is NULL");
+    return pt_copy_out(t->ctx, (u64*)out, t->cand.p, 2 * (size_t)t->n_cand, true);
+}
+
+int pt_trace_wave_admit(pt_trace* t, const long long* records, long long count, long long* n_winners) {
+    if (!t || !n_winners) return pt_fail(t ? t->ctx : nullptr, PT_E_INVALID, "pt_trace_wave_admit: NULL argument");
+    pt_ctx* ctx = t->ctx;
+    *n_winners = 0; t->n_win = 0;
+    if (count < 0) return pt_fail(ctx, PT_E_INVALID, "negative record count");
+    if (count == 0) return PT_OK;
+    if (!records) return pt_fail(ctx, PT_E_INVALID, "records is NULL");
+    PtBuf<u64> tmp_rec; const u64* rec;
+    PT_TRY(pt_stage_in(ctx, (const u64*)records, 2 * (size_t)count, tmp_rec, &rec));
+    PT_TRY(pt_table_reserve(ctx, t->visited, (u64)count));
+    PtBuf<uint32_t> slot; PtBuf<u64> wtag, wkey, wtag_s, wkey_s; PtBuf<unsigned long long> counter;
+    PT_TRY(slot.alloc(ctx, (size_t)count));
+    PT_TRY(wtag.alloc(ctx, (size_t)count)); PT_TRY(wkey.alloc(ctx, (size_t)count));
+    PT_TRY(counter.alloc(ctx, 1));
+    PT_CUDA(ctx, cudaMemsetAsync(counter.p, 0, sizeof(unsigned long long), ctx->stream));
+    {
+        PT_LAUNCH(ctx, "trace_shard_admit");
+        pt_shard_insert_kernel<<<pt_grid_for((size_t)count, 256), 256, 0, ctx->stream>>>(t->visited.view(), rec, (size_t)count, slot.p,
+                                                                                          &t->counters.p->error);
+        PT_TRY(pt_check_launch(ctx, "pt_shard_insert_kernel"));
+        pt_shard_winners_kernel<<<pt_grid_for((size_t)count, 256), 256, 0, ctx->stream>>>(t->visited.view(), rec, slot.p, (size_t)count,
+                                                                                           wtag.p, wkey.p, counter.p);
+        PT_TRY(pt_check_launch(ctx, "pt_shard_winners_kernel"));
+    }
+    unsigned long long* h = (unsigned long long*)ctx->pinned;
+    PT_CUDA(ctx, cudaMemcpyAsync(h, counter.p, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+    PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    const size_t V = (size_t)*h;
+    PT_TRY(pt_read_counters(t));
+    t->visited.count += (u64)V;
+    t->n_win = (long long)V; *n_winners = (long long)V;
+    PT_TRY(t->win.ensure(ctx, 2 * V + 2, 0));
+    if (V) {
+        PT_TRY(wtag_s.alloc(ctx, V)); PT_TRY(wkey_s.alloc(ctx, V));
+        size_t tmp_bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, wtag.p, wtag_s.p, wkey.p, wkey_s.p, (int)V, 0, 64, ctx->stream);
+        PtBuf<uint8_t> tmp;
+        PT_TRY(tmp.alloc(ctx, tmp_bytes));
+        PT_LAUNCH(ctx, "trace_shard_admit");
+        PT_CUDA(ctx, cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, wtag.p, wtag_s.p, wkey.p, wkey_s.p, (int)V, 0, 64, ctx->stream));
+        pt_interleave_kernel<<<pt_grid_for(V, 256), 256, 0, ctx->stream>>>(wtag_s.p, wkey_s.p, V, t->win.p);
+        PT_TRY(pt_check_launch(ctx, "pt_interleave_kernel"));
+    }
+    return PT_OK;
+}
+
+int pt_trace_wave_winner_tags(pt_trace* t, long long* out) {
+    if (!t) return pt_fail(nullptr, PT_E_INVALID, "trace is NULL");
+    if (t->n_win == 0) return PT_OK;
+    if (!out) return pt_fail(t->ctx, PT_E_INVALID, "output is NULL");
+    pt_ctx* ctx = t->ctx;
+    cudaMemcpyKind kind = pt_is_device_ptr(out) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    PT_CUDA(ctx, cudaMemcpy2DAsync(out, sizeof(u64), t->win.p, 2 * sizeof(u64), sizeof(u64), (size_t)t->n_win, kind, ctx->stream));
+    PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return PT_OK;
+}
+
+int pt_trace_wave_commit(pt_trace* t, const long long* gidx, long long alive, long long global_total) {
+    if (!t) return pt_fail(nullptr, PT_E_INVALID, "trace is NULL");
+    pt_ctx* ctx = t->ctx;
+    const size_t V = (size_t)t->n_win;
+    if (alive < 0 || (size_t)alive > V) return pt_fail(ctx, PT_E_INVALID, "alive count out of range");
+    const long long before = t->n_edges;
+    if (V) {
+        if (!gidx) return pt_fail(ctx, PT_E_INVALID, "gidx is NULL");
+        PtBuf<long long> tmp; const long long* gdev;
+        PT_TRY(pt_stage_in(ctx, gidx, V, tmp, &gdev));
+        PT_TRY(t->edge_key.ensure(ctx, (size_t)(before + alive + 1), (size_t)before));
+        PT_TRY(t->edge_sa.ensure(ctx, (size_t)(before + alive + 1), (size_t)before));
+        PT_TRY(t->edge_gidx.ensure(ctx, (size_t)(before + alive + 1), (size_t)before));
+        PT_LAUNCH(ctx, "trace_shard_commit");
+        pt_shard_commit_kernel<<<pt_grid_for(V, 256), 256, 0, ctx->stream>>>(t->visited.view(), t->win.p, gdev, V, before,
+                                                                             t->edge_key.p, t->edge_sa.p, t->edge_gidx.p);
+        PT_TRY(pt_check_launch(ctx, "pt_shard_commit_kernel"));
+        PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    if ((size_t)alive < V) t->complete = false;
+    t->n_edges = before + alive;
+    t->n_global = global_total;
+    t->n_win = 0;
+    t->expanded_upto = before;
+    PT_TRY(pt_set_range_frontier(t, before, alive));
+    t->n_adj = -1;
+    return PT_OK;
+}
+
+int pt_trace_gidx(pt_trace* t, long long first, long long count, long long* out) {
+    if (!t) return pt_fail(nullptr, PT_E_INVALID, "trace is NULL");
+    if (first < 0 || count < 0 || first + count > t->n_edges) return pt_fail(t->ctx, PT_E_INVALID, "edge range out of bounds");
+    if (count == 0) return PT_OK;
+    if (!out) return pt_fail(t->ctx, PT_E_INVALID, "output is NULL");
+    if (t->world == 1 && t->edge_gidx.count < (size_t)t->n_edges) return pt_fail(t->ctx, PT_E_STATE, "trace is not sharded");
+    return pt_copy_out(t->ctx, (u64*)out, t->edge_gidx.p + first, (size_t)count, true);
+}
+
+}  // extern "C"

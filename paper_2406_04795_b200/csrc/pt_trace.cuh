@@ -53,6 +53,16 @@ struct pt_trace {
     // adjacency cache
     PtBuf<u64> adj;
     long long n_adj = -1;
+
+    // owner-hashed sharded BFS (pt_trace_shard / pt_trace_wave_*): this rank keeps the edges whose base lattice
+    // vertex hashes to it; every local edge carries its GLOBAL admission index
+    int rank = 0, world = 1;
+    PtBuf<u64> edge_gidx;
+    long long n_global = 0;        // edges admitted by all ranks so far
+    PtBuf<u64> cand;               // [n_cand][2] (edge key, tag) of the current wave, bucketed by owner rank
+    long long n_cand = 0;
+    PtBuf<u64> win;                // [n_win][2] (tag, edge key) winners of the last admit, ascending tag
+    long long n_win = 0;
 };
 
 struct pt_cells {

@@ -21,7 +21,7 @@ import ctypes as C
 
 import numpy as np
 
-__all__ = ["cell_slice", "owner_of_cell", "ShardedProof", "CudaEngine"]
+__all__ = ["cell_slice", "owner_of_cell", "rank_winners", "ShardedTrace", "ShardedProof", "CudaEngine"]
 
 
 def cell_slice(total: int, rank: int, world: int) -> tuple[int, int]:
@@ -50,6 +50,120 @@ def owner_of_cell(base, world: int) -> np.ndarray:
     return (h % np.uint64(world)).astype(np.int64)
 
 
+def rank_winners(tag_lists, mine: int, total_before: int, max_edges: int):
+    """Global admission indices of rank `mine`'s winners of one wave.
+
+    `tag_lists[r]` is rank r's ascending tensor of winner tags.  A tag is the reference's slot id of the
+    candidate (parent admission index, coface ordinal), so the wave's new edges are admitted in ascending tag
+    order over ALL ranks: index = total_before + number of winners anywhere with a smaller tag.  Winners at
+    or beyond `max_edges` are dead (-1) and the trace is incomplete, exactly like `_Tracer._admit`
+    (reference tracer.py:239-252).  Returns (gidx int64 tensor, alive, new_total, complete)."""
+    import torch
+    my = tag_lists[mine]
+    below = torch.zeros_like(my)
+    for tags in tag_lists:
+        if tags.numel():
+            below += torch.searchsorted(tags, my)
+    gidx = below + int(total_before)
+    dead = gidx >= int(max_edges)
+    gidx = torch.where(dead, torch.full_like(gidx, -1), gidx)
+    wave_total = sum(int(t.numel()) for t in tag_lists)
+    new_total = min(int(total_before) + wave_total, int(max_edges))
+    complete = int(total_before) + wave_total <= int(max_edges)
+    return gidx, int((~dead).sum().item()), new_total, complete
+
+
+class ShardedTrace:
+    """Owner-hashed BFS over the process group (the north star's multi-GPU trace).
+
+    Rank r owns the edges whose base lattice vertex hashes to r.  Every wave: expand the local frontier,
+    all_to_all the 16-byte candidate records to their owners, admit by minimum tag on the owner, rank the
+    winners' tags over all ranks (all_gather) so that every new edge gets its GLOBAL admission index,
+    commit.  The union of the ranks' edges ordered by that index is the single-GPU (= reference) edge list.
+
+    `engine` implements (records / tags are int64 torch tensors on `engine.tensor_device`):
+        trace_locate(seeds, rank, world) -> (local_frontier, global_total)
+        wave_candidates() -> (records [K, 2] bucketed by owner rank, counts list[int] of length world)
+        wave_admit(records [M, 2]) -> ascending winner tags [V]
+        wave_commit(gidx [V], alive, global_total) -> None
+        trace_counters() -> dict(dropped=..., field_evaluations=..., candidates=...)   (local)
+        local_edges() -> (gidx [E], payload [E, P])
+    """
+
+    def __init__(self, engine, group=None):
+        import torch.distributed as dist
+        self.engine, self.group, self.dist = engine, group, dist
+        self.on = dist.is_available() and dist.is_initialized()
+        self.rank = dist.get_rank(group) if self.on else 0
+        self.world = dist.get_world_size(group) if self.on else 1
+
+    # -- collectives (identity when there is no process group) --
+    def _sum(self, values):
+        import torch
+        t = torch.tensor(list(values), dtype=torch.int64, device=self.engine.tensor_device)
+        if self.world > 1:
+            self.dist.all_reduce(t, group=self.group)
+        return [int(v) for v in t.tolist()]
+
+    def _exchange(self, records, counts):
+        import torch
+        if self.world == 1:
+            return records
+        dev = self.engine.tensor_device
+        send = torch.tensor(counts, dtype=torch.int64, device=dev)
+        recv = torch.zeros_like(send)
+        self.dist.all_to_all_single(recv, send, group=self.group)
+        recv_counts = [int(v) for v in recv.tolist()]
+        out = torch.empty((sum(recv_counts), 2), dtype=torch.int64, device=dev)
+        self.dist.all_to_all_single(out, records.contiguous(), output_split_sizes=recv_counts,
+                                    input_split_sizes=[int(c) for c in counts], group=self.group)
+        return out
+
+    def _gather_var(self, tensor):
+        """all_gather of per-rank tensors with different leading sizes -> list of tensors."""
+        import torch
+        if self.world == 1:
+            return [tensor]
+        dev = self.engine.tensor_device
+        size = torch.tensor([tensor.shape[0]], dtype=torch.int64, device=dev)
+        sizes = [torch.zeros_like(size) for _ in range(self.world)]
+        self.dist.all_gather(sizes, size, group=self.group)
+        sizes = [int(x.item()) for x in sizes]
+        padded = torch.zeros((max(max(sizes), 1),) + tuple(tensor.shape[1:]), dtype=tensor.dtype, device=dev)
+        padded[: tensor.shape[0]] = tensor
+        parts = [torch.empty_like(padded) for _ in range(self.world)]
+        self.dist.all_gather(parts, padded, group=self.group)
+        return [parts[r][: sizes[r]] for r in range(self.world)]
+
+    def run(self, seeds, max_edges: int) -> dict:
+        eng = self.engine
+        local_frontier, total = eng.trace_locate(seeds, self.rank, self.world)
+        frontier = self._sum([local_frontier])[0]
+        levels, complete = 0, total <= max_edges
+        while frontier > 0 and complete:
+            records, counts = eng.wave_candidates()
+            received = self._exchange(records, counts)
+            tags = eng.wave_admit(received)
+            gidx, alive, new_total, complete = rank_winners(self._gather_var(tags), self.rank, total, max_edges)
+            eng.wave_commit(gidx, alive, new_total)
+            frontier, total = new_total - total, new_total
+            levels += 1
+        c = eng.trace_counters()
+        dropped, evaluations, candidates = self._sum([c["dropped"], c["field_evaluations"], c["candidates"]])
+        return dict(trace_edges=total, levels=levels, complete=complete, dropped_out_of_box=dropped,
+                    vertex_evaluations=evaluations, candidates_bfs=candidates,
+                    closure_ok=bool(total > 0 and complete and dropped == 0))
+
+    def gather_edges(self):
+        """Every rank's edges merged in global admission order: (gidx [E], payload [E, P])."""
+        import torch
+        gidx, payload = self.engine.local_edges()
+        all_g = torch.cat(self._gather_var(gidx))
+        all_p = torch.cat(self._gather_var(payload))
+        order = torch.argsort(all_g)
+        return all_g[order], all_p[order]
+
+
 class ShardedProof:
     """trace -> coarse_cells -> refine(+check) with the refinement sharded over the process group.
 
@@ -72,7 +186,16 @@ class ShardedProof:
     def run(self, seeds) -> dict:
         import torch
         dist, eng = self.dist, self.engine
-        info = dict(eng.trace(seeds))
+        if self.world > 1 and hasattr(eng, "trace_locate") and getattr(eng, "shard_trace", True):
+            # owner-hashed BFS; the merged edge list (global admission order) feeds the replicated cell build
+            st = ShardedTrace(eng, self.group)
+            info = st.run(seeds, int(eng.max_edges))
+            if hasattr(eng, "local_points"):
+                eng.local_points()                 # coarse-edge intersection points: each rank solves its own edges
+            _, payload = st.gather_edges()
+            info["cells"] = eng.cells_from_edges(payload)
+        else:
+            info = dict(eng.trace(seeds))
         first, count = cell_slice(info["cells"], self.rank, self.world)
         pts, crossing = eng.candidates(first, count)
         dev = eng.tensor_device
@@ -161,6 +284,102 @@ class CudaEngine:
         return dict(trace_edges=edges, levels=int(st.levels), candidates_bfs=int(st.candidates),
                     vertex_evaluations=int(st.field_evaluations), closure_ok=bool(st.closure_ok),
                     cells=int(lib.pt_cells_count(cells)))
+
+    # ---- ShardedTrace protocol ------------------------------------------------------------------------
+    @property
+    def max_edges(self):
+        return min(int(self.cfg.max_edges), (1 << 31) - 2)
+
+    def trace_locate(self, seeds, rank, world):
+        lib, cabi, torch = self._cabi.lib, self._cabi, self.torch
+        self._drop()
+        if isinstance(seeds, torch.Tensor):
+            ptr, m = seeds.data_ptr(), seeds.shape[0]
+        else:
+            seeds = np.ascontiguousarray(seeds, dtype=np.float64)
+            ptr, m = seeds.ctypes.data, seeds.shape[0]
+        if self.lo is None:
+            raise ValueError("the sharded trace needs TraceConfig.box (all ranks must share one key window)")
+        trace = C.c_void_p()
+        cabi.check(lib.pt_trace_create(self.ctx.handle, self.field, self.n, self.cfg.lattice.scale, self.offset.ctypes.data,
+                                       self.lo.ctypes.data, self.hi.ctypes.data, self.max_edges, float(self.cfg.eps), C.byref(trace)))
+        self._trace, self.world = trace, world
+        cabi.check(lib.pt_trace_locate(trace, C.c_void_p(ptr), m))
+        st = cabi.TraceStats()
+        cabi.check(lib.pt_trace_get_stats(trace, C.byref(st)))
+        total = int(st.visited_edges)
+        cabi.check(lib.pt_trace_shard(trace, rank, world))
+        cabi.check(lib.pt_trace_get_stats(trace, C.byref(st)))
+        return int(st.frontier), total
+
+    def wave_candidates(self):
+        lib, cabi, torch = self._cabi.lib, self._cabi, self.torch
+        counts = np.zeros(self.world, dtype=np.int64)
+        cabi.check(lib.pt_trace_wave_candidates(self._trace, counts.ctypes.data))
+        rec = torch.empty((int(counts.sum()), 2), dtype=torch.int64, device=self.tensor_device)
+        if rec.shape[0]:
+            cabi.check(lib.pt_trace_wave_fetch(self._trace, C.c_void_p(rec.data_ptr())))
+        return rec, [int(c) for c in counts]
+
+    def wave_admit(self, records):
+        lib, cabi, torch = self._cabi.lib, self._cabi, self.torch
+        records = records.contiguous()
+        won = C.c_longlong(0)
+        cabi.check(lib.pt_trace_wave_admit(self._trace, C.c_void_p(records.data_ptr()) if records.shape[0] else None,
+                                           records.shape[0], C.byref(won)))
+        tags = torch.empty(int(won.value), dtype=torch.int64, device=self.tensor_device)
+        if tags.shape[0]:
+            cabi.check(lib.pt_trace_wave_winner_tags(self._trace, C.c_void_p(tags.data_ptr())))
+        return tags
+
+    def wave_commit(self, gidx, alive, global_total):
+        gidx = gidx.contiguous()
+        self._cabi.check(self._cabi.lib.pt_trace_wave_commit(
+            self._trace, C.c_void_p(gidx.data_ptr()) if gidx.shape[0] else None, int(alive), int(global_total)))
+
+    def trace_counters(self):
+        st = self._cabi.TraceStats()
+        self._cabi.check(self._cabi.lib.pt_trace_get_stats(self._trace, C.byref(st)))
+        return dict(dropped=int(st.dropped_out_of_box), field_evaluations=int(st.field_evaluations), candidates=int(st.candidates))
+
+    def local_edges(self):
+        """(gidx [E], payload [E, n + 2] = base coordinates, step mask, sign at base) of this rank's edges."""
+        lib, cabi, torch = self._cabi.lib, self._cabi, self.torch
+        st = cabi.TraceStats()
+        cabi.check(lib.pt_trace_get_stats(self._trace, C.byref(st)))
+        E = int(st.visited_edges)
+        base = np.zeros((E, self.n), dtype=np.int32); mask = np.zeros(E, dtype=np.uint32); sa = np.zeros(E, dtype=np.int8)
+        gidx = np.zeros(E, dtype=np.int64)
+        if E:
+            cabi.check(lib.pt_trace_edges(self._trace, 0, E, base.ctypes.data, mask.ctypes.data, sa.ctypes.data))
+            cabi.check(lib.pt_trace_gidx(self._trace, 0, E, gidx.ctypes.data))
+        payload = np.concatenate([base.astype(np.int64), mask.astype(np.int64)[:, None], sa.astype(np.int64)[:, None]], axis=1)
+        return (torch.from_numpy(gidx).to(self.tensor_device), torch.from_numpy(payload).to(self.tensor_device))
+
+    def local_points(self):
+        """Intersection points of this rank's traced edges (the reference's trace() returns them), kept in HBM."""
+        lib, cabi, torch = self._cabi.lib, self._cabi, self.torch
+        st = cabi.TraceStats()
+        cabi.check(lib.pt_trace_get_stats(self._trace, C.byref(st)))
+        E = int(st.visited_edges)
+        self.trace_points = torch.empty((max(E, 1), self.n), dtype=torch.float64, device=self.tensor_device)
+        if E:
+            cabi.check(lib.pt_trace_points(self._trace, C.c_void_p(self.trace_points.data_ptr())))
+        return self.trace_points[:E]
+
+    def cells_from_edges(self, payload) -> int:
+        """Sorted, deduplicated coarse cells of the merged edge list (every rank builds the same list)."""
+        lib, cabi = self._cabi.lib, self._cabi
+        p = payload.cpu().numpy()
+        base = np.ascontiguousarray(p[:, : self.n], dtype=np.int32)
+        mask = np.ascontiguousarray(p[:, self.n], dtype=np.uint32)
+        if self._cells:
+            lib.pt_cells_destroy(self._cells)
+            self._cells = None
+        cells = C.c_void_p()
+        cabi.check(lib.pt_cells_from_edges(self.ctx.handle, self.n, base.ctypes.data, mask.ctypes.data, base.shape[0], C.byref(cells)))
+        self._cells = cells
+        return int(lib.pt_cells_count(cells))
 
     def _fetch(self, ref, with_labels):
         lib, cabi, torch = self._cabi.lib, self._cabi, self.torch
