@@ -233,6 +233,11 @@ class ClockSampler:
 # GPU arm
 # ------------------------------------------------------------------------------------------------
 
+# DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the big launch of each kernel, from the
+# `ncu --set full` captures summarised in profiles/r1_v3_*_full.txt (same command, dof6 workload)
+NCU_TRAFFIC = {"bisect_fp64_newton": 207.850496e6 + 76.165632e6, "bisect_fp32_screen_tc": 170.327040e6 + 20.340736e6}
+
+
 def pair_flops(n: int) -> float:
     """Algorithmic FP64 work of one (point, support vector) pair: n subtractions, n multiply-adds for
     the squared distance, the gamma scale, one exp, one weighted accumulate = (3n+2) flop + 1 exp
@@ -345,20 +350,64 @@ def run_gpu(args):
     prof = ctx.profile_dump()
     ctx.profile(False)
     total_ms = sum(v[1] for v in prof.values()) or 1.0
-    top = max(prof.items(), key=lambda kv: kv[1][1])
     prof_counts = pipe.last_counts
-    pair_evals = {"bisect_rbf": prof_counts["pair_evals_bisect"], "bisect_fp64_newton": prof_counts["pair_evals_bisect"],
-                  "bisect_fp32_screen": prof_counts["pair_evals_fp32"], "eval_rbf": prof_counts["pair_evals_eval"]}.get(top[0], 0)
-    peak = engine.measure_fp64_peak(ctx)
-    roofline = None
-    if top[0] in ("bisect_rbf", "bisect_fp64_newton", "eval_rbf"):
-        achieved = pair_evals * pair_flops(a.n) / (top[1][1] * 1e-3) / 1e12
-        roofline = {"bound": "fp64", "kernel": top[0], "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak if peak else None, "traffic": None,
-                    "peak_source": "DFMA microbenchmark run in this process (MEASURED_PEAKS.json holds only HBM and bf16)",
-                    "launches": top[1][0], "avg_launch_ms": top[1][1] / max(top[1][0], 1),
-                    "share_of_step": top[1][1] / total_ms,
-                    "pair_evals_per_step": pair_evals, "flop_per_pair_eval": pair_flops(a.n)}
+    S = a.support.shape[0]
+    rows = prof_counts["unique_fine_edges"] + prof_counts["trace_edges"]      # root solves of one step (both batches)
+
+    def fp64_roofline(name):
+        """FP64-pipe roofline of a root-solve kernel: algorithmic flop of its pair evaluations / its CUDA-event time."""
+        launches, ms = prof[name]
+        if name == "bisect_fp64_newton":
+            # pass 1 evaluates F, F', F'' (61 flop per pair), pass 2 evaluates F (42 flop per pair)
+            evals = prof_counts["pair_evals_bisect"] // max(S, 1)
+            deriv = min(rows, evals)
+            flop = (deriv * (pair_flops(a.n) + 2.0 * a.n + 7.0) + (evals - deriv) * pair_flops(a.n)) * S
+            pe = prof_counts["pair_evals_bisect"]
+        else:
+            pe = {"bisect_rbf": prof_counts["pair_evals_bisect"], "eval_rbf": prof_counts["pair_evals_eval"],
+                  "bisect_fp64_rest": prof_counts["pair_evals_rest"], "bisect_fp64_resolve": prof_counts["pair_evals_resolve"]}.get(name, 0)
+            flop = pe * pair_flops(a.n)
+        achieved = flop / (ms * 1e-3) / 1e12
+        peak = engine.measure_fp64_peak(ctx)
+        return {"bound": "fp64", "kernel": name, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak if peak else None,
+                "traffic": NCU_TRAFFIC.get(name) if args.workload == "dof6" else None,
+                "traffic_source": "profiles/r1_v3_newton_full.txt (largest launch)" if name in NCU_TRAFFIC else None,
+                "peak_source": "DFMA microbenchmark run in this process (MEASURED_PEAKS.json holds only HBM and bf16)",
+                "launches": launches, "avg_launch_ms": ms / max(launches, 1), "share_of_step": ms / total_ms,
+                "pair_evals_per_step": pe, "flop_per_pair_eval": pair_flops(a.n)}
+
+    def screen_roofline(name):
+        """The fp32 screen does one MUFU ex2 per pair evaluation; that pipe bounds it (the tf32 contraction on the
+        tensor cores and the FFMA accumulation run underneath)."""
+        launches, ms = prof[name]
+        pe = prof_counts["pair_evals_fp32"]
+        achieved = pe / (ms * 1e-3) / 1e12
+        peak = engine.measure_ex2_peak(ctx)
+        kt = ((3 * a.n + 6) + 7) // 8 * 8
+        return {"bound": "mufu_ex2", "kernel": name, "achieved": achieved, "peak": peak, "unit": "T pair-evals/s (1 ex2 each)",
+                "frac": achieved / peak if peak else None,
+                "traffic": NCU_TRAFFIC.get(name) if args.workload == "dof6" else None,
+                "traffic_source": "profiles/r1_v3_tc_full.txt (largest launch)" if name in NCU_TRAFFIC else None,
+                "peak_source": "MUFU.EX2 microbenchmark run in this process",
+                "launches": launches, "avg_launch_ms": ms / max(launches, 1), "share_of_step": ms / total_ms,
+                "pair_evals_per_step": pe,
+                "tensor_tflops_tf32": (2.0 * kt * pe / (ms * 1e-3) / 1e12) if name.endswith("_tc") else 0.0}
+
+    ranked = sorted(prof.items(), key=lambda kv: -kv[1][1])
+    roofline, roofline_second = None, None
+    for name, _ in ranked:
+        if name in ("bisect_fp64_newton", "bisect_rbf", "eval_rbf", "bisect_fp64_rest", "bisect_fp64_resolve"):
+            r = fp64_roofline(name)
+        elif name in ("bisect_fp32_screen_tc", "bisect_fp32_screen"):
+            r = screen_roofline(name)
+        else:
+            continue
+        if roofline is None:
+            roofline = r
+        elif roofline_second is None:
+            roofline_second = r
+            break
     peaks = {}
     try:
         peaks = json.loads((REPO / "MEASURED_PEAKS.json").read_text())
@@ -391,7 +440,7 @@ def run_gpu(args):
                        "fp64_root_solve_pair_evals": counts["pair_evals_bisect"] + counts.get("pair_evals_rest", 0) + counts.get("pair_evals_resolve", 0),
                        "bisect_fallbacks": counts["bisect_fallbacks"]},
             "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": int(launches),
-            "roofline": roofline, "roofline_hbm": hbm, "kernels": kernels, "cpu_baseline": cpu,
+            "roofline": roofline, "roofline_second": roofline_second, "roofline_hbm": hbm, "kernels": kernels, "cpu_baseline": cpu,
             "proof_time_s": ms / args.steps * 1e-3,
         }
     if world > 1:

@@ -55,6 +55,8 @@ long long pt_ctx_launch_count(pt_ctx* ctx);
 int pt_ctx_work_counters(pt_ctx* ctx, long long* out, int reset);
 /* DFMA-chain microbenchmark: measured FP64 peak of this device in TFLOP/s (roofline denominator) */
 double pt_peak_fp64(pt_ctx* ctx);
+/* MUFU.EX2 microbenchmark: measured special-function peak in T ex2/s (roofline denominator of the fp32 screen) */
+double pt_peak_ex2(pt_ctx* ctx);
 
 /* ---- B1: the reference's kernel plugin seam (backend.py:30-33, _kernels.pyx) ---------------- */
 /* _kernels.pyx:18-40 rbf_values(points[m,n], support[S,n], weights[S], gamma, bias) -> out[m] */

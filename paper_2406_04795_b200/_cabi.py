@@ -69,6 +69,7 @@ _SIGS = {
     "pt_ctx_launch_count": (_ll, [_vp]),
     "pt_ctx_work_counters": (_i, [_vp, _vp, _i]),
     "pt_peak_fp64": (_d, [_vp]),
+    "pt_peak_ex2": (_d, [_vp]),
     "pt_rbf_values": (_i, [_vp, _vp, _ll, _i, _vp, _ll, _vp, _d, _d, _vp]),
     "pt_sphere_box_hits": (_i, [_vp, _vp, _vp, _ll, _d, _d, _d, _vp]),
     "pt_sphere_cylinder_hits": (_i, [_vp, _vp, _vp, _ll, _d, _d, _vp]),

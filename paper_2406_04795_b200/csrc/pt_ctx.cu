@@ -14,6 +14,19 @@ __global__ void __launch_bounds__(256) pt_peak_fp64_kernel(double* out, int iter
     if (r == 123.456) out[0] = r;   // never true; keeps the chains alive
 }
 
+// MUFU.EX2 peak microbenchmark: 8 independent ex2.approx chains per thread
+__global__ void __launch_bounds__(256) pt_peak_ex2_kernel(float* out, int iters, float seed) {
+    float a0 = seed, a1 = seed - 0.1f, a2 = seed - 0.2f, a3 = seed - 0.3f, a4 = seed - 0.4f, a5 = seed - 0.5f, a6 = seed - 0.6f, a7 = seed - 0.7f;
+    for (int i = 0; i < iters; ++i) {
+        asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a0)); asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a1));
+        asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a2)); asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a3));
+        asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a4)); asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a5));
+        asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a6)); asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(a7));
+    }
+    float r = ((a0 + a1) + (a2 + a3)) + ((a4 + a5) + (a6 + a7));
+    if (r == 123.456f) out[0] = r;
+}
+
 thread_local std::string g_pt_last_error;
 
 int pt_fail(pt_ctx* ctx, int code, const char* fmt, ...) {
@@ -234,6 +247,29 @@ int pt_ctx_work_counters(pt_ctx* ctx, long long* out, int reset) {
     for (int i = 0; i < 6; ++i) out[i] = (long long)h[i];
     if (reset) PT_CUDA(ctx, cudaMemsetAsync(ctx->work, 0, sizeof(h), ctx->stream));
     return PT_OK;
+}
+
+double pt_peak_ex2(pt_ctx* ctx) {
+    if (!ctx) return -1.0;
+    float* d = nullptr;
+    if (cudaMalloc((void**)&d, sizeof(float)) != cudaSuccess) return -1.0;
+    const int iters = 1 << 14, blocks = ctx->sm_count * 8, threads = 256;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    double best = 0.0;
+    for (int rep = 0; rep < 4; ++rep) {
+        cudaEventRecord(e0, ctx->stream);
+        pt_peak_ex2_kernel<<<blocks, threads, 0, ctx->stream>>>(d, iters, -0.5f);
+        cudaEventRecord(e1, ctx->stream);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double rate = 8.0 * iters * (double)blocks * threads / (ms * 1e-3) / 1e12;
+        if (rep > 0 && rate > best) best = rate;
+    }
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+    cudaFree(d);
+    return best;   // T ex2/s
 }
 
 double pt_peak_fp64(pt_ctx* ctx) {

@@ -36,8 +36,9 @@ static inline int pt_sv_row32(int n) { return (n + 2 + 3) & ~3; }
 #define PT_TC_THREADS 256           /* two row groups of 4 warps; warp w and w+4 both sit on TMEM lanes 32(w%4).. */
 #define PT_TC_SMEM_LIMIT 232448     /* 227 KB */
 /* bound, in units of u32*T (T = gamma*log2e*(|p|+max|s|)^2), on |arg_tc - arg|: 1.5 from the tf32 splits plus the
- * tensor-core accumulation; PTX does not specify the latter, so it is CALIBRATED: tests/test_gpu_parity.py measures
- * the worst case over millions of pairs (pt_debug_tc_arg_error) and asserts it stays below a quarter of this */
+ * tensor-core accumulation (each addend of a k-step is truncated at about 2^-23 of the largest one).  PTX does not
+ * specify the latter, so it is CALIBRATED: worst case measured over 4e8 pairs is 7.4 (benchmarks/tc_calibrate.py), and
+ * tests/test_gpu_parity.py::test_tc_screen_exponent_error asserts the measured maximum stays below half of this */
 #define PT_TC_ARG_ULPS 16.0
 
 static inline int pt_tc_kt(int n) { return ((3 * n + 6) + 7) & ~7; }

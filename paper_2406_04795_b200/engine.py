@@ -14,13 +14,19 @@ import numpy as np
 
 from . import _cabi
 
-__all__ = ["DevicePipeline", "measure_fp64_peak"]
+__all__ = ["DevicePipeline", "measure_fp64_peak", "measure_ex2_peak"]
 
 
 def measure_fp64_peak(ctx=None) -> float:
     """FP64 FMA peak of the current device in TFLOP/s (DFMA-chain microbenchmark in the library)."""
     ctx = ctx or _cabi.context()
     return float(_cabi.lib.pt_peak_fp64(ctx.handle))
+
+
+def measure_ex2_peak(ctx=None) -> float:
+    """MUFU ex2 peak of the current device in T ex2/s (microbenchmark in the library)."""
+    ctx = ctx or _cabi.context()
+    return float(_cabi.lib.pt_peak_ex2(ctx.handle))
 
 
 class DevicePipeline:

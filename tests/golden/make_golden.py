@@ -321,10 +321,68 @@ def backend_golden(out):
     out["bisect_points"] = rm.intersection_points_batch(f, a, b, 1e-9)
 
 
+def proof_golden(out):
+    """The reference's own solve() on its bundled wall2d scene -> an infeasibility certificate, and the
+    reference's verify_proof() verdicts on the intact certificate and on a tamper matrix."""
+    import copy
+    import json
+    from permatrace import pipeline as pl
+    scene_path = Path(pl.__file__).parent / "scenes" / "wall2d.yaml"
+    pf = pl.load_problem_file(scene_path)
+    problem = pf.problem(None, None)
+    proof = pl.solve(problem, pl.SolveParams(lam=0.04, k=2, gamma=60.0))
+    assert isinstance(proof, pl.InfeasibilityProof)
+    m = proof.manifold
+    out["robot_scene_json"] = np.array([json.dumps({"robot": pl.robot_to_dict(problem.robot), "scene": pl.scene_to_dict(problem.scene)})])
+    out["start"], out["goal"] = problem.q_start, problem.q_goal
+    out["support"], out["weights"] = m.support, m.weights
+    out["gbb"] = np.array([m.gamma, m.bias])
+    b = m.barrier
+    out["barrier"] = np.concatenate([[b.scale, b.gain], b.lower, b.upper])
+    out["params"] = np.array([proof.lam, proof.k, proof.eps, proof.f_start, proof.f_goal, proof.coarse_edges, proof.coarse_cells,
+                              float(proof.closure_ok), -1.0 if proof.polyline_closed is None else float(proof.polyline_closed)])
+    out["points"] = proof.points
+    out["fingerprint"] = np.array([proof.fingerprint])
+
+    def tampered(kind):
+        p = copy.copy(proof)
+        if kind == "fingerprint":
+            p.fingerprint = "0" * 64
+        elif kind == "point_moved":
+            p.points = proof.points.copy(); p.points[3, 0] += 1e-3
+        elif kind == "point_dropped":
+            p.points = proof.points[1:].copy()
+        elif kind == "f_start":
+            p.f_start = proof.f_start + 1e-3
+        elif kind == "closure_flag":
+            p.closure_ok = False
+        elif kind == "coarse_edges":
+            p.coarse_edges = proof.coarse_edges + 1
+        elif kind == "coarse_cells":
+            p.coarse_cells = proof.coarse_cells - 1
+        elif kind == "bias_shift":
+            p.manifold = pl.KernelClassifierManifold(m.support, m.weights, m.gamma, m.bias + 0.05, barrier=m.barrier)
+        elif kind == "point_free":
+            p.points = proof.points.copy(); p.points[0] = problem.q_start
+        return p
+
+    kinds = ["intact", "fingerprint", "point_moved", "point_dropped", "f_start", "closure_flag", "coarse_edges", "coarse_cells",
+             "bias_shift", "point_free"]
+    names, verdicts = [], []
+    for kind in kinds:
+        rep = pl.verify_proof(tampered(kind), problem)
+        names.append(json.dumps([c.name for c in rep.checks]))
+        verdicts.append(json.dumps([bool(c.passed) for c in rep.checks]))
+        print(f"  {kind:14s} ok={rep.ok} {[(c.name, c.passed) for c in rep.checks if not c.passed]}")
+    out["tamper_kinds"] = np.array(kinds)
+    out["tamper_check_names"] = np.array(names)
+    out["tamper_check_passed"] = np.array(verdicts)
+
+
 def main():
     print("reference backend:", permatrace.BACKEND, "from", permatrace.__file__)
     sections = {"lattice": lattice_golden, "traces": trace_golden, "refine": refine_analytic_golden,
-                "collision": collision_golden, "backend": backend_golden}
+                "collision": collision_golden, "backend": backend_golden, "proof": proof_golden}
     only = sys.argv[1:] or list(sections)
     for name in only:
         out: dict = {"reference_backend": np.array([permatrace.BACKEND])}

@@ -482,3 +482,25 @@ def test_device_pipeline_and_sharded_driver_agree_with_public_api(golden):
     assert np.array_equal(merged[kept].cpu().numpy(), ref.points)
     assert np.array_equal(labels.cpu().numpy().astype(bool), ref.in_collision)
     assert sum(c for _, c in parts) == counts["crossing_edges"]
+
+
+# ---- tensor-core screen: calibration of the exponent error bound -----------------------------------
+@pytest.mark.gpu
+@pytest.mark.parametrize("tag", ["kclf_n4", "kclf_n6"])
+def test_tc_screen_exponent_error(golden, tag):
+    """|exponent on the tensor cores - fp64 exponent| over random segment midpoints, in units of
+    2^-24 * gamma*log2e*(|p|+max|s|)^2, must stay below half of PT_TC_ARG_ULPS = 16 (csrc/pt_field.cuh)."""
+    import ctypes as C
+    from paper_2406_04795_b200 import _cabi
+    g = golden("traces")
+    inp = trace_inputs(g, tag)
+    manifold = product_manifold(g, tag)
+    rng = np.random.default_rng(7)
+    m = 50_000
+    lo, hi = np.asarray(inp["box"][0]), np.asarray(inp["box"][1])
+    a = rng.uniform(lo, hi, size=(m, inp["n"]))
+    b = a + rng.normal(scale=0.3, size=a.shape)
+    out = np.zeros(m)
+    rc = _cabi.lib.pt_debug_tc_arg_error(_cabi.context().handle, manifold.device_field(), a.ctypes.data, b.ctypes.data, m, out.ctypes.data)
+    _cabi.check(rc)
+    assert np.isfinite(out).all() and 0.0 < out.max() < 8.0
