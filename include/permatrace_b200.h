@@ -42,6 +42,10 @@ int pt_ctx_synchronize(pt_ctx* ctx);
 /* device blocks freed by the library are cached per context for reuse by the next step; this returns them
  * to the driver (bytes released, or -1) */
 long long pt_ctx_trim(pt_ctx* ctx);
+/* page-locked host blocks for large results (device->host copies into them run at full PCIe speed and need no
+ * staging); freed blocks are cached per context.  pt_host_free may be called from any thread. */
+void* pt_host_alloc(pt_ctx* ctx, long long bytes);
+void pt_host_free(pt_ctx* ctx, void* p);
 /* per-kernel CUDA-event profiler (events on the launching stream) */
 int pt_ctx_profile_enable(pt_ctx* ctx, int on);
 int pt_ctx_profile_reset(pt_ctx* ctx);

@@ -63,6 +63,8 @@ _SIGS = {
     "pt_ctx_set_stream": (_i, [_vp, _vp]),
     "pt_ctx_synchronize": (_i, [_vp]),
     "pt_ctx_trim": (_ll, [_vp]),
+    "pt_host_alloc": (_vp, [_vp, _ll]),
+    "pt_host_free": (None, [_vp, _vp]),
     "pt_ctx_profile_enable": (_i, [_vp, _i]),
     "pt_ctx_profile_reset": (_i, [_vp]),
     "pt_ctx_profile_dump": (_ll, [_vp, C.c_char_p, _ll]),
@@ -208,6 +210,36 @@ class _Context:
 
     def launch_count(self) -> int:
         return int(lib.pt_ctx_launch_count(self.handle))
+
+
+class _PinnedBlock:
+    """Owner of one page-locked host block; numpy arrays built on it keep it alive through `base`."""
+
+    def __init__(self, ctx, nbytes: int, shape, dtype):
+        self._ctx = ctx
+        self._ptr = lib.pt_host_alloc(ctx.handle, max(int(nbytes), 1))
+        if not self._ptr:
+            raise MemoryError("pinned host allocation failed: " + last_error())
+        dt = np.dtype(dtype)
+        self.__array_interface__ = {"shape": tuple(int(v) for v in shape), "typestr": dt.str, "data": (int(self._ptr), False),
+                                    "version": 3}
+
+    def __del__(self):
+        p, self._ptr = getattr(self, "_ptr", None), None
+        if p:
+            try:
+                lib.pt_host_free(self._ctx.handle, p)
+            except Exception:
+                pass
+
+
+def pinned_empty(shape, dtype=np.float64, ctx=None) -> np.ndarray:
+    """Uninitialised numpy array in page-locked memory (for large device->host results)."""
+    if isinstance(shape, int):
+        shape = (shape,)
+    ctx = ctx or context()
+    nbytes = int(np.prod(shape, dtype=np.int64)) * np.dtype(dtype).itemsize
+    return np.asarray(_PinnedBlock(ctx, nbytes, shape, dtype))
 
 
 _lock = threading.Lock()

@@ -100,6 +100,45 @@ void pt_dev_free(pt_ctx* ctx, void* p) {
     ctx->cached_bytes += size;
 }
 
+extern "C" void* pt_host_alloc(pt_ctx* ctx, long long bytes) {
+    if (!ctx || bytes < 0) return nullptr;
+    const size_t want = pt_round_block((size_t)bytes);
+    {
+        std::lock_guard<std::mutex> g(ctx->host_lock);
+        auto it = ctx->host_free_blocks.lower_bound(want);
+        if (it != ctx->host_free_blocks.end() && it->first <= want + want / 4) {
+            void* p = it->second;
+            ctx->host_live_blocks[p] = it->first;
+            ctx->host_free_blocks.erase(it);
+            return p;
+        }
+    }
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, want, cudaHostAllocDefault) != cudaSuccess) {
+        cudaGetLastError();
+        pt_fail(ctx, PT_E_NOMEM, "pinned host allocation of %lld bytes failed", bytes);
+        return nullptr;
+    }
+    std::lock_guard<std::mutex> g(ctx->host_lock);
+    ctx->host_live_blocks[p] = want;
+    return p;
+}
+
+extern "C" void pt_host_free(pt_ctx* ctx, void* p) {
+    if (!ctx || !p) return;
+    std::lock_guard<std::mutex> g(ctx->host_lock);
+    auto it = ctx->host_live_blocks.find(p);
+    if (it == ctx->host_live_blocks.end()) return;
+    ctx->host_free_blocks.emplace(it->second, p);
+    ctx->host_live_blocks.erase(it);
+}
+
+static void pt_host_cache_release(pt_ctx* ctx) {
+    std::lock_guard<std::mutex> g(ctx->host_lock);
+    for (auto& kv : ctx->host_free_blocks) cudaFreeHost(kv.second);
+    ctx->host_free_blocks.clear();
+}
+
 int pt_check_launch(pt_ctx* ctx, const char* what) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return pt_fail(ctx, PT_E_CUDA, "launch of %s failed: %s", what, cudaGetErrorString(e));
@@ -182,6 +221,7 @@ void pt_ctx_destroy(pt_ctx* ctx) {
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
     pt_cache_release(ctx);
     cudaStreamSynchronize(ctx->stream);
+    pt_host_cache_release(ctx);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->work) cudaFree(ctx->work);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -201,6 +241,7 @@ long long pt_ctx_trim(pt_ctx* ctx) {
     const long long released = (long long)ctx->cached_bytes;
     pt_cache_release(ctx);
     cudaStreamSynchronize(ctx->stream);
+    pt_host_cache_release(ctx);
     return released;
 }
 

@@ -8,6 +8,7 @@
 #include <string>
 #include <vector>
 #include <map>
+#include <mutex>
 #include "pt_common.cuh"
 #include "../../include/permatrace_b200.h"
 
@@ -34,6 +35,11 @@ struct pt_ctx {
     std::multimap<size_t, void*> free_blocks;
     std::map<void*, size_t> live_blocks;
     size_t cached_bytes = 0;
+    // cache of pinned host blocks handed to the caller for large results (pt_host_alloc); finalizers of the host
+    // language may free from another thread, hence the lock
+    std::mutex host_lock;
+    std::multimap<size_t, void*> host_free_blocks;
+    std::map<void*, size_t> host_live_blocks;
     // pinned scratch for small device->host readbacks (counters)
     void* pinned = nullptr;
     size_t pinned_bytes = 0;

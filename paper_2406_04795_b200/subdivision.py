@@ -321,8 +321,9 @@ def refine(cells, template: SubdivisionTemplate, manifold, checker, cfg: TraceCo
     st = _cabi.RefineStats()
     _cabi.check(_cabi.lib.pt_refine_get_stats(res.handle, C.byref(st)))
     total = int(st.points)
-    points = np.empty((total, n), dtype=np.float64)
-    labels = np.empty(total, dtype=np.uint8)
+    # large results land in page-locked memory: the device->host copy runs at PCIe speed without staging
+    points = _cabi.pinned_empty((total, n), np.float64, ctx)
+    labels = _cabi.pinned_empty((total,), np.uint8, ctx)
     if total:
         _cabi.check(_cabi.lib.pt_refine_points(res.handle, points.ctypes.data, labels.ctypes.data, None))
     rows = np.zeros((max(nb, 1), 2), dtype=np.int64)
