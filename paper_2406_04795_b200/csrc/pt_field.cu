@@ -28,6 +28,9 @@ int pt_field_dim(const pt_field* f) { return f->d.n; }
 #define PT_EVAL_TILE 256
 
 #define PT_ROW64(N) (((N) + 2) | 1)
+
+// optional row indirection of the evaluation kernel: a compacted list whose length lives on the device
+struct PtRowList { const uint32_t* list; const unsigned long long* count; };
 #define PT_SMEM64(N) ((size_t)(PT_EVAL_TILE * PT_ROW64(N) + 32) * sizeof(double))
 
 // 2^x for x <= ~0 in fp64: x = (32k + i)/32 + r, |r| <= 1/64; 2^r by a degree-6 Taylor polynomial
@@ -116,14 +119,17 @@ __device__ __forceinline__ double pt_rbf_block_sum(const PtFieldDev& f, const do
 
 template <int N, int G>
 __global__ void __launch_bounds__(PT_EVAL_THREADS)
-pt_eval_rbf_kernel(PtFieldDev f, const double* __restrict__ pts, size_t m, double* __restrict__ vals,
+pt_eval_rbf_kernel(PtFieldDev f, PtRowList rows, const double* __restrict__ pts, size_t m_all, double* __restrict__ vals,
                    int8_t* __restrict__ signs, unsigned long long* work) {
     extern __shared__ double tile[];
-    pt_exp_table_init(tile + PT_EVAL_TILE * PT_ROW64(N));
     const int PB = PT_EVAL_THREADS / G;
-    const size_t pi = (size_t)blockIdx.x * PB + threadIdx.x / G;
+    const size_t m = rows.list ? (size_t)*rows.count : m_all;      // optional compacted row list (device-side count)
+    if ((size_t)blockIdx.x * PB >= m) return;
+    pt_exp_table_init(tile + PT_EVAL_TILE * PT_ROW64(N));
+    const size_t idx = (size_t)blockIdx.x * PB + threadIdx.x / G;
     const int g = threadIdx.x % G;
-    const bool valid = pi < m;
+    const bool valid = idx < m;
+    const size_t pi = valid ? (rows.list ? (size_t)rows.list[idx] : idx) : 0;
     double p[N];
 #pragma unroll
     for (int d = 0; d < N; ++d) p[d] = valid ? pts[pi * N + d] : 0.0;
@@ -970,6 +976,10 @@ static int pt_pick_group(pt_ctx* ctx, size_t m, long long S) {
     return 32;
 }
 
+template <int N, int MODE>
+static int pt_screen_tc_launch(pt_ctx* ctx, const pt_field* f, const PtRows& rows, const double* a, const double* b,
+                               const int8_t* sa, double eps, int fresh, double* lo, double* hi, int8_t* sign_out);
+
 template <int N>
 static int pt_eval_launch(pt_ctx* ctx, const pt_field* f, const double* pts, size_t m, double* vals, int8_t* signs) {
     if (f->d.kind != PT_FIELD_RBF) {
@@ -977,22 +987,47 @@ static int pt_eval_launch(pt_ctx* ctx, const pt_field* f, const double* pts, siz
         pt_eval_analytic_kernel<N><<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>(f->d, pts, m, vals, signs);
         return pt_check_launch(ctx, "pt_eval_analytic_kernel");
     }
-    const int G = pt_pick_group(ctx, m, f->d.S);
     const size_t smem = PT_SMEM64(N);
+    const PtRowList none{nullptr, nullptr};
+    // Signs of a large batch (lattice vertices of a BFS wave / of the refinement): the kernel sum runs on the tensor
+    // cores in fp32 (pt_field_tc.cuh, MODE 2) with the screen's rigorous error bound; rows whose fp32 sign is not
+    // proven are rechecked by the fp64 kernel through a compacted list.
+    if (!vals && signs && f->tc_ok && f->precision != 0 && m >= (size_t)PT_TC_M * 32) {
+        if constexpr (N <= 6) {
+            PtBuf<uint32_t> list; PtBuf<unsigned long long> cnt;
+            PT_TRY(list.alloc(ctx, m));
+            PT_TRY(cnt.alloc(ctx, 1));
+            PT_CUDA(ctx, cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), ctx->stream));
+            const PtRows all{nullptr, nullptr, m};
+            {
+                PT_LAUNCH(ctx, "eval_signs_tc");
+                PT_TRY((pt_screen_tc_launch<N, 2>(ctx, f, all, pts, nullptr, nullptr, 1.0, 1, nullptr, nullptr, signs)));
+            }
+            {
+                PT_LAUNCH(ctx, "eval_select");
+                pt_select_flag_kernel<<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>((const uint8_t*)signs, (uint8_t)0, m, list.p, cnt.p);
+                PT_TRY(pt_check_launch(ctx, "pt_select_flag_kernel"));
+            }
+            PT_LAUNCH(ctx, "eval_rbf");
+            const PtRowList sub{list.p, cnt.p};
+            pt_eval_rbf_kernel<N, 4><<<pt_grid_for(m, PT_EVAL_THREADS / 4), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, sub, pts, m, nullptr, signs, ctx->work);
+            return pt_check_launch(ctx, "pt_eval_rbf_kernel");
+        }
+    }
+    const int G = pt_pick_group(ctx, m, f->d.S);
     PT_LAUNCH(ctx, "eval_rbf");
     if (G == 1)
-        pt_eval_rbf_kernel<N, 1><<<pt_grid_for(m, PT_EVAL_THREADS), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, pts, m, vals, signs, ctx->work);
+        pt_eval_rbf_kernel<N, 1><<<pt_grid_for(m, PT_EVAL_THREADS), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, none, pts, m, vals, signs, ctx->work);
     else if (G == 4)
-        pt_eval_rbf_kernel<N, 4><<<pt_grid_for(m, PT_EVAL_THREADS / 4), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, pts, m, vals, signs, ctx->work);
+        pt_eval_rbf_kernel<N, 4><<<pt_grid_for(m, PT_EVAL_THREADS / 4), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, none, pts, m, vals, signs, ctx->work);
     else
-        pt_eval_rbf_kernel<N, 32><<<pt_grid_for(m, PT_EVAL_THREADS / 32), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, pts, m, vals, signs, ctx->work);
+        pt_eval_rbf_kernel<N, 32><<<pt_grid_for(m, PT_EVAL_THREADS / 32), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, none, pts, m, vals, signs, ctx->work);
     return pt_check_launch(ctx, "pt_eval_rbf_kernel");
 }
 
-// fp32 screen on the tensor cores: persistent CTAs (one per SM), each walking chunks of 128 rows
 template <int N, int MODE>
 static int pt_screen_tc_launch(pt_ctx* ctx, const pt_field* f, const PtRows& rows, const double* a, const double* b,
-                               const int8_t* sa, double eps, int fresh, double* lo, double* hi) {
+                               const int8_t* sa, double eps, int fresh, double* lo, double* hi, int8_t* sign_out) {
     if constexpr (N > 6) {
         return pt_fail(ctx, PT_E_STATE, "tensor-core screen is built for n <= 6");
     } else {
@@ -1003,7 +1038,7 @@ static int pt_screen_tc_launch(pt_ctx* ctx, const pt_field* f, const PtRows& row
             configured = true;
         }
         const unsigned grid = pt_grid_for(rows.m, 2 * PT_TC_M, (unsigned)ctx->sm_count);
-        pt_bisect32_tc_kernel<N, MODE><<<grid, PT_TC_THREADS, smem, ctx->stream>>>(f->d, f->tc, rows, a, b, sa, eps, fresh, lo, hi, ctx->work);
+        pt_bisect32_tc_kernel<N, MODE><<<grid, PT_TC_THREADS, smem, ctx->stream>>>(f->d, f->tc, rows, a, b, sa, eps, fresh, lo, hi, sign_out, ctx->work);
         return pt_check_launch(ctx, "pt_bisect32_tc_kernel");
     }
 }
@@ -1048,7 +1083,7 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
     const bool use_tc = f->tc_ok && m >= (size_t)PT_TC_M * 32;
     {
         PT_LAUNCH(ctx, use_tc ? "bisect_fp32_screen_tc" : "bisect_fp32_screen");
-        if (use_tc) PT_TRY((pt_screen_tc_launch<N, 0>(ctx, f, all, a, b, sa, eps, 1, lo.p, hi.p)));
+        if (use_tc) PT_TRY((pt_screen_tc_launch<N, 0>(ctx, f, all, a, b, sa, eps, 1, lo.p, hi.p, nullptr)));
         else PT_G_LAUNCH(pt_bisect32_kernel, smem32, f->d, all, a, b, sa, eps, 1, lo.p, hi.p, ctx->work);
     }
     // rows that stopped while their bracket is still wide: one true fp64 step, then back to fp32
@@ -1066,7 +1101,7 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
         }
         {
             PT_LAUNCH(ctx, use_tc ? "bisect_fp32_screen_tc" : "bisect_fp32_screen");
-            if (use_tc) PT_TRY((pt_screen_tc_launch<N, 0>(ctx, f, sub, a, b, sa, eps, 0, lo.p, hi.p)));
+            if (use_tc) PT_TRY((pt_screen_tc_launch<N, 0>(ctx, f, sub, a, b, sa, eps, 0, lo.p, hi.p, nullptr)));
             else PT_G_LAUNCH(pt_bisect32_kernel, smem32, f->d, sub, a, b, sa, eps, 0, lo.p, hi.p, ctx->work);
         }
     }
@@ -1304,11 +1339,11 @@ int pt_debug_tc_arg_error(pt_ctx* ctx, const pt_field* f, const double* a, const
     const PtRows all{nullptr, nullptr, (size_t)m};
     int rc;
     switch (n) {
-        case 2: rc = pt_screen_tc_launch<2, 1>(ctx, f, all, adev, bdev, sa.p, 1e-9, 1, lo.p, hi.p); break;
-        case 3: rc = pt_screen_tc_launch<3, 1>(ctx, f, all, adev, bdev, sa.p, 1e-9, 1, lo.p, hi.p); break;
-        case 4: rc = pt_screen_tc_launch<4, 1>(ctx, f, all, adev, bdev, sa.p, 1e-9, 1, lo.p, hi.p); break;
-        case 5: rc = pt_screen_tc_launch<5, 1>(ctx, f, all, adev, bdev, sa.p, 1e-9, 1, lo.p, hi.p); break;
-        case 6: rc = pt_screen_tc_launch<6, 1>(ctx, f, all, adev, bdev, sa.p, 1e-9, 1, lo.p, hi.p); break;
+        case 2: rc = pt_screen_tc_launch<2, 1>(ctx, f, all, adev, bdev, sa.p, 1e-9, 1, lo.p, hi.p, nullptr); break;
+        case 3: rc = pt_screen_tc_launch<3, 1>(ctx, f, all, adev, bdev, sa.p, 1e-9, 1, lo.p, hi.p, nullptr); break;
+        case 4: rc = pt_screen_tc_launch<4, 1>(ctx, f, all, adev, bdev, sa.p, 1e-9, 1, lo.p, hi.p, nullptr); break;
+        case 5: rc = pt_screen_tc_launch<5, 1>(ctx, f, all, adev, bdev, sa.p, 1e-9, 1, lo.p, hi.p, nullptr); break;
+        case 6: rc = pt_screen_tc_launch<6, 1>(ctx, f, all, adev, bdev, sa.p, 1e-9, 1, lo.p, hi.p, nullptr); break;
         default: return pt_fail(ctx, PT_E_INVALID, "dimension %d unsupported by the tensor-core screen", n);
     }
     PT_TRY(rc);

@@ -151,6 +151,8 @@ __device__ __forceinline__ double pt_barrier_fast(const PtFieldDev& f, const dou
 
 // MODE 0: the bisection screen (same contract as pt_bisect32_kernel).
 // MODE 1: calibration -- one evaluation at t = 0.5 per row; hi_io[row] receives max_j |arg_tc - arg_fp64| / (u32*T).
+// MODE 2: sign evaluation at the points a_[row] (lattice vertices): sign_out[row] = +1 / -1 when |F32| > E, i.e. the
+//         fp32 sign is PROVEN equal to the fp64 one, and 0 when it is not -- those rows are rechecked in fp64.
 //
 // Two independent row groups per CTA (warps 0-3 and 4-7, 128 rows each, one row per thread = one TMEM lane): every
 // bisection level ends in a serial stretch (decide, move the bracket, rewrite A, wait for the first MMA), and while
@@ -159,7 +161,7 @@ template <int N, int MODE>
 __global__ void __launch_bounds__(PT_TC_THREADS, 1)
 pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __restrict__ a_, const double* __restrict__ b_,
                       const int8_t* __restrict__ signs_a, double eps, int fresh, double* __restrict__ lo_io,
-                      double* __restrict__ hi_io, unsigned long long* work) {
+                      double* __restrict__ hi_io, int8_t* __restrict__ sign_out, unsigned long long* work) {
     extern __shared__ __align__(1024) unsigned char pt_tc_smem[];
     constexpr int KT = ((3 * N + 6) + 7) & ~7;
     constexpr int KC = KT / 4;           // 16-byte K chunks
@@ -225,7 +227,10 @@ pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __res
         double a[N], diff[N], p[N];
         double seg = 0.0, lo = 0.0, hi = 1.0;
         int sa = 1;
-        if (valid) {
+        if (valid && MODE == 2) {
+#pragma unroll
+            for (int d = 0; d < N; ++d) { a[d] = a_[ei * N + d]; diff[d] = 0.0; }
+        } else if (valid) {
             double b[N];
 #pragma unroll
             for (int d = 0; d < N; ++d) { a[d] = a_[ei * N + d]; b[d] = b_[ei * N + d]; }
@@ -236,7 +241,8 @@ pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __res
 #pragma unroll
             for (int d = 0; d < N; ++d) { a[d] = 0.0; diff[d] = 0.0; }
         }
-        bool active = valid && (MODE == 1 || __dmul_rn(seg, __dsub_rn(hi, lo)) > eps);
+        bool active = valid && (MODE != 0 || __dmul_rn(seg, __dsub_rn(hi, lo)) > eps);
+        int8_t sign_certain = 0;
         unsigned iters = 0;
         double calib = 0.0;
         while (pt_group_or(group, active)) {
@@ -293,7 +299,7 @@ pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __res
                     uint32_t (&cur)[32] = (blk & 1) ? r1 : r0;
                     uint32_t (&nxt)[32] = (blk & 1) ? r0 : r1;
                     if (blk + 1 < PT_TC_N / 32) pt_tmem_ld32(taddr + (uint32_t)(blk + 1) * 32, nxt);
-                    if (MODE == 0) {
+                    if (MODE != 1) {
                         float fa = 0.f, fb = 0.f;
 #pragma unroll
                         for (int c4 = 0; c4 < 8; ++c4) {
@@ -323,7 +329,7 @@ pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __res
                         }
                     }
                 }
-                if (MODE == 0) {
+                if (MODE != 1) {
                     // pairwise fp32 sum of the four chains (34 roundings at most), one conversion per tile
                     acc += (double)((fa_t[0] + fa_t[1]) + (fa_t[2] + fa_t[3]));
                     ab += (double)((fb_t[0] + fb_t[1]) + (fb_t[2] + fb_t[3]));
@@ -345,7 +351,10 @@ pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __res
                 // ex2.approx, weight rounding, products and the 32-term fp32 chains (+2 pairwise levels) add < 80 u relative
                 const double rel = 1.01 * (PT_TC_ARG_ULPS * PT_U32 * gl * pn * pn * PT_LN2) + 80.0 * PT_U32;
                 const double E = 2.0 * rel * ab + eb + 1e-280;
-                if (active) {
+                if (MODE == 2) {
+                    if (active && fabs(F) > E) sign_certain = F > 0.0 ? (int8_t)1 : (int8_t)-1;
+                    active = false;
+                } else if (active) {
                     if (fabs(F) > E) {
                         if ((F > 0.0 ? 1 : -1) == sa) lo = mid; else hi = mid;
                         ++iters;
@@ -362,8 +371,10 @@ pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __res
             for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
             if ((tid & 31) == 0 && mine) atomicAdd(&work[2], (unsigned long long)mine);
             if (valid) { lo_io[ei] = lo; hi_io[ei] = hi; }
+        } else if (MODE == 1) {
+            if (valid) hi_io[ei] = calib;
         } else if (valid) {
-            hi_io[ei] = calib;
+            sign_out[ei] = sign_certain;
         }
     }
     pt_tc_fence_before();

@@ -504,3 +504,23 @@ def test_tc_screen_exponent_error(golden, tag):
     rc = _cabi.lib.pt_debug_tc_arg_error(_cabi.context().handle, manifold.device_field(), a.ctypes.data, b.ctypes.data, m, out.ctypes.data)
     _cabi.check(rc)
     assert np.isfinite(out).all() and 0.0 < out.max() < 8.0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tag", ["kclf_n4", "kclf_n6"])
+def test_tc_sign_evaluation_equals_fp64_signs(golden, tag):
+    """Large sign batches run on the tensor cores with an FP64 recheck of every unproven row: the signs must equal
+    those of the FP64 values, including at points ON the zero set (the golden intersection points) and within
+    1e-12 .. 1e-6 of it."""
+    g = golden("traces")
+    inp = trace_inputs(g, tag)
+    manifold = product_manifold(g, tag)
+    rng = np.random.default_rng(11)
+    lo, hi = np.asarray(inp["box"][0]), np.asarray(inp["box"][1])
+    on = g[f"{tag}_points"]
+    near = np.concatenate([on + rng.normal(scale=s, size=on.shape) for s in (0.0, 1e-12, 1e-9, 1e-6)])
+    pts = np.concatenate([rng.uniform(lo, hi, size=(30_000, inp["n"])), near])
+    values = manifold.values(pts)
+    signs = manifold.signs(pts)
+    assert signs.shape == (pts.shape[0],) and set(np.unique(signs)) <= {-1, 1}
+    assert np.array_equal(signs, np.where(values > 0.0, 1, -1))
