@@ -242,18 +242,33 @@ __global__ void pt_dedup_hash_kernel(int n, const double* __restrict__ pts, size
     idx[i] = (uint32_t)i;
 }
 
+// directory of the sorted grid keys: hash(cell) -> first position of the cell's run
+__global__ void pt_dedup_directory_kernel(const u64* __restrict__ gkey_sorted, size_t count, PtTable dir, unsigned* err) {
+    const size_t a = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= count) return;
+    const u64 gk = gkey_sorted[a];
+    if (a > 0 && gkey_sorted[a - 1] == gk) return;
+    bool ins;
+    const u64 slot = pt_table_insert(dir, gk, ins, err);
+    dir.ent[2 * slot + 1] = (u64)a;
+}
+
 #define PT_DD_UNDECIDED 0
 #define PT_DD_KEPT 1
 #define PT_DD_REMOVED 2
 
-// one resolution round: a point is removed if an earlier kept point lies within eps, kept once
-// every earlier point within eps is removed
-__global__ void pt_dedup_round_kernel(int n, const double* __restrict__ pts, size_t count, double cell, double eps,
-                                      const u64* __restrict__ gkey_sorted, const uint32_t* __restrict__ idx_sorted,
-                                      uint8_t* state, PtFineCounters* ctr) {
-    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= count) return;
-    if (state[i] != PT_DD_UNDECIDED) return;
+// Greedy first-keeper resolution: a point is removed if an earlier kept point lies within eps, kept once every
+// earlier point within eps is removed.
+// Round 1 (all points) does the spatial search once and CACHES the earlier neighbours within eps (almost always
+// 0..2 of them); undecided points go to a compacted list.  Later rounds (pt_dedup_follow_kernel) only look at the
+// cached neighbours' states.  A point with more than PT_DD_NBR neighbours redoes the search every round.
+#define PT_DD_NBR 8
+#define PT_DD_OVERFLOW 0xFFu
+
+__device__ __forceinline__ int pt_dedup_search(int n, const double* __restrict__ pts, size_t count, double cell, double eps,
+                                               const u64* __restrict__ gkey_sorted, const uint32_t* __restrict__ idx_sorted,
+                                               const PtTable& dir, const uint8_t* state, size_t i, uint32_t* nbr, int& nbc) {
+    // returns 2 if an earlier KEPT point is within eps, 1 if an earlier undecided one is, else 0
     double p[PT_NMAX]; long long lo[PT_NMAX], hi[PT_NMAX];
     int ncomb = 1;
     for (int d = 0; d < n; ++d) {
@@ -263,6 +278,7 @@ __global__ void pt_dedup_round_kernel(int n, const double* __restrict__ pts, siz
         if (hi[d] != lo[d]) ncomb <<= 1;
     }
     bool any_kept = false, any_undecided = false;
+    nbc = 0;
     for (int comb = 0; comb < ncomb && !any_kept; ++comb) {
         long long c[PT_NMAX]; int bit = 0;
         for (int d = 0; d < n; ++d) {
@@ -270,24 +286,90 @@ __global__ void pt_dedup_round_kernel(int n, const double* __restrict__ pts, siz
             else c[d] = lo[d];
         }
         const u64 gk = pt_grid_hash(n, c);
-        size_t a = 0, b = count;
-        while (a < b) { size_t mid = (a + b) >> 1; if (gkey_sorted[mid] < gk) a = mid + 1; else b = mid; }
+        u64 slot;
+        if (!pt_table_find(dir, gk, slot)) continue;          // no point in that cell
+        size_t a = (size_t)dir.ent[2 * slot + 1];
         for (; a < count && gkey_sorted[a] == gk; ++a) {
             const size_t j = idx_sorted[a];
-            if (j >= i) continue;
-            const uint8_t sj = ((volatile uint8_t*)state)[j];
-            if (sj == PT_DD_REMOVED) continue;
+            if (j >= i) break;           // the sort is stable: a cell's run is in ascending point order
             double s = 0.0;
             for (int d = 0; d < n; ++d) { double df = __dsub_rn(pts[j * n + d], p[d]); s = __dadd_rn(s, __dmul_rn(df, df)); }
             if (sqrt(s) <= eps) {
+                if (nbr) { if (nbc < PT_DD_NBR) nbr[nbc] = (uint32_t)j; ++nbc; }
+                const uint8_t sj = ((volatile const uint8_t*)state)[j];
+                if (sj == PT_DD_REMOVED) continue;
                 if (sj == PT_DD_KEPT) { any_kept = true; break; }
                 any_undecided = true;
             }
         }
     }
-    if (any_kept) state[i] = PT_DD_REMOVED;
-    else if (!any_undecided) state[i] = PT_DD_KEPT;
-    else atomicAdd(&ctr->undecided, 1ull);
+    return any_kept ? 2 : (any_undecided ? 1 : 0);
+}
+
+__global__ void pt_dedup_round_kernel(int n, const double* __restrict__ pts, size_t count, double cell, double eps,
+                                      const u64* __restrict__ gkey_sorted, const uint32_t* __restrict__ idx_sorted, PtTable dir,
+                                      uint8_t* state, uint32_t* __restrict__ nbr, uint8_t* __restrict__ nbc_out,
+                                      uint32_t* __restrict__ undecided, PtFineCounters* ctr) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool pending = false;
+    if (i < count) {
+        uint32_t mine[PT_DD_NBR];
+        int nbc = 0;
+        const int verdict = pt_dedup_search(n, pts, count, cell, eps, gkey_sorted, idx_sorted, dir, state, i, mine, nbc);
+        if (verdict == 2) state[i] = PT_DD_REMOVED;
+        else if (verdict == 0) state[i] = PT_DD_KEPT;
+        else {
+            pending = true;
+            for (int q = 0; q < PT_DD_NBR; ++q) nbr[i * PT_DD_NBR + q] = q < nbc ? mine[q] : 0u;
+            nbc_out[i] = nbc > PT_DD_NBR ? (uint8_t)PT_DD_OVERFLOW : (uint8_t)nbc;
+        }
+    }
+    const unsigned ballot = __ballot_sync(0xffffffffu, pending);
+    if (ballot) {
+        const int lane = threadIdx.x & 31, leader = __ffs(ballot) - 1;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(&ctr->undecided, (unsigned long long)__popc(ballot));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (pending) undecided[base + __popc(ballot & ((1u << lane) - 1u))] = (uint32_t)i;
+    }
+}
+
+__global__ void pt_dedup_follow_kernel(int n, const double* __restrict__ pts, size_t count, double cell, double eps,
+                                       const u64* __restrict__ gkey_sorted, const uint32_t* __restrict__ idx_sorted, PtTable dir,
+                                       uint8_t* state, const uint32_t* __restrict__ nbr, const uint8_t* __restrict__ nbc_in,
+                                       const uint32_t* __restrict__ list_in, size_t list_count,
+                                       uint32_t* __restrict__ list_out, PtFineCounters* ctr) {
+    const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool pending = false;
+    uint32_t i = 0;
+    if (t < list_count) {
+        i = list_in[t];
+        int verdict;
+        const uint8_t nbc = nbc_in[i];
+        if (nbc == PT_DD_OVERFLOW) {
+            int dummy;
+            verdict = pt_dedup_search(n, pts, count, cell, eps, gkey_sorted, idx_sorted, dir, state, (size_t)i, nullptr, dummy);
+        } else {
+            bool any_kept = false, any_undecided = false;
+            for (int q = 0; q < nbc; ++q) {
+                const uint8_t sj = ((volatile const uint8_t*)state)[nbr[(size_t)i * PT_DD_NBR + q]];
+                if (sj == PT_DD_KEPT) { any_kept = true; break; }
+                if (sj != PT_DD_REMOVED) any_undecided = true;
+            }
+            verdict = any_kept ? 2 : (any_undecided ? 1 : 0);
+        }
+        if (verdict == 2) state[i] = PT_DD_REMOVED;
+        else if (verdict == 0) state[i] = PT_DD_KEPT;
+        else pending = true;
+    }
+    const unsigned ballot = __ballot_sync(0xffffffffu, pending);
+    if (ballot) {
+        const int lane = threadIdx.x & 31, leader = __ffs(ballot) - 1;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(&ctr->undecided, (unsigned long long)__popc(ballot));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (pending) list_out[base + __popc(ballot & ((1u << lane) - 1u))] = i;
+    }
 }
 
 __global__ void pt_flag_kept_kernel(const uint8_t* __restrict__ state, size_t count, uint8_t* __restrict__ flag) {
@@ -353,7 +435,8 @@ static int pt_dedup_label_impl(pt_ctx* ctx, int n, const double* upts, const u64
     if (U > 0) {
         if (U >= (1ull << 32)) return pt_fail(ctx, PT_E_NOMEM, "more than 2^32 distinct fine edges in one refine call");
         PT_CUDA(ctx, cudaMemsetAsync(state.p, PT_DD_UNDECIDED, U, ctx->stream));
-        const double cell = 16.0 * eps_dedup;
+        // 8 eps cells: a point's eps-ball touches ~(1 + 1/4)^n cells (3.8 at n = 6) holding about one point each
+        const double cell = 8.0 * eps_dedup;
         PtBuf<u64> gk, gks; PtBuf<uint32_t> gi, gis;
         PT_TRY(gk.alloc(ctx, U)); PT_TRY(gks.alloc(ctx, U)); PT_TRY(gi.alloc(ctx, U)); PT_TRY(gis.alloc(ctx, U));
         {
@@ -370,16 +453,39 @@ static int pt_dedup_label_impl(pt_ctx* ctx, int n, const double* upts, const u64
             PT_CUDA(ctx, cub::DeviceRadixSort::SortPairs(tmp.p, tb, gk.p, gks.p, gi.p, gis.p, (long long)U, 0, 64, ctx->stream));
             ctx->launches++;
         }
-        for (;;) {
+        PtHashTable dir;
+        PT_TRY(pt_table_init(ctx, dir, 2 * (u64)U));
+        {
+            PT_LAUNCH(ctx, "dedup_directory");
+            pt_dedup_directory_kernel<<<pt_grid_for(U, 256), 256, 0, ctx->stream>>>(gks.p, U, dir.view(), &ctr.p->error);
+            PT_TRY(pt_check_launch(ctx, "pt_dedup_directory_kernel"));
+        }
+        PtBuf<uint32_t> nbr, list_a, list_b; PtBuf<uint8_t> nbc;
+        PT_TRY(nbr.alloc(ctx, U * PT_DD_NBR)); PT_TRY(nbc.alloc(ctx, U));
+        PT_TRY(list_a.alloc(ctx, U)); PT_TRY(list_b.alloc(ctx, U));
+        PT_CUDA(ctx, cudaMemsetAsync(&ctr.p->undecided, 0, sizeof(unsigned long long), ctx->stream));
+        {
+            PT_LAUNCH(ctx, "dedup_round");
+            pt_dedup_round_kernel<<<pt_grid_for(U, 128), 128, 0, ctx->stream>>>(n, upts, U, cell, eps_dedup, gks.p, gis.p, dir.view(), state.p,
+                                                                                nbr.p, nbc.p, list_a.p, ctr.p);
+            PT_TRY(pt_check_launch(ctx, "pt_dedup_round_kernel"));
+        }
+        ++rounds;
+        PT_TRY(pt_read_fine_counters(ctx, ctr.p, &hc, rg));
+        uint32_t* lin = list_a.p; uint32_t* lout = list_b.p;
+        while (hc.undecided != 0) {
+            const size_t pending = (size_t)hc.undecided;
+            if (getenv("PT_DEBUG_COUNTS")) fprintf(stderr, "[pt] dedup round %lld: %zu of %zu undecided\n", rounds, pending, U);
             PT_CUDA(ctx, cudaMemsetAsync(&ctr.p->undecided, 0, sizeof(unsigned long long), ctx->stream));
             {
-                PT_LAUNCH(ctx, "dedup_round");
-                pt_dedup_round_kernel<<<pt_grid_for(U, 128), 128, 0, ctx->stream>>>(n, upts, U, cell, eps_dedup, gks.p, gis.p, state.p, ctr.p);
-                PT_TRY(pt_check_launch(ctx, "pt_dedup_round_kernel"));
+                PT_LAUNCH(ctx, "dedup_follow");
+                pt_dedup_follow_kernel<<<pt_grid_for(pending, 128), 128, 0, ctx->stream>>>(n, upts, U, cell, eps_dedup, gks.p, gis.p, dir.view(), state.p,
+                                                                                          nbr.p, nbc.p, lin, pending, lout, ctr.p);
+                PT_TRY(pt_check_launch(ctx, "pt_dedup_follow_kernel"));
             }
             ++rounds;
             PT_TRY(pt_read_fine_counters(ctx, ctr.p, &hc, rg));
-            if (hc.undecided == 0) break;
+            uint32_t* sw = lin; lin = lout; lout = sw;
             if (rounds > 100000) return pt_fail(ctx, PT_E_STATE, "eps-dedup did not converge");
         }
         // compact the kept points, order preserved
