@@ -65,6 +65,22 @@ __global__ void pt_pack_tc_kernel(const double* __restrict__ support, const doub
     wt[j] = w;
 }
 
+// 2^x on the FMA pipe (the MUFU pipe is the screen's limiter, so every fourth exponential goes here): round to
+// nearest integer by the magic-number trick, degree-5 polynomial on [-1/2, 1/2] (relative error 3.7 u32 including the
+// fp32 Horner rounding -- same class as ex2.approx), exponent field add.  Arguments below -125 flush to 2^-125 ~ 0.
+__device__ __forceinline__ float pt_ex2_poly(float x) {
+    x = fmaxf(x, -125.0f);
+    const float t = x + 12582912.0f;             // 1.5 * 2^23: low mantissa bits of t hold round(x)
+    const float f = x - (t - 12582912.0f);
+    float p = 0.0013266970636323094f;
+    p = fmaf(p, f, 0.009675459936261177f);
+    p = fmaf(p, f, 0.05550742521882057f);
+    p = fmaf(p, f, 0.24022121727466583f);
+    p = fmaf(p, f, 0.6931469440460205f);
+    p = fmaf(p, f, 1.0000001192092896f);
+    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 // ---- raw PTX wrappers ------------------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t pt_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void pt_mbar_init(uint32_t bar, uint32_t count) {
@@ -307,7 +323,7 @@ pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __res
                             const float e0 = pt_ex2(__uint_as_float(cur[c4 * 4 + 0]));
                             const float e1 = pt_ex2(__uint_as_float(cur[c4 * 4 + 1]));
                             const float e2 = pt_ex2(__uint_as_float(cur[c4 * 4 + 2]));
-                            const float e3 = pt_ex2(__uint_as_float(cur[c4 * 4 + 3]));
+                            const float e3 = pt_ex2_poly(__uint_as_float(cur[c4 * 4 + 3]));
                             fa = fmaf(w4.x, e0, fa); fb = fmaf(fabsf(w4.x), e0, fb);
                             fa = fmaf(w4.y, e1, fa); fb = fmaf(fabsf(w4.y), e1, fb);
                             fa = fmaf(w4.z, e2, fa); fb = fmaf(fabsf(w4.z), e2, fb);
