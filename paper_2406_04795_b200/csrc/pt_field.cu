@@ -31,27 +31,26 @@ int pt_field_dim(const pt_field* f) { return f->d.n; }
 
 // optional row indirection of the evaluation kernel: a compacted list whose length lives on the device
 struct PtRowList { const uint32_t* list; const unsigned long long* count; };
-#define PT_SMEM64(N) ((size_t)(PT_EVAL_TILE * PT_ROW64(N) + 32) * sizeof(double))
+#define PT_EXP_TAB 256   /* entries of the 2^(i/256) table behind every tile */
+#define PT_SMEM64(N) ((size_t)(PT_EVAL_TILE * PT_ROW64(N) + PT_EXP_TAB) * sizeof(double))
 
-// 2^x for x <= ~0 in fp64: x = (32k + i)/32 + r, |r| <= 1/64; 2^r by a degree-6 Taylor polynomial
-// (truncation 3e-18), 2^(i/32) from a 32-entry shared-memory table, 2^k by an exponent-field add.
+// 2^x for x <= ~0 in fp64: x = (256k + i)/256 + r, |r| <= 1/512; 2^r by a degree-4 Taylor polynomial
+// (truncation 3.8e-17), 2^(i/256) from a 256-entry shared-memory table, 2^k by an exponent-field add.
 // Arguments below -1000 are clamped (the term is < 1e-300 of its weight).  Branch-free on purpose so
 // independent rows interleave; non-finite points are handled once per point (PtPoint64::poison).
 __device__ __forceinline__ double pt_exp2_neg(double x, const double* __restrict__ tab) {
     if ((unsigned)__double2hiint(x) > 0xC08F4000u) x = -1000.0;   // x < -1000 (integer compare: keeps the FP64 pipe free)
-    const double MAGIC = 6755399441055744.0;   // 1.5 * 2^52: the low word of x*32 + MAGIC is round(32 x)
-    const double t = fma(x, 32.0, MAGIC);
+    const double MAGIC = 6755399441055744.0;   // 1.5 * 2^52: the low word of x*256 + MAGIC is round(256 x)
+    const double t = fma(x, 256.0, MAGIC);
     const int mi = __double2loint(t);
-    const double r = fma(t - MAGIC, -0.03125, x);
-    double p = 0.00015403530393381606;
-    p = fma(p, r, 0.0013333558146428441);
-    p = fma(p, r, 0.009618129107628477);
+    const double r = fma(t - MAGIC, -0.00390625, x);
+    double p = 0.009618129107628477;
     p = fma(p, r, 0.055504108664821576);
     p = fma(p, r, 0.2402265069591007);
     p = fma(p, r, 0.6931471805599453);
     p = fma(p, r, 1.0);
-    const double v = tab[mi & 31] * p;
-    return __hiloint2double(__double2hiint(v) + ((mi >> 5) << 20), __double2loint(v));
+    const double v = tab[mi & (PT_EXP_TAB - 1)] * p;
+    return __hiloint2double(__double2hiint(v) + ((mi >> 8) << 20), __double2loint(v));
 }
 
 // per-point constants of the expanded exponent: -gamma*log2(e)*|p - s|^2 = c_s + c_p + sum_d p_d s'_d with
@@ -80,7 +79,7 @@ __device__ __forceinline__ double pt_rbf_term(const double* __restrict__ row, co
 }
 
 __device__ __forceinline__ void pt_exp_table_init(double* tab) {
-    if (threadIdx.x < 32) tab[threadIdx.x] = exp2((double)threadIdx.x * 0.03125);
+    for (int i = threadIdx.x; i < PT_EXP_TAB; i += blockDim.x) tab[i] = exp2((double)i * (1.0 / PT_EXP_TAB));
 }
 
 // accumulate this lane's share of sum_j w_j k(p, s_j); all threads of the block must call it
@@ -641,7 +640,7 @@ pt_bisect_newton_kernel(PtFieldDev f, double sum_abs_w, const double* __restrict
         pt_rbf_block_sum_d<N, G>(f, p[0], diff[0], seg2[0], g, tile, F0[0], D1[0], D2[0], AB[0]);
     }
     // per-row state that must survive pass 2 lives in shared memory (keeps the evaluation loop's registers free)
-    double* st = tile + PT_EVAL_TILE * PT_ROW64(N) + 32;
+    double* st = tile + PT_EVAL_TILE * PT_ROW64(N) + PT_EXP_TAB;
 #define PT_ST(field, k) st[((field) * PPT + (k)) * THREADS + threadIdx.x]
     enum { ST_LO, ST_W, ST_DL, ST_SMIN, ST_ETA, ST_AD2, ST_K, ST_DT, ST_XH, ST_TF, ST_FIELDS };
     bool need[PPT], to_slow[PPT], one_step[PPT];
@@ -881,7 +880,7 @@ pt_bisect_rest_warp_kernel(PtFieldDev f, PtRows rows, const double* __restrict__
     if ((size_t)blockIdx.x * warps_per_block >= total) return;
     double* tab = tile + (size_t)f.S * ROW;
     for (long long i = threadIdx.x; i < f.S * ROW; i += PT_RESTW_THREADS) tile[i] = f.sv[i];
-    if (threadIdx.x < 32) tab[threadIdx.x] = exp2((double)threadIdx.x * 0.03125);
+    for (int i = threadIdx.x; i < PT_EXP_TAB; i += PT_RESTW_THREADS) tab[i] = exp2((double)i * (1.0 / PT_EXP_TAB));
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const size_t warp0 = (size_t)blockIdx.x * warps_per_block + (threadIdx.x >> 5);
@@ -1127,7 +1126,7 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
             PT_TRY(pt_check_launch(ctx, "pt_select_flag_kernel"));
         }
         PT_LAUNCH(ctx, "bisect_fp64_rest");
-        const size_t smem_w = ((size_t)f->d.S * PT_ROW64(N) + 32) * sizeof(double);
+        const size_t smem_w = ((size_t)f->d.S * PT_ROW64(N) + PT_EXP_TAB) * sizeof(double);
         if (smem_w <= PT_TC_SMEM_LIMIT) {
             // support set resident in shared memory, one warp per row, persistent CTAs
             static bool configured = false;
