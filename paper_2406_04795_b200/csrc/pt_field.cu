@@ -872,7 +872,7 @@ __global__ void __launch_bounds__(PT_RESTW_THREADS, 1)
 pt_bisect_rest_warp_kernel(PtFieldDev f, PtRows rows, const double* __restrict__ a_, const double* __restrict__ b_,
                            const int8_t* __restrict__ signs_a, const double* __restrict__ lo_in, const double* __restrict__ hi_in,
                            const double* __restrict__ jlo_in, const double* __restrict__ jhi_in,
-                           double eps, double* __restrict__ out, unsigned long long* work) {
+                           double eps, double* __restrict__ out, unsigned long long* next_row, unsigned long long* work) {
     extern __shared__ double tile[];
     const int ROW = PT_ROW64(N);
     const size_t total = pt_rows_total(rows);
@@ -883,11 +883,14 @@ pt_bisect_rest_warp_kernel(PtFieldDev f, PtRows rows, const double* __restrict__
     for (int i = threadIdx.x; i < PT_EXP_TAB; i += PT_RESTW_THREADS) tab[i] = exp2((double)i * (1.0 / PT_EXP_TAB));
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const size_t warp0 = (size_t)blockIdx.x * warps_per_block + (threadIdx.x >> 5);
-    const size_t nwarps = (size_t)gridDim.x * warps_per_block;
     const int S = (int)f.S;
     unsigned iters = 0;
-    for (size_t idx = warp0; idx < total; idx += nwarps) {
+    // rows need 1..30 evaluations: warps pull the next row from a device-side counter instead of striding
+    for (;;) {
+        unsigned long long take = 0;
+        if (lane == 0) take = atomicAdd(next_row, 1ull);
+        const size_t idx = (size_t)__shfl_sync(0xffffffffu, take, 0);
+        if (idx >= total) break;
         const size_t ei = rows.list ? (size_t)rows.list[idx] : idx;
         double a[N], diff[N], p[N];
         {
@@ -1067,8 +1070,8 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
     PT_TRY(jhi.alloc(ctx, m));
     PT_TRY(list.alloc(ctx, m));
     PT_TRY(slow.alloc(ctx, m));
-    PT_TRY(cnt.alloc(ctx, 4));
-    PT_CUDA(ctx, cudaMemsetAsync(cnt.p, 0, 4 * sizeof(unsigned long long), ctx->stream));
+    PT_TRY(cnt.alloc(ctx, 6));
+    PT_CUDA(ctx, cudaMemsetAsync(cnt.p, 0, 6 * sizeof(unsigned long long), ctx->stream));
     const size_t smem32 = (size_t)PT_TILE32 * PtRow32<N>::value * sizeof(float);
     const PtRows all{nullptr, nullptr, m};
 #define PT_G_LAUNCH(KERNEL, SMEM, ...)                                                            \
@@ -1135,7 +1138,8 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
                 configured = true;
             }
             const unsigned gridw = pt_grid_for(m, PT_RESTW_THREADS / 32, (unsigned)ctx->sm_count);
-            pt_bisect_rest_warp_kernel<N><<<gridw, PT_RESTW_THREADS, smem_w, ctx->stream>>>(f->d, sub, a, b, sa, lo.p, hi.p, jlo.p, jhi.p, eps, out, ctx->work);
+            pt_bisect_rest_warp_kernel<N><<<gridw, PT_RESTW_THREADS, smem_w, ctx->stream>>>(f->d, sub, a, b, sa, lo.p, hi.p, jlo.p, jhi.p, eps, out,
+                                                                                            cnt.p + (kind == 2 ? 4 : 5), ctx->work);
             PT_TRY(pt_check_launch(ctx, "pt_bisect_rest_warp_kernel"));
         } else {
             // larger support sets: tiles through shared memory, 4 lanes per row; the block-stride loop ends at the device-side count
