@@ -73,7 +73,31 @@ def rank_winners(tag_lists, mine: int, total_before: int, max_edges: int):
     return gidx, int((~dead).sum().item()), new_total, complete
 
 
-class ShardedTrace:
+class _Transport:
+    """Collective helpers shared by the drivers.  Buffers live on `engine.tensor_device`; when the process group
+    cannot move that memory itself (gloo with CUDA tensors: CPU tests of the CUDA engine, or a box without NCCL)
+    they are staged through the host for the collective only."""
+
+    def _init_transport(self, engine, group):
+        import torch
+        import torch.distributed as dist
+        self.engine, self.group, self.dist = engine, group, dist
+        self.on = dist.is_available() and dist.is_initialized()
+        self.rank = dist.get_rank(group) if self.on else 0
+        self.world = dist.get_world_size(group) if self.on else 1
+        dev = engine.tensor_device
+        staged = self.on and dist.get_backend(group) == "gloo" and torch.device(dev).type == "cuda"
+        self.comm_device = torch.device("cpu") if staged else dev
+
+    def _out(self, t):
+        return t.to(self.comm_device) if t.device != self.comm_device else t
+
+    def _back(self, t):
+        dev = self.engine.tensor_device
+        return t.to(dev) if t.device != dev else t
+
+
+class ShardedTrace(_Transport):
     """Owner-hashed BFS over the process group (the north star's multi-GPU trace).
 
     Rank r owns the edges whose base lattice vertex hashes to r.  Every wave: expand the local frontier,
@@ -91,16 +115,12 @@ class ShardedTrace:
     """
 
     def __init__(self, engine, group=None):
-        import torch.distributed as dist
-        self.engine, self.group, self.dist = engine, group, dist
-        self.on = dist.is_available() and dist.is_initialized()
-        self.rank = dist.get_rank(group) if self.on else 0
-        self.world = dist.get_world_size(group) if self.on else 1
+        self._init_transport(engine, group)
 
     # -- collectives (identity when there is no process group) --
     def _sum(self, values):
         import torch
-        t = torch.tensor(list(values), dtype=torch.int64, device=self.engine.tensor_device)
+        t = torch.tensor(list(values), dtype=torch.int64, device=self.comm_device)
         if self.world > 1:
             self.dist.all_reduce(t, group=self.group)
         return [int(v) for v in t.tolist()]
@@ -109,31 +129,31 @@ class ShardedTrace:
         import torch
         if self.world == 1:
             return records
-        dev = self.engine.tensor_device
+        dev = self.comm_device
         send = torch.tensor(counts, dtype=torch.int64, device=dev)
         recv = torch.zeros_like(send)
         self.dist.all_to_all_single(recv, send, group=self.group)
         recv_counts = [int(v) for v in recv.tolist()]
         out = torch.empty((sum(recv_counts), 2), dtype=torch.int64, device=dev)
-        self.dist.all_to_all_single(out, records.contiguous(), output_split_sizes=recv_counts,
+        self.dist.all_to_all_single(out, self._out(records).contiguous(), output_split_sizes=recv_counts,
                                     input_split_sizes=[int(c) for c in counts], group=self.group)
-        return out
+        return self._back(out)
 
     def _gather_var(self, tensor):
         """all_gather of per-rank tensors with different leading sizes -> list of tensors."""
         import torch
         if self.world == 1:
             return [tensor]
-        dev = self.engine.tensor_device
+        dev = self.comm_device
         size = torch.tensor([tensor.shape[0]], dtype=torch.int64, device=dev)
         sizes = [torch.zeros_like(size) for _ in range(self.world)]
         self.dist.all_gather(sizes, size, group=self.group)
         sizes = [int(x.item()) for x in sizes]
         padded = torch.zeros((max(max(sizes), 1),) + tuple(tensor.shape[1:]), dtype=tensor.dtype, device=dev)
-        padded[: tensor.shape[0]] = tensor
+        padded[: tensor.shape[0]] = self._out(tensor)
         parts = [torch.empty_like(padded) for _ in range(self.world)]
         self.dist.all_gather(parts, padded, group=self.group)
-        return [parts[r][: sizes[r]] for r in range(self.world)]
+        return [self._back(parts[r][: sizes[r]]) for r in range(self.world)]
 
     def run(self, seeds, max_edges: int) -> dict:
         eng = self.engine
@@ -164,7 +184,7 @@ class ShardedTrace:
         return all_g[order], all_p[order]
 
 
-class ShardedProof:
+class ShardedProof(_Transport):
     """trace -> coarse_cells -> refine(+check) with the refinement sharded over the process group.
 
     `engine` implements:
@@ -175,13 +195,7 @@ class ShardedProof:
     """
 
     def __init__(self, engine, group=None):
-        import torch.distributed as dist
-        self.engine = engine
-        self.group = group
-        self.dist = dist
-        self.on = dist.is_available() and dist.is_initialized()
-        self.rank = dist.get_rank(group) if self.on else 0
-        self.world = dist.get_world_size(group) if self.on else 1
+        self._init_transport(engine, group)
 
     def run(self, seeds) -> dict:
         import torch
@@ -200,17 +214,17 @@ class ShardedProof:
         pts, crossing = eng.candidates(first, count)
         dev = eng.tensor_device
         n = pts.shape[1]
-        mine = torch.tensor([pts.shape[0], crossing], dtype=torch.int64, device=dev)
+        mine = torch.tensor([pts.shape[0], crossing], dtype=torch.int64, device=self.comm_device)
         if self.world > 1:
             counts = [torch.zeros_like(mine) for _ in range(self.world)]
             dist.all_gather(counts, mine, group=self.group)
             counts = torch.stack(counts).cpu().numpy()
             biggest = int(counts[:, 0].max())
-            padded = torch.zeros((max(biggest, 1), n), dtype=torch.float64, device=dev)
-            padded[: pts.shape[0]] = pts
+            padded = torch.zeros((max(biggest, 1), n), dtype=torch.float64, device=self.comm_device)
+            padded[: pts.shape[0]] = self._out(pts)
             gathered = [torch.empty_like(padded) for _ in range(self.world)]
             dist.all_gather(gathered, padded, group=self.group)
-            merged = torch.cat([gathered[r][: int(counts[r, 0])] for r in range(self.world)], dim=0)
+            merged = self._back(torch.cat([gathered[r][: int(counts[r, 0])] for r in range(self.world)], dim=0))
             crossing_total = int(counts[:, 1].sum())
             crossing_offsets = np.concatenate([[0], np.cumsum(counts[:, 1])[:-1]])
         else:

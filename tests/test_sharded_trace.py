@@ -313,3 +313,59 @@ def test_gpu_shard_kernels_lockstep_equals_reference(tag, world):
     sa = np.zeros(want.shape[0], dtype=np.int8)
     _cabi.check(_cabi.lib.pt_trace_edges(ref._trace, 0, want.shape[0], None, None, sa.ctypes.data))
     assert np.array_equal(all_p[order][:, -1], sa.astype(np.int64))
+
+
+# ---- GPU: two real processes (gloo process group, both CUDA engines on device 0) -----------------------
+
+def _gpu_worker(rank, world, port, tag, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["LOCAL_RANK"] = "0"
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2406_04795_b200 as P
+        from paper_2406_04795_b200.distributed import CudaEngine, ShardedProof
+        from tests.conftest import oracle_model, robot_scene_dicts
+        from tests.test_gpu_parity import product_manifold
+        from paper_2406_04795_b200 import collision as CO
+        g = Golden("traces")
+        inp = trace_inputs(g, tag)
+        manifold = product_manifold(g, tag)
+        cfg = P.TraceConfig(P.LatticeConfig(inp["n"], inp["scale"], tuple(inp["offset"])), box=inp["box"], eps=inp["eps"],
+                            max_edges=inp["max_edges"])
+        rd, sd = robot_scene_dicts(inp["n"], 3)
+        problem = type("Pb", (), {})()
+        problem.robot, problem.scene = CO.robot_from_dict(rd), CO.scene_from_dict(sd)
+        checker = P.not_free_checker(problem)
+        eng = CudaEngine(manifold, cfg, P.build_template(inp["n"], 2), checker, device_index=0)
+        res = ShardedProof(eng).run(inp["seeds"])
+        out[rank] = dict(points=res["points"].cpu().numpy(), labels=res["in_collision"].cpu().numpy(), edges=res["trace_edges"],
+                         cells=res["cells"], crossing=res["crossing_edges"], closure=res["closure_ok"], levels=res["levels"])
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gpu_two_process_sharded_proof_equals_reference():
+    """trace (owner-hashed BFS with a real all_to_all per wave) -> cells -> sharded refine -> merged dedup + labels,
+    two processes, against the reference's golden refinement of the same manifold."""
+    tag = "kclf_n3"
+    g = Golden("traces")
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, tag, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(600)
+        assert p.exitcode == 0
+    want_pts, want_lab = g[f"{tag}_refine_points"], g[f"{tag}_refine_labels"]
+    for r in range(2):
+        res = out[r]
+        assert res["edges"] == int(g[f"{tag}_stats"][2]) and res["closure"] and res["levels"] == int(g[f"{tag}_stats"][0])
+        assert res["cells"] == g[f"{tag}_cells_base"].shape[0]
+        assert res["crossing"] == int(g[f"{tag}_refine_batches"][:, 2].sum())
+        assert res["points"].shape == want_pts.shape
+        assert np.allclose(res["points"], want_pts, rtol=1e-5, atol=1e-8)
+        assert np.array_equal(res["labels"], want_lab)
