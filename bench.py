@@ -254,10 +254,17 @@ def run_gpu(args):
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
+    os.environ["PERMATRACE_B200_DEVICE"] = str(local)     # the library's default context follows this rank's GPU
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL over NVLink is the transport; PT_BENCH_BACKEND=gloo lets the N > 1 code path be exercised with several
+        # ranks on ONE GPU (collectives staged through the host, see distributed._Transport)
+        backend = os.environ.get("PT_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     wl = build_workload(args.workload)
     a = wl.arrays
     ctx = _cabi.context(local)
@@ -274,6 +281,7 @@ def run_gpu(args):
         sharded = ShardedProof(CudaEngine(wl.manifold, wl.cfg, wl.template, checker, device_index=local))
 
     def barrier():
+        torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -303,7 +311,8 @@ def run_gpu(args):
         barrier()
     ms = e0.elapsed_time(e1)
     launches = ctx.launch_count() - launches0
-    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    comm_dev = "cuda" if (world == 1 or dist.get_backend() == "nccl") else "cpu"
+    t = torch.tensor([ms], dtype=torch.float64, device=comm_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
@@ -326,21 +335,35 @@ def run_gpu(args):
         if rank == 0:
             print(json.dumps({"metric": METRIC, "value": value, "unit": UNIT, "ms_per_step": ms / args.steps, "kernel_only": True}))
         return None
+    def e2e_step_sharded():
+        """N > 1: the multi-GPU public API (distributed.ShardedProof) from host buffers; every rank ends with the
+        merged result and copies it to the host."""
+        from paper_2406_04795_b200.distributed import CudaEngine, ShardedProof
+        manifold = P.KernelClassifierManifold(a.support, a.weights, a.gamma, a.bias, barrier=P.BoxBarrier(lo, hi, scale, gain))
+        eng = CudaEngine(manifold, wl.cfg, wl.template, checker, device_index=local)
+        out = ShardedProof(eng).run(seeds_pinned.numpy())
+        return out, (out["points"].cpu(), out["in_collision"].cpu())
+
+    run_e2e = e2e_step if world == 1 else e2e_step_sharded
     for _ in range(max(args.warmup, 1)):
-        res, ref = e2e_step()      # same binding pattern as the timed loop (two result sets alive at a time)
+        res, ref = run_e2e()      # same binding pattern as the timed loop (two result sets alive at a time)
     barrier()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        res, ref = e2e_step()
+        res, ref = run_e2e()
     barrier()
     e2e_s = time.perf_counter() - t0
-    tt = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    tt = torch.tensor([e2e_s], dtype=torch.float64, device=comm_dev)
     if world > 1:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     e2e_s = float(tt.item())
-    e2e_simplices = len(res.edges) + sum(b.crossing_edges for b in ref.batch_stats)
     h2d = a.support.nbytes + a.weights.nbytes + a.seeds.nbytes
-    d2h = res.points.nbytes + ref.points.nbytes + ref.in_collision.nbytes
+    if world == 1:
+        e2e_simplices = len(res.edges) + sum(b.crossing_edges for b in ref.batch_stats)
+        d2h = res.points.nbytes + ref.points.nbytes + ref.in_collision.nbytes
+    else:
+        e2e_simplices = res["trace_edges"] + res["crossing_edges"]
+        d2h = ref[0].numel() * 8 + ref[1].numel()
     e2e = {"value": e2e_simplices * args.steps / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
@@ -431,7 +454,7 @@ def run_gpu(args):
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{args.workload}: {a.n}-DoF arm, {len(a.scene_dict['obstacles'])} primitives, "
                                    f"S={a.support.shape[0]} support vectors, lambda={a.lam}, k={a.k}",
-                       "parallelism": "single GPU" if world == 1 else f"trace replicated, refine+check sharded over {world} ranks (cell slices), candidate merge by all_gather",
+                       "parallelism": "single GPU" if world == 1 else f"owner-hashed BFS (all_to_all per wave) + refine/check sharded over {world} ranks (cell slices), candidate merge by all_gather",
                        "l2_policy": "per-step working set (hash tables + fine-edge arrays) exceeds the 126 MB L2; "
                                     "all tables are rebuilt from empty every step",
                        "trace_edges": counts["trace_edges"], "coarse_cells": counts["cells"],
