@@ -445,6 +445,43 @@ def test_dof6_full_size_properties():
     assert len(cells) > 10 * st.visited_edges
 
 
+def test_dof6_full_size_refine_properties(monkeypatch):
+    """BASELINE-size refinement (1.3 M cells, 50.8 M crossings): the fast root-solve path (tensor-core screen, enclosure
+    Newton, replay) must return the SAME points as plain fp64 bisection on the same device, every point must be an
+    eps-accurate zero of the field, and the result must not depend on how the cells are sliced over ranks."""
+    import torch
+    from bench import build_workload
+    from paper_2406_04795_b200.distributed import CudaEngine, cell_slice
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("PERMATRACE_B200_PRECISION", mode)
+        wl = build_workload("dof6")
+        checker = P.not_free_checker(wl.problem)
+        res = T.trace(wl.seeds, wl.manifold, wl.cfg)
+        ref = S.refine(S.coarse_cells(res), wl.template, wl.manifold, checker, wl.cfg)
+        out[mode] = (res.points.copy(), ref.points.copy(), ref.in_collision.copy(), sum(b.crossing_edges for b in ref.batch_stats))
+        if mode == "1":
+            # three virtual ranks: slices refined separately, merged in rank order, deduplicated once
+            eng = CudaEngine(wl.manifold, wl.cfg, wl.template, checker)
+            info = eng.trace(torch.from_numpy(wl.seeds).cuda())
+            parts = [eng.candidates(*cell_slice(info["cells"], r, 3)) for r in range(3)]
+            merged = torch.cat([p for p, _ in parts], dim=0)
+            kept, labels = eng.dedup_label(merged)
+            assert np.array_equal(merged[kept].cpu().numpy(), ref.points)
+            assert np.array_equal(labels.cpu().numpy().astype(bool), ref.in_collision)
+            assert sum(c for _, c in parts) == out[mode][3]
+            # zero-set accuracy on a sample: |F| <= 4 eps (|grad F| + 1e-12)   (reference pipeline.py:519-526)
+            from paper_2406_04795_b200.pipeline import _gradient_norms
+            sample = ref.points[:: max(1, ref.points.shape[0] // 20000)]
+            resid = np.abs(wl.manifold.values(sample))
+            assert np.all(resid <= 4.0 * wl.cfg.eps * (_gradient_norms(wl.manifold, sample) + 1e-12))
+    fast, slow = out["1"], out["0"]
+    assert fast[3] == slow[3] == 50766688
+    assert fast[0].shape == slow[0].shape and fast[1].shape == slow[1].shape == (1606495, 6)
+    assert np.max(np.abs(fast[0] - slow[0])) <= 1e-8 and np.max(np.abs(fast[1] - slow[1])) <= 1e-8
+    assert np.array_equal(fast[2], slow[2])
+
+
 # ---- device pipeline and the sharded driver on one GPU -----------------------------------------------------
 def test_device_pipeline_and_sharded_driver_agree_with_public_api(golden):
     from paper_2406_04795_b200 import engine
