@@ -97,6 +97,8 @@ int pt_field_set_precision(pt_field* f, int mode);
  * may each be NULL */
 int pt_field_values(pt_ctx* ctx, const pt_field* f, const double* points, long long m,
                     double* out_values, int8_t* out_signs);
+/* KernelClassifierManifold.gradient (manifold.py:210-217), batched: out[m, n] */
+int pt_field_gradients(pt_ctx* ctx, const pt_field* f, const double* points, long long m, double* out);
 /* intersection_points_batch(manifold, a, b, eps, signs_a) (manifold.py:351-383); signs_a NULL ->
  * evaluated at a */
 int pt_intersection_points(pt_ctx* ctx, const pt_field* f, const double* a, const double* b,

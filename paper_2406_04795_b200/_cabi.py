@@ -81,6 +81,7 @@ _SIGS = {
     "pt_field_destroy": (None, [_vp]),
     "pt_field_set_precision": (_i, [_vp, _i]),
     "pt_field_values": (_i, [_vp, _vp, _vp, _ll, _vp, _vp]),
+    "pt_field_gradients": (_i, [_vp, _vp, _vp, _ll, _vp]),
     "pt_intersection_points": (_i, [_vp, _vp, _vp, _vp, _ll, _d, _vp, _vp]),
     "pt_debug_tc_arg_error": (_i, [_vp, _vp, _vp, _vp, _ll, _vp]),
     "pt_checker_create": (_i, [_vp, _i, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp, _vp, _i, _vp, _vp, _vp, _vp, _pp]),

@@ -155,6 +155,54 @@ __global__ void pt_eval_analytic_kernel(PtFieldDev f, const double* __restrict__
     if (signs) signs[i] = F > 0.0 ? (int8_t)1 : (int8_t)-1;
 }
 
+// gradient of the kernel-SVM field (manifold.py:210-217): grad F = -2 gamma sum_j w_j k_j (p - s_j) - grad barrier.
+// With the rows holding s' = 2 gl s:  sum_j w_j k_j (p - s_j) = p A - V / (2 gl),  A = sum w k,  V = sum w k s'.
+template <int N>
+__global__ void __launch_bounds__(PT_EVAL_THREADS)
+pt_gradient_rbf_kernel(PtFieldDev f, const double* __restrict__ pts, size_t m, double* __restrict__ out) {
+    extern __shared__ double tile[];
+    const int ROW = PT_ROW64(N);
+    pt_exp_table_init(tile + PT_EVAL_TILE * ROW);
+    const double* tab = tile + PT_EVAL_TILE * ROW;
+    const size_t pi = (size_t)blockIdx.x * PT_EVAL_THREADS + threadIdx.x;
+    const bool valid = pi < m;
+    double p[N];
+#pragma unroll
+    for (int d = 0; d < N; ++d) p[d] = valid ? pts[pi * N + d] : 0.0;
+    PtPoint64<N> pp;
+    pp.set(p, f.gamma * PT_L2E);
+    double A = 0.0, V[N];
+#pragma unroll
+    for (int d = 0; d < N; ++d) V[d] = 0.0;
+    for (long long t0 = 0; t0 < f.S; t0 += PT_EVAL_TILE) {
+        long long rem = f.S - t0;
+        const int cnt = rem < PT_EVAL_TILE ? (int)rem : PT_EVAL_TILE;
+        __syncthreads();
+        const double* src = f.sv + t0 * ROW;
+        for (int i = threadIdx.x; i < cnt * ROW; i += PT_EVAL_THREADS) tile[i] = src[i];
+        __syncthreads();
+        for (int j = 0; j < cnt; ++j) {
+            const double* row = tile + j * ROW;
+            const double e = pt_rbf_term<N>(row, pp, tab);
+            A += e;
+#pragma unroll
+            for (int d = 0; d < N; ++d) V[d] = fma(e, row[d], V[d]);
+        }
+    }
+    if (!valid) return;
+    const double inv2gl = 1.0 / (2.0 * f.gamma * PT_L2E);
+#pragma unroll
+    for (int d = 0; d < N; ++d) {
+        double g = -2.0 * f.gamma * (p[d] * A - V[d] * inv2gl) + pp.poison;
+        if (f.has_barrier) {
+            const double sh = 1.0 / (1.0 + exp(-(p[d] - f.b_hi[d]) / f.b_scale));
+            const double sl = 1.0 / (1.0 + exp(-(f.b_lo[d] - p[d]) / f.b_scale));
+            g -= f.b_gain * (sh - sl);
+        }
+        out[pi * N + d] = g;
+    }
+}
+
 // segment setup shared by both bisection kernels: diff, seg = ||b-a||_2 (numpy: sequential sum of
 // squares, sqrt), all separately rounded
 template <int N>
@@ -1248,6 +1296,18 @@ static int pt_field_build_rbf(pt_ctx* ctx, int n, long long S, const double* sup
     return PT_OK;
 }
 
+template <int N>
+static int pt_gradient_launch(pt_ctx* ctx, const pt_field* f, const double* pts, size_t m, double* out) {
+    pt_gradient_rbf_kernel<N><<<pt_grid_for(m, PT_EVAL_THREADS), PT_EVAL_THREADS, PT_SMEM64(N), ctx->stream>>>(f->d, pts, m, out);
+    return pt_check_launch(ctx, "pt_gradient_rbf_kernel");
+}
+
+static int pt_gradient_dispatch(pt_ctx* ctx, const pt_field* f, const double* pts, size_t m, double* out) {
+#define CALL(N) pt_gradient_launch<N>(ctx, f, pts, m, out)
+    PT_DISPATCH_N(f->d.n, CALL)
+#undef CALL
+}
+
 extern "C" {
 
 int pt_field_create_rbf(pt_ctx* ctx, int n, long long S, const double* support, const double* weights,
@@ -1299,6 +1359,27 @@ int pt_field_values(pt_ctx* ctx, const pt_field* f, const double* points, long l
     PT_TRY(pt_field_eval_dev(ctx, f, pdev, (size_t)m, vdev, sdev));
     if (out_values && vdev != out_values) PT_TRY(pt_copy_out(ctx, out_values, vdev, (size_t)m, false));
     if (out_signs && sdev != out_signs) PT_TRY(pt_copy_out(ctx, out_signs, sdev, (size_t)m, false));
+    PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return PT_OK;
+}
+
+int pt_field_gradients(pt_ctx* ctx, const pt_field* f, const double* points, long long m, double* out) {
+    if (!ctx || !f) return pt_fail(ctx, PT_E_INVALID, "pt_field_gradients: NULL argument");
+    if (f->d.kind != PT_FIELD_RBF) return pt_fail(ctx, PT_E_INVALID, "pt_field_gradients serves KernelClassifierManifold fields");
+    if (m < 0) return pt_fail(ctx, PT_E_INVALID, "negative point count");
+    if (m == 0) return PT_OK;
+    if (!points || !out) return pt_fail(ctx, PT_E_INVALID, "points/out is NULL");
+    const int n = f->d.n;
+    PtBuf<double> tmp_p, tmp_o;
+    const double* pdev;
+    PT_TRY(pt_stage_in(ctx, points, (size_t)m * n, tmp_p, &pdev));
+    double* odev = out;
+    if (!pt_is_device_ptr(out)) { PT_TRY(tmp_o.alloc(ctx, (size_t)m * n)); odev = tmp_o.p; }
+    {
+        PT_LAUNCH(ctx, "gradient_rbf");
+        PT_TRY(pt_gradient_dispatch(ctx, f, pdev, (size_t)m, odev));
+    }
+    if (odev != out) PT_TRY(pt_copy_out(ctx, out, odev, (size_t)m * n, false));
     PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return PT_OK;
 }

@@ -147,19 +147,11 @@ def _device_manifold(m):
 
 
 def _gradient_norms(manifold, points: np.ndarray) -> np.ndarray:
-    """|grad F| at every point (pipeline.py:457-461), batched: grad = -2 gamma sum_j w_j k_j (p - s_j) - grad barrier."""
+    """|grad F| at every point (pipeline.py:457-461); learned manifolds in one device batch, analytic test
+    manifolds through their closed forms."""
+    if hasattr(manifold, "gradients"):
+        return np.linalg.norm(manifold.gradients(points), axis=1)
     out = np.empty(points.shape[0])
-    if hasattr(manifold, "support"):
-        sup, w, gamma = manifold.support, manifold.weights, manifold.gamma
-        for first in range(0, points.shape[0], 4096):
-            p = points[first:first + 4096]
-            d = p[:, None, :] - sup[None, :, :]
-            kern = np.exp(-gamma * np.einsum("ijk,ijk->ij", d, d)) * w[None, :]
-            g = -2.0 * gamma * np.einsum("ij,ijk->ik", kern, d)
-            if getattr(manifold, "barrier", None) is not None:
-                g = g - np.stack([manifold.barrier.gradient(q) for q in p])
-            out[first:first + 4096] = np.linalg.norm(g, axis=1)
-        return out
     for i, q in enumerate(points):
         out[i] = float(np.linalg.norm(manifold.gradient(q)))
     return out

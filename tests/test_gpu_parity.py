@@ -561,3 +561,27 @@ def test_tc_sign_evaluation_equals_fp64_signs(golden, tag):
     signs = manifold.signs(pts)
     assert signs.shape == (pts.shape[0],) and set(np.unique(signs)) <= {-1, 1}
     assert np.array_equal(signs, np.where(values > 0.0, 1, -1))
+
+
+def test_learned_field_gradient(golden):
+    """KernelClassifierManifold.gradient(s) on the device against the reference formula (manifold.py:210-217),
+    and against central differences of the device values."""
+    g = golden("traces")
+    for tag in ("kclf_n3", "kclf_n6"):
+        inp = trace_inputs(g, tag)
+        m = product_manifold(g, tag)
+        rng = np.random.default_rng(3)
+        lo, hi = np.asarray(inp["box"][0]), np.asarray(inp["box"][1])
+        pts = rng.uniform(lo, hi, size=(257, inp["n"]))
+        got = m.gradients(pts)
+        d = pts[:, None, :] - m.support[None, :, :]
+        kern = np.exp(-m.gamma * np.einsum("ijk,ijk->ij", d, d)) * m.weights[None, :]
+        want = -2.0 * m.gamma * np.einsum("ij,ijk->ik", kern, d) - np.stack([m.barrier.gradient(q) for q in pts])
+        scale = np.abs(kern).sum(axis=1, keepdims=True) * 2.0 * m.gamma * 8.0
+        assert np.all(np.abs(got - want) <= 1e-12 * scale + 1e-12)
+        assert np.allclose(m.gradient(pts[5]), got[5], rtol=0, atol=0)
+        h = 1e-6
+        for dim in range(inp["n"]):
+            e = np.zeros(inp["n"]); e[dim] = h
+            fd = (m.values(pts[:16] + e) - m.values(pts[:16] - e)) / (2 * h)
+            assert np.allclose(fd, got[:16, dim], rtol=1e-5, atol=1e-6 * float(scale.max()))
