@@ -96,27 +96,6 @@ class _Transport:
         dev = self.engine.tensor_device
         return t.to(dev) if t.device != dev else t
 
-
-class ShardedTrace(_Transport):
-    """Owner-hashed BFS over the process group (the north star's multi-GPU trace; SURVEY.md section 8e).
-
-    Rank r owns the edges whose base lattice vertex hashes to r.  Every wave: expand the local frontier,
-    all_to_all the 16-byte candidate records to their owners, admit by minimum tag on the owner, rank the
-    winners' tags over all ranks (all_gather) so that every new edge gets its GLOBAL admission index,
-    commit.  The union of the ranks' edges ordered by that index is the single-GPU (= reference) edge list.
-
-    `engine` implements (records / tags are int64 torch tensors on `engine.tensor_device`):
-        trace_locate(seeds, rank, world) -> (local_frontier, global_total)
-        wave_candidates() -> (records [K, 2] bucketed by owner rank, counts list[int] of length world)
-        wave_admit(records [M, 2]) -> ascending winner tags [V]
-        wave_commit(gidx [V], alive, global_total) -> None
-        trace_counters() -> dict(dropped=..., field_evaluations=..., candidates=...)   (local)
-        local_edges() -> (gidx [E], payload [E, P])
-    """
-
-    def __init__(self, engine, group=None):
-        self._init_transport(engine, group)
-
     # -- collectives (identity when there is no process group) --
     def _sum(self, values):
         import torch
@@ -154,6 +133,27 @@ class ShardedTrace(_Transport):
         parts = [torch.empty_like(padded) for _ in range(self.world)]
         self.dist.all_gather(parts, padded, group=self.group)
         return [self._back(parts[r][: sizes[r]]) for r in range(self.world)]
+
+
+class ShardedTrace(_Transport):
+    """Owner-hashed BFS over the process group (the north star's multi-GPU trace; SURVEY.md section 8e).
+
+    Rank r owns the edges whose base lattice vertex hashes to r.  Every wave: expand the local frontier,
+    all_to_all the 16-byte candidate records to their owners, admit by minimum tag on the owner, rank the
+    winners' tags over all ranks (all_gather) so that every new edge gets its GLOBAL admission index,
+    commit.  The union of the ranks' edges ordered by that index is the single-GPU (= reference) edge list.
+
+    `engine` implements (records / tags are int64 torch tensors on `engine.tensor_device`):
+        trace_locate(seeds, rank, world) -> (local_frontier, global_total)
+        wave_candidates() -> (records [K, 2] bucketed by owner rank, counts list[int] of length world)
+        wave_admit(records [M, 2]) -> ascending winner tags [V]
+        wave_commit(gidx [V], alive, global_total) -> None
+        trace_counters() -> dict(dropped=..., field_evaluations=..., candidates=...)   (local)
+        local_edges() -> (gidx [E], payload [E, P])
+    """
+
+    def __init__(self, engine, group=None):
+        self._init_transport(engine, group)
 
     def run(self, seeds, max_edges: int) -> dict:
         eng = self.engine
@@ -229,8 +229,15 @@ class ShardedProof(_Transport):
             crossing_offsets = np.concatenate([[0], np.cumsum(counts[:, 1])[:-1]])
         else:
             merged, crossing_total, crossing_offsets = pts, int(crossing), np.zeros(1, dtype=np.int64)
-        kept, labels = eng.dedup_label(merged)
-        points = merged[kept]
+        if self.world > 1 and hasattr(eng, "label"):
+            # every rank runs the same deterministic dedup; the collision check of the kept points shards trivially
+            kept, _ = eng.dedup_label(merged, label=False)
+            points = merged[kept]
+            lo_i, cnt_i = cell_slice(points.shape[0], self.rank, self.world)
+            labels = torch.cat(self._gather_var(eng.label(points[lo_i:lo_i + cnt_i])))
+        else:
+            kept, labels = eng.dedup_label(merged)
+            points = merged[kept]
         info.update(
             crossing_edges=crossing_total, crossing_edges_local=int(crossing), candidates_local=int(pts.shape[0]),
             candidates=int(merged.shape[0]), points=points, in_collision=labels.to(torch.bool),
@@ -427,10 +434,11 @@ class CudaEngine:
             if sub:
                 lib.pt_cells_destroy(sub)
 
-    def dedup_label(self, points):
+    def dedup_label(self, points, label: bool = True):
+        """Greedy eps-dedup of `points` (priority order); with `label` also the collision labels of the kept points."""
         lib, cabi = self._cabi.lib, self._cabi
         ref = C.c_void_p()
-        ck = getattr(self.checker, "device_checker", None)
+        ck = getattr(self.checker, "device_checker", None) if label else None
         points = points.contiguous()
         cabi.check(lib.pt_dedup_label(self.ctx.handle, self.n, C.c_void_p(points.data_ptr()), points.shape[0],
                                       float(self.eps_dedup), ck.handle if ck is not None else None, C.byref(ref)))
@@ -439,3 +447,15 @@ class CudaEngine:
             return kept, labels
         finally:
             lib.pt_refine_destroy(ref)
+
+    def label(self, points):
+        """Non-free mask (outside the limits or in collision) of device points: uint8 tensor."""
+        lib, cabi, torch = self._cabi.lib, self._cabi, self.torch
+        points = points.contiguous()
+        out = torch.zeros(points.shape[0], dtype=torch.uint8, device=self.tensor_device)
+        ck = getattr(self.checker, "device_checker", None)
+        if ck is not None and points.shape[0]:
+            cabi.check(lib.pt_batch_check(self.ctx.handle, ck.handle, C.c_void_p(points.data_ptr()), points.shape[0],
+                                          1, C.c_void_p(out.data_ptr()), None))
+        return out
+
