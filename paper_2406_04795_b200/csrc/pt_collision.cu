@@ -6,6 +6,8 @@
 //   sphere_cylinder_hits    _kernels.pyx:79-104
 //   sphere_sphere_hits      _kernels.pyx:107-122   touching counts
 //   batch_check/_batch_hits collision.py:278-329 ; _not_free_checker pipeline.py:256-270
+#include <stdlib.h>
+#include <math.h>
 #include "pt_internal.cuh"
 
 #define PT_MAX_JOINTS 16
@@ -25,6 +27,8 @@ struct pt_checker {
     std::vector<int> sphere_order;   // position in link-sorted order -> original sphere index
     PtBuf<int> sphere_orig;    // same, on device (for fk output ordering)
     size_t model_doubles = 0;
+    // fp32 screen (pt_check32_kernel): bound on |gap32 - gap| for every (sphere, obstacle) pair of this model; 0 = off
+    float gap_margin = 0.f;
 };
 
 __device__ __forceinline__ bool pt_hit_box(double cx, double cy, double cz, double r, double lx, double ly, double lz) {
@@ -137,20 +141,145 @@ __device__ __forceinline__ bool pt_sphere_vs_scene(const double* obs, int no, co
     return false;
 }
 
+// ---- fp32 screen ------------------------------------------------------------------------------------------
+// The same walk in fp32: FK, obstacle-frame transform and the signed gap (distance to the primitive minus the sphere
+// radius; the reference's branch tests are exactly "gap <= 0") of every (sphere, obstacle) pair.  With `margin` a
+// bound on |gap32 - gap|, gap32 < -margin is a certain hit and gap32 > margin a certain miss; a configuration with an
+// undecided pair (and no certain hit) is marked 2 and decided by the fp64 kernel.
+__device__ __forceinline__ float pt_gap_box32(float cx, float cy, float cz, float r, float lx, float ly, float lz) {
+    const float dx = fabsf(cx) - 0.5f * lx, dy = fabsf(cy) - 0.5f * ly, dz = fabsf(cz) - 0.5f * lz;
+    const float ox = fmaxf(dx, 0.f), oy = fmaxf(dy, 0.f), oz = fmaxf(dz, 0.f);
+    const float outside = sqrtf(ox * ox + oy * oy + oz * oz);
+    const float inside = fminf(fmaxf(dx, fmaxf(dy, dz)), 0.f);
+    return outside + inside - r;
+}
+__device__ __forceinline__ float pt_gap_cylinder32(float cx, float cy, float cz, float r, float height, float radius) {
+    const float dz = fabsf(cz) - 0.5f * height, dr = sqrtf(cx * cx + cy * cy) - radius;
+    const float oz = fmaxf(dz, 0.f), orr = fmaxf(dr, 0.f);
+    return sqrtf(oz * oz + orr * orr) + fminf(fmaxf(dz, dr), 0.f) - r;
+}
+
+__global__ void __launch_bounds__(128)
+pt_check32_kernel(const double* __restrict__ model, int nj, int ns, int no, const double* __restrict__ q_, size_t m,
+                  int mode, float margin, uint8_t* __restrict__ out) {
+    extern __shared__ __align__(16) float smf[];
+    // joints and spheres as in the fp64 layout; every obstacle repacked into four float4 (one LDS.128 each):
+    //   (R00, R10, R20, tx) (R01, R11, R21, ty) (R02, R12, R22, tz) (dim0, dim1, dim2, type)
+    const int head = nj * PT_JSTRIDE + ns * PT_SSTRIDE;
+    const int head4 = (head + 3) & ~3;
+    for (int i = threadIdx.x; i < head; i += blockDim.x) smf[i] = (float)model[i];
+    float4* OB4 = reinterpret_cast<float4*>(smf + head4);
+    for (int i = threadIdx.x; i < no * 4; i += blockDim.x) {
+        const double* O = model + head + (i >> 2) * PT_OSTRIDE;
+        const int part = i & 3;
+        OB4[i] = part < 3 ? make_float4((float)O[1 + part], (float)O[4 + part], (float)O[7 + part], (float)O[10 + part])
+                          : make_float4((float)O[13], (float)O[14], (float)O[15], (float)O[0]);
+    }
+    __syncthreads();
+    const float* J = smf;
+    const float* SP = smf + nj * PT_JSTRIDE;
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    float q[PT_MAX_JOINTS];
+    bool inside = true;
+    for (int j = 0; j < nj; ++j) {
+        const double qd = q_[i * nj + j];
+        // the limit test stays exact: compare the fp64 value with the fp64 limits
+        inside = inside && (qd >= model[j * PT_JSTRIDE + 16]) && (qd <= model[j * PT_JSTRIDE + 17]);
+        q[j] = (float)qd;
+    }
+    if (mode != PT_LIMIT_IGNORE && !inside) { out[i] = 1; return; }
+    float R[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+    float t[3] = {0, 0, 0};
+    int sp = 0;
+    bool hit = false, undecided = false;
+    for (int link = 0; link <= nj && !hit; ++link) {
+        if (link > 0) {
+            const float* Jp = J + (link - 1) * PT_JSTRIDE;
+            float Rn[9];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) t[a] += R[3 * a] * Jp[13] + R[3 * a + 1] * Jp[14] + R[3 * a + 2] * Jp[15];
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+                for (int k = 0; k < 3; ++k) Rn[3 * a + k] = R[3 * a] * Jp[4 + k] + R[3 * a + 1] * Jp[7 + k] + R[3 * a + 2] * Jp[10 + k];
+            if (Jp[0] == 0.f) {
+                const float kx = Jp[1], ky = Jp[2], kz = Jp[3];
+                float sn, cs;
+                sincosf(q[link - 1], &sn, &cs);
+                const float omc = 1.f - cs;
+                const float A[9] = {cs + omc * kx * kx, -sn * kz + omc * kx * ky, sn * ky + omc * kx * kz,
+                                    sn * kz + omc * ky * kx, cs + omc * ky * ky, -sn * kx + omc * ky * kz,
+                                    -sn * ky + omc * kz * kx, sn * kx + omc * kz * ky, cs + omc * kz * kz};
+#pragma unroll
+                for (int a = 0; a < 3; ++a)
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) R[3 * a + k] = Rn[3 * a] * A[k] + Rn[3 * a + 1] * A[3 + k] + Rn[3 * a + 2] * A[6 + k];
+            } else {
+#pragma unroll
+                for (int a = 0; a < 9; ++a) R[a] = Rn[a];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) t[a] += (R[3 * a] * Jp[1] + R[3 * a + 1] * Jp[2] + R[3 * a + 2] * Jp[3]) * q[link - 1];
+            }
+        }
+        while (sp < ns && (int)SP[sp * PT_SSTRIDE] == link && !hit) {
+            const float* S = SP + sp * PT_SSTRIDE;
+            const float cx = R[0] * S[1] + R[1] * S[2] + R[2] * S[3] + t[0];
+            const float cy = R[3] * S[1] + R[4] * S[2] + R[5] * S[3] + t[1];
+            const float cz = R[6] * S[1] + R[7] * S[2] + R[8] * S[3] + t[2];
+            const float r = S[4];
+            for (int o = 0; o < no; ++o) {
+                const float4 A = OB4[4 * o], B = OB4[4 * o + 1], Cc = OB4[4 * o + 2], D = OB4[4 * o + 3];
+                const float dx = cx - A.w, dy = cy - B.w, dz = cz - Cc.w;
+                const float lx = dx * A.x + dy * A.y + dz * A.z;
+                const float ly = dx * B.x + dy * B.y + dz * B.z;
+                const float lz = dx * Cc.x + dy * Cc.y + dz * Cc.z;
+                const int type = (int)D.w;
+                float gap;
+                if (type == 0) gap = pt_gap_box32(lx, ly, lz, r, D.x, D.y, D.z);
+                else if (type == 1) gap = pt_gap_cylinder32(lx, ly, lz, r, D.x, D.y);
+                else gap = sqrtf(lx * lx + ly * ly + lz * lz) - (r + D.x);
+                if (gap < -margin) { hit = true; break; }
+                if (!(gap > margin)) undecided = true;     // also catches NaN
+            }
+            ++sp;
+        }
+    }
+    out[i] = hit ? 1 : (undecided ? 2 : 0);
+}
+
+__global__ void pt_check_select_kernel(const uint8_t* __restrict__ flag, size_t m, uint32_t* __restrict__ list,
+                                       unsigned long long* count) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool take = i < m && flag[i] == 2;
+    const unsigned ballot = __ballot_sync(0xffffffffu, take);
+    if (ballot) {
+        const int lane = threadIdx.x & 31, leader = __ffs(ballot) - 1;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(count, (unsigned long long)__popc(ballot));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (take) list[base + __popc(ballot & ((1u << lane) - 1u))] = (uint32_t)i;
+    }
+}
+
 // mode: PT_LIMIT_ERROR -> out-of-limit rows recorded in *first_bad (atomicMin) and marked 1
 //       PT_LIMIT_UNFREE -> out-of-limit rows marked 1 without testing; PT_LIMIT_IGNORE -> always test
 __global__ void __launch_bounds__(128)
-pt_check_kernel(const double* __restrict__ model, int nj, int ns, int no, const double* __restrict__ q_, size_t m,
-                int mode, uint8_t* __restrict__ out, unsigned long long* first_bad) {
+pt_check_kernel(const double* __restrict__ model, int nj, int ns, int no, const double* __restrict__ q_, size_t m_all,
+                int mode, uint8_t* __restrict__ out, unsigned long long* first_bad, const uint32_t* __restrict__ list,
+                const unsigned long long* __restrict__ list_count) {
     extern __shared__ double sm[];
+    const size_t m = list ? (size_t)*list_count : m_all;        // optional compacted row list (device-side count)
+    if ((size_t)blockIdx.x * blockDim.x >= m) return;
     const int total = nj * PT_JSTRIDE + ns * PT_SSTRIDE + no * PT_OSTRIDE;
     for (int i = threadIdx.x; i < total; i += blockDim.x) sm[i] = model[i];
     __syncthreads();
     const double* J = sm;
     const double* SP = sm + nj * PT_JSTRIDE;
     const double* OB = SP + ns * PT_SSTRIDE;
-    size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= m) return;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= m) return;
+    const size_t i = list ? (size_t)list[idx] : idx;
     double q[PT_MAX_JOINTS];
     bool inside = true;
     for (int j = 0; j < nj; ++j) {
@@ -217,10 +346,30 @@ int pt_checker_run_dev(pt_ctx* ctx, const pt_checker* ck, const double* q_dev, s
     PT_TRY(bad.alloc(ctx, 1));
     PT_CUDA(ctx, cudaMemsetAsync(bad.p, 0xFF, sizeof(unsigned long long), ctx->stream));
     const size_t smem = ck->model_doubles * sizeof(double);
+    if (ck->gap_margin > 0.f && mode != PT_LIMIT_ERROR && m >= 4096 && m < (1ull << 32)) {
+        // fp32 screen, then the fp64 kernel on the undecided configurations only
+        PtBuf<uint32_t> list; PtBuf<unsigned long long> cnt;
+        PT_TRY(list.alloc(ctx, m));
+        PT_TRY(cnt.alloc(ctx, 1));
+        PT_CUDA(ctx, cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), ctx->stream));
+        {
+            PT_LAUNCH(ctx, "collision_screen_fp32");
+            pt_check32_kernel<<<pt_grid_for(m, 128), 128, (ck->model_doubles + 4) * sizeof(float), ctx->stream>>>(
+                ck->model.p, ck->nj, ck->ns, ck->no, q_dev, m, mode, ck->gap_margin, out_dev);
+            PT_TRY(pt_check_launch(ctx, "pt_check32_kernel"));
+            pt_check_select_kernel<<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>(out_dev, m, list.p, cnt.p);
+            PT_TRY(pt_check_launch(ctx, "pt_check_select_kernel"));
+        }
+        PT_LAUNCH(ctx, "collision_check");
+        pt_check_kernel<<<pt_grid_for(m, 128), 128, smem, ctx->stream>>>(ck->model.p, ck->nj, ck->ns, ck->no, q_dev, m,
+                                                                           mode, out_dev, bad.p, list.p, cnt.p);
+        PT_TRY(pt_check_launch(ctx, "pt_check_kernel"));
+        return PT_OK;
+    }
     {
         PT_LAUNCH(ctx, "collision_check");
         pt_check_kernel<<<pt_grid_for(m, 128), 128, smem, ctx->stream>>>(ck->model.p, ck->nj, ck->ns, ck->no, q_dev, m,
-                                                                           mode, out_dev, bad.p);
+                                                                           mode, out_dev, bad.p, nullptr, nullptr);
         PT_TRY(pt_check_launch(ctx, "pt_check_kernel"));
     }
     if (mode == PT_LIMIT_ERROR) {
@@ -329,7 +478,36 @@ int pt_checker_create(pt_ctx* ctx, int nj, const int* joint_kind, const double* 
     cudaMemcpyAsync(ck->sphere_orig.p, ck->sphere_order.data(), ns * sizeof(int), cudaMemcpyHostToDevice, ctx->stream);
     cudaError_t e = cudaStreamSynchronize(ctx->stream);
     if (e != cudaSuccess) { delete ck; return pt_fail(ctx, PT_E_CUDA, "model upload failed: %s", cudaGetErrorString(e)); }
+    {
+        // |gap32 - gap| <= 64 u32 (nj + 2) * (chain reach + farthest obstacle + largest primitive): every fp32
+        // operation of the walk errs by at most u32 times a coordinate bounded by that length; 64 covers the op count
+        // per joint (two 3x3 products, Rodrigues, sincosf) with a wide allowance
+        double reach = 0.0, far = 0.0, dims = 0.0;
+        for (int j = 0; j < nj; ++j) {
+            double tn = 0.0;
+            for (int k = 0; k < 3; ++k) tn += joint_trans[3 * j + k] * joint_trans[3 * j + k];
+            reach += sqrt(tn);
+            if (joint_kind[j] != 0) reach += fmax(fabs(joint_limits[2 * j]), fabs(joint_limits[2 * j + 1]));
+        }
+        double off = 0.0;
+        for (int sidx = 0; sidx < ns; ++sidx) {
+            double on = 0.0;
+            for (int k = 0; k < 3; ++k) on += sphere_offset[3 * sidx + k] * sphere_offset[3 * sidx + k];
+            off = fmax(off, sqrt(on) + fabs(sphere_radius[sidx]));
+        }
+        for (int o = 0; o < no; ++o) {
+            double tn = 0.0;
+            for (int k = 0; k < 3; ++k) { tn += obs_trans[3 * o + k] * obs_trans[3 * o + k]; dims = fmax(dims, fabs(obs_dims[3 * o + k])); }
+            far = fmax(far, sqrt(tn));
+        }
+        const double length = reach + off + far + dims + 1.0;
+        const char* env = getenv("PERMATRACE_B200_PRECISION");
+        const bool plain = env && env[0] == '0';
+        ck->gap_margin = plain ? 0.f : (float)(64.0 * 5.9604644775390625e-08 * (nj + 2) * length);
+        if (!(ck->gap_margin < 1e-2f)) ck->gap_margin = 0.f;     // hopelessly large model: fp64 only
+    }
     if (ck->model_doubles * sizeof(double) > 48 * 1024) {
+        cudaFuncSetAttribute(pt_check32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)((ck->model_doubles + 4) * sizeof(float)));
         cudaFuncSetAttribute(pt_check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(ck->model_doubles * sizeof(double)));
         cudaFuncSetAttribute(pt_fk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(ck->model_doubles * sizeof(double)));
     }

@@ -585,3 +585,38 @@ def test_learned_field_gradient(golden):
             e = np.zeros(inp["n"]); e[dim] = h
             fd = (m.values(pts[:16] + e) - m.values(pts[:16] - e)) / (2 * h)
             assert np.allclose(fd, got[:16, dim], rtol=1e-5, atol=1e-6 * float(scale.max()))
+
+
+def test_collision_fp32_screen_equals_fp64(monkeypatch):
+    """Large batches go through the fp32 screen (certain hit / certain miss / undecided -> fp64 kernel): the masks
+    must equal the plain fp64 kernel's on random configurations, on configurations dragged onto obstacle surfaces
+    (bisected along segments between a free and a colliding configuration), and on out-of-limit rows."""
+    from tests.conftest import robot_scene_dicts
+    for n, nobs in ((6, 8), (4, 3)):
+        rd, sd = robot_scene_dicts(n, nobs)
+        rng = np.random.default_rng(5)
+        q = rng.uniform(-1.6, 1.6, size=(60_000, n))            # limits are +-1.5: some rows are outside
+        masks = {}
+        for mode in ("0", "1"):
+            monkeypatch.setenv("PERMATRACE_B200_PRECISION", mode)
+            robot, scene = CO.robot_from_dict(rd), CO.scene_from_dict(sd)
+            masks[mode] = CO.batch_check(q, robot, scene, on_limit="unfree")
+            if mode == "0":
+                # touching configurations: bisect free/colliding pairs with the fp64 kernel to ~1e-9 of the surface
+                inside = np.all(np.abs(q) <= 1.5, axis=1)
+                free = q[inside & ~masks["0"]][:4000]
+                coll = q[inside & masks["0"]][:4000]
+                k = min(len(free), len(coll))
+                a, b = free[:k].copy(), coll[:k].copy()
+                for _ in range(30):
+                    mid = 0.5 * (a + b)
+                    hit = CO.batch_check(mid, robot, scene, on_limit="unfree")
+                    b[hit], a[~hit] = mid[hit], mid[~hit]
+                near = np.concatenate([a, b, 0.5 * (a + b)])
+                near = np.concatenate([near, near + rng.normal(scale=1e-6, size=near.shape)])
+                masks["near0"] = CO.batch_check(near, robot, scene, on_limit="unfree")
+            else:
+                masks["near1"] = CO.batch_check(near, robot, scene, on_limit="unfree")
+        assert masks["0"].sum() > 1000 and (~masks["0"]).sum() > 1000
+        assert np.array_equal(masks["0"], masks["1"])
+        assert near.shape[0] >= 4096 and np.array_equal(masks["near0"], masks["near1"])
