@@ -620,3 +620,31 @@ def test_collision_fp32_screen_equals_fp64(monkeypatch):
         assert masks["0"].sum() > 1000 and (~masks["0"]).sum() > 1000
         assert np.array_equal(masks["0"], masks["1"])
         assert near.shape[0] >= 4096 and np.array_equal(masks["near0"], masks["near1"])
+
+
+def test_large_support_set_fallback_paths(monkeypatch):
+    """S = 4096 support vectors do not fit one CTA's shared memory: the root solve then uses the SIMT fp32 screen and the
+    tiled rest kernel.  Fast path == plain fp64 bisection on the same device, and the trace is unchanged."""
+    from paper_2406_04795_b200.scenes import synthetic_support
+    from bench import _train_numpy
+    n, lam, k = 4, 0.3, 2
+    pos, neg, rng = synthetic_support(n, 4096, 0.9, 1.5, seed=3)
+    support, weights = _train_numpy(pos, neg, 2.0, 1e-3)
+    sigma = 0.5
+    lo, hi = -1.5 * np.ones(n), 1.5 * np.ones(n)
+    coarse = lam * k
+    margin = max(3.0 * coarse, 2.0 * sigma + (1.0 + 2.0 * np.sqrt(n)) * coarse)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("PERMATRACE_B200_PRECISION", mode)
+        m = M.KernelClassifierManifold(support, weights, 2.0, lam * 2.0, barrier=M.BoxBarrier(lo, hi, sigma / 4.0, 2.0 / sigma))
+        cfg = T.TraceConfig(L.LatticeConfig(n, coarse), box=(tuple(lo - margin), tuple(hi + margin)), eps=1e-9)
+        seeds = M.sample_seeds(m, (lo, hi), 12, rng=np.random.default_rng(1), min_separation=coarse / 2.0)
+        res = T.trace(seeds, m, cfg)
+        ref = S.refine(S.coarse_cells(res), S.build_template(n, k), m, lambda p: np.zeros(len(p), dtype=bool), cfg)
+        out[mode] = (res.edges.arrays(), res.points.copy(), ref.points.copy(), res.stats.closure_ok)
+    assert out["1"][3] and out["0"][3]
+    for a, b in zip(out["0"][0], out["1"][0]):
+        assert np.array_equal(a, b)
+    assert out["0"][1].shape == out["1"][1].shape and out["0"][2].shape == out["1"][2].shape and out["1"][2].shape[0] > 4096
+    assert np.max(np.abs(out["0"][1] - out["1"][1])) <= 1e-8 and np.max(np.abs(out["0"][2] - out["1"][2])) <= 1e-8
