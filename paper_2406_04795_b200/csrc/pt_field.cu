@@ -19,7 +19,9 @@ struct pt_field {
     // tensor-core screen (pt_field_tc.cuh): packed tf32 support operand; tc_ok = it fits one CTA's shared memory
     PtBuf<float> tc_bt, tc_wt;
     PtTcDev tc;
-    bool tc_ok = false;
+    bool tc_ok = false;          // the tf32 operand exists (n <= 6)
+    bool tc_resident = false;    // ... and the whole support set fits one CTA's shared memory (persistent kernel)
+    bool tc_levels = false;      // force the level-synchronous driver (PERMATRACE_B200_TC_LEVELS=1)
 };
 
 int pt_field_dim(const pt_field* f) { return f->d.n; }
@@ -1042,7 +1044,7 @@ static int pt_eval_launch(pt_ctx* ctx, const pt_field* f, const double* pts, siz
     // Signs of a large batch (lattice vertices of a BFS wave / of the refinement): the kernel sum runs on the tensor
     // cores in fp32 (pt_field_tc.cuh, MODE 2) with the screen's rigorous error bound; rows whose fp32 sign is not
     // proven are rechecked by the fp64 kernel through a compacted list.
-    if (!vals && signs && f->tc_ok && f->precision != 0 && m >= (size_t)PT_TC_M * 32) {
+    if (!vals && signs && f->tc_resident && f->precision != 0 && m >= (size_t)PT_TC_M * 32) {
         if constexpr (N <= 6) {
             PtBuf<uint32_t> list; PtBuf<unsigned long long> cnt;
             PT_TRY(list.alloc(ctx, m));
@@ -1088,8 +1090,60 @@ static int pt_screen_tc_launch(pt_ctx* ctx, const pt_field* f, const PtRows& row
             configured = true;
         }
         const unsigned grid = pt_grid_for(rows.m, 2 * PT_TC_M, (unsigned)ctx->sm_count);
-        pt_bisect32_tc_kernel<N, MODE><<<grid, PT_TC_THREADS, smem, ctx->stream>>>(f->d, f->tc, rows, a, b, sa, eps, fresh, lo, hi, sign_out, ctx->work);
+        const PtTcLevel whole{0, f->tc.spad, nullptr, nullptr, 1};
+        pt_bisect32_tc_kernel<N, MODE><<<grid, PT_TC_THREADS, smem, ctx->stream>>>(f->d, f->tc, rows, a, b, sa, eps, fresh, lo, hi, sign_out, whole, ctx->work);
         return pt_check_launch(ctx, "pt_bisect32_tc_kernel");
+    }
+}
+
+// Level-synchronous screen (pt_field_tc.cuh, MODE 3): per bisection level one launch per support chunk over the rows
+// that are still active (compacted, device-side counts -- no host synchronisation), then the decision kernel.  Serves
+// support sets that do not fit one CTA's shared memory; every launch re-stages its chunk (<= 192 KB per CTA from L2).
+#define PT_SCREEN_MAX_LEVELS 10
+template <int N>
+static int pt_screen_levels_launch(pt_ctx* ctx, const pt_field* f, const PtRows& rows, const double* a, const double* b,
+                                   const int8_t* sa, double eps, int fresh, double* lo, double* hi) {
+    if constexpr (N > 6) {
+        return pt_fail(ctx, PT_E_STATE, "tensor-core screen is built for n <= 6");
+    } else {
+        const size_t m = rows.m;
+        const int spad = f->tc.spad;
+        const int cmax = pt_tc_chunk_rows(N);
+        const int nchunks = (spad + cmax - 1) / cmax;
+        int cs = (((spad + nchunks - 1) / nchunks) + PT_TC_N - 1) / PT_TC_N * PT_TC_N;
+        static bool configured = false;
+        if (!configured) {
+            PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect32_tc_kernel<N, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_TC_SMEM_LIMIT));
+            configured = true;
+        }
+        PtBuf<double> acc, ab; PtBuf<uint32_t> la, lb; PtBuf<unsigned long long> cnt;
+        PT_TRY(acc.alloc(ctx, m)); PT_TRY(ab.alloc(ctx, m));
+        PT_TRY(la.alloc(ctx, m)); PT_TRY(lb.alloc(ctx, m));
+        PT_TRY(cnt.alloc(ctx, PT_SCREEN_MAX_LEVELS + 2));
+        PT_CUDA(ctx, cudaMemsetAsync(cnt.p, 0, (PT_SCREEN_MAX_LEVELS + 2) * sizeof(unsigned long long), ctx->stream));
+        pt_screen_filter_kernel<N><<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>(rows, a, b, eps, fresh, lo, hi, la.p, cnt.p);
+        PT_TRY(pt_check_launch(ctx, "pt_screen_filter_kernel"));
+        uint32_t* lin = la.p; uint32_t* lout = lb.p;
+        const unsigned grid = pt_grid_for(m, 2 * PT_TC_M, (unsigned)ctx->sm_count);
+        for (int level = 0; level < PT_SCREEN_MAX_LEVELS; ++level) {
+            const PtRows sub{lin, cnt.p + level, m};
+            for (int c = 0; c < nchunks; ++c) {
+                const int j0 = c * cs;
+                const int rows_c = (j0 + cs <= spad) ? cs : (spad - j0);
+                if (rows_c <= 0) break;
+                const size_t kc = (size_t)pt_tc_kt(N) / 4;
+                const size_t smem = kc * (size_t)rows_c * 16 + 2 * kc * PT_TC_M * 16 + (size_t)rows_c * 4 + 64;
+                const PtTcLevel lv{j0, rows_c, acc.p, ab.p, c == 0 ? 1 : 0};
+                pt_bisect32_tc_kernel<N, 3><<<grid, PT_TC_THREADS, smem, ctx->stream>>>(f->d, f->tc, sub, a, b, sa, eps, 0, lo, hi,
+                                                                                         nullptr, lv, ctx->work);
+                PT_TRY(pt_check_launch(ctx, "pt_bisect32_tc_kernel"));
+            }
+            pt_screen_decide_kernel<N><<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>(f->d, lin, cnt.p + level, a, b, sa, eps, lo, hi,
+                                                                                      acc.p, ab.p, lout, cnt.p + level + 1, ctx->work);
+            PT_TRY(pt_check_launch(ctx, "pt_screen_decide_kernel"));
+            uint32_t* sw = lin; lin = lout; lout = sw;
+        }
+        return PT_OK;
     }
 }
 
@@ -1131,9 +1185,11 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
     } while (0)
     // batches that fill the machine screen on the tensor cores (tcgen05), small ones on the SIMT kernel
     const bool use_tc = f->tc_ok && m >= (size_t)PT_TC_M * 32;
+    const bool by_level = use_tc && (!f->tc_resident || f->tc_levels);
     {
         PT_LAUNCH(ctx, use_tc ? "bisect_fp32_screen_tc" : "bisect_fp32_screen");
-        if (use_tc) PT_TRY((pt_screen_tc_launch<N, 0>(ctx, f, all, a, b, sa, eps, 1, lo.p, hi.p, nullptr)));
+        if (by_level) PT_TRY((pt_screen_levels_launch<N>(ctx, f, all, a, b, sa, eps, 1, lo.p, hi.p)));
+        else if (use_tc) PT_TRY((pt_screen_tc_launch<N, 0>(ctx, f, all, a, b, sa, eps, 1, lo.p, hi.p, nullptr)));
         else PT_G_LAUNCH(pt_bisect32_kernel, smem32, f->d, all, a, b, sa, eps, 1, lo.p, hi.p, ctx->work);
     }
     // rows that stopped while their bracket is still wide: one true fp64 step, then back to fp32
@@ -1151,7 +1207,8 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
         }
         {
             PT_LAUNCH(ctx, use_tc ? "bisect_fp32_screen_tc" : "bisect_fp32_screen");
-            if (use_tc) PT_TRY((pt_screen_tc_launch<N, 0>(ctx, f, sub, a, b, sa, eps, 0, lo.p, hi.p, nullptr)));
+            if (by_level) PT_TRY((pt_screen_levels_launch<N>(ctx, f, sub, a, b, sa, eps, 0, lo.p, hi.p)));
+            else if (use_tc) PT_TRY((pt_screen_tc_launch<N, 0>(ctx, f, sub, a, b, sa, eps, 0, lo.p, hi.p, nullptr)));
             else PT_G_LAUNCH(pt_bisect32_kernel, smem32, f->d, sub, a, b, sa, eps, 0, lo.p, hi.p, ctx->work);
         }
     }
@@ -1277,7 +1334,7 @@ static int pt_field_build_rbf(pt_ctx* ctx, int n, long long S, const double* sup
         f->d.sv32 = f->sv32.p;
         // tensor-core screen operand, when the whole packed support set fits one CTA's shared memory
         const char* tc_env = getenv("PERMATRACE_B200_TC");
-        if (!(tc_env && tc_env[0] == '0') && n <= 6 && pt_tc_smem_bytes(n, S) <= PT_TC_SMEM_LIMIT) {
+        if (!(tc_env && tc_env[0] == '0') && n <= 6) {
             const int kt = pt_tc_kt(n), spad = (int)pt_tc_spad(S);
             rc = f->tc_bt.alloc(ctx, (size_t)kt * spad);
             if (rc == PT_OK) rc = f->tc_wt.alloc(ctx, (size_t)spad);
@@ -1288,6 +1345,9 @@ static int pt_field_build_rbf(pt_ctx* ctx, int n, long long S, const double* sup
             if (rc != PT_OK) { delete f; return rc; }
             f->tc.bt = f->tc_bt.p; f->tc.wt = f->tc_wt.p; f->tc.spad = spad; f->tc.kt = kt;
             f->tc_ok = true;
+            f->tc_resident = pt_tc_smem_bytes(n, S) <= PT_TC_SMEM_LIMIT;
+            const char* lv_env = getenv("PERMATRACE_B200_TC_LEVELS");
+            f->tc_levels = lv_env && lv_env[0] == '1';
             cudaStreamSynchronize(ctx->stream);   // sdev/wdev may be staging buffers released on return
         }
     }
@@ -1412,7 +1472,7 @@ int pt_intersection_points(pt_ctx* ctx, const pt_field* f, const double* a, cons
 
 int pt_debug_tc_arg_error(pt_ctx* ctx, const pt_field* f, const double* a, const double* b, long long m, double* out) {
     if (!ctx || !f || !a || !b || !out || m <= 0) return pt_fail(ctx, PT_E_INVALID, "pt_debug_tc_arg_error: bad argument");
-    if (f->d.kind != PT_FIELD_RBF || !f->tc_ok) return pt_fail(ctx, PT_E_STATE, "field has no tensor-core operand");
+    if (f->d.kind != PT_FIELD_RBF || !f->tc_resident) return pt_fail(ctx, PT_E_STATE, "field has no resident tensor-core operand");
     const int n = f->d.n;
     PtBuf<double> ta, tb, lo, hi; PtBuf<int8_t> sa;
     const double *adev, *bdev;

@@ -47,6 +47,13 @@ static inline size_t pt_tc_smem_bytes(int n, long long S) {
     const size_t kc = (size_t)pt_tc_kt(n) / 4;
     return kc * (size_t)pt_tc_spad(S) * 16 + 2 * kc * PT_TC_M * 16 + (size_t)pt_tc_spad(S) * 4 + 64;
 }
+// largest support chunk (multiple of PT_TC_N rows) that fits one CTA's shared memory next to the A operands
+static inline int pt_tc_chunk_rows(int n) {
+    const size_t kc = (size_t)pt_tc_kt(n) / 4;
+    const size_t fixed = 2 * kc * PT_TC_M * 16 + 64;
+    const size_t per_row = kc * 16 + 4;
+    return (int)(((PT_TC_SMEM_LIMIT - fixed) / per_row) / PT_TC_N) * PT_TC_N;
+}
 
 struct PtTcDev {
     const float* bt;   // [KT/4][Spad][4] tf32 pieces of the support side, UMMA K-major core-matrix order

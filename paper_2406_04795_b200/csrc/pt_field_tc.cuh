@@ -165,10 +165,22 @@ __device__ __forceinline__ double pt_barrier_fast(const PtFieldDev& f, const dou
     return gs * (double)acc;
 }
 
+// MODE 3 arguments: one bisection level of the listed rows against ONE chunk [j0, j0+cs) of the support set; the
+// partial sums are stored (first chunk) or added to acc[row] / ab[row].  Other modes: j0 = 0, cs = spad.
+struct PtTcLevel {
+    int j0, cs;
+    double* acc;
+    double* ab;
+    int first_chunk;
+};
+
 // MODE 0: the bisection screen (same contract as pt_bisect32_kernel).
 // MODE 1: calibration -- one evaluation at t = 0.5 per row; hi_io[row] receives max_j |arg_tc - arg_fp64| / (u32*T).
 // MODE 2: sign evaluation at the points a_[row] (lattice vertices): sign_out[row] = +1 / -1 when |F32| > E, i.e. the
 //         fp32 sign is PROVEN equal to the fp64 one, and 0 when it is not -- those rows are rechecked in fp64.
+// MODE 3: level-synchronous screen for support sets larger than one CTA's shared memory (and, optionally, for all):
+//         ONE evaluation at the midpoint of every listed row's current bracket against one support chunk; the
+//         decision is taken by pt_screen_decide_kernel once all chunks of the level have been added.
 //
 // Two independent row groups per CTA (warps 0-3 and 4-7, 128 rows each, one row per thread = one TMEM lane): every
 // bisection level ends in a serial stretch (decide, move the bracket, rewrite A, wait for the first MMA), and while
@@ -177,16 +189,17 @@ template <int N, int MODE>
 __global__ void __launch_bounds__(PT_TC_THREADS, 1)
 pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __restrict__ a_, const double* __restrict__ b_,
                       const int8_t* __restrict__ signs_a, double eps, int fresh, double* __restrict__ lo_io,
-                      double* __restrict__ hi_io, int8_t* __restrict__ sign_out, unsigned long long* work) {
+                      double* __restrict__ hi_io, int8_t* __restrict__ sign_out, PtTcLevel lv, unsigned long long* work) {
     extern __shared__ __align__(1024) unsigned char pt_tc_smem[];
     constexpr int KT = ((3 * N + 6) + 7) & ~7;
     constexpr int KC = KT / 4;           // 16-byte K chunks
-    const int spad = tc.spad;
-    const int ntiles = spad / PT_TC_N;
+    const int spad = tc.spad;            // row stride of the packed operand in global memory
+    const int cs = lv.cs;                // support rows resident in this launch
+    const int ntiles = cs / PT_TC_N;
     float* sB = reinterpret_cast<float*>(pt_tc_smem);
-    float* sA0 = sB + (size_t)KC * spad * 4;                    // A of group 0, then group 1
+    float* sA0 = sB + (size_t)KC * cs * 4;                      // A of group 0, then group 1
     float* sW = sA0 + 2 * (size_t)KC * PT_TC_M * 4;
-    unsigned long long* sBar = reinterpret_cast<unsigned long long*>(sW + spad);
+    unsigned long long* sBar = reinterpret_cast<unsigned long long*>(sW + cs);
     uint32_t* sTmem = reinterpret_cast<uint32_t*>(sBar + 4);
 
     const int tid = threadIdx.x, warp = tid >> 5;
@@ -206,10 +219,13 @@ pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __res
     {
         const uint4* src = reinterpret_cast<const uint4*>(tc.bt);
         uint4* dst = reinterpret_cast<uint4*>(sB);
-        for (int i = tid; i < KC * spad; i += PT_TC_THREADS) dst[i] = src[i];
-        const uint4* ws = reinterpret_cast<const uint4*>(tc.wt);
+        for (int i = tid; i < KC * cs; i += PT_TC_THREADS) {
+            const int c = i / cs, j = i - c * cs;
+            dst[i] = src[(size_t)c * spad + lv.j0 + j];
+        }
+        const uint4* ws = reinterpret_cast<const uint4*>(tc.wt + lv.j0);
         uint4* wd = reinterpret_cast<uint4*>(sW);
-        for (int i = tid; i < spad / 4; i += PT_TC_THREADS) wd[i] = ws[i];
+        for (int i = tid; i < cs / 4; i += PT_TC_THREADS) wd[i] = ws[i];
     }
     pt_fence_async_smem();
     pt_tc_fence_before();
@@ -229,8 +245,8 @@ pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __res
 #pragma unroll
         for (int ks = 0; ks < KT / 8; ++ks) {
             const uint64_t da = pt_umma_desc(sA_u32 + (uint32_t)(2 * ks) * (PT_TC_M * 16), PT_TC_M * 16, 128);
-            const uint64_t db = pt_umma_desc(sB_u32 + (uint32_t)(2 * ks) * (uint32_t)(spad * 16) + (uint32_t)tile * (PT_TC_N * 16),
-                                             (uint32_t)(spad * 16), 128);
+            const uint64_t db = pt_umma_desc(sB_u32 + (uint32_t)(2 * ks) * (uint32_t)(cs * 16) + (uint32_t)tile * (PT_TC_N * 16),
+                                             (uint32_t)(cs * 16), 128);
             pt_umma_tf32(tmem_base + (uint32_t)buf * PT_TC_N, da, db, PT_TC_IDESC, ks > 0 ? 1u : 0u);
         }
         pt_umma_commit(bar_u32[buf]);
@@ -252,7 +268,7 @@ pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __res
             for (int d = 0; d < N; ++d) { a[d] = a_[ei * N + d]; b[d] = b_[ei * N + d]; }
             seg = pt_segment<N>(a, b, diff);
             sa = signs_a[ei];
-            if (!fresh && MODE == 0) { lo = lo_io[ei]; hi = hi_io[ei]; }
+            if ((!fresh && MODE == 0) || MODE == 3) { lo = lo_io[ei]; hi = hi_io[ei]; }
         } else {
 #pragma unroll
             for (int d = 0; d < N; ++d) { a[d] = 0.0; diff[d] = 0.0; }
@@ -334,7 +350,7 @@ pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __res
                         // calibration: exact exponent from the fp64 rows (row layout: 2 gl s_d, w, -gl |s|^2)
                         const int ROW = PT_ROW64(N);
                         for (int c = 0; c < 32; ++c) {
-                            const long long j = (long long)t * PT_TC_N + blk * 32 + c;
+                            const long long j = (long long)lv.j0 + (long long)t * PT_TC_N + blk * 32 + c;
                             if (j < f.S) {
                                 const double* srow = f.sv + j * ROW;
                                 double ex = srow[N + 1] - gl * p2;
@@ -357,7 +373,13 @@ pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __res
                 }
             }
             const double pn = sqrt(p2) + f.smax;
-            if (MODE == 1) {
+            if (MODE == 3) {
+                if (valid) {
+                    if (lv.first_chunk) { lv.acc[ei] = acc; lv.ab[ei] = ab; }
+                    else { lv.acc[ei] += acc; lv.ab[ei] += ab; }
+                }
+                active = false;
+            } else if (MODE == 1) {
                 calib = calib / (PT_U32 * gl * pn * pn);
                 active = false;
             } else {
@@ -389,12 +411,88 @@ pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __res
             if (valid) { lo_io[ei] = lo; hi_io[ei] = hi; }
         } else if (MODE == 1) {
             if (valid) hi_io[ei] = calib;
-        } else if (valid) {
-            sign_out[ei] = sign_certain;
+        } else if (MODE == 2) {
+            if (valid) sign_out[ei] = sign_certain;
         }
     }
     pt_tc_fence_before();
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*sTmem), "r"(512u));
+}
+
+// ---- level-synchronous driver kernels (MODE 3) ------------------------------------------------------------------
+// rows of `rows` whose bracket still needs a step -> list_out (fresh: brackets start at [0, 1])
+template <int N>
+__global__ void pt_screen_filter_kernel(PtRows rows, const double* __restrict__ a_, const double* __restrict__ b_, double eps,
+                                        int fresh, double* __restrict__ lo_io, double* __restrict__ hi_io,
+                                        uint32_t* __restrict__ list_out, unsigned long long* count_out) {
+    const size_t total = pt_rows_total(rows);
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool take = false; size_t ei = 0;
+    if (idx < total) {
+        ei = rows.list ? (size_t)rows.list[idx] : idx;
+        double a[N], b[N], diff[N];
+#pragma unroll
+        for (int d = 0; d < N; ++d) { a[d] = a_[ei * N + d]; b[d] = b_[ei * N + d]; }
+        const double seg = pt_segment<N>(a, b, diff);
+        double lo = 0.0, hi = 1.0;
+        if (fresh) { lo_io[ei] = lo; hi_io[ei] = hi; } else { lo = lo_io[ei]; hi = hi_io[ei]; }
+        take = __dmul_rn(seg, __dsub_rn(hi, lo)) > eps;
+    }
+    const unsigned ballot = __ballot_sync(0xffffffffu, take);
+    if (ballot) {
+        const int lane = threadIdx.x & 31, leader = __ffs(ballot) - 1;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(count_out, (unsigned long long)__popc(ballot));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (take) list_out[base + __popc(ballot & ((1u << lane) - 1u))] = (uint32_t)ei;
+    }
+}
+
+// the decision of one level: F32 = bias + acc - barrier against E; certain -> move the bracket, still active -> list_out
+template <int N>
+__global__ void pt_screen_decide_kernel(PtFieldDev f, const uint32_t* __restrict__ list_in, const unsigned long long* count_in,
+                                        const double* __restrict__ a_, const double* __restrict__ b_,
+                                        const int8_t* __restrict__ signs_a, double eps, double* __restrict__ lo_io,
+                                        double* __restrict__ hi_io, const double* __restrict__ acc_, const double* __restrict__ ab_,
+                                        uint32_t* __restrict__ list_out, unsigned long long* count_out, unsigned long long* work) {
+    const size_t total = (size_t)*count_in;
+    const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool active = false; uint32_t ei = 0; unsigned stepped = 0;
+    if (idx < total) {
+        ei = list_in[idx];
+        double a[N], b[N], diff[N], p[N];
+#pragma unroll
+        for (int d = 0; d < N; ++d) { a[d] = a_[(size_t)ei * N + d]; b[d] = b_[(size_t)ei * N + d]; }
+        const double seg = pt_segment<N>(a, b, diff);
+        double lo = lo_io[ei], hi = hi_io[ei];
+        const double mid = __dmul_rn(0.5, __dadd_rn(lo, hi));
+        double p2 = 0.0;
+#pragma unroll
+        for (int d = 0; d < N; ++d) { p[d] = __dadd_rn(a[d], __dmul_rn(mid, diff[d])); p2 = fma(p[d], p[d], p2); }
+        const double gl = f.gamma * PT_L2E;
+        const double pn = sqrt(p2) + f.smax;
+        double F = f.bias + acc_[ei], eb = 0.0;
+        if (f.has_barrier) F -= pt_barrier_fast<N>(f, p, 1.0 / f.b_scale, eb);
+        const double rel = 1.01 * (PT_TC_ARG_ULPS * PT_U32 * gl * pn * pn * PT_LN2) + 80.0 * PT_U32;
+        const double E = 2.0 * rel * ab_[ei] + eb + 1e-280;
+        if (fabs(F) > E) {
+            if ((F > 0.0 ? 1 : -1) == signs_a[ei]) { lo = mid; lo_io[ei] = mid; } else { hi = mid; hi_io[ei] = mid; }
+            stepped = 1;
+            const double w = __dsub_rn(hi, lo);
+            active = __dmul_rn(seg, w) > eps && w > PT_FP32_STOP_WIDTH;
+        }
+    }
+    const unsigned ballot = __ballot_sync(0xffffffffu, active);
+    const unsigned sb = __ballot_sync(0xffffffffu, stepped != 0);
+    const int lane = threadIdx.x & 31;
+    if (lane == 0 && sb) atomicAdd(&work[2], (unsigned long long)__popc(sb));
+    if (ballot) {
+        const int leader = __ffs(ballot) - 1;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(count_out, (unsigned long long)__popc(ballot));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (active) list_out[base + __popc(ballot & ((1u << lane) - 1u))] = ei;
+    }
 }
 #endif
