@@ -6,6 +6,7 @@
 //                              until seg*(hi-lo) <= eps  (manifold.py:368-383)
 //   *_analytic_*               same for sphere/ellipsoid/plane fields, arithmetic ordered like numpy
 #include <stdlib.h>
+#include <cub/cub.cuh>
 #include "pt_internal.cuh"
 #include "pt_field.cuh"
 
@@ -806,7 +807,7 @@ pt_bisect_newton_kernel(PtFieldDev f, double sum_abs_w, const double* __restrict
                 } else open = true;
                 if (!open) PT_ST(ST_TF, k) = __dmul_rn(0.5, __dadd_rn(L, H));
                 else {
-                    // a midpoint inside J needs a true fp64 evaluation: pt_bisect_rest_kernel continues from [L, H],
+                    // a midpoint inside J needs a true fp64 evaluation: the rest kernels continue from [L, H],
                     // still skipping every midpoint outside J
                     to_slow[k] = true;
                     PT_ST(ST_LO, k) = L; PT_ST(ST_W, k) = H - L;
@@ -830,7 +831,7 @@ pt_bisect_newton_kernel(PtFieldDev f, double sum_abs_w, const double* __restrict
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
         if (valid[k] && g == 0) {
-            slow[ei[k]] = to_slow[k] ? (one_step[k] ? 2 : 1) : 0;
+            slow[ei[k]] = to_slow[k] ? (one_step[k] ? 2 : 1) : 0;      // open rows: 2 = root enclosed, 1 = no proof
             if (to_slow[k]) {
                 const double l = PT_ST(ST_LO, k);
                 lo_io[ei[k]] = l; hi_io[ei[k]] = l + PT_ST(ST_W, k);
@@ -850,148 +851,204 @@ pt_bisect_newton_kernel(PtFieldDev f, double sum_abs_w, const double* __restrict
 #undef PT_ST
 }
 
-// K4: plain fp64 bisection of the listed rows from their stored brackets
-template <int N, int G>
-__global__ void __launch_bounds__(PT_EVAL_THREADS)
-pt_bisect_rest_kernel(PtFieldDev f, PtRows rows, const double* __restrict__ a_, const double* __restrict__ b_,
-                      const int8_t* __restrict__ signs_a, const double* __restrict__ lo_in, const double* __restrict__ hi_in,
-                      const double* __restrict__ jlo_in, const double* __restrict__ jhi_in,
-                      double eps, double* __restrict__ out, unsigned long long* work) {
-    extern __shared__ double tile[];
-    pt_exp_table_init(tile + PT_EVAL_TILE * PT_ROW64(N));
-    const int PB = PT_EVAL_THREADS / G;
-    const size_t total = pt_rows_total(rows);
-    const int g = threadIdx.x % G;
-    for (size_t blk = blockIdx.x; blk * PB < total; blk += gridDim.x) {
-    const size_t idx = blk * PB + threadIdx.x / G;
-    const bool valid = idx < total;
-    const size_t ei = valid ? (rows.list ? (size_t)rows.list[idx] : idx) : 0;
-    double a[N], diff[N], p[N];
-    double seg = 0.0, lo = 0.0, hi = 1.0, jlo = -1e300, jhi = 1e300;
-    int sa = 1;
-    if (valid) {
-        double b[N];
-#pragma unroll
-        for (int d = 0; d < N; ++d) { a[d] = a_[ei * N + d]; b[d] = b_[ei * N + d]; }
-        seg = pt_segment<N>(a, b, diff);
-        sa = signs_a[ei]; lo = lo_in[ei]; hi = hi_in[ei];
-        if (jlo_in) { jlo = jlo_in[ei]; jhi = jhi_in[ei]; }
-    } else {
-#pragma unroll
-        for (int d = 0; d < N; ++d) { a[d] = 0.0; diff[d] = 0.0; }
-    }
-    bool active = valid && __dmul_rn(seg, __dsub_rn(hi, lo)) > eps;
-    unsigned iters = 0;
-    while (__syncthreads_or(active ? 1 : 0)) {
-        // midpoints outside [jlo, jhi] have a proven sign (see pt_bisect_newton_kernel): replay those steps exactly
-        while (active) {
-            const double mq = __dmul_rn(0.5, __dadd_rn(lo, hi));
-            if (mq < jlo) lo = mq; else if (mq > jhi) hi = mq; else break;
-            active = __dmul_rn(seg, __dsub_rn(hi, lo)) > eps;
-        }
-        const double mid = __dmul_rn(0.5, __dadd_rn(lo, hi));
-#pragma unroll
-        for (int d = 0; d < N; ++d) p[d] = __dadd_rn(a[d], __dmul_rn(mid, diff[d]));
-        double F = f.bias + pt_rbf_block_sum<N, G>(f, p, g, tile);
-        if (f.has_barrier) F -= pt_barrier_group<N, G>(f, p, g);
-        if (active) {
-            if ((F > 0.0 ? 1 : -1) == sa) lo = mid; else hi = mid;
-            active = __dmul_rn(seg, __dsub_rn(hi, lo)) > eps;
-            ++iters;
-        }
-    }
-    {
-        unsigned mine = (g == 0) ? iters : 0u;
-        for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
-        if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&work[4], (unsigned long long)mine);
-    }
-    if (valid && g == 0) {
-        const double t = __dmul_rn(0.5, __dadd_rn(lo, hi));
-#pragma unroll
-        for (int d = 0; d < N; ++d) out[ei * N + d] = __dadd_rn(a[d], __dmul_rn(t, diff[d]));
-    }
-    }   // block-stride loop over the list
-}
-
 // K4 with the whole support set resident in shared memory and one WARP per row: rows need very different numbers
 // of true evaluations (0..30), so nothing here is block-synchronous -- a warp takes a row, replays the certain
 // midpoints, evaluates the open ones with its 32 lanes splitting the support set, writes the point, takes the next.
 #define PT_RESTW_THREADS 512
+// Same idea for support sets larger than shared memory: the support set passes through shared memory in chunks, so an
+// evaluation round is block-synchronous (all 16 warps evaluate their current row's open midpoint against chunk after
+// chunk), but every warp still owns its row: it replays, decides, finishes and pulls the next row on its own.
 template <int N>
 __global__ void __launch_bounds__(PT_RESTW_THREADS, 1)
 pt_bisect_rest_warp_kernel(PtFieldDev f, PtRows rows, const double* __restrict__ a_, const double* __restrict__ b_,
                            const int8_t* __restrict__ signs_a, const double* __restrict__ lo_in, const double* __restrict__ hi_in,
                            const double* __restrict__ jlo_in, const double* __restrict__ jhi_in,
-                           double eps, double* __restrict__ out, unsigned long long* next_row, unsigned long long* work) {
+                           double eps, double* __restrict__ out, int chunk_rows, unsigned long long* next_row,
+                           unsigned long long* work) {
     extern __shared__ double tile[];
     const int ROW = PT_ROW64(N);
     const size_t total = pt_rows_total(rows);
     const int warps_per_block = PT_RESTW_THREADS / 32;
     if ((size_t)blockIdx.x * warps_per_block >= total) return;
-    double* tab = tile + (size_t)f.S * ROW;
-    for (long long i = threadIdx.x; i < f.S * ROW; i += PT_RESTW_THREADS) tile[i] = f.sv[i];
+    const int S = (int)f.S;
+    const int nchunks = (S + chunk_rows - 1) / chunk_rows;
+    double* tab = tile + (size_t)chunk_rows * ROW;
     for (int i = threadIdx.x; i < PT_EXP_TAB; i += PT_RESTW_THREADS) tab[i] = exp2((double)i * (1.0 / PT_EXP_TAB));
+    if (nchunks == 1) for (long long i = threadIdx.x; i < (long long)S * ROW; i += PT_RESTW_THREADS) tile[i] = f.sv[i];
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    const int S = (int)f.S;
     unsigned iters = 0;
-    // rows need 1..30 evaluations: warps pull the next row from a device-side counter instead of striding
+    // per-warp row state (replicated over the lanes)
+    size_t ei = 0;
+    double a[N], diff[N], p[N];
+    double seg = 0.0, lo = 0.0, hi = 1.0, jlo = -1e300, jhi = 1e300, mid = 0.5;
+    int sa = 1;
+    bool have = false, exhausted = false;
+#pragma unroll
+    for (int d = 0; d < N; ++d) { a[d] = 0.0; diff[d] = 0.0; p[d] = 0.0; }
     for (;;) {
-        unsigned long long take = 0;
-        if (lane == 0) take = atomicAdd(next_row, 1ull);
-        const size_t idx = (size_t)__shfl_sync(0xffffffffu, take, 0);
-        if (idx >= total) break;
-        const size_t ei = rows.list ? (size_t)rows.list[idx] : idx;
-        double a[N], diff[N], p[N];
-        {
-            double b[N];
+        // bring this warp to a row with an open midpoint: replay certain steps, retire finished rows, pull new ones
+        while (!exhausted) {
+            if (!have) {
+                unsigned long long take = 0;
+                if (lane == 0) take = atomicAdd(next_row, 1ull);
+                const size_t idx = (size_t)__shfl_sync(0xffffffffu, take, 0);
+                if (idx >= total) { exhausted = true; break; }
+                ei = rows.list ? (size_t)rows.list[idx] : idx;
+                double b[N];
 #pragma unroll
-            for (int d = 0; d < N; ++d) { a[d] = a_[ei * N + d]; b[d] = b_[ei * N + d]; }
-        const double seg = pt_segment<N>(a, b, diff);
-        const int sa = signs_a[ei];
-        double lo = lo_in[ei], hi = hi_in[ei];
-        const double jlo = jlo_in ? jlo_in[ei] : -1e300, jhi = jhi_in ? jhi_in[ei] : 1e300;
-        bool active = __dmul_rn(seg, __dsub_rn(hi, lo)) > eps;
-        while (active) {
+                for (int d = 0; d < N; ++d) { a[d] = a_[ei * N + d]; b[d] = b_[ei * N + d]; }
+                seg = pt_segment<N>(a, b, diff);
+                sa = signs_a[ei]; lo = lo_in[ei]; hi = hi_in[ei];
+                jlo = jlo_in ? jlo_in[ei] : -1e300; jhi = jhi_in ? jhi_in[ei] : 1e300;
+                have = true;
+            }
             // midpoints outside [jlo, jhi] have a proven sign (see pt_bisect_newton_kernel): replay those steps exactly
-            double mid;
-            while (true) {
+            bool open = false;
+            while (__dmul_rn(seg, __dsub_rn(hi, lo)) > eps) {
                 mid = __dmul_rn(0.5, __dadd_rn(lo, hi));
-                if (mid < jlo) lo = mid; else if (mid > jhi) hi = mid; else break;
-                active = __dmul_rn(seg, __dsub_rn(hi, lo)) > eps;
-                if (!active) break;
+                if (mid < jlo) lo = mid; else if (mid > jhi) hi = mid; else { open = true; break; }
             }
-            if (!active) break;
+            if (open) break;
+            if (lane == 0) {
+                const double t = __dmul_rn(0.5, __dadd_rn(lo, hi));
 #pragma unroll
-            for (int d = 0; d < N; ++d) p[d] = __dadd_rn(a[d], __dmul_rn(mid, diff[d]));
-            PtPoint64<N> pp;
-            pp.set(p, f.gamma * PT_L2E);
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-            int j = lane;
-            for (; j + 96 < S; j += 128) {
-                s0 += pt_rbf_term<N>(tile + (size_t)j * ROW, pp, tab);
-                s1 += pt_rbf_term<N>(tile + (size_t)(j + 32) * ROW, pp, tab);
-                s2 += pt_rbf_term<N>(tile + (size_t)(j + 64) * ROW, pp, tab);
-                s3 += pt_rbf_term<N>(tile + (size_t)(j + 96) * ROW, pp, tab);
+                for (int d = 0; d < N; ++d) out[ei * N + d] = __dadd_rn(a[d], __dmul_rn(t, diff[d]));
             }
-            for (; j < S; j += 32) s0 += pt_rbf_term<N>(tile + (size_t)j * ROW, pp, tab);
+            have = false;
+        }
+        const bool work_here = have && !exhausted;
+        if (nchunks > 1) { if (!__syncthreads_or(work_here ? 1 : 0)) break; }
+        else if (!work_here) break;
+#pragma unroll
+        for (int d = 0; d < N; ++d) p[d] = __dadd_rn(a[d], __dmul_rn(mid, diff[d]));
+        PtPoint64<N> pp;
+        pp.set(p, f.gamma * PT_L2E);
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        for (int c = 0; c < nchunks; ++c) {
+            const int j0 = c * chunk_rows;
+            const int cnt = (S - j0) < chunk_rows ? (S - j0) : chunk_rows;
+            if (nchunks > 1) {
+                __syncthreads();
+                const double* src = f.sv + (size_t)j0 * ROW;
+                for (int i = threadIdx.x; i < cnt * ROW; i += PT_RESTW_THREADS) tile[i] = src[i];
+                __syncthreads();
+            }
+            if (work_here) {
+                int j = lane;
+                for (; j + 96 < cnt; j += 128) {
+                    s0 += pt_rbf_term<N>(tile + (size_t)j * ROW, pp, tab);
+                    s1 += pt_rbf_term<N>(tile + (size_t)(j + 32) * ROW, pp, tab);
+                    s2 += pt_rbf_term<N>(tile + (size_t)(j + 64) * ROW, pp, tab);
+                    s3 += pt_rbf_term<N>(tile + (size_t)(j + 96) * ROW, pp, tab);
+                }
+                for (; j < cnt; j += 32) s0 += pt_rbf_term<N>(tile + (size_t)j * ROW, pp, tab);
+            }
+        }
+        if (work_here) {
             double acc = ((s0 + s1) + (s2 + s3)) + pp.poison;
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
             double F = f.bias + acc;
             if (f.has_barrier) F -= pt_barrier_group<N, 32>(f, p, lane);
             if ((F > 0.0 ? 1 : -1) == sa) lo = mid; else hi = mid;
-            active = __dmul_rn(seg, __dsub_rn(hi, lo)) > eps;
             ++iters;
-        }
-        if (lane == 0) {
-            const double t = __dmul_rn(0.5, __dadd_rn(lo, hi));
-#pragma unroll
-            for (int d = 0; d < N; ++d) out[ei * N + d] = __dadd_rn(a[d], __dmul_rn(t, diff[d]));
-        }
         }
     }
     if (lane == 0 && iters) atomicAdd(&work[4], (unsigned long long)iters);
+}
+
+// K4 for support sets that do not fit in shared memory: step-synchronous.  One launch = ONE true evaluation for every
+// listed row (two rows per thread, support tiles through shared memory like the Newton kernel): replay the certain
+// midpoints, evaluate the open one, decide, replay again; rows that still have an open midpoint go to the next list
+// (device-side counts, no host synchronisation), finished rows write their point.
+template <int N>
+__global__ void __launch_bounds__(128, 4)
+pt_bisect_step_kernel(PtFieldDev f, const uint32_t* __restrict__ list_in, const unsigned long long* __restrict__ count_in,
+                      const double* __restrict__ a_, const double* __restrict__ b_, const int8_t* __restrict__ signs_a,
+                      double* __restrict__ lo_io, double* __restrict__ hi_io, const double* __restrict__ jlo_in,
+                      const double* __restrict__ jhi_in, double eps, double* __restrict__ out,
+                      uint32_t* __restrict__ list_out, unsigned long long* count_out, unsigned long long* work) {
+    extern __shared__ double tile[];
+    const size_t total = (size_t)*count_in;
+    if ((size_t)blockIdx.x * 256 >= total) return;
+    pt_exp_table_init(tile + PT_EVAL_TILE * PT_ROW64(N));
+    uint32_t ei[2]; bool valid[2], active[2] = {false, false};
+    double p[2][N], diff[2][N], seg[2], seg2[2], lo[2], hi[2], jlo[2], jhi[2], mid[2];
+    int sa[2];
+    auto replay = [&](int k) {
+        // midpoints outside [jlo, jhi] have a proven sign (see pt_bisect_newton_kernel): take those steps exactly
+        while (active[k]) {
+            const double mq = __dmul_rn(0.5, __dadd_rn(lo[k], hi[k]));
+            if (mq < jlo[k]) lo[k] = mq; else if (mq > jhi[k]) hi[k] = mq; else break;
+            active[k] = __dmul_rn(seg[k], __dsub_rn(hi[k], lo[k])) > eps;
+        }
+    };
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const size_t idx = (size_t)blockIdx.x * 256 + (size_t)k * 128 + threadIdx.x;
+        valid[k] = idx < total;
+        ei[k] = valid[k] ? list_in[idx] : 0u;
+        seg[k] = 0.0; lo[k] = 0.0; hi[k] = 1.0; jlo[k] = -1e300; jhi[k] = 1e300; sa[k] = 1;
+#pragma unroll
+        for (int d = 0; d < N; ++d) { p[k][d] = 0.0; diff[k][d] = 0.0; }
+        if (valid[k]) {
+            double a[N], b[N];
+#pragma unroll
+            for (int d = 0; d < N; ++d) { a[d] = a_[(size_t)ei[k] * N + d]; b[d] = b_[(size_t)ei[k] * N + d]; }
+            seg[k] = pt_segment<N>(a, b, diff[k]);
+            sa[k] = signs_a[ei[k]]; lo[k] = lo_io[ei[k]]; hi[k] = hi_io[ei[k]];
+            jlo[k] = jlo_in[ei[k]]; jhi[k] = jhi_in[ei[k]];
+        }
+        seg2[k] = seg[k] * seg[k];
+        active[k] = valid[k] && __dmul_rn(seg[k], __dsub_rn(hi[k], lo[k])) > eps;
+        replay(k);
+        mid[k] = __dmul_rn(0.5, __dadd_rn(lo[k], hi[k]));
+        if (valid[k]) {
+#pragma unroll
+            for (int d = 0; d < N; ++d) p[k][d] = __dadd_rn(a_[(size_t)ei[k] * N + d], __dmul_rn(mid[k], diff[k][d]));
+        }
+    }
+    unsigned iters = 0;
+    if (__syncthreads_or((active[0] || active[1]) ? 1 : 0)) {
+        double F[2], u1[2], u2[2], u3[2];
+        pt_rbf_block_sum_x2<N, 128, false>(f, p, diff, seg2, tile, F, u1, u2, u3);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            double Fk = f.bias + F[k];
+            if (f.has_barrier) Fk -= pt_barrier_value<N>(f, p[k]);
+            if (active[k]) {
+                if ((Fk > 0.0 ? 1 : -1) == sa[k]) lo[k] = mid[k]; else hi[k] = mid[k];
+                active[k] = __dmul_rn(seg[k], __dsub_rn(hi[k], lo[k])) > eps;
+                ++iters;
+                replay(k);
+            }
+        }
+    }
+    for (int off = 16; off > 0; off >>= 1) iters += __shfl_xor_sync(0xffffffffu, iters, off);
+    if ((threadIdx.x & 31) == 0 && iters) atomicAdd(&work[4], (unsigned long long)iters);
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        if (valid[k]) {
+            if (active[k]) { lo_io[ei[k]] = lo[k]; hi_io[ei[k]] = hi[k]; }
+            else {
+                const double t = __dmul_rn(0.5, __dadd_rn(lo[k], hi[k]));
+#pragma unroll
+                for (int d = 0; d < N; ++d) {
+                    const double av = a_[(size_t)ei[k] * N + d];
+                    out[(size_t)ei[k] * N + d] = __dadd_rn(av, __dmul_rn(t, diff[k][d]));
+                }
+            }
+        }
+        const unsigned ballot = __ballot_sync(0xffffffffu, active[k]);
+        if (ballot) {
+            const int lane = threadIdx.x & 31, leader = __ffs(ballot) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(count_out, (unsigned long long)__popc(ballot));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (active[k]) list_out[base + __popc(ballot & ((1u << lane) - 1u))] = ei[k];
+        }
+    }
 }
 
 // pack raw (support[S][n], weights[S]) into the fp64 row layout [2*gl*s_0.., w, -gl*|s|^2, pad] and the fp32
@@ -1220,45 +1277,60 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
         else pt_bisect_newton_kernel<N, 32><<<grid, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, a, b, sa, lo.p, hi.p, m, eps, out, slow.p, jlo.p, jhi.p, ctx->work);
         PT_TRY(pt_check_launch(ctx, "pt_bisect_newton_kernel"));
     }
-    // open rows: (2) root enclosed, a few midpoints inside the enclosure need a true evaluation; (1) no proof --
-    // plain bisection.  Separate launches so that the short rows do not wait for the long ones.
-    PtBuf<uint32_t> list2;
-    PT_TRY(list2.alloc(ctx, m));
-    for (int kind = 2; kind >= 1; --kind) {
-        unsigned long long* c = cnt.p + (kind == 2 ? 2 : 3);
-        uint32_t* lp = kind == 2 ? list.p : list2.p;
-        const PtRows sub{lp, c, m};
+    // open rows: (2) root enclosed, a few midpoints inside the enclosure need a true evaluation; (1) no proof -- plain
+    // bisection.  The bulk of the enclosed rows needs 1..4 evaluations: a few step-synchronous launches over the
+    // compacted list of rows that still have an open midpoint (two rows per thread, Newton-kernel efficiency).  The long
+    // tail and the unproven rows (~20 evaluations each, few rows) finish in the warp-per-row kernel.
+    {
+        PtBuf<uint32_t> list2, list3; PtBuf<unsigned long long> steps;
+        // with the support set resident in shared memory the warp-per-row kernel takes the enclosed rows directly (a few
+        // hundred 256-row blocks would not fill the machine); otherwise four step launches thin the list out first
+        const bool resident = ((size_t)f->d.S * PT_ROW64(N) + PT_EXP_TAB) * sizeof(double) <= PT_TC_SMEM_LIMIT;
+        const int max_steps = 4;
+        const int n_steps = resident ? 0 : max_steps;
+        PT_TRY(list2.alloc(ctx, m)); PT_TRY(list3.alloc(ctx, m));
+        PT_TRY(steps.alloc(ctx, max_steps + 5));
+        PT_CUDA(ctx, cudaMemsetAsync(steps.p, 0, (max_steps + 5) * sizeof(unsigned long long), ctx->stream));
         {
             PT_LAUNCH(ctx, "bisect_select");
-            pt_select_flag_kernel<<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>(slow.p, (uint8_t)kind, m, lp, c);
+            pt_select_flag_kernel<<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>(slow.p, (uint8_t)2, m, list.p, steps.p);
+            PT_TRY(pt_check_launch(ctx, "pt_select_flag_kernel"));
+            pt_select_flag_kernel<<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>(slow.p, (uint8_t)1, m, list3.p, steps.p + max_steps + 1);
             PT_TRY(pt_check_launch(ctx, "pt_select_flag_kernel"));
         }
         PT_LAUNCH(ctx, "bisect_fp64_rest");
-        const size_t smem_w = ((size_t)f->d.S * PT_ROW64(N) + PT_EXP_TAB) * sizeof(double);
-        if (smem_w <= PT_TC_SMEM_LIMIT) {
-            // support set resident in shared memory, one warp per row, persistent CTAs
-            static bool configured = false;
-            if (!configured) {
-                PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_rest_warp_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_TC_SMEM_LIMIT));
-                configured = true;
-            }
-            const unsigned gridw = pt_grid_for(m, PT_RESTW_THREADS / 32, (unsigned)ctx->sm_count);
-            pt_bisect_rest_warp_kernel<N><<<gridw, PT_RESTW_THREADS, smem_w, ctx->stream>>>(f->d, sub, a, b, sa, lo.p, hi.p, jlo.p, jhi.p, eps, out,
-                                                                                            cnt.p + (kind == 2 ? 4 : 5), ctx->work);
-            PT_TRY(pt_check_launch(ctx, "pt_bisect_rest_warp_kernel"));
-        } else {
-            // larger support sets: tiles through shared memory, 4 lanes per row; the block-stride loop ends at the device-side count
-            const unsigned grid4 = pt_grid_for(m, PT_EVAL_THREADS / 4, 1u << 16);
-            pt_bisect_rest_kernel<N, 4><<<grid4, PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, sub, a, b, sa, lo.p, hi.p, jlo.p, jhi.p, eps, out, ctx->work);
-            PT_TRY(pt_check_launch(ctx, "pt_bisect_rest_kernel"));
+        uint32_t* lin = list.p; uint32_t* lout = list2.p;
+        for (int step = 0; step < n_steps; ++step) {
+            pt_bisect_step_kernel<N><<<pt_grid_for(m, 256), 128, smem, ctx->stream>>>(f->d, lin, steps.p + step, a, b, sa, lo.p, hi.p, jlo.p, jhi.p,
+                                                                                      eps, out, lout, steps.p + step + 1, ctx->work);
+            PT_TRY(pt_check_launch(ctx, "pt_bisect_step_kernel"));
+            uint32_t* sw = lin; lin = lout; lout = sw;
         }
+        // support rows per shared-memory chunk of the warp-per-row kernel (the whole set when it fits)
+        const size_t row_bytes = (size_t)PT_ROW64(N) * sizeof(double);
+        long long chunk_rows = (long long)((PT_TC_SMEM_LIMIT - PT_EXP_TAB * sizeof(double)) / row_bytes);
+        if (chunk_rows > f->d.S) chunk_rows = f->d.S;
+        const size_t smem_w = (size_t)chunk_rows * row_bytes + PT_EXP_TAB * sizeof(double);
+        static bool configured = false;
+        if (!configured) {
+            PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_rest_warp_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_TC_SMEM_LIMIT));
+            configured = true;
+        }
+        const unsigned gridw = pt_grid_for(m, PT_RESTW_THREADS / 32, (unsigned)ctx->sm_count);
+        const PtRows tail{lin, steps.p + n_steps, m}, unproven{list3.p, steps.p + max_steps + 1, m};
+        pt_bisect_rest_warp_kernel<N><<<gridw, PT_RESTW_THREADS, smem_w, ctx->stream>>>(f->d, tail, a, b, sa, lo.p, hi.p, jlo.p, jhi.p, eps, out,
+                                                                                        (int)chunk_rows, steps.p + max_steps + 2, ctx->work);
+        PT_TRY(pt_check_launch(ctx, "pt_bisect_rest_warp_kernel"));
+        pt_bisect_rest_warp_kernel<N><<<gridw, PT_RESTW_THREADS, smem_w, ctx->stream>>>(f->d, unproven, a, b, sa, lo.p, hi.p, jlo.p, jhi.p, eps, out,
+                                                                                        (int)chunk_rows, steps.p + max_steps + 3, ctx->work);
+        PT_TRY(pt_check_launch(ctx, "pt_bisect_rest_warp_kernel"));
     }
 #undef PT_G_LAUNCH
     if (getenv("PT_DEBUG_COUNTS")) {
-        unsigned long long h[4];
+        unsigned long long h[2];
         cudaMemcpyAsync(h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream);
         cudaStreamSynchronize(ctx->stream);
-        fprintf(stderr, "[pt] root solve m=%zu resolve_round1=%llu resolve_round2=%llu enclosed_open=%llu unproven=%llu tc=%d\n", m, h[0], h[1], h[2], h[3], (int)use_tc);
+        fprintf(stderr, "[pt] root solve m=%zu resolve_round1=%llu resolve_round2=%llu tc=%d\n", m, h[0], h[1], (int)use_tc);
     }
     return PT_OK;
 }
