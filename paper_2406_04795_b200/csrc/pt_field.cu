@@ -1272,8 +1272,11 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
     {
         PT_LAUNCH(ctx, "bisect_fp64_newton");
         const size_t smem_nt = smem + 10 * 256 * sizeof(double);   // + per-row state (10 fields x rows per block)
-        if (G == 1) pt_bisect_newton_kernel<N, 1><<<pt_grid_for(m, 256), 128, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, a, b, sa, lo.p, hi.p, m, eps, out, slow.p, jlo.p, jhi.p, ctx->work);
-        else if (G == 4) pt_bisect_newton_kernel<N, 4><<<grid, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, a, b, sa, lo.p, hi.p, m, eps, out, slow.p, jlo.p, jhi.p, ctx->work);
+        // mid-size batches (a trace's coarse edges): 4 lanes per row give several blocks per SM, 32 lanes waste the tiles
+        const int Gn = G == 32 && m >= 16384 ? 4 : G;
+        const unsigned grid = pt_grid_for(m, PT_EVAL_THREADS / Gn);
+        if (Gn == 1) pt_bisect_newton_kernel<N, 1><<<pt_grid_for(m, 256), 128, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, a, b, sa, lo.p, hi.p, m, eps, out, slow.p, jlo.p, jhi.p, ctx->work);
+        else if (Gn == 4) pt_bisect_newton_kernel<N, 4><<<grid, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, a, b, sa, lo.p, hi.p, m, eps, out, slow.p, jlo.p, jhi.p, ctx->work);
         else pt_bisect_newton_kernel<N, 32><<<grid, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, a, b, sa, lo.p, hi.p, m, eps, out, slow.p, jlo.p, jhi.p, ctx->work);
         PT_TRY(pt_check_launch(ctx, "pt_bisect_newton_kernel"));
     }

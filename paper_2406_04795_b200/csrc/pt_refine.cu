@@ -200,13 +200,33 @@ pt_ref_edges_kernel(PtRefGeom rg, PtTable fe, const u64* __restrict__ cell_keys,
     }
 }
 
-// R4: pull (val, key) pairs out of the fine-edge table
-__global__ void pt_ref_extract_kernel(PtTable fe, u64* __restrict__ vals, u64* __restrict__ keys, unsigned long long* counter) {
-    u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x;
-    bool live = false; u64 k = 0, v = 0;
-    if (i <= fe.cap_mask) { k = fe.ent[2 * i]; v = fe.ent[2 * i + 1]; live = k != PT_EMPTY; }
-    unsigned long long pos = pt_warp_append64(counter, live);
-    if (live) { vals[pos] = v; keys[pos] = k; }
+// R4: pull (val, key) pairs out of the fine-edge table.  Each thread scans a few slots; positions come from a
+// block-wide scan and ONE atomic per block (a per-warp atomic on the single counter serialises at this table size).
+#define PT_EXTRACT_THREADS 256
+#define PT_EXTRACT_PER_THREAD 4
+__global__ void __launch_bounds__(PT_EXTRACT_THREADS)
+pt_ref_extract_kernel(PtTable fe, u64* __restrict__ vals, u64* __restrict__ keys, unsigned long long* counter) {
+    typedef cub::BlockScan<int, PT_EXTRACT_THREADS> Scan;
+    __shared__ typename Scan::TempStorage temp;
+    __shared__ unsigned long long block_base;
+    const u64 first = ((u64)blockIdx.x * PT_EXTRACT_THREADS + threadIdx.x) * PT_EXTRACT_PER_THREAD;
+    u64 k[PT_EXTRACT_PER_THREAD], v[PT_EXTRACT_PER_THREAD];
+    int mine = 0;
+#pragma unroll
+    for (int q = 0; q < PT_EXTRACT_PER_THREAD; ++q) {
+        const u64 i = first + q;
+        k[q] = PT_EMPTY; v[q] = 0;
+        if (i <= fe.cap_mask) { k[q] = fe.ent[2 * i]; v[q] = fe.ent[2 * i + 1]; }
+        mine += k[q] != PT_EMPTY;
+    }
+    int offset, total;
+    Scan(temp).ExclusiveSum(mine, offset, total);
+    if (threadIdx.x == 0) block_base = total ? atomicAdd(counter, (unsigned long long)total) : 0ull;
+    __syncthreads();
+    unsigned long long pos = block_base + (unsigned long long)offset;
+#pragma unroll
+    for (int q = 0; q < PT_EXTRACT_PER_THREAD; ++q)
+        if (k[q] != PT_EMPTY) { vals[pos] = v[q]; keys[pos] = k[q]; ++pos; }
 }
 
 __global__ void pt_ref_endpoints_kernel(PtRefGeom rg, const u64* __restrict__ vals, const u64* __restrict__ keys, size_t first,
@@ -712,7 +732,7 @@ static int pt_refine_impl(pt_ctx* ctx, const pt_field* field, const pt_cells* ce
         PT_CUDA(ctx, cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long), ctx->stream));
         {
             PT_LAUNCH(ctx, "refine_extract");
-            pt_ref_extract_kernel<<<pt_grid_for(fet.capacity, 256), 256, 0, ctx->stream>>>(fet.view(), vraw.p, kraw.p, cnt.p);
+            pt_ref_extract_kernel<<<pt_grid_for(fet.capacity, PT_EXTRACT_THREADS * PT_EXTRACT_PER_THREAD), PT_EXTRACT_THREADS, 0, ctx->stream>>>(fet.view(), vraw.p, kraw.p, cnt.p);
             PT_TRY(pt_check_launch(ctx, "pt_ref_extract_kernel"));
         }
         size_t tb = 0;
