@@ -154,13 +154,17 @@ pt_ref_signs_kernel(PtRefGeom rg, PtTable fv, size_t ncells, const int16_t* __re
     if (lane == 0) ccount[w] = (unsigned long long)count;
 }
 
-// R3: canonical fine edges, first-occurrence tag
+// R3: canonical fine edges, first-occurrence tag.  The kernel is instruction-bound, and only ~20 % of a cell's template
+// edges cross: each warp first compacts the crossing edge indices of its cell into shared memory (cheap: two sign-bit
+// tests per edge), then runs the expensive part (fine vertices, key packing, table insert, atomicMin) on dense lanes.
+#define PT_RE_SEG 1024    /* template edges per compaction segment */
 __global__ void __launch_bounds__(256)
 pt_ref_edges_kernel(PtRefGeom rg, PtTable fe, const u64* __restrict__ cell_keys, size_t ncells, const int8_t* __restrict__ tv,
                     const int16_t* __restrict__ te, const uint32_t* __restrict__ csign, const unsigned long long* __restrict__ coff,
                     unsigned long long tag_base, PtFineCounters* ctr) {
+    __shared__ uint16_t clist[8][PT_RE_SEG];
     const size_t w = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     if (w >= ncells) return;
     const int n = rg.coarse.n;
     int base[PT_NMAX]; uint8_t perm[PT_NMAX];
@@ -168,36 +172,50 @@ pt_ref_edges_kernel(PtRefGeom rg, PtTable fe, const u64* __restrict__ cell_keys,
     uint32_t sw[PT_SIGN_WORDS];
     for (int i = 0; i < rg.W; ++i) sw[i] = csign[w * rg.W + i];
     unsigned long long running = tag_base + coff[w];
-    for (int e0 = 0; e0 < rg.E; e0 += 32) {
-        const int e = e0 + lane;
-        bool cross = false; int i0 = 0, i1 = 0; unsigned s0 = 0, s1 = 0;
-        if (e < rg.E) {
-            i0 = te[2 * e]; i1 = te[2 * e + 1];
-            s0 = (sw[i0 >> 5] >> (i0 & 31)) & 1u; s1 = (sw[i1 >> 5] >> (i1 & 31)) & 1u;
-            cross = s0 != s1;
-        }
-        const unsigned ballot = __ballot_sync(0xffffffffu, cross);
-        bool inserted = false;
-        if (cross) {
-            const unsigned long long tag = running + (unsigned long long)__popc(ballot & ((1u << lane) - 1u));
-            int fa[PT_NMAX], fb[PT_NMAX];
-            pt_fine_vertex(rg, base, perm, tv + i0 * n, fa);
-            pt_fine_vertex(rg, base, perm, tv + i1 * n, fb);
-            bool neg = false; uint32_t mask = 0;
-            for (int d = 0; d < n; ++d) { int df = fb[d] - fa[d]; if (df) mask |= 1u << d; if (df < 0) neg = true; }
-            const int* lo = neg ? fb : fa;
-            const unsigned sbase = neg ? s1 : s0;
-            u64 bk;
-            if (!pt_pack_vertex(rg.fine, lo, bk)) atomicOr(&ctr->error, PT_ERR_KEY_RANGE);
-            else {
-                u64 slot = pt_table_insert(fe, pt_edge_key(rg.fine, bk, mask), inserted, &ctr->error);
-                atomicMin(&fe.ent[2 * slot + 1], (tag << 1) | (u64)sbase);
+    unsigned int fresh = 0;
+    for (int seg0 = 0; seg0 < rg.E; seg0 += PT_RE_SEG) {
+        const int seg1 = seg0 + PT_RE_SEG < rg.E ? seg0 + PT_RE_SEG : rg.E;
+        int total = 0;
+        for (int e0 = seg0; e0 < seg1; e0 += 32) {
+            const int e = e0 + lane;
+            bool cross = false;
+            if (e < seg1) {
+                const int i0 = te[2 * e], i1 = te[2 * e + 1];
+                cross = ((sw[i0 >> 5] >> (i0 & 31)) & 1u) != ((sw[i1 >> 5] >> (i1 & 31)) & 1u);
             }
+            const unsigned ballot = __ballot_sync(0xffffffffu, cross);
+            if (cross) clist[wib][total + __popc(ballot & ((1u << lane) - 1u))] = (uint16_t)e;
+            total += __popc(ballot);
         }
-        const unsigned ib = __ballot_sync(0xffffffffu, inserted);
-        if (lane == 0 && ib) atomicAdd(&ctr->n_edges, (unsigned long long)__popc(ib));
-        running += __popc(ballot);
+        __syncwarp();
+        for (int c0 = 0; c0 < total; c0 += 32) {
+            const int c = c0 + lane;
+            bool inserted = false;
+            if (c < total) {
+                const int e = clist[wib][c];
+                const int i0 = te[2 * e], i1 = te[2 * e + 1];
+                const unsigned s0 = (sw[i0 >> 5] >> (i0 & 31)) & 1u, s1 = (sw[i1 >> 5] >> (i1 & 31)) & 1u;
+                const unsigned long long tag = running + (unsigned long long)c;
+                int fa[PT_NMAX], fb[PT_NMAX];
+                pt_fine_vertex(rg, base, perm, tv + i0 * n, fa);
+                pt_fine_vertex(rg, base, perm, tv + i1 * n, fb);
+                bool neg = false; uint32_t mask = 0;
+                for (int d = 0; d < n; ++d) { int df = fb[d] - fa[d]; if (df) mask |= 1u << d; if (df < 0) neg = true; }
+                const int* lo = neg ? fb : fa;
+                const unsigned sbase = neg ? s1 : s0;
+                u64 bk;
+                if (!pt_pack_vertex(rg.fine, lo, bk)) atomicOr(&ctr->error, PT_ERR_KEY_RANGE);
+                else {
+                    u64 slot = pt_table_insert(fe, pt_edge_key(rg.fine, bk, mask), inserted, &ctr->error);
+                    atomicMin(&fe.ent[2 * slot + 1], (tag << 1) | (u64)sbase);
+                }
+            }
+            fresh += __popc(__ballot_sync(0xffffffffu, inserted));
+        }
+        running += (unsigned long long)total;
+        __syncwarp();
     }
+    if (lane == 0 && fresh) atomicAdd(&ctr->n_edges, (unsigned long long)fresh);
 }
 
 // R4: pull (val, key) pairs out of the fine-edge table.  Each thread scans a few slots; positions come from a
