@@ -297,16 +297,16 @@ __global__ void pt_dedup_directory_kernel(const u64* __restrict__ gkey_sorted, s
 
 // Greedy first-keeper resolution: a point is removed if an earlier kept point lies within eps, kept once every
 // earlier point within eps is removed.
-// Round 1 (all points) does the spatial search once and CACHES the earlier neighbours within eps (almost always
-// 0..2 of them); undecided points go to a compacted list.  Later rounds (pt_dedup_follow_kernel) only look at the
-// cached neighbours' states.  A point with more than PT_DD_NBR neighbours redoes the search every round.
-#define PT_DD_NBR 8
-#define PT_DD_OVERFLOW 0xFFu
-
+// Round 1 (all points) does the spatial search and decides every point that has no undecided earlier neighbour;
+// the others go to a compacted list together with their neighbour COUNT.  A second pass over that list writes
+// the neighbours into a CSR array (exclusive scan of the counts), and the follow-up rounds only look at the
+// states of a point's recorded neighbours -- no spatial search, no launch over all points.
+template <bool COLLECT>
 __device__ __forceinline__ int pt_dedup_search(int n, const double* __restrict__ pts, size_t count, double cell, double eps,
                                                const u64* __restrict__ gkey_sorted, const uint32_t* __restrict__ idx_sorted,
                                                const PtTable& dir, const uint8_t* state, size_t i, uint32_t* nbr, int& nbc) {
-    // returns 2 if an earlier KEPT point is within eps, 1 if an earlier undecided one is, else 0
+    // returns 2 if an earlier KEPT point is within eps, 1 if an earlier undecided one is, else 0 (COLLECT: states are
+    // ignored and every earlier neighbour within eps is written to nbr); nbc = earlier neighbours within eps seen
     double p[PT_NMAX]; long long lo[PT_NMAX], hi[PT_NMAX];
     int ncomb = 1;
     for (int d = 0; d < n; ++d) {
@@ -333,7 +333,8 @@ __device__ __forceinline__ int pt_dedup_search(int n, const double* __restrict__
             double s = 0.0;
             for (int d = 0; d < n; ++d) { double df = __dsub_rn(pts[j * n + d], p[d]); s = __dadd_rn(s, __dmul_rn(df, df)); }
             if (sqrt(s) <= eps) {
-                if (nbr) { if (nbc < PT_DD_NBR) nbr[nbc] = (uint32_t)j; ++nbc; }
+                if (COLLECT) { nbr[nbc++] = (uint32_t)j; continue; }
+                ++nbc;
                 const uint8_t sj = ((volatile const uint8_t*)state)[j];
                 if (sj == PT_DD_REMOVED) continue;
                 if (sj == PT_DD_KEPT) { any_kept = true; break; }
@@ -346,56 +347,13 @@ __device__ __forceinline__ int pt_dedup_search(int n, const double* __restrict__
 
 __global__ void pt_dedup_round_kernel(int n, const double* __restrict__ pts, size_t count, double cell, double eps,
                                       const u64* __restrict__ gkey_sorted, const uint32_t* __restrict__ idx_sorted, PtTable dir,
-                                      uint8_t* state, uint32_t* __restrict__ nbr, uint8_t* __restrict__ nbc_out,
-                                      uint32_t* __restrict__ undecided, PtFineCounters* ctr) {
+                                      uint8_t* state, uint32_t* __restrict__ undecided, uint32_t* __restrict__ nbc_out,
+                                      PtFineCounters* ctr) {
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool pending = false;
+    int nbc = 0;
     if (i < count) {
-        uint32_t mine[PT_DD_NBR];
-        int nbc = 0;
-        const int verdict = pt_dedup_search(n, pts, count, cell, eps, gkey_sorted, idx_sorted, dir, state, i, mine, nbc);
-        if (verdict == 2) state[i] = PT_DD_REMOVED;
-        else if (verdict == 0) state[i] = PT_DD_KEPT;
-        else {
-            pending = true;
-            for (int q = 0; q < PT_DD_NBR; ++q) nbr[i * PT_DD_NBR + q] = q < nbc ? mine[q] : 0u;
-            nbc_out[i] = nbc > PT_DD_NBR ? (uint8_t)PT_DD_OVERFLOW : (uint8_t)nbc;
-        }
-    }
-    const unsigned ballot = __ballot_sync(0xffffffffu, pending);
-    if (ballot) {
-        const int lane = threadIdx.x & 31, leader = __ffs(ballot) - 1;
-        unsigned long long base = 0;
-        if (lane == leader) base = atomicAdd(&ctr->undecided, (unsigned long long)__popc(ballot));
-        base = __shfl_sync(0xffffffffu, base, leader);
-        if (pending) undecided[base + __popc(ballot & ((1u << lane) - 1u))] = (uint32_t)i;
-    }
-}
-
-__global__ void pt_dedup_follow_kernel(int n, const double* __restrict__ pts, size_t count, double cell, double eps,
-                                       const u64* __restrict__ gkey_sorted, const uint32_t* __restrict__ idx_sorted, PtTable dir,
-                                       uint8_t* state, const uint32_t* __restrict__ nbr, const uint8_t* __restrict__ nbc_in,
-                                       const uint32_t* __restrict__ list_in, size_t list_count,
-                                       uint32_t* __restrict__ list_out, PtFineCounters* ctr) {
-    const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    bool pending = false;
-    uint32_t i = 0;
-    if (t < list_count) {
-        i = list_in[t];
-        int verdict;
-        const uint8_t nbc = nbc_in[i];
-        if (nbc == PT_DD_OVERFLOW) {
-            int dummy;
-            verdict = pt_dedup_search(n, pts, count, cell, eps, gkey_sorted, idx_sorted, dir, state, (size_t)i, nullptr, dummy);
-        } else {
-            bool any_kept = false, any_undecided = false;
-            for (int q = 0; q < nbc; ++q) {
-                const uint8_t sj = ((volatile const uint8_t*)state)[nbr[(size_t)i * PT_DD_NBR + q]];
-                if (sj == PT_DD_KEPT) { any_kept = true; break; }
-                if (sj != PT_DD_REMOVED) any_undecided = true;
-            }
-            verdict = any_kept ? 2 : (any_undecided ? 1 : 0);
-        }
+        const int verdict = pt_dedup_search<false>(n, pts, count, cell, eps, gkey_sorted, idx_sorted, dir, state, i, nullptr, nbc);
         if (verdict == 2) state[i] = PT_DD_REMOVED;
         else if (verdict == 0) state[i] = PT_DD_KEPT;
         else pending = true;
@@ -406,7 +364,51 @@ __global__ void pt_dedup_follow_kernel(int n, const double* __restrict__ pts, si
         unsigned long long base = 0;
         if (lane == leader) base = atomicAdd(&ctr->undecided, (unsigned long long)__popc(ballot));
         base = __shfl_sync(0xffffffffu, base, leader);
-        if (pending) list_out[base + __popc(ballot & ((1u << lane) - 1u))] = i;
+        if (pending) {
+            const unsigned long long pos = base + __popc(ballot & ((1u << lane) - 1u));
+            undecided[pos] = (uint32_t)i; nbc_out[pos] = (uint32_t)nbc;
+        }
+    }
+}
+
+// neighbours of the listed points into csr[off[pos] ...] (same search, same order as the counting pass)
+__global__ void pt_dedup_collect_kernel(int n, const double* __restrict__ pts, size_t count, double cell, double eps,
+                                        const u64* __restrict__ gkey_sorted, const uint32_t* __restrict__ idx_sorted, PtTable dir,
+                                        const uint32_t* __restrict__ list, size_t list_count, const uint32_t* __restrict__ off,
+                                        uint32_t* __restrict__ csr) {
+    const size_t pos = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pos >= list_count) return;
+    int nbc;
+    pt_dedup_search<true>(n, pts, count, cell, eps, gkey_sorted, idx_sorted, dir, nullptr, (size_t)list[pos], csr + off[pos], nbc);
+}
+
+// one follow-up round over list positions: decided points drop out, the rest goes to list_out
+__global__ void pt_dedup_follow_kernel(uint8_t* state, const uint32_t* __restrict__ point_of, const uint32_t* __restrict__ off,
+                                       const uint32_t* __restrict__ csr, const uint32_t* __restrict__ list_in, size_t list_count,
+                                       uint32_t* __restrict__ list_out, PtFineCounters* ctr) {
+    const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    bool pending = false;
+    uint32_t pos = 0;
+    if (t < list_count) {
+        pos = list_in[t];
+        const uint32_t i = point_of[pos];
+        bool any_kept = false, any_undecided = false;
+        for (uint32_t q = off[pos]; q < off[pos + 1]; ++q) {
+            const uint8_t sj = ((volatile const uint8_t*)state)[csr[q]];
+            if (sj == PT_DD_KEPT) { any_kept = true; break; }
+            if (sj != PT_DD_REMOVED) any_undecided = true;
+        }
+        if (any_kept) state[i] = PT_DD_REMOVED;
+        else if (!any_undecided) state[i] = PT_DD_KEPT;
+        else pending = true;
+    }
+    const unsigned ballot = __ballot_sync(0xffffffffu, pending);
+    if (ballot) {
+        const int lane = threadIdx.x & 31, leader = __ffs(ballot) - 1;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(&ctr->undecided, (unsigned long long)__popc(ballot));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (pending) list_out[base + __popc(ballot & ((1u << lane) - 1u))] = pos;
     }
 }
 
@@ -498,33 +500,59 @@ static int pt_dedup_label_impl(pt_ctx* ctx, int n, const double* upts, const u64
             pt_dedup_directory_kernel<<<pt_grid_for(U, 256), 256, 0, ctx->stream>>>(gks.p, U, dir.view(), &ctr.p->error);
             PT_TRY(pt_check_launch(ctx, "pt_dedup_directory_kernel"));
         }
-        PtBuf<uint32_t> nbr, list_a, list_b; PtBuf<uint8_t> nbc;
-        PT_TRY(nbr.alloc(ctx, U * PT_DD_NBR)); PT_TRY(nbc.alloc(ctx, U));
-        PT_TRY(list_a.alloc(ctx, U)); PT_TRY(list_b.alloc(ctx, U));
+        PtBuf<uint32_t> point_of, nbc, off, csr, list_a, list_b;
+        PT_TRY(point_of.alloc(ctx, U)); PT_TRY(nbc.alloc(ctx, U + 1));
         PT_CUDA(ctx, cudaMemsetAsync(&ctr.p->undecided, 0, sizeof(unsigned long long), ctx->stream));
         {
             PT_LAUNCH(ctx, "dedup_round");
             pt_dedup_round_kernel<<<pt_grid_for(U, 128), 128, 0, ctx->stream>>>(n, upts, U, cell, eps_dedup, gks.p, gis.p, dir.view(), state.p,
-                                                                                nbr.p, nbc.p, list_a.p, ctr.p);
+                                                                                point_of.p, nbc.p, ctr.p);
             PT_TRY(pt_check_launch(ctx, "pt_dedup_round_kernel"));
         }
         ++rounds;
         PT_TRY(pt_read_fine_counters(ctx, ctr.p, &hc, rg));
-        uint32_t* lin = list_a.p; uint32_t* lout = list_b.p;
-        while (hc.undecided != 0) {
-            const size_t pending = (size_t)hc.undecided;
-            if (getenv("PT_DEBUG_COUNTS")) fprintf(stderr, "[pt] dedup round %lld: %zu of %zu undecided\n", rounds, pending, U);
-            PT_CUDA(ctx, cudaMemsetAsync(&ctr.p->undecided, 0, sizeof(unsigned long long), ctx->stream));
+        const size_t pending1 = (size_t)hc.undecided;
+        if (pending1 > 0) {
+            // CSR of the undecided points' earlier neighbours
+            PT_TRY(off.alloc(ctx, pending1 + 1));
+            PT_TRY(list_a.alloc(ctx, pending1)); PT_TRY(list_b.alloc(ctx, pending1));
+            PT_CUDA(ctx, cudaMemsetAsync(nbc.p + pending1, 0, sizeof(uint32_t), ctx->stream));
+            size_t tb3 = 0;
+            cub::DeviceScan::ExclusiveSum(nullptr, tb3, nbc.p, off.p, (int)(pending1 + 1), ctx->stream);
+            PT_TRY(tmp.alloc(ctx, tb3));
             {
                 PT_LAUNCH(ctx, "dedup_follow");
-                pt_dedup_follow_kernel<<<pt_grid_for(pending, 128), 128, 0, ctx->stream>>>(n, upts, U, cell, eps_dedup, gks.p, gis.p, dir.view(), state.p,
-                                                                                          nbr.p, nbc.p, lin, pending, lout, ctr.p);
-                PT_TRY(pt_check_launch(ctx, "pt_dedup_follow_kernel"));
+                PT_CUDA(ctx, cub::DeviceScan::ExclusiveSum(tmp.p, tb3, nbc.p, off.p, (int)(pending1 + 1), ctx->stream));
+                ctx->launches++;
             }
-            ++rounds;
-            PT_TRY(pt_read_fine_counters(ctx, ctr.p, &hc, rg));
-            uint32_t* sw = lin; lin = lout; lout = sw;
-            if (rounds > 100000) return pt_fail(ctx, PT_E_STATE, "eps-dedup did not converge");
+            uint32_t* h32 = (uint32_t*)ctx->pinned;
+            PT_CUDA(ctx, cudaMemcpyAsync(h32, off.p + pending1, sizeof(uint32_t), cudaMemcpyDeviceToHost, ctx->stream));
+            PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+            const size_t total_nbr = (size_t)*h32;
+            PT_TRY(csr.alloc(ctx, total_nbr + 1));
+            {
+                PT_LAUNCH(ctx, "dedup_follow");
+                pt_dedup_collect_kernel<<<pt_grid_for(pending1, 128), 128, 0, ctx->stream>>>(n, upts, U, cell, eps_dedup, gks.p, gis.p, dir.view(),
+                                                                                             point_of.p, pending1, off.p, csr.p);
+                PT_TRY(pt_check_launch(ctx, "pt_dedup_collect_kernel"));
+                pt_iota32_kernel<<<pt_grid_for(pending1, 256), 256, 0, ctx->stream>>>(list_a.p, pending1);
+                PT_TRY(pt_check_launch(ctx, "pt_iota32_kernel"));
+            }
+            uint32_t* lin = list_a.p; uint32_t* lout = list_b.p;
+            size_t pending = pending1;
+            while (pending != 0) {
+                PT_CUDA(ctx, cudaMemsetAsync(&ctr.p->undecided, 0, sizeof(unsigned long long), ctx->stream));
+                {
+                    PT_LAUNCH(ctx, "dedup_follow");
+                    pt_dedup_follow_kernel<<<pt_grid_for(pending, 128), 128, 0, ctx->stream>>>(state.p, point_of.p, off.p, csr.p, lin, pending, lout, ctr.p);
+                    PT_TRY(pt_check_launch(ctx, "pt_dedup_follow_kernel"));
+                }
+                ++rounds;
+                PT_TRY(pt_read_fine_counters(ctx, ctr.p, &hc, rg));
+                pending = (size_t)hc.undecided;
+                uint32_t* sw = lin; lin = lout; lout = sw;
+                if (rounds > 100000) return pt_fail(ctx, PT_E_STATE, "eps-dedup did not converge");
+            }
         }
         // compact the kept points, order preserved
         PtBuf<uint8_t> flag; PtBuf<uint32_t> iota; PtBuf<long long> nsel;
