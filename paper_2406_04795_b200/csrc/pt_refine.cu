@@ -275,7 +275,8 @@ __global__ void pt_dedup_hash_kernel(int n, const double* __restrict__ pts, size
     size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= count) return;
     long long c[PT_NMAX];
-    for (int d = 0; d < n; ++d) c[d] = (long long)floor(pts[i * n + d] / cell);
+    const double inv = 1.0 / cell;   // the grid only has to be monotone and identical in the hash and search kernels
+    for (int d = 0; d < n; ++d) c[d] = (long long)floor(pts[i * n + d] * inv);
     gkey[i] = pt_grid_hash(n, c);
     idx[i] = (uint32_t)i;
 }
@@ -309,10 +310,11 @@ __device__ __forceinline__ int pt_dedup_search(int n, const double* __restrict__
     // ignored and every earlier neighbour within eps is written to nbr); nbc = earlier neighbours within eps seen
     double p[PT_NMAX]; long long lo[PT_NMAX], hi[PT_NMAX];
     int ncomb = 1;
+    const double inv = 1.0 / cell;
     for (int d = 0; d < n; ++d) {
         p[d] = pts[i * n + d];
-        lo[d] = (long long)floor((p[d] - eps) / cell);
-        hi[d] = (long long)floor((p[d] + eps) / cell);
+        lo[d] = (long long)floor((p[d] - eps) * inv);
+        hi[d] = (long long)floor((p[d] + eps) * inv);
         if (hi[d] != lo[d]) ncomb <<= 1;
     }
     bool any_kept = false, any_undecided = false;
