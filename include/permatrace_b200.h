@@ -90,8 +90,13 @@ int pt_field_create_rbf(pt_ctx* ctx, int n, long long S, const double* support,
  * plane [normal[n], offset].  Host pointers. */
 int pt_field_create_analytic(pt_ctx* ctx, int kind, int n, const double* params, pt_field** out);
 void pt_field_destroy(pt_field* f);
-/* precision policy: 0 = FP64 everywhere (default); 1 = FP32 screening with an FP64 recheck of
- * every value whose sign is not certain under the rigorous FP32 error bound */
+/* precision policy (default 1; environment PERMATRACE_B200_PRECISION overrides at creation):
+ *   0 = plain FP64 everywhere (bisection exactly as the reference loop, manifold.py:368-383);
+ *   1 = fast path with the same results: FP32 screening on the tensor cores (tcgen05, tf32 x3 split) where the FP32 sign
+ *       is PROVEN equal to the FP64 one, FP64 recheck of every unproven value, Newton root location with a rigorous
+ *       enclosure that replays the reference's bisection decisions.
+ * PERMATRACE_B200_TC=0 keeps mode 1 on the SIMT kernels; PERMATRACE_B200_TC_LEVELS=1 forces the level-synchronous
+ * tensor-core driver that serves support sets beyond one CTA's shared memory. */
 int pt_field_set_precision(pt_field* f, int mode);
 /* ImplicitManifold.values / .signs (manifold.py:54-72): out_values (f64) and out_signs (i8, +1/-1)
  * may each be NULL */
