@@ -23,6 +23,7 @@ struct pt_field {
     bool tc_ok = false;          // the tf32 operand exists (n <= 6)
     bool tc_resident = false;    // ... and the whole support set fits one CTA's shared memory (persistent kernel)
     bool tc_levels = false;      // force the level-synchronous driver (PERMATRACE_B200_TC_LEVELS=1)
+    bool tc4 = false;            // n = 6 and the 5-chunk operand + four A buffers fit: four row groups per CTA
 };
 
 int pt_field_dim(const pt_field* f) { return f->d.n; }
@@ -1146,6 +1147,19 @@ static int pt_screen_tc_launch(pt_ctx* ctx, const pt_field* f, const PtRows& row
             PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect32_tc_kernel<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_TC_SMEM_LIMIT));
             configured = true;
         }
+        if constexpr (N == 6 && MODE == 0) {
+            if (f->tc4) {
+                const size_t smem4 = (size_t)5 * f->tc.spad * 16 + 4 * (size_t)6 * PT_TC_M * 16 + (size_t)f->tc.spad * 4 + 64;
+                static bool configured4 = false;
+                if (!configured4) {
+                    PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect32_tc4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_TC_SMEM_LIMIT));
+                    configured4 = true;
+                }
+                const unsigned grid4 = pt_grid_for(rows.m, 4 * PT_TC_M, (unsigned)ctx->sm_count);
+                pt_bisect32_tc4_kernel<<<grid4, PT_TC4_THREADS, smem4, ctx->stream>>>(f->d, f->tc, rows, a, b, sa, eps, fresh, lo, hi, ctx->work);
+                return pt_check_launch(ctx, "pt_bisect32_tc4_kernel");
+            }
+        }
         const unsigned grid = pt_grid_for(rows.m, 2 * PT_TC_M, (unsigned)ctx->sm_count);
         const PtTcLevel whole{0, f->tc.spad, nullptr, nullptr, 1};
         pt_bisect32_tc_kernel<N, MODE><<<grid, PT_TC_THREADS, smem, ctx->stream>>>(f->d, f->tc, rows, a, b, sa, eps, fresh, lo, hi, sign_out, whole, ctx->work);
@@ -1423,6 +1437,9 @@ static int pt_field_build_rbf(pt_ctx* ctx, int n, long long S, const double* sup
             f->tc_resident = pt_tc_smem_bytes(n, S) <= PT_TC_SMEM_LIMIT;
             const char* lv_env = getenv("PERMATRACE_B200_TC_LEVELS");
             f->tc_levels = lv_env && lv_env[0] == '1';
+            const char* g4_env = getenv("PERMATRACE_B200_TC4");
+            const size_t smem4 = (size_t)5 * spad * 16 + 4 * (size_t)6 * PT_TC_M * 16 + (size_t)spad * 4 + 64;
+            f->tc4 = n == 6 && smem4 <= PT_TC_SMEM_LIMIT && !(g4_env && g4_env[0] == '0');
             cudaStreamSynchronize(ctx->stream);   // sdev/wdev may be staging buffers released on return
         }
     }

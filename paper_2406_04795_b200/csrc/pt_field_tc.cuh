@@ -420,6 +420,199 @@ pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __res
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*sTmem), "r"(512u));
 }
 
+// ---- four row groups per CTA (n = 6) ---------------------------------------------------------------------------
+// Same screen with FOUR independent 128-row groups per CTA (16 warps, four per SM sub-partition instead of two), so that
+// the serial stretches of a group (level boundary, waiting for its MMA) are covered by three others.  What makes it fit:
+//   * shared memory: the K = 24 operand of n = 6 has an exact duplicate 16-byte chunk (columns 16..19 = s_h[0..3] =
+//     columns 0..3), so B is stored as 5 chunks instead of 6 (160 KB at S = 2048) and the third k-step's descriptor
+//     simply points at chunk 0 with a leading-byte offset that reaches chunk 4;
+//   * TMEM: one 128-column accumulator per group (4 x 128 = 512 columns); the MMA of a group's next tile is issued when
+//     the group has drained the current one -- the wait is hidden by the other groups;
+//   * registers (128 per thread): the segment endpoints are re-read from L2 at every level instead of living in
+//     registers, and the accumulator is read through one 32-register window.
+#define PT_TC4_THREADS 512
+static_assert(PT_TC_N == 128, "the four-group kernel assumes 128-column tiles");
+
+__global__ void __launch_bounds__(PT_TC4_THREADS, 1)
+pt_bisect32_tc4_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __restrict__ a_, const double* __restrict__ b_,
+                       const int8_t* __restrict__ signs_a, double eps, int fresh, double* __restrict__ lo_io,
+                       double* __restrict__ hi_io, unsigned long long* work) {
+    constexpr int N = 6, KT = 24, KC = 6, BC = 5;     // BC: distinct B chunks
+    extern __shared__ __align__(1024) unsigned char pt_tc_smem[];
+    const int spad = tc.spad;
+    const int ntiles = spad / PT_TC_N;
+    float* sB = reinterpret_cast<float*>(pt_tc_smem);
+    float* sA0 = sB + (size_t)BC * spad * 4;
+    float* sW = sA0 + 4 * (size_t)KC * PT_TC_M * 4;
+    unsigned long long* sBar = reinterpret_cast<unsigned long long*>(sW + spad);
+    uint32_t* sTmem = reinterpret_cast<uint32_t*>(sBar + 4);
+
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int row = tid & (PT_TC_M - 1), group = tid >> 7;
+    const size_t total = pt_rows_total(rows);
+    if ((size_t)blockIdx.x * (4 * PT_TC_M) >= total) return;
+
+    if (tid == 0) {
+        for (int i = 0; i < 4; ++i) pt_mbar_init(pt_smem_u32(&sBar[i]), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(pt_smem_u32(sTmem)), "r"(512u));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::);
+    }
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(tc.bt);
+        uint4* dst = reinterpret_cast<uint4*>(sB);
+        for (int i = tid; i < BC * spad; i += PT_TC4_THREADS) {
+            const int c = i / spad, j = i - c * spad;
+            dst[i] = src[(size_t)(c < 4 ? c : 5) * spad + j];          // global chunk 4 duplicates chunk 0
+        }
+        const uint4* ws = reinterpret_cast<const uint4*>(tc.wt);
+        uint4* wd = reinterpret_cast<uint4*>(sW);
+        for (int i = tid; i < spad / 4; i += PT_TC4_THREADS) wd[i] = ws[i];
+    }
+    pt_fence_async_smem();
+    pt_tc_fence_before();
+    __syncthreads();
+    pt_tc_fence_after();
+    const uint32_t tmem_base = *sTmem + (uint32_t)group * PT_TC_N;
+    float* sA = sA0 + (size_t)group * KC * PT_TC_M * 4;
+    const uint32_t sA_u32 = pt_smem_u32(sA), sB_u32 = pt_smem_u32(sB);
+    const uint32_t bar_u32 = pt_smem_u32(&sBar[group]);
+    uint32_t phase = 0u;
+    const double gl = f.gamma * PT_L2E;
+    const double inv_scale = f.has_barrier ? 1.0 / f.b_scale : 0.0;
+    const bool leader = row == 0;
+    const uint32_t chunk_bytes = (uint32_t)spad * 16u;
+
+    auto issue_tile = [&](int tile) {
+        const uint32_t tb = sB_u32 + (uint32_t)tile * (PT_TC_N * 16);
+        // k-step 0: chunks (0, 1); k-step 1: chunks (2, 3); k-step 2: chunks (0, 4) -- chunk 0 doubles as columns 16..19
+        pt_umma_tf32(tmem_base, pt_umma_desc(sA_u32, PT_TC_M * 16, 128), pt_umma_desc(tb, chunk_bytes, 128), PT_TC_IDESC, 0u);
+        pt_umma_tf32(tmem_base, pt_umma_desc(sA_u32 + 2 * (PT_TC_M * 16), PT_TC_M * 16, 128),
+                     pt_umma_desc(tb + 2 * chunk_bytes, chunk_bytes, 128), PT_TC_IDESC, 1u);
+        pt_umma_tf32(tmem_base, pt_umma_desc(sA_u32 + 4 * (PT_TC_M * 16), PT_TC_M * 16, 128),
+                     pt_umma_desc(tb, 4 * chunk_bytes, 128), PT_TC_IDESC, 1u);
+        pt_umma_commit(bar_u32);
+    };
+
+    for (size_t chunk = (size_t)blockIdx.x * 4 + group; chunk * PT_TC_M < total; chunk += (size_t)gridDim.x * 4) {
+        const size_t idx = chunk * PT_TC_M + row;
+        const bool valid = idx < total;
+        const size_t ei = valid ? (rows.list ? (size_t)rows.list[idx] : idx) : 0;
+        double seg = 0.0, lo = 0.0, hi = 1.0;
+        int sa = 1;
+        if (valid) {
+            double a[N], b[N], diff[N];
+#pragma unroll
+            for (int d = 0; d < N; ++d) { a[d] = a_[ei * N + d]; b[d] = b_[ei * N + d]; }
+            seg = pt_segment<N>(a, b, diff);
+            sa = signs_a[ei];
+            if (!fresh) { lo = lo_io[ei]; hi = hi_io[ei]; }
+        }
+        bool active = valid && __dmul_rn(seg, __dsub_rn(hi, lo)) > eps;
+        unsigned iters = 0;
+        while (pt_group_or(group, active)) {
+            const double mid = __dmul_rn(0.5, __dadd_rn(lo, hi));
+            double p2 = 0.0;
+            {
+                // this point's row of A (endpoints re-read from L2: they must not live in registers across the epilogue)
+                float col[KT];
+#pragma unroll
+                for (int k = 0; k < KT; ++k) col[k] = 0.f;
+#pragma unroll
+                for (int d = 0; d < N; ++d) {
+                    const double av = valid ? a_[ei * N + d] : 0.0, bv = valid ? b_[ei * N + d] : 0.0;
+                    const double pd = __dadd_rn(av, __dmul_rn(mid, __dsub_rn(bv, av)));
+                    p2 = fma(pd, pd, p2);
+                    float h, l, ll;
+                    pt_tf32_split3(2.0 * gl * pd, h, l, ll);
+                    col[d] = h; col[(N + 2) + d] = h; col[2 * (N + 2) + d] = l;
+                }
+                float ch, cl, cll;
+                pt_tf32_split3(-gl * p2, ch, cl, cll);
+                col[N] = ch;               col[N + 1] = 1.f;
+                col[(N + 2) + N] = cl;     col[(N + 2) + N + 1] = 1.f;
+                col[2 * (N + 2) + N] = cll; col[2 * (N + 2) + N + 1] = 1.f;
+#pragma unroll
+                for (int c = 0; c < KC; ++c)
+                    *reinterpret_cast<float4*>(sA + ((size_t)c * PT_TC_M + row) * 4) =
+                        make_float4(col[4 * c], col[4 * c + 1], col[4 * c + 2], col[4 * c + 3]);
+            }
+            pt_fence_async_smem();
+            pt_group_sync(group);
+            if (leader) { pt_tc_fence_after(); issue_tile(0); }
+            double acc = 0.0, ab = 0.0;
+            const uint32_t taddr = tmem_base + ((uint32_t)((warp & 3) * 32) << 16);
+            for (int t = 0; t < ntiles; ++t) {
+                pt_mbar_wait(bar_u32, phase);
+                phase ^= 1u;
+                pt_tc_fence_after();
+                const float* wrow = sW + t * PT_TC_N;
+                float fa_t[4], fb_t[4];
+#pragma unroll
+                for (int blk = 0; blk < 4; ++blk) {
+                    uint32_t cur[32];
+                    pt_tmem_ld32(taddr + (uint32_t)blk * 32, cur);
+                    pt_tmem_wait_ld();
+                    float fa = 0.f, fb = 0.f;
+#pragma unroll
+                    for (int c4 = 0; c4 < 8; ++c4) {
+                        const float4 w4 = *reinterpret_cast<const float4*>(wrow + blk * 32 + c4 * 4);
+                        const float e0 = pt_ex2(__uint_as_float(cur[c4 * 4 + 0]));
+                        const float e1 = pt_ex2(__uint_as_float(cur[c4 * 4 + 1]));
+                        const float e2 = pt_ex2(__uint_as_float(cur[c4 * 4 + 2]));
+                        const float e3 = pt_ex2_poly(__uint_as_float(cur[c4 * 4 + 3]));
+                        fa = fmaf(w4.x, e0, fa); fb = fmaf(fabsf(w4.x), e0, fb);
+                        fa = fmaf(w4.y, e1, fa); fb = fmaf(fabsf(w4.y), e1, fb);
+                        fa = fmaf(w4.z, e2, fa); fb = fmaf(fabsf(w4.z), e2, fb);
+                        fa = fmaf(w4.w, e3, fa); fb = fmaf(fabsf(w4.w), e3, fb);
+                    }
+                    fa_t[blk] = fa; fb_t[blk] = fb;
+                }
+                acc += (double)((fa_t[0] + fa_t[1]) + (fa_t[2] + fa_t[3]));
+                ab += (double)((fb_t[0] + fb_t[1]) + (fb_t[2] + fb_t[3]));
+                pt_tc_fence_before();
+                if (t + 1 < ntiles) {
+                    pt_group_sync(group);
+                    if (leader) { pt_tc_fence_after(); issue_tile(t + 1); }
+                }
+            }
+            // decision (the midpoint is recomputed from the endpoints)
+            double p[N];
+            p2 = 0.0;
+#pragma unroll
+            for (int d = 0; d < N; ++d) {
+                const double av = valid ? a_[ei * N + d] : 0.0, bv = valid ? b_[ei * N + d] : 0.0;
+                p[d] = __dadd_rn(av, __dmul_rn(mid, __dsub_rn(bv, av)));
+                p2 = fma(p[d], p[d], p2);
+            }
+            const double pn = sqrt(p2) + f.smax;
+            double F = f.bias + acc, eb = 0.0;
+            if (f.has_barrier) F -= pt_barrier_fast<N>(f, p, inv_scale, eb);
+            const double rel = 1.01 * (PT_TC_ARG_ULPS * PT_U32 * gl * pn * pn * PT_LN2) + 80.0 * PT_U32;
+            const double E = 2.0 * rel * ab + eb + 1e-280;
+            if (active) {
+                if (fabs(F) > E) {
+                    if ((F > 0.0 ? 1 : -1) == sa) lo = mid; else hi = mid;
+                    ++iters;
+                    const double w = __dsub_rn(hi, lo);
+                    active = __dmul_rn(seg, w) > eps && w > PT_FP32_STOP_WIDTH;
+                } else {
+                    active = false;
+                }
+            }
+        }
+        unsigned mine = iters;
+        for (int off = 16; off > 0; off >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, off);
+        if ((tid & 31) == 0 && mine) atomicAdd(&work[2], (unsigned long long)mine);
+        if (valid) { lo_io[ei] = lo; hi_io[ei] = hi; }
+    }
+    pt_tc_fence_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(*sTmem), "r"(512u));
+}
+
 // ---- level-synchronous driver kernels (MODE 3) ------------------------------------------------------------------
 // rows of `rows` whose bracket still needs a step -> list_out (fresh: brackets start at [0, 1])
 template <int N>

@@ -453,8 +453,9 @@ def test_dof6_full_size_refine_properties(monkeypatch):
     from bench import build_workload
     from paper_2406_04795_b200.distributed import CudaEngine, cell_slice
     out = {}
-    for mode in ("1", "0"):
-        monkeypatch.setenv("PERMATRACE_B200_PRECISION", mode)
+    for mode in ("1", "0", "1-two-groups"):
+        monkeypatch.setenv("PERMATRACE_B200_PRECISION", mode[0])
+        monkeypatch.setenv("PERMATRACE_B200_TC4", "0" if mode == "1-two-groups" else "1")
         wl = build_workload("dof6")
         checker = P.not_free_checker(wl.problem)
         res = T.trace(wl.seeds, wl.manifold, wl.cfg)
@@ -480,6 +481,11 @@ def test_dof6_full_size_refine_properties(monkeypatch):
     assert fast[0].shape == slow[0].shape and fast[1].shape == slow[1].shape == (1606495, 6)
     assert np.max(np.abs(fast[0] - slow[0])) <= 1e-8 and np.max(np.abs(fast[1] - slow[1])) <= 1e-8
     assert np.array_equal(fast[2], slow[2])
+    # the four-group and the two-group tensor-core screens only differ in which signs fp32 manages to prove
+    two = out["1-two-groups"]
+    assert two[3] == fast[3] and two[1].shape == fast[1].shape
+    assert np.max(np.abs(fast[0] - two[0])) <= 1e-8 and np.max(np.abs(fast[1] - two[1])) <= 1e-8
+    assert np.array_equal(fast[2], two[2])
 
 
 # ---- device pipeline and the sharded driver on one GPU -----------------------------------------------------
