@@ -1,10 +1,10 @@
-"""The slice of ``permatrace/pipeline.py`` that sits on the hot path.
+"""The slice of ``permatrace/pipeline.py`` that sits on the hot path, and its two callers.
 
-`Problem` (pipeline.py:80-107), the non-free checker the refinement stage calls (pipeline.py:256-270)
-and -- the first "next" row of SURVEY.md section 8f -- the certificate verifier `verify_proof`
-(pipeline.py:464-580), whose expensive part re-runs trace + coarse_cells + refine on the device path.
-The solve loop and the text formats stay in the reference package; INTEGRATION.md shows how they bind
-to this module.
+`Problem` (pipeline.py:80-107), the non-free checker the refinement stage calls (pipeline.py:256-270), and the
+"next" rows of SURVEY.md section 8f: the certificate verifier `verify_proof` (pipeline.py:464-580), whose expensive
+part re-runs trace + coarse_cells + refine on the device path, and the learn -> trace -> refine -> check loop `solve`
+(pipeline.py:284-430) with the roadmap of `planner.py` feeding it.  The text formats (INFPROOF / KCLF / EDGEMESH) stay in
+the reference package; INTEGRATION.md shows how they bind to this module.
 """
 
 from __future__ import annotations
@@ -12,6 +12,7 @@ from __future__ import annotations
 import hashlib
 import json
 import time
+import warnings
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -20,7 +21,8 @@ from .collision import (RobotModel, Scene, _check, config_in_collision, device_c
                         scene_to_dict)
 
 __all__ = ["Problem", "not_free_checker", "_not_free_checker", "fingerprint", "InfeasibilityProof", "CheckResult",
-           "VerifyReport", "verify_proof"]
+           "VerifyReport", "verify_proof", "ProblemFile", "load_problem_file", "SolveParams", "SolveStats", "Plan",
+           "SolveTimeout", "solve"]
 
 
 @dataclass
@@ -81,6 +83,118 @@ def _not_free_checker(problem, accumulator: list | None = None):
 
 
 not_free_checker = _not_free_checker
+
+
+# ---- scene files and solve parameters (reference pipeline.py:120-208) -----------------------------------
+
+_SCENE_PARAM_KEYS = {
+    "lambda": ("lam", float), "k": ("k", int), "eps": ("eps", float), "gamma": ("gamma", float),
+    "seeds": ("seeds", int), "samples": ("samples_per_iter", int), "margin": ("trace_margin", float),
+    "regularization": ("regularization", float), "push": ("push", float),
+}
+
+
+@dataclass
+class SolveParams:
+    """Resolution and budget knobs of `solve`; same fields and defaults as the reference (pipeline.py:172-205).
+    `push=None` means lam * sqrt(2 gamma) (about one fine cell into the blocked side), `trace_margin=None` the
+    reference's box inflation rule."""
+
+    lam: float = 0.05
+    k: int = 2
+    eps: float = 1e-9
+    seeds: int = 20
+    seed_tol: float = 1e-8
+    memory_budget: int = 64 * 2**20
+    rng_seed: int = 0
+    workers: int = 1
+    samples_per_iter: int = 500
+    max_iters: int = 50
+    timeout: float = 300.0
+    gamma: float | None = None
+    regularization: float = 1e-3
+    push: float | None = None
+    knn: int = 10
+    max_edges: int = 10_000_000
+    trace_margin: float | None = None
+
+    def __post_init__(self):
+        if self.lam <= 0 or self.k < 1 or self.eps <= 0:
+            raise ValueError("lam, k and eps must be positive")
+        if self.seeds < 1 or self.samples_per_iter < 1 or self.max_iters < 1:
+            raise ValueError("seeds, samples_per_iter and max_iters must be positive")
+
+
+@dataclass
+class ProblemFile:
+    """Parsed scene file: models plus optional suggested endpoints / parameters (pipeline.py:120-156)."""
+
+    robot: RobotModel
+    scene: Scene
+    start: np.ndarray | None
+    goal: np.ndarray | None
+    params: dict
+
+    def problem(self, start=None, goal=None) -> Problem:
+        start = self.start if start is None else start
+        goal = self.goal if goal is None else goal
+        if start is None or goal is None:
+            raise ValueError("scene file has no endpoints; pass --start/--goal")
+        return Problem(self.robot, self.scene, start, goal)
+
+    def solve_params(self, **overrides) -> SolveParams:
+        """SolveParams from the file's params block; keyword overrides win."""
+        params = SolveParams()
+        for key, value in self.params.items():
+            if key not in _SCENE_PARAM_KEYS:
+                raise ValueError(f"unknown scene parameter {key!r}")
+            attr, cast = _SCENE_PARAM_KEYS[key]
+            setattr(params, attr, cast(value))
+        for attr, value in overrides.items():
+            if not hasattr(params, attr):
+                raise ValueError(f"unknown solve parameter {attr!r}")
+            setattr(params, attr, value)
+        params.__post_init__()
+        return params
+
+
+def problem_file_from_dict(data, origin: str = "<dict>") -> ProblemFile:
+    from .collision import robot_from_dict, scene_from_dict
+    if not isinstance(data, dict) or "robot" not in data or "scene" not in data:
+        raise ValueError(f"{origin}: expected top-level robot: and scene: sections")
+    prob = data.get("problem") or {}
+    start = np.asarray(prob["start"], dtype=np.float64) if "start" in prob else None
+    goal = np.asarray(prob["goal"], dtype=np.float64) if "goal" in prob else None
+    return ProblemFile(robot_from_dict(data["robot"]), scene_from_dict(data["scene"]), start, goal,
+                       dict(prob.get("params") or {}))
+
+
+def load_problem_file(path) -> ProblemFile:
+    """YAML scene file in the reference schema (pipeline.py:159-168)."""
+    import yaml
+    with open(path) as fh:
+        return problem_file_from_dict(yaml.safe_load(fh), str(path))
+
+
+@dataclass
+class SolveStats:
+    iterations: list = field(default_factory=list)
+    outcome: str = ""
+    seconds: float = 0.0
+
+
+@dataclass
+class Plan:
+    """Collision-free path, validated at half the roadmap step."""
+
+    path: list
+    stats: SolveStats
+
+
+@dataclass
+class SolveTimeout:
+    reason: str
+    stats: SolveStats
 
 
 # ---- certificates (reference pipeline.py:110-117, :232-253, :434-580) -----------------------------
@@ -241,3 +355,145 @@ def _reconstruction_check(proof, manifold, points: np.ndarray) -> CheckResult:
     if gap > tol:
         return CheckResult(name, False, f"point sets differ by {gap:.3g} > {tol:.3g}")
     return CheckResult(name, True, f"{points.shape[0]} points reproduced within {tol:.3g}")
+
+
+# ---- the solve loop (reference pipeline.py:272-430) ----------------------------------------------------
+
+def _drop_blocked_segment(roadmap, path) -> bool:
+    """Re-validate a found path at half step; cut the first failing roadmap edge (pipeline.py:272-281)."""
+    i = roadmap.first_blocked_segment(path, roadmap.delta / 2.0)
+    if i is None:
+        return False
+    u, v = roadmap.index_of(path[i]), roadmap.index_of(path[i + 1])
+    roadmap.neighbors[u].pop(v, None)
+    roadmap.neighbors[v].pop(u, None)
+    return True
+
+
+def _learn_manifold(labels, lo, hi, params: SolveParams):
+    """Separating field of one iteration: ridge classifier + limit-box barrier + bias push (pipeline.py:327-349).
+    Returns (manifold, gamma, sigma)."""
+    from .manifold import BoxBarrier, KernelClassifierManifold, median_gamma, train_classifier
+    gamma = params.gamma
+    if gamma is None:
+        gamma = median_gamma(np.vstack([labels.positive, labels.negative]))
+    sigma = 1.0 / np.sqrt(2.0 * gamma)
+    barrier = BoxBarrier(lo, hi, scale=sigma / 4.0, gain=2.0 / sigma)
+    manifold = train_classifier(labels.positive, labels.negative, gamma=gamma, regularization=params.regularization,
+                                barrier=barrier)
+    push = params.lam * np.sqrt(2.0 * gamma) if params.push is None else params.push
+    if push:
+        manifold = KernelClassifierManifold(manifold.support, manifold.weights, manifold.gamma,
+                                            bias=manifold.bias + push, barrier=barrier,
+                                            train_accuracy=manifold.train_accuracy)
+    return manifold, gamma, sigma
+
+
+def solve(problem: Problem, params: SolveParams | None = None):
+    """Search for a `Plan` or an `InfeasibilityProof`; `SolveTimeout` when neither (reference pipeline.py:284-430).
+
+    Same loop, same random stream (one generator shared by the roadmap and the seed sampler, consumed in the
+    reference's order), same per-iteration record keys.  The roadmap's collision work goes to the device in one
+    batch per `grow` / `insert_free_points`, seeds are projected in one batched Newton iteration, and trace,
+    coarse_cells, refine, the non-free labels and the self-verification run on the device path.
+    """
+    from .lattice import LatticeConfig
+    from .manifold import sample_seeds
+    from .planner import Roadmap, find_path, grow, insert_free_points, labeled_samples
+    from .subdivision import build_template, coarse_cells, refine
+    from .tracer import TraceConfig, trace
+
+    params = params or SolveParams()
+    t0 = time.perf_counter()
+    deadline = t0 + params.timeout
+    stats = SolveStats()
+    n = problem.dof
+    lo, hi = problem.limits()
+    rng = np.random.default_rng(params.rng_seed)
+    roadmap = Roadmap(problem.robot, problem.scene, delta=params.lam / 4.0, knn=params.knn, rng=rng)
+    roadmap.add_config(problem.q_start, free=True)
+    roadmap.add_config(problem.q_goal, free=True)
+    template = build_template(n, params.k)
+    coarse = params.lam * params.k
+    scene_id = fingerprint(problem)
+
+    def finish(outcome: str, value):
+        stats.outcome = outcome
+        stats.seconds = time.perf_counter() - t0
+        return value
+
+    for iteration in range(1, params.max_iters + 1):
+        record: dict = {"iteration": iteration}
+        stats.iterations.append(record)
+        if time.perf_counter() > deadline:
+            return finish("timeout", SolveTimeout("wall-clock timeout", stats))
+        grow(roadmap, params.samples_per_iter)
+        record["roadmap"] = len(roadmap)
+        path = find_path(roadmap, problem.q_start, problem.q_goal)
+        while path is not None and _drop_blocked_segment(roadmap, path):
+            path = find_path(roadmap, problem.q_start, problem.q_goal)
+        if path is not None:
+            return finish("plan", Plan([np.asarray(q) for q in path], stats))
+        labels = labeled_samples(roadmap, problem.q_start)
+        record["positive"], record["negative"] = len(labels.positive), len(labels.negative)
+        if len(labels.positive) == 0 or len(labels.negative) == 0:
+            continue
+
+        t = time.perf_counter()
+        manifold, gamma, sigma = _learn_manifold(labels, lo, hi, params)
+        record["train_s"] = time.perf_counter() - t
+        margin = params.trace_margin
+        if margin is None:
+            margin = max(3.0 * coarse, 2.0 * sigma + (1.0 + 2.0 * np.sqrt(n)) * coarse)
+        cfg = TraceConfig(lattice=LatticeConfig(n, coarse), box=(tuple(lo - margin), tuple(hi + margin)),
+                          max_edges=params.max_edges, workers=params.workers, eps=params.eps)
+        f_start, f_goal = (float(v) for v in manifold.values(np.stack([problem.q_start, problem.q_goal])))
+        if (f_start > 0.0) == (f_goal > 0.0):
+            record["skip"] = "no separation"
+            continue
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")            # sparse zero sets fail many draws
+            seeds = sample_seeds(manifold, (lo, hi), params.seeds, tol=params.seed_tol, rng=rng,
+                                 min_separation=coarse / 2.0)
+        if seeds.shape[0] == 0:
+            record["skip"] = "no seeds"
+            continue
+
+        t = time.perf_counter()
+        result = trace(seeds, manifold, cfg)
+        record["trace_s"] = time.perf_counter() - t
+        record["edges"] = len(result.edges)
+        if not len(result.edges) or not result.closure_ok:
+            record["skip"] = "trace not closed"
+            record["dropped"] = result.stats.dropped_out_of_box
+            record["complete"] = result.stats.complete
+            continue
+        cells = coarse_cells(result)
+        record["cells"] = len(cells)
+        check_times: list = []
+        checker = _not_free_checker(problem, check_times)
+        t = time.perf_counter()
+        refined = refine(cells, template, manifold, checker, cfg, memory_budget=params.memory_budget)
+        record["refine_s"] = time.perf_counter() - t
+        record["check_s"] = float(sum(check_times))
+        record["points"] = int(refined.points.shape[0])
+        record["free_points"] = int(refined.free_points.shape[0])
+        if refined.free_points.shape[0]:
+            # the zero set still touches free space: feed those configurations back into the roadmap
+            insert_free_points(roadmap, refined.free_points, dedup_tol=params.lam / 4.0)
+            continue
+        if refined.points.shape[0] == 0:
+            record["skip"] = "empty refinement"
+            continue
+
+        proof = InfeasibilityProof(
+            manifold=manifold, lam=params.lam, k=params.k, eps=params.eps, points=np.array(refined.points),
+            f_start=f_start, f_goal=f_goal, fingerprint=scene_id, closure_ok=result.stats.closure_ok,
+            polyline_closed=result.stats.polyline_closed, coarse_edges=len(result.edges), coarse_cells=len(cells),
+            meta={"generator": "permatrace-b200", "iterations": str(iteration), "support": str(manifold.support.shape[0])})
+        report = verify_proof(proof, problem)
+        if report.ok:
+            proof.stats = stats
+            return finish("proof", proof)
+        record["skip"] = "self-verification failed: " + report.first_failure()
+    return finish("timeout", SolveTimeout("iteration budget exhausted", stats))

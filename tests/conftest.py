@@ -122,6 +122,8 @@ def oracle_model(robot_dict, scene_dict):
 
     def pose(o):
         o = o or {}
+        if "rotation" in o:                     # canonical form written by robot_to_dict / scene_to_dict
+            return np.asarray(o["rotation"], dtype=np.float64), np.asarray(o["translation"], dtype=np.float64)
         return rpy(o.get("rpy", (0, 0, 0))), np.asarray(o.get("xyz", (0, 0, 0)), dtype=np.float64)
 
     joints = []

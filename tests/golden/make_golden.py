@@ -379,10 +379,69 @@ def proof_golden(out):
     out["tamper_check_passed"] = np.array(verdicts)
 
 
+def solve_golden(out):
+    """The reference's own solve() on its three bundled scenes (wall2d -> proof, gap2d -> plan, arm3wall -> proof):
+    the per-iteration record of the loop (roadmap size, class sizes, trace/refine counts, skips), the roadmap the
+    planner ended with, and the outcome (certificate points / plan path).  Pins `pipeline.solve` + `planner`."""
+    import json
+    import time
+    from permatrace import pipeline as pl
+    keys = ("iteration", "roadmap", "positive", "negative", "edges", "cells", "points", "free_points")
+    for name in ("wall2d", "gap2d", "arm3wall"):
+        pf = pl.load_problem_file(Path(pl.__file__).parent / "scenes" / f"{name}.yaml")
+        problem = pf.problem(None, None)
+        params = pf.solve_params(timeout=3600.0)
+        captured = {}
+        stats_cls, roadmap_cls = pl.SolveStats, pl.Roadmap
+
+        def stats_factory():
+            captured["stats"] = stats_cls()
+            return captured["stats"]
+
+        def roadmap_factory(*a, **kw):
+            captured["roadmap"] = roadmap_cls(*a, **kw)
+            return captured["roadmap"]
+
+        pl.SolveStats, pl.Roadmap = stats_factory, roadmap_factory
+        try:
+            t0 = time.perf_counter()
+            outcome = pl.solve(problem, params)
+            dt = time.perf_counter() - t0
+        finally:
+            pl.SolveStats, pl.Roadmap = stats_cls, roadmap_cls
+        rec = captured["stats"].iterations
+        out[f"{name}/records"] = np.array([[float(r.get(k, -1)) for k in keys] for r in rec])
+        out[f"{name}/skips"] = np.array([r.get("skip", "") for r in rec])
+        rm_ = captured["roadmap"]
+        out[f"{name}/roadmap_configs"] = np.asarray(rm_.configs)
+        out[f"{name}/roadmap_free"] = np.asarray(rm_.free)
+        out[f"{name}/roadmap_degree"] = np.array([len(d) for d in rm_.neighbors])
+        out[f"{name}/robot_scene_json"] = np.array([json.dumps({"robot": pl.robot_to_dict(problem.robot), "scene": pl.scene_to_dict(problem.scene)})])
+        out[f"{name}/start"], out[f"{name}/goal"] = problem.q_start, problem.q_goal
+        out[f"{name}/params_json"] = np.array([json.dumps(pf.params)])
+        out[f"{name}/seconds"] = np.array([dt])
+        if isinstance(outcome, pl.InfeasibilityProof):
+            m = outcome.manifold
+            out[f"{name}/outcome"] = np.array(["proof"])
+            out[f"{name}/support"], out[f"{name}/weights"] = m.support, m.weights
+            out[f"{name}/gbb"] = np.array([m.gamma, m.bias])
+            out[f"{name}/points"] = outcome.points
+            out[f"{name}/counts"] = np.array([outcome.coarse_edges, outcome.coarse_cells, int(outcome.meta["iterations"])])
+            out[f"{name}/f"] = np.array([outcome.f_start, outcome.f_goal])
+            print(f"  {name}: proof after {outcome.meta['iterations']} iterations, {outcome.points.shape[0]} points, {dt:.1f} s")
+        elif isinstance(outcome, pl.Plan):
+            out[f"{name}/outcome"] = np.array(["plan"])
+            out[f"{name}/path"] = np.asarray(outcome.path)
+            print(f"  {name}: plan with {len(outcome.path)} waypoints after {len(rec)} iterations, {dt:.1f} s")
+        else:
+            raise AssertionError(f"{name}: unexpected outcome {outcome!r}")
+    out["record_keys"] = np.array(keys)
+
+
 def main():
     print("reference backend:", permatrace.BACKEND, "from", permatrace.__file__)
     sections = {"lattice": lattice_golden, "traces": trace_golden, "refine": refine_analytic_golden,
-                "collision": collision_golden, "backend": backend_golden, "proof": proof_golden}
+                "collision": collision_golden, "backend": backend_golden, "proof": proof_golden, "solve": solve_golden}
     only = sys.argv[1:] or list(sections)
     for name in only:
         out: dict = {"reference_backend": np.array([permatrace.BACKEND])}
