@@ -234,8 +234,8 @@ class ClockSampler:
 # ------------------------------------------------------------------------------------------------
 
 # DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the big launch of each kernel, from the
-# `ncu --set full` captures summarised in profiles/r1_v6_*_full.txt (same command, dof6 workload)
-NCU_TRAFFIC = {"bisect_fp64_newton": 206.695168e6 + 74.322944e6, "bisect_fp32_screen_tc": 171.079168e6 + 21.591296e6}
+# `ncu --set full` captures summarised in profiles/r1_v7_*_full.txt (same command, dof6 workload)
+NCU_TRAFFIC = {"bisect_fp64_newton": 206.831104e6 + 76.694016e6, "bisect_fp32_screen_tc": 170.094592e6 + 19.643648e6}
 
 
 def pair_flops(n: int) -> float:
@@ -396,7 +396,7 @@ def run_gpu(args):
         return {"bound": "fp64", "kernel": name, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak if peak else None,
                 "traffic": NCU_TRAFFIC.get(name) if args.workload == "dof6" else None,
-                "traffic_source": "profiles/r1_v6_newton_full.txt (largest launch)" if name in NCU_TRAFFIC else None,
+                "traffic_source": "profiles/r1_v7_newton_full.txt (largest launch)" if name in NCU_TRAFFIC else None,
                 "peak_source": "DFMA microbenchmark run in this process (MEASURED_PEAKS.json holds only HBM and bf16)",
                 "launches": launches, "avg_launch_ms": ms / max(launches, 1), "share_of_step": ms / total_ms,
                 "pair_evals_per_step": pe, "flop_per_pair_eval": pair_flops(a.n)}
@@ -412,7 +412,7 @@ def run_gpu(args):
         return {"bound": "mufu_ex2", "kernel": name, "achieved": achieved, "peak": peak, "unit": "T pair-evals/s (1 ex2 each)",
                 "frac": achieved / peak if peak else None,
                 "traffic": NCU_TRAFFIC.get(name) if args.workload == "dof6" else None,
-                "traffic_source": "profiles/r1_v6_tc_screen_full.txt (largest launch)" if name in NCU_TRAFFIC else None,
+                "traffic_source": "profiles/r1_v7_tc4_screen_full.txt (largest launch)" if name in NCU_TRAFFIC else None,
                 "peak_source": "MUFU.EX2 microbenchmark run in this process",
                 "launches": launches, "avg_launch_ms": ms / max(launches, 1), "share_of_step": ms / total_ms,
                 "pair_evals_per_step": pe,
