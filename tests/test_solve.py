@@ -222,3 +222,52 @@ def test_solve_proves_infeasibility_like_the_reference(golden, name):
     assert np.max(np.abs(outcome.points - ref)) <= 1e-5 * max(1.0, np.abs(ref).max())
     assert np.allclose([outcome.f_start, outcome.f_goal], g[f"{name}/f"], rtol=1e-9, atol=1e-12)
     assert PL.verify_proof(outcome, problem).ok
+
+
+@pytest.mark.gpu
+def test_solve_is_deterministic_and_records_stats(golden):
+    """Reference test_pipeline.py:137-147: a rerun yields the same certificate, and every iteration leaves a record."""
+    from paper_2406_04795_b200 import pipeline as PL
+    g = golden("solve")
+    _, a = _solve(g, "wall2d")
+    _, b = _solve(g, "wall2d")
+    assert isinstance(a, PL.InfeasibilityProof) and isinstance(b, PL.InfeasibilityProof)
+    assert np.array_equal(a.points, b.points) and np.array_equal(a.manifold.weights, b.manifold.weights)
+    assert (a.coarse_edges, a.coarse_cells, a.f_start, a.f_goal) == (b.coarse_edges, b.coarse_cells, b.f_start, b.f_goal)
+    assert a.stats.outcome == "proof" and a.stats.seconds > 0.0
+    assert len(a.stats.iterations) == int(a.meta["iterations"])
+    last = a.stats.iterations[-1]
+    assert {"roadmap", "positive", "negative", "train_s", "trace_s", "edges", "cells", "refine_s", "points", "free_points"} <= set(last)
+    assert last["free_points"] == 0 and last["points"] == a.points.shape[0]
+
+
+@pytest.mark.gpu
+def test_solve_budgets(golden):
+    """Reference test_pipeline.py:181-196: an expired clock and an exhausted iteration budget both end in SolveTimeout."""
+    from paper_2406_04795_b200 import pipeline as PL
+    g = golden("solve")
+    _, outcome = _solve(g, "wall2d", max_iters=1)
+    assert isinstance(outcome, PL.SolveTimeout) and outcome.reason == "iteration budget exhausted"
+    assert outcome.stats.outcome == "timeout" and len(outcome.stats.iterations) == 1
+    robot, scene, _ = _problem(g, "wall2d")
+    pf = PL.ProblemFile(robot, scene, g["wall2d/start"], g["wall2d/goal"], json.loads(str(g["wall2d/params_json"][0])))
+    outcome = PL.solve(pf.problem(), pf.solve_params(timeout=0.0))
+    assert isinstance(outcome, PL.SolveTimeout) and outcome.reason == "wall-clock timeout"
+
+
+@pytest.mark.gpu
+def test_problem_rejects_bad_endpoints(golden):
+    """Reference test_pipeline.py:50-62."""
+    from paper_2406_04795_b200 import pipeline as PL
+    g = golden("solve")
+    robot, scene, _ = _problem(g, "wall2d")
+    with pytest.raises(ValueError):
+        PL.Problem(robot, scene, [0.5, 0.5], g["wall2d/goal"])            # inside the wall
+    with pytest.raises(ValueError):
+        PL.Problem(robot, scene, [1.5, 0.5], g["wall2d/goal"])            # outside the limits
+    with pytest.raises(ValueError):
+        PL.Problem(robot, scene, [0.15, 0.5, 0.0], g["wall2d/goal"])      # wrong width
+    a, b = PL.Problem(robot, scene, g["wall2d/start"], g["wall2d/goal"]), None
+    robot2, scene2, _ = _problem(g, "gap2d")
+    b = PL.Problem(robot2, scene2, g["gap2d/start"], g["gap2d/goal"])
+    assert PL.fingerprint(a) != PL.fingerprint(b) and len(PL.fingerprint(a)) == 64
