@@ -740,7 +740,9 @@ pt_bisect_newton_kernel(PtFieldDev f, double sum_abs_w, const double* __restrict
             const double pn = sqrt(p2) + f.smax + w * seg[k];
             const double T = f.gamma * PT_L2E * pn * pn;
             const double ceta = PT_U64 * (1.01 * (double)(4 * N + 3) * T * PT_LN2 + 1.25 * (double)f.S + 400.0);
-            const double A = 1.25 * AB[k];   // sum|w|k varies by < 7 % across a bracket of width 2^-7
+            // A >= sum|w|k anywhere in the bracket: between the midpoint and a point at |x - m| <= w (in t) a kernel term
+            // grows by at most exp(gamma | |x-s|^2 - |m-s|^2 |) <= exp(2 gamma pn seg w + gamma seg^2 w^2)
+            const double A = 1.0001 * exp(w * (2.0 * f.gamma * pn * seg[k] + f.gamma * seg2[k] * w)) * AB[k];
             eta = ceta * A + 64.0 * PT_U64 * (1.1 * fabs(B0) + fabs(f.bias)) + 1e-290;
             const double gmax = 2.0 * f.gamma * pn * seg[k];
             const double etaD = (ceta + 16.0 * PT_U64) * gmax * A;
@@ -1142,19 +1144,13 @@ static int pt_screen_tc_launch(pt_ctx* ctx, const pt_field* f, const PtRows& row
         return pt_fail(ctx, PT_E_STATE, "tensor-core screen is built for n <= 6");
     } else {
         const size_t smem = pt_tc_smem_bytes(N, f->d.S);
-        static bool configured = false;
-        if (!configured) {
-            PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect32_tc_kernel<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_TC_SMEM_LIMIT));
-            configured = true;
-        }
+        // per launch: the attribute is per device, and a process may hold contexts on several devices (~1 us)
+        PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect32_tc_kernel<N, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_TC_SMEM_LIMIT));
         if constexpr (N == 6 && MODE == 0) {
             if (f->tc4) {
                 const size_t smem4 = (size_t)5 * f->tc.spad * 16 + 4 * (size_t)6 * PT_TC_M * 16 + (size_t)f->tc.spad * 4 + 64;
-                static bool configured4 = false;
-                if (!configured4) {
-                    PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect32_tc4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_TC_SMEM_LIMIT));
-                    configured4 = true;
-                }
+                // per launch: the attribute is per device, and a process may hold contexts on several devices (~1 us)
+                PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect32_tc4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_TC_SMEM_LIMIT));
                 const unsigned grid4 = pt_grid_for(rows.m, 4 * PT_TC_M, (unsigned)ctx->sm_count);
                 pt_bisect32_tc4_kernel<<<grid4, PT_TC4_THREADS, smem4, ctx->stream>>>(f->d, f->tc, rows, a, b, sa, eps, fresh, lo, hi, ctx->work);
                 return pt_check_launch(ctx, "pt_bisect32_tc4_kernel");
@@ -1182,11 +1178,8 @@ static int pt_screen_levels_launch(pt_ctx* ctx, const pt_field* f, const PtRows&
         const int cmax = pt_tc_chunk_rows(N);
         const int nchunks = (spad + cmax - 1) / cmax;
         int cs = (((spad + nchunks - 1) / nchunks) + PT_TC_N - 1) / PT_TC_N * PT_TC_N;
-        static bool configured = false;
-        if (!configured) {
-            PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect32_tc_kernel<N, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_TC_SMEM_LIMIT));
-            configured = true;
-        }
+        // per launch: the attribute is per device, and a process may hold contexts on several devices (~1 us)
+        PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect32_tc_kernel<N, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_TC_SMEM_LIMIT));
         PtBuf<double> acc, ab; PtBuf<uint32_t> la, lb; PtBuf<unsigned long long> cnt;
         PT_TRY(acc.alloc(ctx, m)); PT_TRY(ab.alloc(ctx, m));
         PT_TRY(la.alloc(ctx, m)); PT_TRY(lb.alloc(ctx, m));
@@ -1328,11 +1321,8 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
         long long chunk_rows = (long long)((PT_TC_SMEM_LIMIT - PT_EXP_TAB * sizeof(double)) / row_bytes);
         if (chunk_rows > f->d.S) chunk_rows = f->d.S;
         const size_t smem_w = (size_t)chunk_rows * row_bytes + PT_EXP_TAB * sizeof(double);
-        static bool configured = false;
-        if (!configured) {
-            PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_rest_warp_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_TC_SMEM_LIMIT));
-            configured = true;
-        }
+        // per launch: the attribute is per device, and a process may hold contexts on several devices (~1 us)
+        PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_rest_warp_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, PT_TC_SMEM_LIMIT));
         const unsigned gridw = pt_grid_for(m, PT_RESTW_THREADS / 32, (unsigned)ctx->sm_count);
         const PtRows tail{lin, steps.p + n_steps, m}, unproven{list3.p, steps.p + max_steps + 1, m};
         pt_bisect_rest_warp_kernel<N><<<gridw, PT_RESTW_THREADS, smem_w, ctx->stream>>>(f->d, tail, a, b, sa, lo.p, hi.p, jlo.p, jhi.p, eps, out,
