@@ -317,6 +317,8 @@ __global__ void pt_bisect_analytic_kernel(PtFieldDev f, const double* __restrict
 //   K4 pt_bisect_rbf_kernel   rows whose proof or verification failed finish by plain fp64 bisection from
 //                             their (always true) bisection bracket.
 #define PT_TILE32 512
+#define PT_NEWTON_RETRIES 24          /* proof attempts (each one true step) a row may take before plain bisection */
+#define PT_RESOLVE_ROUNDS 9           /* true fp64 steps a wide bracket may take before the Newton kernel: 2^-7 needs 7 */
 #define PT_HANDOFF_WIDTH 0.0078125   /* 2^-7: brackets wider than this never enter K3 */
 #define PT_FP32_STOP_WIDTH 0.001953125 /* 2^-9: fp32 screening stops here; deeper levels are mostly uncertain anyway */
 
@@ -648,14 +650,16 @@ __device__ __forceinline__ void pt_rbf_block_sum_x2(const PtFieldDev& f, const d
 
 template <int N, int G>
 __global__ void __launch_bounds__(G == 1 ? 128 : PT_EVAL_THREADS, G == 1 ? PT_NEWTON_MINB : 1)
-pt_bisect_newton_kernel(PtFieldDev f, double sum_abs_w, const double* __restrict__ a_, const double* __restrict__ b_,
+pt_bisect_newton_kernel(PtFieldDev f, double sum_abs_w, PtRows rows, const double* __restrict__ a_, const double* __restrict__ b_,
                         const int8_t* __restrict__ signs_a, double* __restrict__ lo_io, double* __restrict__ hi_io,
-                        size_t m, double eps, double* __restrict__ out, uint8_t* __restrict__ slow,
+                        double eps, double* __restrict__ out, uint8_t* __restrict__ slow,
                         double* __restrict__ jlo_out, double* __restrict__ jhi_out, unsigned long long* work) {
     constexpr int PPT = (G == 1) ? 2 : 1;
     constexpr int THREADS = (G == 1) ? 128 : PT_EVAL_THREADS;
     constexpr int GROUPS = THREADS / G;
     extern __shared__ double tile[];
+    const size_t m = pt_rows_total(rows);                      // all rows, or a compacted list with a device-side count
+    if ((size_t)blockIdx.x * (GROUPS * PPT) >= m) return;
     pt_exp_table_init(tile + PT_EVAL_TILE * PT_ROW64(N));
     const int g = threadIdx.x % G;
     size_t ei[PPT];
@@ -666,6 +670,7 @@ pt_bisect_newton_kernel(PtFieldDev f, double sum_abs_w, const double* __restrict
     for (int k = 0; k < PPT; ++k) {
         ei[k] = (size_t)blockIdx.x * (GROUPS * PPT) + (size_t)k * GROUPS + threadIdx.x / G;
         valid[k] = ei[k] < m;
+        if (valid[k] && rows.list) ei[k] = rows.list[ei[k]];
         seg[k] = 0.0; lo[k] = 0.0; hi[k] = 1.0; sa[k] = 1;
         if (valid[k]) {
             double a[N], b[N];
@@ -718,6 +723,13 @@ pt_bisect_newton_kernel(PtFieldDev f, double sum_abs_w, const double* __restrict
         need[k] = valid[k] && !finished0 && !shallow;
         to_slow[k] = shallow;
         double tf = mid[k], x = mid[k], smin = 1.0, eta = 0.0, ad2 = 0.0, K = 0.0, Dt = 1.0;
+        if (shallow) {
+            // too wide for a proof attempt: the midpoint evaluation is still a true bisection step
+            ++evals;
+            if ((F0[k] > 0.0 ? 1 : -1) == sa[k]) lo[k] = mid[k]; else hi[k] = mid[k];
+            w = hi[k] - lo[k];
+            if (!(__dmul_rn(seg[k], w) > eps)) { to_slow[k] = false; tf = __dmul_rn(0.5, __dadd_rn(lo[k], hi[k])); }
+        }
         if (need[k]) {
             ++evals;
             if ((F0[k] > 0.0 ? 1 : -1) == sa[k]) lo[k] = mid[k]; else hi[k] = mid[k];
@@ -1236,8 +1248,8 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
     PT_TRY(jhi.alloc(ctx, m));
     PT_TRY(list.alloc(ctx, m));
     PT_TRY(slow.alloc(ctx, m));
-    PT_TRY(cnt.alloc(ctx, 6));
-    PT_CUDA(ctx, cudaMemsetAsync(cnt.p, 0, 6 * sizeof(unsigned long long), ctx->stream));
+    PT_TRY(cnt.alloc(ctx, PT_RESOLVE_ROUNDS + 2));
+    PT_CUDA(ctx, cudaMemsetAsync(cnt.p, 0, (PT_RESOLVE_ROUNDS + 2) * sizeof(unsigned long long), ctx->stream));
     const size_t smem32 = (size_t)PT_TILE32 * PtRow32<N>::value * sizeof(float);
     const PtRows all{nullptr, nullptr, m};
 #define PT_G_LAUNCH(KERNEL, SMEM, ...)                                                            \
@@ -1256,20 +1268,41 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
         else if (use_tc) PT_TRY((pt_screen_tc_launch<N, 0>(ctx, f, all, a, b, sa, eps, 1, lo.p, hi.p, nullptr)));
         else PT_G_LAUNCH(pt_bisect32_kernel, smem32, f->d, all, a, b, sa, eps, 1, lo.p, hi.p, ctx->work);
     }
-    // rows that stopped while their bracket is still wide: one true fp64 step, then back to fp32
-    for (int round = 0; round < 2; ++round) {
+    // Rows that stopped while their bracket is still wider than the Newton hand-off width take true fp64 bisection steps
+    // (one evaluation per listed row and round) until they are narrow enough; after the first two steps they go back
+    // through the fp32 screen -- unless the screen is not getting anywhere on this field (ill-conditioned weights make
+    // its error bound larger than |F| almost everywhere: seen with S = 16 384), which one look at the first list's size
+    // tells.  Lists shrink round by round (device-side counts).
+    PtBuf<uint32_t> list_b; PtBuf<unsigned long long> ncnt;
+    PT_TRY(list_b.alloc(ctx, m));
+    PT_TRY(ncnt.alloc(ctx, PT_NEWTON_RETRIES));
+    PT_CUDA(ctx, cudaMemsetAsync(ncnt.p, 0, PT_NEWTON_RETRIES * sizeof(unsigned long long), ctx->stream));
+    bool screen_pays = true;
+    uint32_t* lcur = list.p; uint32_t* lnext = list_b.p;
+    for (int round = 0; round < (screen_pays ? 2 : PT_RESOLVE_ROUNDS); ++round) {
         unsigned long long* c = cnt.p + round;
-        const PtRows sub{list.p, c, m};
+        const PtRows prev = round == 0 ? all : PtRows{lcur, cnt.p + round - 1, m};
+        uint32_t* lout = round == 0 ? lcur : lnext;
+        const PtRows sub{lout, c, m};
         {
             PT_LAUNCH(ctx, "bisect_select");
-            pt_select_shallow_kernel<N><<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>(all, a, b, lo.p, hi.p, eps, list.p, c);
+            pt_select_shallow_kernel<N><<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>(prev, a, b, lo.p, hi.p, eps, lout, c);
             PT_TRY(pt_check_launch(ctx, "pt_select_shallow_kernel"));
+        }
+        if (round == 0) {
+            unsigned long long shallow = 0;
+            PT_CUDA(ctx, cudaMemcpyAsync(&shallow, c, sizeof(shallow), cudaMemcpyDeviceToHost, ctx->stream));
+            PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+            if (shallow == 0) break;
+            screen_pays = 10 * shallow < 9 * (unsigned long long)m;     // the first pass left > 90 % of the rows wide: it will not get better
+        } else {
+            uint32_t* sw = lcur; lcur = lnext; lnext = sw;
         }
         {
             PT_LAUNCH(ctx, "bisect_fp64_resolve");
             PT_G_LAUNCH(pt_bisect_resolve_kernel, smem, f->d, sub, a, b, sa, lo.p, hi.p, ctx->work);
         }
-        {
+        if (round < 2 && screen_pays) {
             PT_LAUNCH(ctx, use_tc ? "bisect_fp32_screen_tc" : "bisect_fp32_screen");
             if (by_level) PT_TRY((pt_screen_levels_launch<N>(ctx, f, sub, a, b, sa, eps, 0, lo.p, hi.p)));
             else if (use_tc) PT_TRY((pt_screen_tc_launch<N, 0>(ctx, f, sub, a, b, sa, eps, 0, lo.p, hi.p, nullptr)));
@@ -1282,17 +1315,45 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
         // mid-size batches (a trace's coarse edges): 4 lanes per row give several blocks per SM, 32 lanes waste the tiles
         const int Gn = G == 32 && m >= 16384 ? 4 : G;
         const unsigned grid = pt_grid_for(m, PT_EVAL_THREADS / Gn);
-        if (Gn == 1) pt_bisect_newton_kernel<N, 1><<<pt_grid_for(m, 256), 128, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, a, b, sa, lo.p, hi.p, m, eps, out, slow.p, jlo.p, jhi.p, ctx->work);
-        else if (Gn == 4) pt_bisect_newton_kernel<N, 4><<<grid, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, a, b, sa, lo.p, hi.p, m, eps, out, slow.p, jlo.p, jhi.p, ctx->work);
-        else pt_bisect_newton_kernel<N, 32><<<grid, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, a, b, sa, lo.p, hi.p, m, eps, out, slow.p, jlo.p, jhi.p, ctx->work);
+#define PT_NEWTON_LAUNCH(ROWS)                                                                                                     \
+        do {                                                                                                                       \
+            if (Gn == 1) pt_bisect_newton_kernel<N, 1><<<pt_grid_for(m, 256), 128, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, ROWS, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, ctx->work); \
+            else if (Gn == 4) pt_bisect_newton_kernel<N, 4><<<grid, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, ROWS, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, ctx->work); \
+            else pt_bisect_newton_kernel<N, 32><<<grid, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, ROWS, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, ctx->work);       \
+        } while (0)
+        PT_NEWTON_LAUNCH(all);
         PT_TRY(pt_check_launch(ctx, "pt_bisect_newton_kernel"));
+        // Rows without a proof yet (bracket still too wide for the monotonicity bound: flat or strongly curved stretches,
+        // ill-conditioned weights) come back: every attempt is a true bisection step plus a new proof attempt on the
+        // halved bracket, over the shrinking list of such rows.
+        for (int retry = 0; retry < PT_NEWTON_RETRIES; ++retry) {
+            unsigned long long* c = ncnt.p + retry;
+            pt_select_flag_kernel<<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>(slow.p, (uint8_t)1, m, list.p, c);
+            PT_TRY(pt_check_launch(ctx, "pt_select_flag_kernel"));
+            unsigned long long left = 0;
+            PT_CUDA(ctx, cudaMemcpyAsync(&left, c, sizeof(left), cudaMemcpyDeviceToHost, ctx->stream));
+            PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+            if (left == 0) break;
+            // lanes per row by the size of the list: small lists would leave a thread-per-row launch latency-bound
+            const PtRows again{list.p, c, m};
+            const int Gr = pt_pick_group(ctx, (size_t)left, f->d.S);
+            const int Gl = Gr == 32 && left >= 16384 ? 4 : Gr;
+            const unsigned gl_ = pt_grid_for((size_t)left, PT_EVAL_THREADS / Gl);
+            if (Gl == 1) pt_bisect_newton_kernel<N, 1><<<pt_grid_for((size_t)left, 256), 128, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, again, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, ctx->work);
+            else if (Gl == 4) pt_bisect_newton_kernel<N, 4><<<gl_, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, again, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, ctx->work);
+            else pt_bisect_newton_kernel<N, 32><<<gl_, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, again, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, ctx->work);
+            PT_TRY(pt_check_launch(ctx, "pt_bisect_newton_kernel"));
+        }
+#undef PT_NEWTON_LAUNCH
     }
+    PtBuf<unsigned long long> steps;
+    unsigned long long* steps_dbg = nullptr;
     // open rows: (2) root enclosed, a few midpoints inside the enclosure need a true evaluation; (1) no proof -- plain
     // bisection.  The bulk of the enclosed rows needs 1..4 evaluations: a few step-synchronous launches over the
     // compacted list of rows that still have an open midpoint (two rows per thread, Newton-kernel efficiency).  The long
     // tail and the unproven rows (~20 evaluations each, few rows) finish in the warp-per-row kernel.
     {
-        PtBuf<uint32_t> list2, list3; PtBuf<unsigned long long> steps;
+        PtBuf<uint32_t> list2, list3;
         // with the support set resident in shared memory the warp-per-row kernel takes the enclosed rows directly (a few
         // hundred 256-row blocks would not fill the machine); otherwise four step launches thin the list out first
         const bool resident = ((size_t)f->d.S * PT_ROW64(N) + PT_EXP_TAB) * sizeof(double) <= PT_TC_SMEM_LIMIT;
@@ -1301,6 +1362,7 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
         PT_TRY(list2.alloc(ctx, m)); PT_TRY(list3.alloc(ctx, m));
         PT_TRY(steps.alloc(ctx, max_steps + 5));
         PT_CUDA(ctx, cudaMemsetAsync(steps.p, 0, (max_steps + 5) * sizeof(unsigned long long), ctx->stream));
+        steps_dbg = steps.p;
         {
             PT_LAUNCH(ctx, "bisect_select");
             pt_select_flag_kernel<<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>(slow.p, (uint8_t)2, m, list.p, steps.p);
@@ -1334,6 +1396,16 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
     }
 #undef PT_G_LAUNCH
     if (getenv("PT_DEBUG_COUNTS")) {
+        unsigned long long hs[16];
+        cudaMemcpyAsync(hs, steps_dbg, 9 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream);
+        cudaStreamSynchronize(ctx->stream);
+        fprintf(stderr, "[pt] open rows: enclosed=%llu unproven=%llu after-steps=%llu\n", hs[0], hs[5], hs[4]);
+        unsigned long long hn[PT_NEWTON_RETRIES];
+        cudaMemcpyAsync(hn, ncnt.p, sizeof(hn), cudaMemcpyDeviceToHost, ctx->stream);
+        cudaStreamSynchronize(ctx->stream);
+        fprintf(stderr, "[pt] proof retries:");
+        for (int i = 0; i < PT_NEWTON_RETRIES; ++i) fprintf(stderr, " %llu", hn[i]);
+        fprintf(stderr, "\n");
         unsigned long long h[2];
         cudaMemcpyAsync(h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream);
         cudaStreamSynchronize(ctx->stream);

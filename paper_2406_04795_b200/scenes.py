@@ -70,4 +70,6 @@ BENCH_CONFIGS = {
     "dof6-stress": dict(n=6, support=2048, lam=0.2, r_split=1.3, obstacles=48),
     # support set of the size the reference's own solve loop ends with (arm3wall: 4 199 roadmap samples)
     "dof6-s4096": dict(n=6, support=4096, lam=0.35, r_split=1.3, obstacles=8),
+    # the support-set size the SURVEY expects for real 6-DoF proofs (10^3..10^4 roadmap samples): 8 support chunks
+    "dof6-s16384": dict(n=6, support=16384, lam=0.35, r_split=1.3, obstacles=8),
 }
