@@ -654,3 +654,38 @@ def test_large_support_set_fallback_paths(monkeypatch):
         assert np.array_equal(a, b)
     assert out["0"][1].shape == out["1"][1].shape and out["0"][2].shape == out["1"][2].shape and out["1"][2].shape[0] > 4096
     assert np.max(np.abs(out["0"][1] - out["1"][1])) <= 1e-8 and np.max(np.abs(out["0"][2] - out["1"][2])) <= 1e-8
+
+
+@pytest.mark.gpu
+def test_ill_conditioned_field_root_solve(monkeypatch):
+    """Barely regularised ridge weights (sum|w| ~ 10^5 x the field's scale): the fp32 screen proves next to nothing, so the
+    root solve runs on its fp64 machinery alone -- resolve rounds instead of the screen, proof retries over shrinking
+    lists, wide rows stepping inside the Newton kernel.  Same traced edges and the same points as plain fp64 bisection,
+    up to the evaluation noise of such a field."""
+    from paper_2406_04795_b200.scenes import synthetic_support
+    from bench import _train_numpy
+    n, lam, k = 4, 0.3, 2
+    pos, neg, rng = synthetic_support(n, 2048, 0.9, 1.5, seed=5)
+    support, weights = _train_numpy(pos, neg, 2.0, 1e-7)
+    assert np.abs(weights).sum() > 1e4
+    sigma = 0.5
+    lo, hi = -1.5 * np.ones(n), 1.5 * np.ones(n)
+    coarse = lam * k
+    margin = max(3.0 * coarse, 2.0 * sigma + (1.0 + 2.0 * np.sqrt(n)) * coarse)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("PERMATRACE_B200_PRECISION", mode)
+        m = M.KernelClassifierManifold(support, weights, 2.0, lam * 2.0, barrier=M.BoxBarrier(lo, hi, sigma / 4.0, 2.0 / sigma))
+        cfg = T.TraceConfig(L.LatticeConfig(n, coarse), box=(tuple(lo - margin), tuple(hi + margin)), eps=1e-9)
+        seeds = M.sample_seeds(m, (lo, hi), 12, rng=np.random.default_rng(1), min_separation=coarse / 2.0)
+        res = T.trace(seeds, m, cfg)
+        ref = S.refine(S.coarse_cells(res), S.build_template(n, k), m, lambda p: np.zeros(len(p), dtype=bool), cfg,
+                       eps_dedup=1e-12)
+        out[mode] = (res.edges.arrays(), res.points.copy(), ref.points.copy(), res.stats.closure_ok)
+    for a, b in zip(out["0"][0], out["1"][0]):
+        assert np.array_equal(a, b)
+    assert out["0"][1].shape == out["1"][1].shape and out["0"][2].shape == out["1"][2].shape and out["1"][2].shape[0] > 4096
+    assert np.max(np.abs(out["0"][1] - out["1"][1])) <= 1e-7 and np.max(np.abs(out["0"][2] - out["1"][2])) <= 1e-7
+    resid = np.abs(m.values(out["1"][2]))
+    from paper_2406_04795_b200.pipeline import _gradient_norms
+    assert np.all(resid <= 4.0 * 1e-9 * (_gradient_norms(m, out["1"][2]) + 1e-12) + 1e-9 * np.abs(weights).sum() * 1e-3)
