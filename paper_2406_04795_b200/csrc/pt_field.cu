@@ -317,6 +317,9 @@ __global__ void pt_bisect_analytic_kernel(PtFieldDev f, const double* __restrict
 //   K4 pt_bisect_rbf_kernel   rows whose proof or verification failed finish by plain fp64 bisection from
 //                             their (always true) bisection bracket.
 #define PT_TILE32 512
+#ifndef PT_RETRY_ERR_RATIO
+#define PT_RETRY_ERR_RATIO 8.0
+#endif
 #define PT_NEWTON_RETRIES 24          /* proof attempts (each one true step) a row may take before plain bisection */
 #define PT_RESOLVE_ROUNDS 9           /* true fp64 steps a wide bracket may take before the Newton kernel: 2^-7 needs 7 */
 #define PT_HANDOFF_WIDTH 0.0078125   /* 2^-7: brackets wider than this never enter K3 */
@@ -653,7 +656,7 @@ __global__ void __launch_bounds__(G == 1 ? 128 : PT_EVAL_THREADS, G == 1 ? PT_NE
 pt_bisect_newton_kernel(PtFieldDev f, double sum_abs_w, PtRows rows, const double* __restrict__ a_, const double* __restrict__ b_,
                         const int8_t* __restrict__ signs_a, double* __restrict__ lo_io, double* __restrict__ hi_io,
                         double eps, double* __restrict__ out, uint8_t* __restrict__ slow,
-                        double* __restrict__ jlo_out, double* __restrict__ jhi_out, unsigned long long* work) {
+                        double* __restrict__ jlo_out, double* __restrict__ jhi_out, double retry_ratio, unsigned long long* work) {
     constexpr int PPT = (G == 1) ? 2 : 1;
     constexpr int THREADS = (G == 1) ? 128 : PT_EVAL_THREADS;
     constexpr int GROUPS = THREADS / G;
@@ -824,9 +827,12 @@ pt_bisect_newton_kernel(PtFieldDev f, double sum_abs_w, PtRows rows, const doubl
                 else {
                     // a midpoint inside J needs a true fp64 evaluation: the rest kernels continue from [L, H],
                     // still skipping every midpoint outside J
+                    // ... unless the enclosure is limited by the model error of this attempt (a wide starting bracket) rather
+                    // than by the evaluation noise: then the row retries from the replayed bracket, which costs two
+                    // evaluations and normally closes it
                     to_slow[k] = true;
                     PT_ST(ST_LO, k) = L; PT_ST(ST_W, k) = H - L;
-                    one_step[k] = sane;
+                    one_step[k] = sane && !(err > retry_ratio * zeta);
                     if (sane) { PT_ST(ST_AD2, k) = Jlo; PT_ST(ST_K, k) = Jhi; }
                 }
             }
@@ -1311,15 +1317,16 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
     }
     {
         PT_LAUNCH(ctx, "bisect_fp64_newton");
+        static const double retry_ratio = getenv("PERMATRACE_B200_RETRY_RATIO") ? atof(getenv("PERMATRACE_B200_RETRY_RATIO")) : PT_RETRY_ERR_RATIO;
         const size_t smem_nt = smem + 10 * 256 * sizeof(double);   // + per-row state (10 fields x rows per block)
         // mid-size batches (a trace's coarse edges): 4 lanes per row give several blocks per SM, 32 lanes waste the tiles
         const int Gn = G == 32 && m >= 16384 ? 4 : G;
         const unsigned grid = pt_grid_for(m, PT_EVAL_THREADS / Gn);
 #define PT_NEWTON_LAUNCH(ROWS)                                                                                                     \
         do {                                                                                                                       \
-            if (Gn == 1) pt_bisect_newton_kernel<N, 1><<<pt_grid_for(m, 256), 128, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, ROWS, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, ctx->work); \
-            else if (Gn == 4) pt_bisect_newton_kernel<N, 4><<<grid, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, ROWS, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, ctx->work); \
-            else pt_bisect_newton_kernel<N, 32><<<grid, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, ROWS, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, ctx->work);       \
+            if (Gn == 1) pt_bisect_newton_kernel<N, 1><<<pt_grid_for(m, 256), 128, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, ROWS, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, retry_ratio, ctx->work); \
+            else if (Gn == 4) pt_bisect_newton_kernel<N, 4><<<grid, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, ROWS, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, retry_ratio, ctx->work); \
+            else pt_bisect_newton_kernel<N, 32><<<grid, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, ROWS, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, retry_ratio, ctx->work);       \
         } while (0)
         PT_NEWTON_LAUNCH(all);
         PT_TRY(pt_check_launch(ctx, "pt_bisect_newton_kernel"));
@@ -1339,9 +1346,9 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
             const int Gr = pt_pick_group(ctx, (size_t)left, f->d.S);
             const int Gl = Gr == 32 && left >= 16384 ? 4 : Gr;
             const unsigned gl_ = pt_grid_for((size_t)left, PT_EVAL_THREADS / Gl);
-            if (Gl == 1) pt_bisect_newton_kernel<N, 1><<<pt_grid_for((size_t)left, 256), 128, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, again, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, ctx->work);
-            else if (Gl == 4) pt_bisect_newton_kernel<N, 4><<<gl_, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, again, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, ctx->work);
-            else pt_bisect_newton_kernel<N, 32><<<gl_, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, again, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, ctx->work);
+            if (Gl == 1) pt_bisect_newton_kernel<N, 1><<<pt_grid_for((size_t)left, 256), 128, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, again, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, retry_ratio, ctx->work);
+            else if (Gl == 4) pt_bisect_newton_kernel<N, 4><<<gl_, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, again, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, retry_ratio, ctx->work);
+            else pt_bisect_newton_kernel<N, 32><<<gl_, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, again, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, retry_ratio, ctx->work);
             PT_TRY(pt_check_launch(ctx, "pt_bisect_newton_kernel"));
         }
 #undef PT_NEWTON_LAUNCH
