@@ -389,7 +389,8 @@ def run_gpu(args):
             pe = prof_counts["pair_evals_bisect"]
         else:
             pe = {"bisect_rbf": prof_counts["pair_evals_bisect"], "eval_rbf": prof_counts["pair_evals_eval"],
-                  "bisect_fp64_rest": prof_counts["pair_evals_rest"], "bisect_fp64_resolve": prof_counts["pair_evals_resolve"]}.get(name, 0)
+                  "bisect_fp64_rest": prof_counts["pair_evals_rest"], "bisect_fp64_resolve": prof_counts["pair_evals_resolve"],
+                  "bisect_fp64_retry": prof_counts["pair_evals_retry"]}.get(name, 0)
             flop = pe * pair_flops(a.n)
         achieved = flop / (ms * 1e-3) / 1e12
         peak = engine.measure_fp64_peak(ctx)
@@ -421,7 +422,7 @@ def run_gpu(args):
     ranked = sorted(prof.items(), key=lambda kv: -kv[1][1])
     roofline, roofline_second = None, None
     for name, _ in ranked:
-        if name in ("bisect_fp64_newton", "bisect_rbf", "eval_rbf", "bisect_fp64_rest", "bisect_fp64_resolve"):
+        if name in ("bisect_fp64_newton", "bisect_rbf", "eval_rbf", "bisect_fp64_rest", "bisect_fp64_resolve", "bisect_fp64_retry"):
             r = fp64_roofline(name)
         elif name in ("bisect_fp32_screen_tc", "bisect_fp32_screen"):
             r = screen_roofline(name)

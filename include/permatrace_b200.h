@@ -57,6 +57,9 @@ long long pt_ctx_launch_count(pt_ctx* ctx);
  * bisection evaluations, [3] root solves handed to plain fp64 bisection, [4] fp64 evaluations spent there,
  * [5] fp64 single-step resolves; reset != 0 zeroes them */
 int pt_ctx_work_counters(pt_ctx* ctx, long long* out, int reset);
+/* fp64 field evaluations spent in proof retries of the root solve (rows whose first enclosure attempt failed),
+ * as of the last pt_ctx_work_counters call */
+long long pt_ctx_retry_evaluations(pt_ctx* ctx);
 /* DFMA-chain microbenchmark: measured FP64 peak of this device in TFLOP/s (roofline denominator) */
 double pt_peak_fp64(pt_ctx* ctx);
 /* MUFU.EX2 microbenchmark: measured special-function peak in T ex2/s (roofline denominator of the fp32 screen) */

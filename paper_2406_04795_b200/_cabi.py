@@ -70,6 +70,7 @@ _SIGS = {
     "pt_ctx_profile_dump": (_ll, [_vp, C.c_char_p, _ll]),
     "pt_ctx_launch_count": (_ll, [_vp]),
     "pt_ctx_work_counters": (_i, [_vp, _vp, _i]),
+    "pt_ctx_retry_evaluations": (C.c_longlong, [_vp]),
     "pt_peak_fp64": (_d, [_vp]),
     "pt_peak_ex2": (_d, [_vp]),
     "pt_rbf_values": (_i, [_vp, _vp, _ll, _i, _vp, _ll, _vp, _d, _d, _vp]),

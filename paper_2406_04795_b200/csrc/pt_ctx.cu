@@ -206,8 +206,8 @@ int pt_ctx_create(int device, pt_ctx** out) {
     }
     ctx->pinned_bytes = 1 << 16;
     PT_CUDA(ctx, cudaMallocHost(&ctx->pinned, ctx->pinned_bytes));
-    PT_CUDA(ctx, cudaMalloc((void**)&ctx->work, 8 * sizeof(unsigned long long)));
-    PT_CUDA(ctx, cudaMemset(ctx->work, 0, 8 * sizeof(unsigned long long)));
+    PT_CUDA(ctx, cudaMalloc((void**)&ctx->work, 16 * sizeof(unsigned long long)));
+    PT_CUDA(ctx, cudaMemset(ctx->work, 0, 16 * sizeof(unsigned long long)));
     *out = ctx;
     return PT_OK;
 }
@@ -282,13 +282,16 @@ long long pt_ctx_launch_count(pt_ctx* ctx) { return ctx ? ctx->launches : -1; }
 
 int pt_ctx_work_counters(pt_ctx* ctx, long long* out, int reset) {
     if (!ctx || !out) return pt_fail(ctx, PT_E_INVALID, "pt_ctx_work_counters: NULL argument");
-    unsigned long long h[8];
+    unsigned long long h[16];
     PT_CUDA(ctx, cudaMemcpyAsync(h, ctx->work, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
     PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     for (int i = 0; i < 6; ++i) out[i] = (long long)h[i];
+    ctx->retry_evals = (long long)h[8];          // the proof retries count into a second bank (work + 8)
     if (reset) PT_CUDA(ctx, cudaMemsetAsync(ctx->work, 0, sizeof(h), ctx->stream));
     return PT_OK;
 }
+
+long long pt_ctx_retry_evaluations(pt_ctx* ctx) { return ctx ? ctx->retry_evals : -1; }
 
 double pt_peak_ex2(pt_ctx* ctx) {
     if (!ctx) return -1.0;

@@ -1316,7 +1316,6 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
         }
     }
     {
-        PT_LAUNCH(ctx, "bisect_fp64_newton");
         static const double retry_ratio = getenv("PERMATRACE_B200_RETRY_RATIO") ? atof(getenv("PERMATRACE_B200_RETRY_RATIO")) : PT_RETRY_ERR_RATIO;
         const size_t smem_nt = smem + 10 * 256 * sizeof(double);   // + per-row state (10 fields x rows per block)
         // mid-size batches (a trace's coarse edges): 4 lanes per row give several blocks per SM, 32 lanes waste the tiles
@@ -1328,8 +1327,11 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
             else if (Gn == 4) pt_bisect_newton_kernel<N, 4><<<grid, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, ROWS, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, retry_ratio, ctx->work); \
             else pt_bisect_newton_kernel<N, 32><<<grid, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, ROWS, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, retry_ratio, ctx->work);       \
         } while (0)
-        PT_NEWTON_LAUNCH(all);
-        PT_TRY(pt_check_launch(ctx, "pt_bisect_newton_kernel"));
+        {
+            PT_LAUNCH(ctx, "bisect_fp64_newton");
+            PT_NEWTON_LAUNCH(all);
+            PT_TRY(pt_check_launch(ctx, "pt_bisect_newton_kernel"));
+        }
         // Rows without a proof yet (bracket still too wide for the monotonicity bound: flat or strongly curved stretches,
         // ill-conditioned weights) come back: every attempt is a true bisection step plus a new proof attempt on the
         // halved bracket, over the shrinking list of such rows.
@@ -1342,13 +1344,14 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
             PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
             if (left == 0) break;
             // lanes per row by the size of the list: small lists would leave a thread-per-row launch latency-bound
+            PT_LAUNCH(ctx, "bisect_fp64_retry");
             const PtRows again{list.p, c, m};
             const int Gr = pt_pick_group(ctx, (size_t)left, f->d.S);
             const int Gl = Gr == 32 && left >= 16384 ? 4 : Gr;
             const unsigned gl_ = pt_grid_for((size_t)left, PT_EVAL_THREADS / Gl);
-            if (Gl == 1) pt_bisect_newton_kernel<N, 1><<<pt_grid_for((size_t)left, 256), 128, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, again, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, retry_ratio, ctx->work);
-            else if (Gl == 4) pt_bisect_newton_kernel<N, 4><<<gl_, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, again, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, retry_ratio, ctx->work);
-            else pt_bisect_newton_kernel<N, 32><<<gl_, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, again, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, retry_ratio, ctx->work);
+            if (Gl == 1) pt_bisect_newton_kernel<N, 1><<<pt_grid_for((size_t)left, 256), 128, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, again, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, retry_ratio, ctx->work + 8);
+            else if (Gl == 4) pt_bisect_newton_kernel<N, 4><<<gl_, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, again, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, retry_ratio, ctx->work + 8);
+            else pt_bisect_newton_kernel<N, 32><<<gl_, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, again, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, retry_ratio, ctx->work + 8);
             PT_TRY(pt_check_launch(ctx, "pt_bisect_newton_kernel"));
         }
 #undef PT_NEWTON_LAUNCH

@@ -30,6 +30,7 @@ struct pt_ctx {
     int sm_count = 148;
     // device-side work counters: [0] bisection field evaluations (rows x iterations), [1] points evaluated
     unsigned long long* work = nullptr;
+    long long retry_evals = 0;           // snapshot taken by pt_ctx_work_counters
     // size-bucketed cache of device blocks (all work is ordered on `stream`, so a freed block can be handed
     // out again at once): after the first step the hot path makes no driver allocation calls at all
     std::multimap<size_t, void*> free_blocks;
