@@ -99,7 +99,11 @@ void pt_field_destroy(pt_field* f);
  *       is PROVEN equal to the FP64 one, FP64 recheck of every unproven value, Newton root location with a rigorous
  *       enclosure that replays the reference's bisection decisions.
  * PERMATRACE_B200_TC=0 keeps mode 1 on the SIMT kernels; PERMATRACE_B200_TC_LEVELS=1 forces the level-synchronous
- * tensor-core driver that serves support sets beyond one CTA's shared memory. */
+ * tensor-core driver that serves support sets beyond one CTA's shared memory; PERMATRACE_B200_TC4=0 selects the
+ * two-group screen kernel where the four-group one (n = 6, resident support set) would run;
+ * PERMATRACE_B200_RETRY_RATIO (default 8) is the enclosure-width / noise-width ratio above which an open row retries
+ * the proof from its replayed bracket instead of evaluating its open midpoints one by one.  None of these changes a
+ * result. */
 int pt_field_set_precision(pt_field* f, int mode);
 /* ImplicitManifold.values / .signs (manifold.py:54-72): out_values (f64) and out_signs (i8, +1/-1)
  * may each be NULL */
