@@ -11,9 +11,13 @@ __global__ void pt_cell_counts_kernel(PtGeom g, const u64* __restrict__ edge_key
     if (i == count) ncell[i] = 0;
 }
 
+// A cell is a coface of many traced edges (dof6: 14 M emitted keys for 1.3 M distinct cells).  Before the sort a
+// direct-mapped "last key seen" table (no probing, L2-resident) drops a key whose slot already holds it; distinct keys
+// sharing a slot just pass through more than once.  Whatever survives is compacted through a warp-aggregated counter
+// and still goes through sort + unique, so the filter can only shrink the sort, never change the result.
 __global__ void __launch_bounds__(256)
-pt_cell_cofaces_kernel(PtGeom g, const u64* __restrict__ edge_key, size_t count, const unsigned long long* __restrict__ off,
-                       u64* __restrict__ keys, unsigned* err) {
+pt_cell_cofaces_kernel(PtGeom g, const u64* __restrict__ edge_key, size_t count, u64* __restrict__ seen, unsigned seen_mask,
+                       u64* __restrict__ keys, unsigned long long* __restrict__ n_out, unsigned* err) {
     const size_t w = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= count) return;
@@ -22,15 +26,29 @@ pt_cell_cofaces_kernel(PtGeom g, const u64* __restrict__ edge_key, size_t count,
     int u[PT_NMAX];
     pt_unpack_vertex(g, pt_edge_vkey(g, ek), u);
     const int nc = pt_ncellcofaces(g.n, s);
-    const unsigned long long o = off[w];
-    for (int t = lane; t < nc; t += 32) {
-        uint32_t y; uint8_t perm[PT_NMAX];
-        pt_cellcoface(g.n, s, t, y, perm);
-        int base[PT_NMAX];
-        pt_apply_masks(g.n, u, 0u, y, base);
-        u64 bk;
-        if (!pt_pack_vertex(g, base, bk)) { atomicOr(err, PT_ERR_KEY_RANGE); bk = 0; }
-        keys[o + t] = pt_cell_key(bk, pt_perm_rank(g.n, perm));
+    for (int t0 = 0; t0 < nc; t0 += 32) {
+        const int t = t0 + lane;
+        bool emit = false;
+        u64 key = 0;
+        if (t < nc) {
+            uint32_t y; uint8_t perm[PT_NMAX];
+            pt_cellcoface(g.n, s, t, y, perm);
+            int base[PT_NMAX];
+            pt_apply_masks(g.n, u, 0u, y, base);
+            u64 bk;
+            if (!pt_pack_vertex(g, base, bk)) { atomicOr(err, PT_ERR_KEY_RANGE); bk = 0; }
+            key = pt_cell_key(bk, pt_perm_rank(g.n, perm));
+            const unsigned slot = (unsigned)(pt_mix(key) & seen_mask);
+            emit = atomicExch((unsigned long long*)&seen[slot], (unsigned long long)(key + 1)) != (unsigned long long)(key + 1);
+        }
+        const unsigned ballot = __ballot_sync(0xffffffffu, emit);
+        if (ballot) {
+            const int leader = __ffs(ballot) - 1;
+            unsigned long long base_out = 0;
+            if (lane == leader) base_out = atomicAdd(n_out, (unsigned long long)__popc(ballot));
+            base_out = __shfl_sync(0xffffffffu, base_out, leader);
+            if (emit) keys[base_out + __popc(ballot & ((1u << lane) - 1u))] = key;
+        }
     }
 }
 
@@ -107,20 +125,32 @@ static int pt_cells_build(pt_ctx* ctx, const PtGeom& geom, const u64* edge_key_d
     unsigned long long* h = (unsigned long long*)ctx->pinned;
     cudaMemcpyAsync(h, off.p + E, sizeof(*h), cudaMemcpyDeviceToHost, ctx->stream);
     if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) { delete c; return pt_fail(ctx, PT_E_CUDA, "cell count scan failed"); }
-    const size_t total = (size_t)*h;
-    PtBuf<u64> raw, sorted; PtBuf<unsigned> err; PtBuf<long long> nsel;
-    rc = raw.alloc(ctx, total);
-    if (rc == PT_OK) rc = sorted.alloc(ctx, total);
+    const size_t emitted = (size_t)*h;
+    PtBuf<u64> raw, sorted, seen; PtBuf<unsigned> err; PtBuf<long long> nsel; PtBuf<unsigned long long> nkept;
+    // "last key seen" filter: a power of two of 8-byte slots around the number of emitted keys / 4, at most 32 MB (L2)
+    size_t slots = 1u << 12;
+    while (slots < emitted / 4 && slots < ((size_t)1 << 22)) slots <<= 1;
+    rc = raw.alloc(ctx, emitted);
+    if (rc == PT_OK) rc = seen.alloc(ctx, slots);
     if (rc == PT_OK) rc = err.alloc(ctx, 1);
     if (rc == PT_OK) rc = nsel.alloc(ctx, 1);
+    if (rc == PT_OK) rc = nkept.alloc(ctx, 1);
     if (rc != PT_OK) { delete c; return rc; }
     cudaMemsetAsync(err.p, 0, sizeof(unsigned), ctx->stream);
+    cudaMemsetAsync(nkept.p, 0, sizeof(unsigned long long), ctx->stream);
+    cudaMemsetAsync(seen.p, 0, slots * sizeof(u64), ctx->stream);          // stored values are key + 1, so 0 = empty
     {
         PT_LAUNCH(ctx, "cells_cofaces");
-        pt_cell_cofaces_kernel<<<pt_grid_for(E * 32, 256), 256, 0, ctx->stream>>>(geom, edge_key_dev, E, off.p, raw.p, err.p);
+        pt_cell_cofaces_kernel<<<pt_grid_for(E * 32, 256), 256, 0, ctx->stream>>>(geom, edge_key_dev, E, seen.p, (unsigned)(slots - 1),
+                                                                                 raw.p, nkept.p, err.p);
         rc = pt_check_launch(ctx, "pt_cell_cofaces_kernel");
         if (rc != PT_OK) { delete c; return rc; }
     }
+    cudaMemcpyAsync(h, nkept.p, sizeof(*h), cudaMemcpyDeviceToHost, ctx->stream);
+    if (cudaStreamSynchronize(ctx->stream) != cudaSuccess) { delete c; return pt_fail(ctx, PT_E_CUDA, "cell coface enumeration failed"); }
+    const size_t total = (size_t)*h;
+    rc = sorted.alloc(ctx, total > 0 ? total : 1);
+    if (rc != PT_OK) { delete c; return rc; }
     const int key_bits = geom.n * geom.bits + PT_CELL_RANK_BITS;
     size_t tb1 = 0, tb2 = 0;
     cub::DeviceRadixSort::SortKeys(nullptr, tb1, raw.p, sorted.p, (long long)total, 0, key_bits, ctx->stream);
