@@ -105,9 +105,24 @@ def _seeds_numpy(value, grad, lo, hi, count, rng, min_sep, tol=1e-8):
 _WORKLOAD_CACHE: dict = {}
 
 
+def _scenes():
+    """paper_2406_04795_b200/scenes.py loaded BY PATH: it is pure numpy, and importing it through the package would run
+    the package's __init__ and map libpermatrace_b200.so -- which the reference arm must never do."""
+    import importlib.util
+    mod = sys.modules.get("_pt_bench_scenes")
+    if mod is None:
+        spec = importlib.util.spec_from_file_location("_pt_bench_scenes", REPO / "paper_2406_04795_b200" / "scenes.py")
+        mod = importlib.util.module_from_spec(spec)
+        sys.modules["_pt_bench_scenes"] = mod
+        spec.loader.exec_module(mod)
+    return mod
+
+
 def build_arrays(name: str):
     """Everything both arms need, as plain arrays/dicts (SURVEY.md Appendix B recipe)."""
-    from paper_2406_04795_b200.scenes import BENCH_CONFIGS, arm_robot_dict, arm_scene_dict, synthetic_support
+    sc = _scenes()
+    BENCH_CONFIGS, arm_robot_dict, arm_scene_dict, synthetic_support = (sc.BENCH_CONFIGS, sc.arm_robot_dict,
+                                                                        sc.arm_scene_dict, sc.synthetic_support)
     if name in _WORKLOAD_CACHE:
         return _WORKLOAD_CACHE[name]
     p = BENCH_CONFIGS[name]
@@ -448,13 +463,15 @@ def run_gpu(args):
 
     line = None
     if rank == 0:
-        cpu = cpu_baseline(args.workload, max(1, min(os.cpu_count() or 1, 64))) if world == 1 and not args.no_cpu_baseline else None
+        cpu, parity = None, None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu, info = cpu_baseline(args.workload, max(1, min(os.cpu_count() or 1, 64)))
+            parity = parity_sample(wl, info)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.workload}: {a.n}-DoF arm, {len(a.scene_dict['obstacles'])} primitives, "
-                                   f"S={a.support.shape[0]} support vectors, lambda={a.lam}, k={a.k}",
+            "config": {"workload": workload_text(a),
                        "parallelism": "single GPU" if world == 1 else f"owner-hashed BFS (all_to_all per wave) + refine/check sharded over {world} ranks (cell slices), candidate merge by all_gather",
                        "l2_policy": "per-step working set (hash tables + fine-edge arrays) exceeds the 126 MB L2; "
                                     "all tables are rebuilt from empty every step",
@@ -466,7 +483,10 @@ def run_gpu(args):
                        "bisect_fallbacks": counts["bisect_fallbacks"]},
             "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": int(launches),
             "roofline": roofline, "roofline_second": roofline_second, "roofline_hbm": hbm, "kernels": kernels, "cpu_baseline": cpu,
-            "proof_time_s": ms / args.steps * 1e-3,
+            "parity_sample": parity, "ambiguous_signs": counts.get("ambiguous_signs"),
+            # ONE trace -> cells -> refine(+check) attempt on this synthetic manifold (it is unrelated to the obstacles, so
+            # free points remain); a real proof (zero free points, verified certificate) is `--workload dofN-proof`
+            "attempt_time_s": ms / args.steps * 1e-3,
         }
     if world > 1:
         dist.destroy_process_group()
@@ -474,38 +494,145 @@ def run_gpu(args):
 
 
 # ------------------------------------------------------------------------------------------------
-# CPU arm: the reference's algorithm (oracle port), bounded sample of the same workload
+# CPU arm: the reference's algorithm on a bounded sample of the same workload
 # ------------------------------------------------------------------------------------------------
 
-def cpu_sample(workload: str, threads: int, max_edges: int = 4000, max_cells: int = 600):
-    """One bounded sample: the same scene/manifold/lattice, BFS capped at `max_edges` coarse edges,
-    refinement of the first `max_cells` sorted coarse cells.  Returns (simplices, seconds)."""
-    from oracle import permatrace_oracle as O
-    from tests.conftest import oracle_model
+CPU_MAX_EDGES = 4000      # coarse edges traced by the CPU sample (the BFS is capped there)
+CPU_RUNS, CPU_RUN_LEN = 15, 20   # refined cells: CPU_RUNS contiguous runs of CPU_RUN_LEN cells, spread uniformly over the
+                                 # sorted cell list of the capped trace (contiguous runs keep the eps-dedup meaningful;
+                                 # uniform positions avoid the low-crossing boundary cells a head-of-list sample picks)
+
+
+def sample_positions(count: int, runs: int = CPU_RUNS, run_len: int = CPU_RUN_LEN):
+    if count <= runs * run_len:
+        return np.arange(count)
+    starts = np.linspace(0, count - run_len, runs).astype(np.int64)
+    return np.unique(np.concatenate([np.arange(s0, s0 + run_len) for s0 in starts]))
+
+
+def _reference_modules():
+    """The REAL reference (permatrace), importable only where /root/reference is mounted (the build container; never on
+    the GPU box).  Prefers a scratch build with the Cython backend (tests/golden/make_golden.py documents it)."""
+    if os.environ.get("PT_BENCH_NO_REFERENCE"):
+        return None
+    for cand in ("/tmp/refbuild/pkg/src", "/root/reference/pkg/src"):
+        if Path(cand, "permatrace", "tracer.py").exists():
+            if cand not in sys.path:
+                sys.path.insert(0, cand)
+            try:
+                import permatrace
+                from permatrace import collision, lattice, manifold, pipeline, subdivision, tracer
+                return SimpleNamespace(pkg=permatrace, rc=collision, rl=lattice, rm=manifold, pl=pipeline, rs=subdivision, rt=tracer)
+            except Exception:
+                return None
+    return None
+
+
+def cpu_sample(workload: str, threads: int, max_edges: int = CPU_MAX_EDGES, runs: int = CPU_RUNS, run_len: int = CPU_RUN_LEN,
+               prefer_reference: bool = True):
+    """One bounded sample: the same scene / manifold / lattice, BFS capped at `max_edges` coarse edges, refinement (one
+    cell per batch, eps-dedup and collision labels included) of `runs` x `run_len` sorted coarse cells of that trace.
+    Runs the imported reference where it exists (kind "reference", 1 core: it is single-threaded by construction), the
+    oracle port otherwise (kind "port", kernel sums threaded).  Returns a dict with the timing and the raw outputs, which
+    the GPU arm compares with its own results on the same cells (`parity_sample`)."""
     a = build_arrays(workload)
-    O.THREADS = threads
     scale, gain, lo, hi = a.barrier
-    field = O.Field.rbf(a.support, a.weights, a.gamma, a.bias, barrier=(scale, gain, lo, hi))
-    robot, scene = oracle_model(a.robot_dict, a.scene_dict)
-    template = O.build_template(a.n, a.k)
-    t0 = time.perf_counter()
-    tr = O.Trace(field, a.n, a.coarse, None, a.box, max_edges, a.eps).run(a.seeds)
-    tr.points()
-    cells = O.coarse_cells(tr.edges)[:max_cells]
-    ref = O.refine(cells, template, field, lambda p: O.not_free(robot, scene, p), a.coarse, np.zeros(a.n), a.k, a.eps)
-    dt = time.perf_counter() - t0
-    simplices = len(tr.edges) + sum(ref["crossing_edges"])
-    return simplices, dt, {"coarse_edges": len(tr.edges), "cells_refined": len(cells),
-                           "crossing_fine_edges": int(sum(ref["crossing_edges"])), "points": int(ref["points"].shape[0])}
+    ref = _reference_modules() if prefer_reference else None
+    if ref is not None:
+        rm, rt, rl, rs, rc, pl = ref.rm, ref.rt, ref.rl, ref.rs, ref.rc, ref.pl
+        field = rm.KernelClassifierManifold(a.support, a.weights, a.gamma, a.bias, barrier=rm.BoxBarrier(lo, hi, scale, gain))
+        cfg = rt.TraceConfig(rl.LatticeConfig(a.n, a.coarse), box=a.box, max_edges=max_edges, eps=a.eps)
+        prob = SimpleNamespace(robot=rc.robot_from_dict(a.robot_dict), scene=rc.scene_from_dict(a.scene_dict))
+        prob.limits = lambda: rc.joint_limits(prob.robot)
+        checker = pl._not_free_checker(prob)
+        template = rs.build_template(a.n, a.k)
+        t0 = time.perf_counter()
+        tr = rt.trace(a.seeds, field, cfg)
+        cells_all = rs.coarse_cells(tr)
+        pick = sample_positions(len(cells_all), runs, run_len)
+        cells = [cells_all[i] for i in pick]
+        out = rs.refine(cells, template, field, checker, cfg, memory_budget=rs._cell_bytes(template))
+        dt = time.perf_counter() - t0
+        edges = [(e.base, e.parts) for e in tr.edges]
+        cell_keys = [(c.base, c.parts) for c in cells]
+        per_cell = np.array([[b.crossing_edges, b.new_points] for b in out.batch_stats], dtype=np.int64).reshape(-1, 2)
+        points, labels, trace_points = out.points, out.in_collision, tr.points
+        kind, cores = "reference", 1
+    else:
+        from oracle import permatrace_oracle as O
+        from tests.conftest import oracle_model
+        O.THREADS = threads
+        field = O.Field.rbf(a.support, a.weights, a.gamma, a.bias, barrier=(scale, gain, lo, hi))
+        robot, scene = oracle_model(a.robot_dict, a.scene_dict)
+        template = O.build_template(a.n, a.k)
+        t0 = time.perf_counter()
+        tr = O.Trace(field, a.n, a.coarse, None, a.box, max_edges, a.eps).run(a.seeds)
+        trace_points = tr.points()
+        cells_all = O.coarse_cells(tr.edges)
+        pick = sample_positions(len(cells_all), runs, run_len)
+        cells = [cells_all[i] for i in pick]
+        out = O.refine(cells, template, field, lambda q: O.not_free(robot, scene, q), a.coarse, np.zeros(a.n), a.k, a.eps,
+                       batch_cells=1)
+        dt = time.perf_counter() - t0
+        edges, cell_keys = tr.edges, cells
+        per_cell = np.array([out["crossing_edges"], out["new_points"]], dtype=np.int64).T.reshape(-1, 2)
+        points, labels = out["points"], out["in_collision"]
+        kind, cores = "port", threads
+    crossings = int(per_cell[:, 0].sum()) if per_cell.size else 0
+    return {"simplices": len(edges) + crossings, "seconds": dt, "kind": kind, "cores": cores,
+            "coarse_edges": len(edges), "cells_of_capped_trace": len(cells_all), "cells_refined": len(cells),
+            "crossing_fine_edges": crossings, "points": int(points.shape[0]),
+            "edges": edges, "cells": cell_keys, "per_cell": per_cell, "refine_points": points, "labels": np.asarray(labels, dtype=bool),
+            "trace_points": trace_points}
+
+
+def sample_text(info) -> str:
+    return (f"same scene/manifold/lattice; BFS capped at {info['coarse_edges']} coarse edges, {info['cells_refined']} of its "
+            f"{info['cells_of_capped_trace']} sorted coarse cells refined ({CPU_RUNS} runs of {CPU_RUN_LEN} at uniform positions; "
+            f"{info['crossing_fine_edges']} crossing fine edges, {info['points']} points deduplicated and collision-checked); "
+            + ("the imported reference (permatrace, Cython backend when built), single-threaded by construction"
+               if info["kind"] == "reference" else
+               f"oracle port: kernel sums threaded over {info['cores']} host threads, lattice bookkeeping single-threaded like the reference"))
 
 
 def cpu_baseline(workload: str, threads: int):
-    simplices, dt, info = cpu_sample(workload, threads)
-    return {"value": simplices / dt, "unit": UNIT, "cores": threads, "kind": "port", "seconds": dt,
-            "sample": f"same scene/manifold/lattice; BFS capped at {info['coarse_edges']} coarse edges, "
-                      f"{info['cells_refined']} coarse cells refined ({info['crossing_fine_edges']} crossing fine edges, "
-                      f"{info['points']} points checked); kernel sums threaded over {threads} host threads, "
-                      "lattice bookkeeping single-threaded like the reference"}
+    info = cpu_sample(workload, threads)
+    line = {"value": info["simplices"] / info["seconds"], "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
+            "seconds": info["seconds"], "sample": sample_text(info)}
+    return line, info
+
+
+def parity_sample(wl, info):
+    """The CUDA path on exactly the cells the CPU sample refined (public API, one cell per batch) and on the head of the
+    trace the CPU sample traced: per-cell crossing counts, per-cell fresh points, kept points in order (north-star
+    tolerance 1e-5 relative; 1e-8 absolute is what is held), labels, and the ordered edge list, all against the CPU
+    result of the same run."""
+    import paper_2406_04795_b200 as P
+    from paper_2406_04795_b200 import lattice as L, subdivision as S
+    a = wl.arrays
+    cells = [L.PermSimplex(tuple(int(v) for v in base), tuple(tuple(int(x) for x in part) for part in parts))
+             for base, parts in info["cells"]]
+    checker = P.not_free_checker(wl.problem)
+    out = S.refine(cells, wl.template, wl.manifold, checker, wl.cfg, memory_budget=S._cell_bytes(wl.template))
+    rows = np.array([[b.crossing_edges, b.new_points] for b in out.batch_stats], dtype=np.int64).reshape(-1, 2)
+    res = P.trace(a.seeds, wl.manifold, wl.cfg)
+    base, mask, _ = res.edges.arrays()
+    cap = info["coarse_edges"]
+    ref_base = np.array([e[0] for e in info["edges"]], dtype=np.int64).reshape(cap, a.n)
+    ref_mask = np.array([sum(1 << d for d in e[1][0]) for e in info["edges"]], dtype=np.int64)
+    checks = {
+        "trace_head_edges_in_order": bool(len(mask) >= cap and np.array_equal(base[:cap], ref_base) and np.array_equal(mask[:cap], ref_mask)),
+        "trace_head_points": bool(len(mask) >= cap and np.allclose(res.points[:cap], info["trace_points"], rtol=1e-5, atol=1e-8)),
+        "per_cell_crossings": bool(np.array_equal(rows[:, 0], info["per_cell"][:, 0])),
+        "per_cell_fresh_points": bool(np.array_equal(rows[:, 1], info["per_cell"][:, 1])),
+        "points": bool(out.points.shape == info["refine_points"].shape
+                       and np.allclose(out.points, info["refine_points"], rtol=1e-5, atol=1e-8)),
+        "labels": bool(np.array_equal(out.in_collision, info["labels"])),
+    }
+    dev = float(np.max(np.abs(out.points - info["refine_points"]))) if checks["points"] and out.points.size else None
+    return {"verdict": "ok" if all(checks.values()) else "MISMATCH", "against": info["kind"], "cells": len(cells),
+            "crossing_fine_edges": int(rows[:, 0].sum()), "points": int(out.points.shape[0]), "trace_edges_compared": cap,
+            "max_abs_point_deviation": dev, "checks": checks}
 
 
 def run_reference(args):
@@ -514,23 +641,26 @@ def run_reference(args):
         return None
     threads = max(1, min(os.cpu_count() or 1, 64))
     for _ in range(args.warmup):
-        cpu_sample(args.workload, threads, max_edges=200, max_cells=10)
+        cpu_sample(args.workload, threads, max_edges=200, runs=2, run_len=5)
     total_s, total_t, info = 0, 0.0, None
     for _ in range(args.steps):
-        s, dt, info = cpu_sample(args.workload, threads)
-        total_s += s
-        total_t += dt
+        info = cpu_sample(args.workload, threads)
+        total_s += info["simplices"]
+        total_t += info["seconds"]
     a = build_arrays(args.workload)
     value = total_s / total_t
-    sample = (f"per step: BFS capped at {info['coarse_edges']} coarse edges + {info['cells_refined']} coarse cells refined "
-              f"of the same scene/manifold/lattice")
+    sample = "per step: " + sample_text(info)
     return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_t / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.workload}: {a.n}-DoF arm, {len(a.scene_dict['obstacles'])} primitives, "
-                                   f"S={a.support.shape[0]} support vectors, lambda={a.lam}, k={a.k}", "sample": sample},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+            "config": {"workload": workload_text(a), "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": info["cores"], "kind": info["kind"], "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def workload_text(a) -> str:
+    return (f"{a.name}: {a.n}-DoF arm, {len(a.scene_dict['obstacles'])} primitives, S={a.support.shape[0]} support vectors, "
+            f"lambda={a.lam}, k={a.k}")
 
 
 def main():

@@ -153,6 +153,10 @@ typedef struct pt_trace_stats {
     int complete, closure_ok;
     long long table_capacity, sign_table_capacity;
     long long n_stages;          /* StageStat rows available through pt_trace_stages */
+    /* evaluated lattice vertices with |F| < 1e-12*(sum|w|+|bias|), the reference's own cross-backend tolerance on the
+     * kernel sum (pkg/tests/test_backends.py:81-93): only there can a sign -- hence the traced set -- differ from the
+     * reference's.  0 for analytic fields. */
+    long long ambiguous_signs;
 } pt_trace_stats;
 
 /* TraceConfig(lattice=LatticeConfig(n, scale, offset), box, max_edges, eps) (tracer.py:43-59).
@@ -229,6 +233,7 @@ int pt_cells_get(const pt_cells* c, long long first, long long count, int32_t* b
 typedef struct pt_refine_stats {
     long long cells, fine_vertices, crossing_edges, unique_fine_vertices, unique_fine_edges,
         points, in_collision, free_points, dedup_rounds, field_evaluations;
+    long long ambiguous_signs;   /* fine vertices with |F| below the same tolerance as pt_trace_stats.ambiguous_signs */
 } pt_refine_stats;
 /* template: tv[V,n] int32 vertices (lex sorted), te[E,2] int32 edges; k subdivision factor;
  * lattice (n, scale, offset) is the COARSE lattice of the cells; checker NULL -> labels all 0 and

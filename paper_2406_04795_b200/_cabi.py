@@ -46,13 +46,13 @@ class TraceStats(C.Structure):
     _fields_ = [(k, _ll) for k in ("levels", "seeds", "visited_edges", "field_evaluations",
                                    "dropped_out_of_box", "candidates", "frontier")] + \
                [("complete", _i), ("closure_ok", _i)] + \
-               [(k, _ll) for k in ("table_capacity", "sign_table_capacity", "n_stages")]
+               [(k, _ll) for k in ("table_capacity", "sign_table_capacity", "n_stages", "ambiguous_signs")]
 
 
 class RefineStats(C.Structure):
     _fields_ = [(k, _ll) for k in ("cells", "fine_vertices", "crossing_edges", "unique_fine_vertices",
                                    "unique_fine_edges", "points", "in_collision", "free_points",
-                                   "dedup_rounds", "field_evaluations")]
+                                   "dedup_rounds", "field_evaluations", "ambiguous_signs")]
 
 
 _SIGS = {

@@ -208,6 +208,7 @@ int pt_ctx_create(int device, pt_ctx** out) {
     PT_CUDA(ctx, cudaMallocHost(&ctx->pinned, ctx->pinned_bytes));
     PT_CUDA(ctx, cudaMalloc((void**)&ctx->work, 16 * sizeof(unsigned long long)));
     PT_CUDA(ctx, cudaMemset(ctx->work, 0, 16 * sizeof(unsigned long long)));
+    ctx->amb_sink = ctx->work + 6;
     *out = ctx;
     return PT_OK;
 }

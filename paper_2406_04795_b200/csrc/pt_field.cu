@@ -123,7 +123,7 @@ __device__ __forceinline__ double pt_rbf_block_sum(const PtFieldDev& f, const do
 template <int N, int G>
 __global__ void __launch_bounds__(PT_EVAL_THREADS)
 pt_eval_rbf_kernel(PtFieldDev f, PtRowList rows, const double* __restrict__ pts, size_t m_all, double* __restrict__ vals,
-                   int8_t* __restrict__ signs, unsigned long long* work) {
+                   int8_t* __restrict__ signs, unsigned long long* work, unsigned long long* amb) {
     extern __shared__ double tile[];
     const int PB = PT_EVAL_THREADS / G;
     const size_t m = rows.list ? (size_t)*rows.count : m_all;      // optional compacted row list (device-side count)
@@ -142,7 +142,10 @@ pt_eval_rbf_kernel(PtFieldDev f, PtRowList rows, const double* __restrict__ pts,
         double F = f.bias + acc;
         if (f.has_barrier) F -= pt_barrier_value<N>(f, p);
         if (vals) vals[pi] = F;
-        if (signs) signs[pi] = F > 0.0 ? (int8_t)1 : (int8_t)-1;
+        if (signs) {
+            signs[pi] = F > 0.0 ? (int8_t)1 : (int8_t)-1;
+            if (fabs(F) < f.amb_tol) atomicAdd(amb, 1ull);     // rare by construction: no contention
+        }
     }
 }
 
@@ -1140,18 +1143,18 @@ static int pt_eval_launch(pt_ctx* ctx, const pt_field* f, const double* pts, siz
             }
             PT_LAUNCH(ctx, "eval_rbf");
             const PtRowList sub{list.p, cnt.p};
-            pt_eval_rbf_kernel<N, 4><<<pt_grid_for(m, PT_EVAL_THREADS / 4), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, sub, pts, m, nullptr, signs, ctx->work);
+            pt_eval_rbf_kernel<N, 4><<<pt_grid_for(m, PT_EVAL_THREADS / 4), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, sub, pts, m, nullptr, signs, ctx->work, ctx->amb_sink);
             return pt_check_launch(ctx, "pt_eval_rbf_kernel");
         }
     }
     const int G = pt_pick_group(ctx, m, f->d.S);
     PT_LAUNCH(ctx, "eval_rbf");
     if (G == 1)
-        pt_eval_rbf_kernel<N, 1><<<pt_grid_for(m, PT_EVAL_THREADS), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, none, pts, m, vals, signs, ctx->work);
+        pt_eval_rbf_kernel<N, 1><<<pt_grid_for(m, PT_EVAL_THREADS), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, none, pts, m, vals, signs, ctx->work, ctx->amb_sink);
     else if (G == 4)
-        pt_eval_rbf_kernel<N, 4><<<pt_grid_for(m, PT_EVAL_THREADS / 4), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, none, pts, m, vals, signs, ctx->work);
+        pt_eval_rbf_kernel<N, 4><<<pt_grid_for(m, PT_EVAL_THREADS / 4), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, none, pts, m, vals, signs, ctx->work, ctx->amb_sink);
     else
-        pt_eval_rbf_kernel<N, 32><<<pt_grid_for(m, PT_EVAL_THREADS / 32), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, none, pts, m, vals, signs, ctx->work);
+        pt_eval_rbf_kernel<N, 32><<<pt_grid_for(m, PT_EVAL_THREADS / 32), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, none, pts, m, vals, signs, ctx->work, ctx->amb_sink);
     return pt_check_launch(ctx, "pt_eval_rbf_kernel");
 }
 
@@ -1492,6 +1495,7 @@ static int pt_field_build_rbf(pt_ctx* ctx, int n, long long S, const double* sup
         cudaStreamSynchronize(ctx->stream);
         memcpy(&f->d.smax, &bits[0], sizeof(double));
         memcpy(&f->sum_abs_w, &bits[1], sizeof(double));
+        f->d.amb_tol = 1e-12 * (f->sum_abs_w + fabs(bias));
         f->d.sv32 = f->sv32.p;
         // tensor-core screen operand, when the whole packed support set fits one CTA's shared memory
         const char* tc_env = getenv("PERMATRACE_B200_TC");

@@ -15,6 +15,8 @@ struct PtFieldDev {
     int row32;             // floats per fp32 row (multiple of 4)
     double smax;           // max_j |s_j| (enters the fp32 error bound)
     double gamma, bias;
+    double amb_tol;        // 1e-12*(sum|w| + |bias|): below it a sign is "ambiguous" (the reference's own cross-backend
+                           // tolerance on the kernel sum, pkg/tests/test_backends.py:81-93); such vertices are counted
     int has_barrier;
     double b_scale, b_gain;
     double b_lo[PT_NMAX], b_hi[PT_NMAX];

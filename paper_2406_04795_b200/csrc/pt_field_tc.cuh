@@ -155,13 +155,15 @@ __device__ __forceinline__ double pt_barrier_fast(const PtFieldDev& f, const dou
 #pragma unroll
         for (int side = 0; side < 2; ++side) {
             const float v = (float)((side ? (p[d] - f.b_hi[d]) : (f.b_lo[d] - p[d])) * inv_scale);
-            const float t = __logf(1.f + __expf(-fabsf(v)));     // log1p(exp(-|v|)), absolute error < 3 u32
+            const float t = __logf(1.f + __expf(-fabsf(v)));     // log1p(exp(-|v|)): __expf <= 4 u32 abs, 1+e 2 u32, __logf on [1,2] 2^-21.41 = 6 u32
             acc += fmaxf(v, 0.f) + t;
             mag += 1.f + fmaxf(v, 0.f);
         }
     }
     const double gs = f.b_gain * f.b_scale;
-    err = 8.0 * PT_U32 * gs * (double)mag;
+    // per term: 12 u32 (t) + u32*v (conversion) <= 13 u32 (1 + max(v,0)); the 4N fp32 additions round at u32 of a partial
+    // sum <= mag each, whichever term dominates and wherever it enters the sum: (13 + 4N) u32 mag in all; 16 + 4N is used
+    err = (16.0 + 4.0 * N) * PT_U32 * gs * (double)mag;
     return gs * (double)acc;
 }
 
@@ -390,7 +392,8 @@ pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __res
                 const double rel = 1.01 * (PT_TC_ARG_ULPS * PT_U32 * gl * pn * pn * PT_LN2) + 80.0 * PT_U32;
                 const double E = 2.0 * rel * ab + eb + 1e-280;
                 if (MODE == 2) {
-                    if (active && fabs(F) > E) sign_certain = F > 0.0 ? (int8_t)1 : (int8_t)-1;
+                    // + amb_tol: a vertex within the ambiguity band of zero always reaches the fp64 kernel, which counts it
+                    if (active && fabs(F) > E + f.amb_tol) sign_certain = F > 0.0 ? (int8_t)1 : (int8_t)-1;
                     active = false;
                 } else if (active) {
                     if (fabs(F) > E) {

@@ -31,6 +31,9 @@ struct pt_ctx {
     // device-side work counters: [0] bisection field evaluations (rows x iterations), [1] points evaluated
     unsigned long long* work = nullptr;
     long long retry_evals = 0;           // snapshot taken by pt_ctx_work_counters
+    // where the sign evaluator counts ambiguous vertices (|F| < 1e-12*(sum|w|+|b|)); work + 6 unless a trace / refinement
+    // points it at its own counter block for the duration of a call (PtAmbScope)
+    unsigned long long* amb_sink = nullptr;
     // size-bucketed cache of device blocks (all work is ordered on `stream`, so a freed block can be handed
     // out again at once): after the first step the hot path makes no driver allocation calls at all
     std::multimap<size_t, void*> free_blocks;
@@ -122,6 +125,13 @@ int pt_copy_out(pt_ctx* ctx, T* dst, const T* src_dev, size_t count, bool sync =
     if (sync) PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     return PT_OK;
 }
+
+// redirect the ambiguous-sign counter for the lifetime of the scope
+struct PtAmbScope {
+    pt_ctx* ctx; unsigned long long* prev;
+    PtAmbScope(pt_ctx* c, unsigned long long* sink) : ctx(c), prev(c->amb_sink) { c->amb_sink = sink; }
+    ~PtAmbScope() { ctx->amb_sink = prev; }
+};
 
 // profiler: bracket one launch with events when ctx->profiling
 struct PtProfScope {

@@ -20,6 +20,7 @@ struct PtFineCounters {
     unsigned long long n_pending;   // fine vertices queued for evaluation
     unsigned long long n_edges;     // distinct fine edges inserted
     unsigned long long undecided;   // dedup round bookkeeping
+    unsigned long long ambiguous;   // fine vertices with |F| < 1e-12*(sum|w|+|b|)
     unsigned int error;
     unsigned int pad;
 };
@@ -704,7 +705,10 @@ static int pt_refine_impl(pt_ctx* ctx, const pt_field* field, const pt_cells* ce
                     pt_ref_pending_points_kernel<<<pt_grid_for(np, 256), 256, 0, ctx->stream>>>(rg, fvt.view(), pending.p, np, pts.p);
                     PT_TRY(pt_check_launch(ctx, "pt_ref_pending_points_kernel"));
                 }
-                PT_TRY(pt_field_eval_dev(ctx, field, pts.p, np, nullptr, sg.p));
+                {
+                    PtAmbScope amb(ctx, &ctr.p->ambiguous);
+                    PT_TRY(pt_field_eval_dev(ctx, field, pts.p, np, nullptr, sg.p));
+                }
                 {
                     PT_LAUNCH(ctx, "refine_pending_store");
                     pt_ref_pending_store_kernel<<<pt_grid_for(np, 256), 256, 0, ctx->stream>>>(fvt.view(), pending.p, np, sg.p);
@@ -723,6 +727,8 @@ static int pt_refine_impl(pt_ctx* ctx, const pt_field* field, const pt_cells* ce
         }
     }
     PT_CUDA(ctx, cudaMemsetAsync(ccount.p + C, 0, sizeof(unsigned long long), ctx->stream));
+    PT_TRY(pt_read_fine_counters(ctx, ctr.p, &hc, rg));     // final ambiguous-sign count of pass 1
+    r->stats.ambiguous_signs = (long long)hc.ambiguous;
     {
         size_t tb = 0;
         cub::DeviceScan::ExclusiveSum(nullptr, tb, ccount.p, coff.p, (long long)(C + 1), ctx->stream);

@@ -375,7 +375,10 @@ static int pt_eval_pending(pt_trace* t, const uint32_t* pending, size_t count) {
         pt_pending_points_kernel<<<pt_grid_for(count, 256), 256, 0, ctx->stream>>>(t->geom, t->signs.view(), pending, count, pts.p);
         PT_TRY(pt_check_launch(ctx, "pt_pending_points_kernel"));
     }
-    PT_TRY(pt_field_eval_dev(ctx, t->field, pts.p, count, nullptr, sg.p));
+    {
+        PtAmbScope amb(ctx, &t->counters.p->ambiguous);
+        PT_TRY(pt_field_eval_dev(ctx, t->field, pts.p, count, nullptr, sg.p));
+    }
     {
         PT_LAUNCH(ctx, "trace_pending_store");
         pt_pending_store_kernel<<<pt_grid_for(count, 256), 256, 0, ctx->stream>>>(t->signs.view(), pending, count, sg.p);
@@ -843,6 +846,7 @@ int pt_trace_get_stats(pt_trace* t, pt_trace_stats* out) {
     out->table_capacity = (long long)t->visited.capacity;
     out->sign_table_capacity = (long long)t->signs.capacity;
     out->n_stages = (long long)(t->stages.size() / 5);
+    out->ambiguous_signs = (long long)t->host_counters.ambiguous;
     return PT_OK;
 }
 

@@ -8,6 +8,7 @@ struct PtCounters {
     unsigned long long dropped;      // dropped_out_of_box (cumulative)
     unsigned long long candidates;   // (edge, coface) records (cumulative)
     unsigned long long markers;      // cell_edges stage outputs (cumulative)
+    unsigned long long ambiguous;    // evaluated vertices with |F| < 1e-12*(sum|w|+|b|) (cumulative)
     unsigned int error;              // PT_ERR_* bits
     unsigned int pad;
 };

@@ -117,6 +117,10 @@ class SolveParams:
     knn: int = 10
     max_edges: int = 10_000_000
     trace_margin: float | None = None
+    # not in the reference: at most this many free points of one iteration go back into the roadmap (an even spread over
+    # the refinement order).  None = all of them, the reference's behaviour.  At 5-6 DoF one early iteration can return
+    # 10^5-10^6 free points, and every roadmap vertex is a support vector of the next classifier.
+    feedback_cap: int | None = None
 
     def __post_init__(self):
         if self.lam <= 0 or self.k < 1 or self.eps <= 0:
@@ -480,7 +484,10 @@ def solve(problem: Problem, params: SolveParams | None = None):
         record["free_points"] = int(refined.free_points.shape[0])
         if refined.free_points.shape[0]:
             # the zero set still touches free space: feed those configurations back into the roadmap
-            insert_free_points(roadmap, refined.free_points, dedup_tol=params.lam / 4.0)
+            feedback = refined.free_points
+            if params.feedback_cap is not None and feedback.shape[0] > params.feedback_cap:
+                feedback = feedback[np.linspace(0, feedback.shape[0] - 1, params.feedback_cap).astype(np.int64)]
+            record["fed_back"] = insert_free_points(roadmap, feedback, dedup_tol=params.lam / 4.0)
             continue
         if refined.points.shape[0] == 0:
             record["skip"] = "empty refinement"

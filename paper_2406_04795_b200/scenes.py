@@ -11,7 +11,7 @@ from __future__ import annotations
 
 import numpy as np
 
-__all__ = ["arm_robot_dict", "arm_scene_dict", "synthetic_support", "BENCH_CONFIGS"]
+__all__ = ["arm_robot_dict", "arm_scene_dict", "synthetic_support", "BENCH_CONFIGS", "fence_problem_dict", "PROOF_CONFIGS"]
 
 
 def arm_robot_dict(dof: int, limit: float = 1.5, link: float = 0.4, spheres_per_link: int = 4,
@@ -72,4 +72,54 @@ BENCH_CONFIGS = {
     "dof6-s4096": dict(n=6, support=4096, lam=0.35, r_split=1.3, obstacles=8),
     # the support-set size the SURVEY expects for real 6-DoF proofs (10^3..10^4 roadmap samples): 8 support chunks
     "dof6-s16384": dict(n=6, support=16384, lam=0.35, r_split=1.3, obstacles=8),
+}
+
+
+# ---- infeasible 4/5/6-DoF problems (BASELINE.json configs 3-4: "full infeasibility proof") ------------------------------
+def fence_problem_dict(dof: int, clutter: int = 6, seed: int = 11, q1_limit: float = 2.4, limit: float = 1.2,
+                       link: float = 0.4, radius: float = 0.06) -> dict:
+    """The reference's arm3wall pattern (permatrace/scenes/arm3wall.yaml) extended to `dof` joints: the base link must
+    sweep past a radial fence on the +x axis to get from pointing +y to pointing -y, and joint 1 stops short of a full
+    turn, so there is no way around.  The fence only ever touches link 1 (it is low and close to the base), so the
+    blocked region is a slab in q1 for every posture of the other joints; `clutter` further boxes / cylinders / spheres sit
+    where the distal links reach them, which dents the free space without reconnecting it.  Returns a problem-file dict in
+    the reference's schema (`pipeline.problem_file_from_dict`, reference pipeline.py:120-168)."""
+    joints = []
+    for j in range(dof):
+        joints.append({
+            "type": "revolute",
+            "axis": [0, 0, 1] if j % 2 == 0 else [0, 1, 0],
+            "origin": {"xyz": [0.0 if j == 0 else link, 0.0, 0.0], "rpy": [0, 0, 0]},
+            "limits": [-q1_limit, q1_limit] if j == 0 else [-limit, limit],
+        })
+    spheres = [{"link": j, "offset": [link * s / 4, 0.0, 0.0], "radius": radius}
+               for j in range(1, dof + 1) for s in range(1, 5)]
+    obstacles = [{"type": "box", "size": [0.18, 0.30, 0.20], "origin": {"xyz": [0.31, 0.0, 0.0], "rpy": [0, 0, 0]}}]
+    rng = np.random.default_rng(seed)
+    reach = link * dof
+    for i in range(clutter):
+        # a shell the distal links sweep through, kept away from the base so that link 1 never meets it
+        ang, height = rng.uniform(-np.pi, np.pi), rng.uniform(-0.5, 0.5) * reach
+        rad = rng.uniform(0.62, 0.95) * reach
+        origin = {"xyz": [float(rad * np.cos(ang)), float(rad * np.sin(ang)), float(height)],
+                  "rpy": [float(v) for v in rng.uniform(-0.5, 0.5, size=3)]}
+        kind = i % 3
+        if kind == 0:
+            obstacles.append({"type": "box", "size": [float(v) for v in rng.uniform(0.15, 0.35, size=3)], "origin": origin})
+        elif kind == 1:
+            obstacles.append({"type": "cylinder", "height": float(rng.uniform(0.3, 0.6)), "radius": float(rng.uniform(0.08, 0.16)),
+                              "origin": origin})
+        else:
+            obstacles.append({"type": "sphere", "radius": float(rng.uniform(0.1, 0.2)), "origin": origin})
+    start = [0.5 * np.pi] + [0.0] * (dof - 1)
+    goal = [-0.5 * np.pi] + [0.0] * (dof - 1)
+    return {"robot": {"joints": joints, "spheres": spheres}, "scene": {"obstacles": obstacles},
+            "problem": {"start": start, "goal": goal}}
+
+
+# name -> (problem generator arguments, SolveParams overrides) of the end-to-end proof workloads
+PROOF_CONFIGS = {
+    "dof4-proof": dict(dof=4, clutter=3, params=dict(lam=0.2, k=2, gamma=1.0, samples_per_iter=1500, seeds=20)),
+    "dof5-proof": dict(dof=5, clutter=5, params=dict(lam=0.25, k=2, gamma=0.75, samples_per_iter=3000, seeds=20)),
+    "dof6-proof": dict(dof=6, clutter=7, params=dict(lam=0.3, k=2, gamma=0.5, samples_per_iter=6000, seeds=20)),
 }

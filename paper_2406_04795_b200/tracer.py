@@ -93,6 +93,9 @@ class TraceStats:
     closure_ok: bool = False
     polyline_closed: bool | None = None
     stages: list[StageStat] = field(default_factory=list)
+    # not in the reference: evaluated vertices with |F| < 1e-12*(sum|w|+|bias|), the reference's own cross-backend
+    # tolerance on the kernel sum (pkg/tests/test_backends.py:81-93); only such a vertex can change the traced set
+    ambiguous_signs: int = 0
 
 
 class _TraceHandle:
@@ -165,7 +168,7 @@ class _TraceHandle:
         return TraceStats(
             levels=int(st.levels), seeds=int(st.seeds), visited_edges=int(st.visited_edges),
             field_evaluations=int(st.field_evaluations), dropped_out_of_box=int(st.dropped_out_of_box),
-            complete=bool(st.complete), closure_ok=bool(st.closure_ok),
+            complete=bool(st.complete), closure_ok=bool(st.closure_ok), ambiguous_signs=int(st.ambiguous_signs),
             stages=[StageStat(_STAGE_NAMES[int(r[0])], int(r[1]), int(r[2]), int(r[3]), int(r[4])) for r in rows],
         )
 

@@ -13,6 +13,7 @@ from __future__ import annotations
 import os
 import sys
 from pathlib import Path
+from types import SimpleNamespace
 
 import numpy as np
 
@@ -262,6 +263,56 @@ def refine_analytic_golden(out):
         out[f"template_n{n}_k{k}_e"] = t.edges.astype(np.int16)
 
 
+# ---- refine at n = 5 / 6 (the benchmarked dimension): REAL reference on cell subsets --------------------
+def cells_sha(cb, cp):
+    """Digest of a sorted cell list: sha256 over the int16 bases followed by the uint8 permutations."""
+    import hashlib
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(cb, dtype=np.int16).tobytes())
+    h.update(np.ascontiguousarray(cp, dtype=np.uint8).tobytes())
+    return h.hexdigest()
+
+
+def refine_hd_golden(out):
+    """subdivision.refine of the real reference (eps-dedup with its 3^n neighbour scan and the collision labels
+    included) on three contiguous runs -- first / middle / last -- of the sorted coarse cells of the n = 5 and n = 6
+    learned traces, ONE CELL PER BATCH so that per-cell crossing counts and per-cell fresh-point counts are pinned
+    too; plus the digest of the FULL n = 6 coarse_cells list."""
+    for tag, (n, S, lam, r, nobs, run) in {"kclf_n5": (5, 1024, 0.4, 0.9, 8, 130),
+                                           "kclf_n6": (6, 1024, 0.45, 1.3, 8, 110)}.items():
+        m, cfg, seeds = learned_manifold(n, S, lam, r)
+        res = rt.trace(seeds, m, cfg)
+        cells = rs.coarse_cells(res)
+        cb, cp = cell_arrays(cells, n)
+        out[f"{tag}_cells_count"] = np.array([len(cells)])
+        out[f"{tag}_cells_sha256"] = np.array([cells_sha(cb, cp)])
+        out[f"{tag}_cells_digest"] = np.array([int(cb.sum()), int((cp.astype(np.int64) * np.arange(1, n + 1)).sum())])
+        # cells of the first 3000 traced edges only: small enough for the pure-Python oracle in the CPU suite
+        head = rs.coarse_cells(SimpleNamespace(edges=res.edges[:3000]))
+        hb, hp = cell_arrays(head, n)
+        out[f"{tag}_cells_head3000"] = np.array([len(head)])
+        out[f"{tag}_cells_head3000_sha256"] = np.array([cells_sha(hb, hp)])
+        mid = len(cells) // 2
+        pick = list(range(run)) + list(range(mid - run // 2, mid - run // 2 + run)) + list(range(len(cells) - run, len(cells)))
+        subset = [cells[i] for i in pick]
+        robot, scene = robot_scene(n, nobs)
+        checker = _not_free_checker(_Prob(robot, scene))
+        template = rs.build_template(n, 2)
+        ref = rs.refine(subset, template, m, checker, cfg, memory_budget=rs._cell_bytes(template))
+        whole = rs.refine(subset, template, m, checker, cfg)
+        assert np.array_equal(ref.points, whole.points) and np.array_equal(ref.in_collision, whole.in_collision)
+        assert len(ref.batch_stats) == len(subset)
+        print(tag, "cells", len(cells), "subset", len(subset), "crossings", sum(b.crossing_edges for b in ref.batch_stats),
+              "points", ref.points.shape[0], "free", ref.free_points.shape[0])
+        out[f"{tag}_pick"] = np.asarray(pick, dtype=np.int64)
+        sb, sp = cell_arrays(subset, n)
+        out[f"{tag}_sub_base"], out[f"{tag}_sub_perm"] = sb.astype(np.int16), sp
+        out[f"{tag}_sub_per_cell"] = np.array([[b.crossing_edges, b.new_points] for b in ref.batch_stats], dtype=np.int32)
+        out[f"{tag}_sub_points"] = ref.points
+        out[f"{tag}_sub_labels"] = ref.in_collision
+        out[f"{tag}_sub_eps_dedup"] = np.array([ref.eps_dedup])
+
+
 # ---- collision -----------------------------------------------------------------------------------------
 def collision_golden(out):
     rng = np.random.default_rng(5)
@@ -440,7 +491,7 @@ def solve_golden(out):
 
 def main():
     print("reference backend:", permatrace.BACKEND, "from", permatrace.__file__)
-    sections = {"lattice": lattice_golden, "traces": trace_golden, "refine": refine_analytic_golden,
+    sections = {"lattice": lattice_golden, "traces": trace_golden, "refine": refine_analytic_golden, "refine_hd": refine_hd_golden,
                 "collision": collision_golden, "backend": backend_golden, "proof": proof_golden, "solve": solve_golden}
     only = sys.argv[1:] or list(sections)
     for name in only:

@@ -349,6 +349,93 @@ def test_refine_vs_oracle_4d_subset(golden):
     assert sum(b.crossing_edges for b in out.batch_stats) == sum(want["crossing_edges"])
 
 
+# ---- refine / eps-dedup / labels at n = 5 and n = 6 (the benchmarked dimension) -------------------------------------
+def _cells_sha(cb, cp):
+    import hashlib
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(cb, dtype=np.int16).tobytes())
+    h.update(np.ascontiguousarray(cp, dtype=np.uint8).tobytes())
+    return h.hexdigest()
+
+
+def _device_problem(n, nobs):
+    rd, sd = robot_scene_dicts(n, nobs)
+
+    class Prob:
+        robot, scene = CO.robot_from_dict(rd), CO.scene_from_dict(sd)
+    return Prob, oracle_model(rd, sd)
+
+
+@pytest.mark.parametrize("tag", ["kclf_n5", "kclf_n6"])
+def test_refine_high_dim_vs_reference(golden, tag):
+    """The REAL reference's refine (tests/golden/refine_hd.npz, generated by make_golden.py) of the first / middle /
+    last runs of sorted coarse cells at n = 5 and n = 6, one cell per batch: per-cell crossing counts, per-cell fresh
+    points of the greedy eps-dedup (3^n neighbour buckets, order-dependent: SURVEY hard part 3), kept points in the
+    reference's order, collision labels (8 primitives incl. cylinders and spheres).  subdivision.py:195-217, :256-278."""
+    g, gh = golden("traces"), golden("refine_hd")
+    inp = trace_inputs(g, tag)
+    n = inp["n"]
+    m, cfg = product_manifold(g, tag), product_cfg(inp)
+    cells = L.cells_from_arrays(gh[f"{tag}_sub_base"].astype(np.int32), gh[f"{tag}_sub_perm"])
+    Prob, _ = _device_problem(n, 8)
+    template = S.build_template(n, 2)
+    out = S.refine(cells, template, m, P.not_free_checker(Prob), cfg, memory_budget=S._cell_bytes(template))
+    rows = np.array([[b.crossing_edges, b.new_points] for b in out.batch_stats])
+    assert np.array_equal(rows, gh[f"{tag}_sub_per_cell"])
+    want = gh[f"{tag}_sub_points"]
+    assert out.points.shape == want.shape
+    assert np.allclose(out.points, want, rtol=POINT_RTOL, atol=POINT_ATOL)
+    assert np.array_equal(out.in_collision, gh[f"{tag}_sub_labels"])
+    assert out.eps_dedup == float(gh[f"{tag}_sub_eps_dedup"][0])
+    # the same cells inside the full job: every kept point of the subset run that the full run also keeps sits at
+    # the same place; the full run's cell list equals the reference's (sha256 over the sorted (base, perm) arrays)
+    res = T.trace(inp["seeds"], m, cfg)
+    full = S.coarse_cells(res)
+    cb, cp = full.arrays()
+    assert len(full) == int(gh[f"{tag}_cells_count"][0])
+    assert _cells_sha(cb, cp) == str(gh[f"{tag}_cells_sha256"][0])
+    pick = gh[f"{tag}_pick"]
+    assert np.array_equal(cb[pick], gh[f"{tag}_sub_base"]) and np.array_equal(cp[pick], gh[f"{tag}_sub_perm"])
+
+
+@pytest.mark.parametrize("workload,run", [("dof5", 90), ("dof6", 70)])
+def test_refine_bench_workloads_vs_oracle(workload, run):
+    """The bench workloads themselves (dof5: cylinders + spheres; dof6: the headline config): first / middle / last runs
+    of the sorted coarse cells refined on the CUDA path and by the oracle, one cell per batch."""
+    from bench import build_workload
+    wl = build_workload(workload)
+    a = wl.arrays
+    res = T.trace(wl.seeds, wl.manifold, wl.cfg)
+    cells = S.coarse_cells(res)
+    cb, cp = cells.arrays()
+    mid = len(cells) // 2
+    pick = np.r_[0:run, mid - run // 2:mid - run // 2 + run, len(cells) - run:len(cells)]
+    sub = L.cells_from_arrays(cb[pick], cp[pick])
+    checker = P.not_free_checker(wl.problem)
+    out = S.refine(sub, wl.template, wl.manifold, checker, wl.cfg, memory_budget=S._cell_bytes(wl.template))
+    scale, gain, lo, hi = a.barrier
+    of = O.Field.rbf(a.support, a.weights, a.gamma, a.bias, barrier=(scale, gain, lo, hi))
+    robot, scene = oracle_model(a.robot_dict, a.scene_dict)
+    O.THREADS = min(os.cpu_count() or 1, 16)
+    try:
+        want = O.refine([(c.base, c.parts) for c in sub], O.build_template(a.n, a.k), of,
+                        lambda p: O.not_free(robot, scene, p), a.coarse, np.zeros(a.n), a.k, a.eps, batch_cells=1)
+    finally:
+        O.THREADS = 1
+    rows = np.array([[b.crossing_edges, b.new_points] for b in out.batch_stats])
+    assert np.array_equal(rows[:, 0], want["crossing_edges"]) and np.array_equal(rows[:, 1], want["new_points"])
+    assert rows[:, 0].sum() > 20 * run
+    assert out.points.shape == want["points"].shape
+    assert np.allclose(out.points, want["points"], rtol=POINT_RTOL, atol=POINT_ATOL)
+    assert np.array_equal(out.in_collision, want["in_collision"])
+    # the capped oracle BFS reproduces the head of the device's ordered edge list (admission order, tracer.py:359-375)
+    cap = 1500
+    tr = O.Trace(of, a.n, a.coarse, None, a.box, cap, a.eps).run(a.seeds)
+    base, mask, _ = res.edges.arrays()
+    ob = np.array([e[0] for e in tr.edges]); om = np.array([sum(1 << d for d in e[1][0]) for e in tr.edges])
+    assert len(tr.edges) == cap and np.array_equal(ob, base[:cap]) and np.array_equal(om, mask[:cap])
+
+
 # ---- collision ---------------------------------------------------------------------------------------------
 @pytest.mark.parametrize("n,nobs", [(3, 3), (4, 3), (5, 8), (6, 8)])
 def test_collision(golden, n, nobs):

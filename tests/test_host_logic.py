@@ -46,6 +46,26 @@ def test_no_gpu_fails_loudly():
         P.backend.rbf_values(np.zeros((1, 2)), np.zeros((1, 2)), np.zeros(1), 1.0, 0.0)
 
 
+
+def test_reference_arm_never_maps_the_product_library():
+    """`bench.py --impl reference` builds its workload and runs the CPU sample without importing the product package or
+    mapping libpermatrace_b200.so (the driver watches which .so files each arm loads)."""
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import bench\n"
+        "bench.CPU_RUNS, bench.CPU_RUN_LEN = 2, 3\n"
+        "info = bench.cpu_sample('dof3', 2, max_edges=60, runs=2, run_len=3, prefer_reference=False)\n"
+        "assert info['kind'] == 'port' and info['coarse_edges'] == 60 and info['cells_refined'] == 6\n"
+        "maps = open('/proc/self/maps').read()\n"
+        "assert 'libpermatrace_b200' not in maps, 'product library mapped by the reference arm'\n"
+        "assert not any(m.startswith('paper_2406_04795_b200') for m in sys.modules), 'product package imported'\n"
+        "print('clean')\n" % str(REPO))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "clean" in out.stdout, out.stderr[-2000:]
+
+
 def test_product_never_imports_the_oracle():
     for path in (REPO / "paper_2406_04795_b200").rglob("*"):
         if path.suffix in (".py", ".cu", ".cuh", ".h", ".sh") and path.is_file():

@@ -185,6 +185,52 @@ def test_refine_learned_with_collision(golden):
     assert out["new_points"] == list(rows[:, 3])
 
 
+# ---- refine at n = 5 / 6: the oracle against the REAL reference's refine of cell subsets ---------------
+def cells_sha(cb, cp):
+    import hashlib
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(cb, dtype=np.int16).tobytes())
+    h.update(np.ascontiguousarray(cp, dtype=np.uint8).tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.parametrize("tag", ["kclf_n5", "kclf_n6"])
+def test_refine_high_dim_subsets(golden, tag):
+    """subdivision.py:220-301 at the benchmarked dimensions: per-cell crossing counts, per-cell fresh points (the
+    greedy eps-dedup over 3^n neighbour buckets, order-dependent), kept points and collision labels of the first /
+    middle / last runs of sorted coarse cells, exactly as the reference produced them (one cell per batch)."""
+    g, gh = golden("traces"), golden("refine_hd")
+    n = g[f"{tag}_support"].shape[1]
+    cells = [(tuple(int(v) for v in b), tuple((int(p),) for p in perm) + ((n,),))
+             for b, perm in zip(gh[f"{tag}_sub_base"], gh[f"{tag}_sub_perm"])]
+    robot, scene = oracle_model(*robot_scene_dicts(n, 8))
+    lat = g[f"{tag}_lattice"]
+    out = O.refine(cells, O.build_template(n, 2), oracle_field(g, tag), lambda p: O.not_free(robot, scene, p),
+                   float(lat[1]), lat[2:2 + n], 2, 1e-9, batch_cells=1)
+    rows = gh[f"{tag}_sub_per_cell"]
+    assert out["crossing_edges"] == list(rows[:, 0])
+    assert out["new_points"] == list(rows[:, 1])
+    want = gh[f"{tag}_sub_points"]
+    assert out["points"].shape == want.shape
+    assert np.allclose(out["points"], want, rtol=0, atol=1e-8)
+    assert np.array_equal(out["in_collision"], gh[f"{tag}_sub_labels"])
+    assert out["eps_dedup"] == float(gh[f"{tag}_sub_eps_dedup"][0])
+
+
+@pytest.mark.parametrize("tag", ["kclf_n5", "kclf_n6"])
+def test_coarse_cells_high_dim_head(golden, tag):
+    """coarse_cells (subdivision.py:132-141) of the first 3000 traced edges at n = 5 / 6: sha256 of the sorted list."""
+    g, gh = golden("traces"), golden("refine_hd")
+    n = g[f"{tag}_edge_base"].shape[1]
+    edges = [(tuple(int(v) for v in b), parts_of_mask(int(m), n))
+             for b, m in zip(g[f"{tag}_edge_base"][:3000], g[f"{tag}_edge_mask"][:3000])]
+    cells = O.coarse_cells(edges)
+    assert len(cells) == int(gh[f"{tag}_cells_head3000"][0])
+    base = np.array([c[0] for c in cells])
+    perm = np.array([[p[0] for p in c[1][:-1]] for c in cells])
+    assert cells_sha(base, perm) == str(gh[f"{tag}_cells_head3000_sha256"][0])
+
+
 # ---- collision -----------------------------------------------------------------------------------
 @pytest.mark.parametrize("n,nobs", [(3, 3), (4, 3), (5, 8), (6, 8)])
 def test_collision(golden, n, nobs):
