@@ -60,6 +60,9 @@ int pt_ctx_work_counters(pt_ctx* ctx, long long* out, int reset);
 /* fp64 field evaluations spent in proof retries of the root solve (rows whose first enclosure attempt failed),
  * as of the last pt_ctx_work_counters call */
 long long pt_ctx_retry_evaluations(pt_ctx* ctx);
+/* root solves (edges) that went through the one-pass Taylor-model kernel (csrc/pt_field_taylor.cuh), and of those the
+ * ones it left to the evaluation-based kernels: out[3] of pt_ctx_work_counters; as of the last pt_ctx_work_counters call */
+long long pt_ctx_taylor_rows(pt_ctx* ctx);
 /* DFMA-chain microbenchmark: measured FP64 peak of this device in TFLOP/s (roofline denominator) */
 double pt_peak_fp64(pt_ctx* ctx);
 /* MUFU.EX2 microbenchmark: measured special-function peak in T ex2/s (roofline denominator of the fp32 screen) */

@@ -71,6 +71,7 @@ _SIGS = {
     "pt_ctx_launch_count": (_ll, [_vp]),
     "pt_ctx_work_counters": (_i, [_vp, _vp, _i]),
     "pt_ctx_retry_evaluations": (C.c_longlong, [_vp]),
+    "pt_ctx_taylor_rows": (C.c_longlong, [_vp]),
     "pt_peak_fp64": (_d, [_vp]),
     "pt_peak_ex2": (_d, [_vp]),
     "pt_rbf_values": (_i, [_vp, _vp, _ll, _i, _vp, _ll, _vp, _d, _d, _vp]),

@@ -288,11 +288,13 @@ int pt_ctx_work_counters(pt_ctx* ctx, long long* out, int reset) {
     PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     for (int i = 0; i < 6; ++i) out[i] = (long long)h[i];
     ctx->retry_evals = (long long)h[8];          // the proof retries count into a second bank (work + 8)
+    ctx->taylor_rows = (long long)h[7];          // rows that went through the one-pass Taylor-model kernel
     if (reset) PT_CUDA(ctx, cudaMemsetAsync(ctx->work, 0, sizeof(h), ctx->stream));
     return PT_OK;
 }
 
 long long pt_ctx_retry_evaluations(pt_ctx* ctx) { return ctx ? ctx->retry_evals : -1; }
+long long pt_ctx_taylor_rows(pt_ctx* ctx) { return ctx ? ctx->taylor_rows : -1; }
 
 double pt_peak_ex2(pt_ctx* ctx) {
     if (!ctx) return -1.0;

@@ -24,6 +24,10 @@ struct pt_field {
     bool tc_resident = false;    // ... and the whole support set fits one CTA's shared memory (persistent kernel)
     bool tc_levels = false;      // force the level-synchronous driver (PERMATRACE_B200_TC_LEVELS=1)
     bool tc4 = false;            // n = 6 and the 5-chunk operand + four A buffers fit: four row groups per CTA
+    // one-pass Taylor-model root solve (pt_field_taylor.cuh): sign-sorted rows with log2|w| folded into the exponent
+    PtBuf<double> svt;
+    long long t_pos = 0, t_tot = 0;
+    bool taylor = false;
 };
 
 int pt_field_dim(const pt_field* f) { return f->d.n; }
@@ -600,6 +604,8 @@ pt_bisect_resolve_kernel(PtFieldDev f, PtRows rows, const double* __restrict__ a
 #ifndef PT_NEWTON_MINB
 #define PT_NEWTON_MINB 4
 #endif
+
+#include "pt_field_taylor.cuh"
 
 // two points per thread, each lane walks all support rows (G = 1): the row loads and the loop overhead are shared
 // by four independent chains (2 rows x 2 points), so the FP64 pipe rather than the issue slot is the limiter
@@ -1268,10 +1274,23 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
         else KERNEL<N, 32><<<grid, PT_EVAL_THREADS, SMEM, ctx->stream>>>(__VA_ARGS__);              \
         PT_TRY(pt_check_launch(ctx, #KERNEL));                                                      \
     } while (0)
+    // batches that fill the machine take the one-pass Taylor-model kernel: it either finishes a row or leaves a valid
+    // dyadic bracket (flag 1: no enclosure, flag 2: root enclosed) for the evaluation-based kernels below
+    const bool use_taylor = f->taylor && m >= (size_t)ctx->sm_count * 4 * PT_TAYLOR_THREADS;
     // batches that fill the machine screen on the tensor cores (tcgen05), small ones on the SIMT kernel
     const bool use_tc = f->tc_ok && m >= (size_t)PT_TC_M * 32;
     const bool by_level = use_tc && (!f->tc_resident || f->tc_levels);
-    {
+    if (use_taylor) {
+        PT_LAUNCH(ctx, "bisect_fp64_taylor");
+        PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PT_TAYLOR_SMEM(N)));
+        PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        static const int no_tail = getenv("PERMATRACE_B200_TAYLOR_NOTAIL") ? atoi(getenv("PERMATRACE_B200_TAYLOR_NOTAIL")) : 0;   // timing experiments only
+        const PtTaylorDev td{f->svt.p, f->t_pos, f->t_tot};
+        pt_bisect_taylor_kernel<N><<<pt_grid_for(m, PT_TAYLOR_THREADS), PT_TAYLOR_THREADS, PT_TAYLOR_SMEM(N), ctx->stream>>>(
+            f->d, td, m, a, b, sa, eps, out, lo.p, hi.p, slow.p, jlo.p, jhi.p, ctx->work, no_tail);
+        PT_TRY(pt_check_launch(ctx, "pt_bisect_taylor_kernel"));
+    }
+    if (!use_taylor) {
         PT_LAUNCH(ctx, use_tc ? "bisect_fp32_screen_tc" : "bisect_fp32_screen");
         if (by_level) PT_TRY((pt_screen_levels_launch<N>(ctx, f, all, a, b, sa, eps, 1, lo.p, hi.p)));
         else if (use_tc) PT_TRY((pt_screen_tc_launch<N, 0>(ctx, f, all, a, b, sa, eps, 1, lo.p, hi.p, nullptr)));
@@ -1288,7 +1307,7 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
     PT_CUDA(ctx, cudaMemsetAsync(ncnt.p, 0, PT_NEWTON_RETRIES * sizeof(unsigned long long), ctx->stream));
     bool screen_pays = true;
     uint32_t* lcur = list.p; uint32_t* lnext = list_b.p;
-    for (int round = 0; round < (screen_pays ? 2 : PT_RESOLVE_ROUNDS); ++round) {
+    for (int round = 0; !use_taylor && round < (screen_pays ? 2 : PT_RESOLVE_ROUNDS); ++round) {
         unsigned long long* c = cnt.p + round;
         const PtRows prev = round == 0 ? all : PtRows{lcur, cnt.p + round - 1, m};
         uint32_t* lout = round == 0 ? lcur : lnext;
@@ -1330,7 +1349,7 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
             else if (Gn == 4) pt_bisect_newton_kernel<N, 4><<<grid, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, ROWS, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, retry_ratio, ctx->work); \
             else pt_bisect_newton_kernel<N, 32><<<grid, PT_EVAL_THREADS, smem_nt, ctx->stream>>>(f->d, f->sum_abs_w, ROWS, a, b, sa, lo.p, hi.p, eps, out, slow.p, jlo.p, jhi.p, retry_ratio, ctx->work);       \
         } while (0)
-        {
+        if (!use_taylor) {
             PT_LAUNCH(ctx, "bisect_fp64_newton");
             PT_NEWTON_LAUNCH(all);
             PT_TRY(pt_check_launch(ctx, "pt_bisect_newton_kernel"));
@@ -1497,6 +1516,39 @@ static int pt_field_build_rbf(pt_ctx* ctx, int n, long long S, const double* sup
         memcpy(&f->sum_abs_w, &bits[1], sizeof(double));
         f->d.amb_tol = 1e-12 * (f->sum_abs_w + fabs(bias));
         f->d.sv32 = f->sv32.p;
+        // sign-sorted rows of the Taylor-model root solve (stable partition by an exclusive scan of the sign flags)
+        {
+            const char* ty_env = getenv("PERMATRACE_B200_TAYLOR");
+            if (!(ty_env && ty_env[0] == '0') && f->precision != 0) {
+                PtBuf<unsigned> flag, rank; PtBuf<uint8_t> tmp;
+                size_t tb = 0;
+                rc = flag.alloc(ctx, (size_t)S);
+                if (rc == PT_OK) rc = rank.alloc(ctx, (size_t)S);
+                if (rc != PT_OK) { delete f; return rc; }
+                pt_taylor_flag_kernel<<<pt_grid_for((size_t)S, 256), 256, 0, ctx->stream>>>(wdev, S, flag.p);
+                cub::DeviceScan::ExclusiveSum(nullptr, tb, flag.p, rank.p, (long long)S, ctx->stream);
+                rc = tmp.alloc(ctx, tb);
+                if (rc != PT_OK) { delete f; return rc; }
+                cub::DeviceScan::ExclusiveSum(tmp.p, tb, flag.p, rank.p, (long long)S, ctx->stream);
+                unsigned last[2] = {0, 0};
+                cudaMemcpyAsync(&last[0], rank.p + (S - 1), sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream);
+                cudaMemcpyAsync(&last[1], flag.p + (S - 1), sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream);
+                cudaStreamSynchronize(ctx->stream);
+                const long long n_pos = (long long)last[0] + (long long)last[1], n_neg = S - n_pos;
+                f->t_pos = (n_pos + 1) & ~1ll;
+                f->t_tot = f->t_pos + ((n_neg + 1) & ~1ll);
+                const int rowt = (n + 2) & ~1;
+                rc = f->svt.alloc(ctx, (size_t)f->t_tot * rowt);
+                if (rc != PT_OK) { delete f; return rc; }
+                const long long span = f->t_tot > S ? f->t_tot : S;
+                pt_taylor_pack_kernel<<<pt_grid_for((size_t)span, 256), 256, 0, ctx->stream>>>(sdev, wdev, S, n, rowt, gamma * PT_L2E, flag.p,
+                                                                                              rank.p, f->t_pos, f->t_tot, f->svt.p);
+                rc = pt_check_launch(ctx, "pt_taylor_pack_kernel");
+                if (rc != PT_OK) { delete f; return rc; }
+                cudaStreamSynchronize(ctx->stream);
+                f->taylor = true;
+            }
+        }
         // tensor-core screen operand, when the whole packed support set fits one CTA's shared memory
         const char* tc_env = getenv("PERMATRACE_B200_TC");
         if (!(tc_env && tc_env[0] == '0') && n <= 6) {

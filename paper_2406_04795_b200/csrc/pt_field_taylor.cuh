@@ -1,0 +1,442 @@
+// One-pass root solve of intersection_points_batch (reference manifold.py:351-383) for large batches.
+//
+// Along an edge q(t) = a + t*diff every kernel term is e_j * exp(u_j tau) * exp(c tau^2) with tau = t - 1/2,
+//   e_j = |w_j| exp(-gamma |q(1/2) - s_j|^2),  u_j = -2 gamma (q(1/2) - s_j).diff,  c = -gamma |diff|^2,
+// so ONE fp64 pass over the support set that accumulates the moments  M_k = sum_j sgn(w_j) e_j u_j^k  (k < Q) and the
+// absolute moments  MA_k = sum_j e_j |u_j|^k  (k even, k <= Q)  yields a polynomial model of the field on the WHOLE edge,
+//   F(t) = exp(c tau^2) * [ sum_{k<Q} M_k tau^k / k!  +  R(tau) ] + bias - barrier(q(t)),   |R| <= fac * MA_Q |tau|^Q / Q!,
+// with rigorous bounds on truncation, on the rounding of this pass and on the evaluation noise of the reference's own
+// loop (all relative to sum_j e_j exp(|u_j tau|) <= 2 sum_{k even} MA_k tau^k / k!).  The reference's bisection is then
+// replayed on the model: a midpoint is decided when |model| exceeds the bound; once the bracket is narrow enough for a
+// proof of monotonicity the root of the model is polished by Newton steps, enclosed (mean-value bound with a proven
+// lower bound on |F'|), and the remaining bisection steps are replayed in exact dyadic arithmetic exactly like
+// pt_bisect_newton_kernel does.  Rows that cannot be decided keep their (valid, dyadic) bracket and go on to the
+// evaluation-based kernels: flag 1 = no enclosure (proof retries / plain bisection), flag 2 = root enclosed in J,
+// a midpoint inside J needs a true evaluation.
+//
+// Cost per (edge, support vector) pair: (N+1) + 8 + N + 3 + 1.25 Q + 1 FP64 instructions = 50 at N = 6, Q = 20 --
+// against 45 for the two passes of the Newton kernel PLUS about eight fp32 screen levels, resolves and retries before.
+// The support set streams through shared memory in tiles, so its size is not limited by one CTA's shared memory.
+#pragma once
+
+#define PT_TAYLOR_Q 20
+#define PT_TAYLOR_THREADS 128
+#define PT_TAYLOR_TILE 256
+#define PT_TAYLOR_TRY_WIDTH 0.0625     /* first enclosure attempt once the bracket is this narrow (in t) */
+
+template <int N> struct PtRowT { static const int value = (N + 2) & ~1; };   // 2*gl*s_d (N), c'_s, pad to an even count
+
+struct PtTaylorDev {
+    const double* svt;     // [s_tot][ROWT] rows sorted by the sign of the weight: positive block (padded to even), negative block
+    long long s_pos;       // rows of the positive block (even)
+    long long s_tot;       // all rows (even)
+};
+
+#define PT_TAYLOR_SMEM(N) ((size_t)((PT_TAYLOR_TILE + 1) * PtRowT<N>::value + PT_EXP_TAB + (PT_TAYLOR_Q + 1 + PT_TAYLOR_Q / 2) * PT_TAYLOR_THREADS + 2 + 2 * PT_NMAX) * sizeof(double))
+
+// pack the sign-sorted rows: dest index from an exclusive scan of the "weight >= 0" flags (stable, deterministic)
+__global__ void pt_taylor_flag_kernel(const double* __restrict__ weights, long long S, unsigned* __restrict__ flag) {
+    long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < S) flag[j] = weights[j] >= 0.0 ? 1u : 0u;
+}
+
+__global__ void pt_taylor_pack_kernel(const double* __restrict__ support, const double* __restrict__ weights, long long S, int n,
+                                      int row, double gl, const unsigned* __restrict__ flag, const unsigned* __restrict__ rank,
+                                      long long s_pos_pad, long long s_tot_pad, double* __restrict__ svt) {
+    long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= s_tot_pad) return;
+    if (j < S) {
+        const long long dst = flag[j] ? (long long)rank[j] : s_pos_pad + (j - (long long)rank[j]);
+        double s2 = 0.0;
+        for (int d = 0; d < n; ++d) {
+            const double v = support[j * n + d];
+            svt[dst * row + d] = (2.0 * gl) * v;
+            s2 = fma(v, v, s2);
+        }
+        // log2|w| folded into the constant of the exponent: the term is 2^(c' + c_p + q.s') = |w| k(q, s)
+        svt[dst * row + n] = fma(-gl, s2, log2(fabs(weights[j])));
+        for (int d = n + 1; d < row; ++d) svt[dst * row + d] = 0.0;
+    }
+    // pad rows (at most one per block): exponent -inf, i.e. a zero term
+    const long long n_pos = (long long)rank[S - 1] + (long long)flag[S - 1];
+    const long long n_neg = S - n_pos;
+    long long pad = -1;
+    if (j == 0 && (n_pos & 1)) pad = n_pos;
+    if (j == 1 && (n_neg & 1)) pad = s_pos_pad + n_neg;
+    if (pad >= 0) {
+        for (int d = 0; d < row; ++d) svt[pad * row + d] = 0.0;
+        svt[pad * row + n] = -1.0 / 0.0;
+    }
+}
+
+// one (edge, support row) pair: exponent, exponential, first log-derivative, and the Q+1 moment updates.
+// `sx` = 0 in the positive block, 0x80000000 in the negative one (the sign of the weight, applied by an integer XOR).
+template <int N, int Q>
+__device__ __forceinline__ void pt_taylor_pair(const double* __restrict__ row, const PtPoint64<N>& pp, double pdu,
+                                               const double (&ddu)[N], const double* __restrict__ tab, int sx, double (&acc)[Q + 1]) {
+    double arg = row[N] + pp.cp, u = pdu;
+#pragma unroll
+    for (int d = 0; d < N; ++d) { arg = fma(pp.q[d], row[d], arg); u = fma(ddu[d], row[d], u); }
+    const double ea = pt_exp2_neg(arg, tab);
+    double pw = __hiloint2double(__double2hiint(ea) ^ sx, __double2loint(ea));
+    const double u2 = u * u, u3 = u2 * u, u4 = u2 * u2;
+#pragma unroll
+    for (int k = 0; k < Q; k += 4) {
+        acc[k] += pw;
+        acc[k + 1] = fma(pw, u, acc[k + 1]);
+        acc[k + 2] = fma(pw, u2, acc[k + 2]);
+        acc[k + 3] = fma(pw, u3, acc[k + 3]);
+        pw *= u4;
+    }
+    acc[Q] += fabs(pw);
+}
+
+// front half of a pair: the term e = |w| k(q(1/2), s) (sign applied) and its first log-derivative u
+template <int N>
+__device__ __forceinline__ void pt_taylor_front(const double* __restrict__ row, const PtPoint64<N>& pp, double pdu,
+                                                const double (&ddu)[N], const double* __restrict__ tab, int sx, double& e, double& u) {
+    double arg = row[N] + pp.cp;
+    u = pdu;
+#pragma unroll
+    for (int d = 0; d < N; ++d) { arg = fma(pp.q[d], row[d], arg); u = fma(ddu[d], row[d], u); }
+    const double ea = pt_exp2_neg(arg, tab);
+    e = __hiloint2double(__double2hiint(ea) ^ sx, __double2loint(ea));
+}
+
+// back half: the Q+1 moment updates
+template <int Q>
+__device__ __forceinline__ void pt_taylor_back(double pw, double u, double (&acc)[Q + 1]) {
+    const double u2 = u * u, u3 = u2 * u, u4 = u2 * u2;
+#pragma unroll
+    for (int k = 0; k < Q; k += 4) {
+        acc[k] += pw;
+        acc[k + 1] = fma(pw, u, acc[k + 1]);
+        acc[k + 2] = fma(pw, u2, acc[k + 2]);
+        acc[k + 3] = fma(pw, u3, acc[k + 3]);
+        pw *= u4;
+    }
+    acc[Q] += fabs(pw);
+}
+
+// Software-pipelined over the support rows: the (serial) exponent / exponential chain of row j+1 is issued next to the
+// (parallel) moment updates of row j.  The tile carries one zero pad row behind the last one for the final look-ahead.
+template <int N, int Q>
+__device__ __forceinline__ void pt_taylor_block(const double* __restrict__ svt, long long r0, long long r1, double* tile,
+                                                const double* tab, const PtPoint64<N>& pp, double pdu, const double (&ddu)[N],
+                                                int sx, double (&acc)[Q + 1]) {
+    constexpr int ROW = PtRowT<N>::value;
+    for (long long t0 = r0; t0 < r1; t0 += PT_TAYLOR_TILE) {
+        const long long rem = r1 - t0;
+        const int cnt = rem < PT_TAYLOR_TILE ? (int)rem : PT_TAYLOR_TILE;     // even by construction
+        __syncthreads();
+        const double2* src = reinterpret_cast<const double2*>(svt + t0 * ROW);
+        double2* dst = reinterpret_cast<double2*>(tile);
+        for (int i = threadIdx.x; i < cnt * ROW / 2; i += PT_TAYLOR_THREADS) dst[i] = src[i];
+        if (threadIdx.x < ROW) tile[cnt * ROW + threadIdx.x] = 0.0;
+        __syncthreads();
+        double e0, u0, e1, u1;
+        pt_taylor_front<N>(tile, pp, pdu, ddu, tab, sx, e0, u0);
+#pragma unroll 1
+        for (int j = 0; j < cnt; j += 2) {
+            pt_taylor_front<N>(tile + (j + 1) * ROW, pp, pdu, ddu, tab, sx, e1, u1);
+            pt_taylor_back<Q>(e0, u0, acc);
+            pt_taylor_front<N>(tile + (j + 2) * ROW, pp, pdu, ddu, tab, sx, e0, u0);
+            pt_taylor_back<Q>(e1, u1, acc);
+        }
+    }
+}
+
+// ---- per-row tail: small non-inlined helpers with rolled loops (the tail is executed divergently, a few thousand
+// instructions per row; kept compact so that it stays in the instruction cache next to the hot loop) -----------------
+
+// p(tau) = sum_{k<Q} c_k tau^k, p'(tau) and exp(c tau^2); coefficients in a shared-memory column (stride PT_TAYLOR_THREADS)
+template <int Q>
+__device__ __noinline__ void pt_taylor_model(const double* col, double c, double tau, double* p_out, double* dp_out, double* ex_out) {
+    double p = col[(Q - 1) * PT_TAYLOR_THREADS], dp = 0.0;
+#pragma unroll 1
+    for (int k = Q - 2; k >= 0; --k) { dp = fma(dp, tau, p); p = fma(p, tau, col[k * PT_TAYLOR_THREADS]); }
+    *p_out = p; *dp_out = dp; *ex_out = exp(c * tau * tau);
+}
+
+// 2 * [ sum_{k even < Q} ca_k tau^k + fac * ca_Q tau^Q ]  >=  sum_j e_j exp(|u_j tau|)
+template <int Q>
+__device__ __noinline__ double pt_taylor_cosh(const double* cola, double caQ_fac, double tau) {
+    const double t2 = tau * tau;
+    double s = caQ_fac;
+#pragma unroll 1
+    for (int k = Q / 2 - 1; k >= 0; --k) s = fma(s, t2, cola[k * PT_TAYLOR_THREADS]);
+    return 2.002 * s;
+}
+
+__device__ __noinline__ double pt_powi(double x, int k) {
+    double r = 1.0;
+    while (k) { if (k & 1) r *= x; x *= x; k >>= 1; }
+    return r;
+}
+
+// barrier(q(t)) and its first two t-derivatives along q(t) = a + t*diff; bp = {scale, gain, lo[n], hi[n]} in shared
+// memory, geo = per-thread {a[n], diff[n]}.  One exp + log1p + division per term; a few ulps from the reference's
+// logaddexp, far inside the 64 u |B| the bounds allow for it.
+__device__ __noinline__ void pt_taylor_barrier(const double* bp, const double* geo, int n, double t, double* B, double* B1, double* B2) {
+    const double sc = bp[0], gain = bp[1];
+    double acc = 0.0, b1 = 0.0, b2 = 0.0;
+#pragma unroll 1
+    for (int i = 0; i < 2 * n; ++i) {
+        const int d = i >> 1;
+        const double q = __dadd_rn(geo[d], __dmul_rn(t, geo[n + d]));
+        const double x = (i & 1) ? (q - bp[2 + n + d]) / sc : (bp[2 + d] - q) / sc;      // hi side / lo side
+        const double e = exp(-fabs(x));
+        acc += fmax(x, 0.0) + log1p(e);
+        const double sg = (x > 0.0 ? 1.0 : e) / (1.0 + e);                                // sigmoid(x)
+        const double dq = (i & 1) ? geo[n + d] : -geo[n + d];                             // d x / d t * scale
+        b1 = fma(dq, sg, b1);
+        b2 = fma(dq * dq, sg * (1.0 - sg), b2);
+    }
+    *B = gain * sc * acc; *B1 = gain * b1; *B2 = gain / sc * b2;
+}
+
+// upper bound of the barrier anywhere on the edge: softplus(x) <= exp(x), each coordinate at its worst end
+__device__ __noinline__ double pt_taylor_barrier_max(const double* bp, const double* geo, int n) {
+    const double sc = bp[0], gain = bp[1];
+    double acc = 0.0;
+#pragma unroll 1
+    for (int d = 0; d < n; ++d) {
+        const double q0 = geo[d], q1 = geo[d] + geo[n + d];
+        const double xl = (bp[2 + d] - fmin(q0, q1)) / sc, xh = (fmax(q0, q1) - bp[2 + n + d]) / sc;
+        acc += (xl > 0.0 ? xl + 0.6931471805599453 : exp(xl)) + (xh > 0.0 ? xh + 0.6931471805599453 : exp(xh));
+    }
+    return 1.0001 * gain * sc * acc;
+}
+
+template <int N>
+__global__ void __launch_bounds__(PT_TAYLOR_THREADS, 4)
+pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, size_t m, const double* __restrict__ a_, const double* __restrict__ b_,
+                        const int8_t* __restrict__ signs_a, double eps, double* __restrict__ out, double* __restrict__ lo_io,
+                        double* __restrict__ hi_io, uint8_t* __restrict__ slow, double* __restrict__ jlo_out,
+                        double* __restrict__ jhi_out, unsigned long long* work, int debug_no_tail) {
+    constexpr int Q = PT_TAYLOR_Q, ROW = PtRowT<N>::value, TH = PT_TAYLOR_THREADS;
+    extern __shared__ double sm[];
+    double* tile = sm;
+    double* tab = tile + (PT_TAYLOR_TILE + 1) * ROW;
+    double* col = tab + PT_EXP_TAB + threadIdx.x;          // c_k at col[k*TH], k < Q;  RQ-independent
+    double* cola = col + (Q + 1) * TH;                     // ca_k (k even < Q) at cola[(k/2)*TH]
+    pt_exp_table_init(tab);
+    if (threadIdx.x < 2 + 2 * N) {
+        double* bpw = tab + PT_EXP_TAB + (Q + 1 + Q / 2) * TH;
+        bpw[threadIdx.x] = threadIdx.x == 0 ? f.b_scale : threadIdx.x == 1 ? f.b_gain
+                         : threadIdx.x < 2 + N ? f.b_lo[threadIdx.x - 2] : f.b_hi[threadIdx.x - 2 - N];
+    }
+    const size_t ei = (size_t)blockIdx.x * TH + threadIdx.x;
+    const bool valid = ei < m;
+    double a[N], diff[N];
+    double seg = 0.0;
+    int sa = 1;
+#pragma unroll
+    for (int d = 0; d < N; ++d) { a[d] = 0.0; diff[d] = 0.0; }
+    if (valid) {
+        double b[N];
+#pragma unroll
+        for (int d = 0; d < N; ++d) { a[d] = a_[ei * N + d]; b[d] = b_[ei * N + d]; }
+        seg = pt_segment<N>(a, b, diff);
+        sa = signs_a[ei];
+    }
+    const double seg2 = seg * seg;
+    double mnorm2 = 0.0;
+    {
+        // ---- the pass over the support set: moments about the edge midpoint ----------------------------------------
+        PtPoint64<N> pp;
+        double mc[N], ddu[N], md = 0.0;
+#pragma unroll
+        for (int d = 0; d < N; ++d) {
+            mc[d] = fma(0.5, diff[d], a[d]);
+            md = fma(mc[d], diff[d], md);
+            ddu[d] = diff[d] * PT_LN2;                     // rows hold 2*gamma*log2e*s_d
+            mnorm2 = fma(mc[d], mc[d], mnorm2);
+        }
+        pp.set(mc, f.gamma * PT_L2E);
+        const double pdu = -2.0 * f.gamma * md;
+        double acc[Q + 1];
+#pragma unroll
+        for (int k = 0; k <= Q; ++k) acc[k] = 0.0;
+        pt_taylor_block<N, Q>(tf.svt, 0, tf.s_pos, tile, tab, pp, pdu, ddu, 0, acc);
+#pragma unroll
+        for (int k = 0; k < Q; k += 2) cola[(k / 2) * TH] = acc[k];        // even moments of the positive block
+        pt_taylor_block<N, Q>(tf.svt, tf.s_pos, tf.s_tot, tile, tab, pp, pdu, ddu, (int)0x80000000, acc);
+        double inv_fact = 1.0;
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+            if (k > 1) inv_fact /= (double)k;
+            col[k * TH] = (acc[k] + pp.poison) * inv_fact;
+            if ((k & 1) == 0) cola[(k / 2) * TH] = fabs(2.0 * cola[(k / 2) * TH] - acc[k]) * inv_fact;   // MA_k / k!
+        }
+        col[Q * TH] = acc[Q] * (inv_fact / (double)Q);                      // MA_Q / Q!
+    }
+    if (!valid) return;
+
+    // ---- per-row constants of the bounds --------------------------------------------------------------------------
+    const double c = -f.gamma * seg2;
+    const double ac = fabs(c);
+    const double mn = sqrt(mnorm2);
+    const double pn = mn + f.smax + 0.5 * seg;
+    const double T = f.gamma * PT_L2E * pn * pn;
+    const double gmaxu = 2.0 * f.gamma * seg * (mn + f.smax);
+    const double xmax = 0.5 * gmaxu;
+    const bool model_ok = xmax < 0.8 * (double)(Q + 1);
+    const double fac = 1.0 / (1.0 - xmax / (double)(Q + 1));
+    const double caQ = col[Q * TH];
+    const double ca0 = cola[0];
+    const double RQ = fac * (1.01 * caQ + 1e-40 * ca0);                     // |R(tau)| <= RQ |tau|^Q
+    const double Ctot = PT_U64 * (1.01 * (double)(4 * N + 7) * T * PT_LN2 + 2.3 * (double)f.S + 4.0 * Q
+                                  + (double)(N + 2) * gmaxu + 450.0);
+    const double abias = fabs(f.bias);
+    const double* bp = tab + PT_EXP_TAB + (Q + 1 + Q / 2) * TH;              // barrier parameters (shared)
+    double geo[2 * N];                                                      // dynamically indexed by the helpers
+#pragma unroll
+    for (int d = 0; d < N; ++d) { geo[d] = a[d]; geo[N + d] = diff[d]; }
+    double bsum = 0.0, Bmax = 0.0;                                          // |B'| <= bsum, 0 <= B <= Bmax on the edge
+    if (f.has_barrier) {
+#pragma unroll
+        for (int d = 0; d < N; ++d) bsum += fabs(diff[d]);
+        bsum *= f.b_gain;
+        Bmax = pt_taylor_barrier_max(bp, geo, N);
+    }
+
+    double L = 0.0, H = 1.0;
+    int flag = 1;                 // 0 done, 1 no enclosure, 2 enclosed with open midpoints
+    double Jlo = -1e300, Jhi = 1e300;
+    double D2max = -1.0;
+    if (model_ok && !debug_no_tail) {
+#pragma unroll 1
+        for (;;) {
+            if (!(__dmul_rn(seg, __dsub_rn(H, L)) > eps)) { flag = 0; break; }
+            const double mq = __dmul_rn(0.5, __dadd_rn(L, H));
+            const double tau = mq - 0.5;
+            const double at = fabs(tau);
+            double p, dp, ex, B = 0.0, B1 = 0.0, B2 = 0.0;
+            pt_taylor_model<Q>(col, c, tau, &p, &dp, &ex);
+            const double Ach = pt_taylor_cosh<Q>(cola, fac * caQ, at);
+            const double Ek = 1.001 * ex * (RQ * pt_powi(at, Q) + Ctot * Ach) + 1e-290;
+            const double g0 = fma(ex, p, f.bias);
+            // the barrier is only evaluated when the decision needs it (0 <= B <= Bmax)
+            const double Eb0 = 64.0 * PT_U64 * (1.1 * Bmax + abias);
+            int sgn = 0;
+            if (g0 - Bmax > Ek + Eb0) sgn = 1;
+            else if (g0 < -(Ek + Eb0)) sgn = -1;
+            else if (f.has_barrier) {
+                pt_taylor_barrier(bp, geo, N, mq, &B, &B1, &B2);
+                const double g = g0 - B;
+                if (fabs(g) > Ek + 64.0 * PT_U64 * (1.1 * fabs(B) + abias)) sgn = g > 0.0 ? 1 : -1;
+            }
+            if (sgn == 0) break;                                          // undecided: keep [L, H]
+            if (sgn == sa) L = mq; else H = mq;
+            const double w = H - L;
+            if (!(w <= PT_TAYLOR_TRY_WIDTH)) continue;
+            if (!(__dmul_rn(seg, w) > eps)) continue;
+            // ---- enclosure attempt on [L, H] ------------------------------------------------------------------------
+            if (D2max < 0.0) {
+                // |F''| anywhere on the edge: polynomial part by absolute coefficients, remainder, rounding, barrier
+                double pm0 = 0.0, pm1 = 0.0, pm2 = 0.0, hk = 1.0;     // hk = 0.5^k
+#pragma unroll 1
+                for (int k = 0; k < Q; ++k) {
+                    const double ck = fabs(col[k * TH]);
+                    pm0 = fma(ck, hk, pm0);
+                    pm1 = fma(ck * (double)k, 2.0 * hk, pm1);
+                    pm2 = fma(ck * (double)(k * (k - 1)), 4.0 * hk, pm2);
+                    hk *= 0.5;
+                }
+                const double hq = pt_powi(0.5, Q);
+                const double r0 = RQ * hq, r1 = RQ * (double)Q * 2.0 * hq, r2 = RQ * (double)(Q * (Q - 1)) * 4.0 * hq;
+                const double Ah = pt_taylor_cosh<Q>(cola, fac * caQ, 0.5);
+                double b2 = 0.0;
+                if (f.has_barrier) {
+#pragma unroll
+                    for (int d = 0; d < N; ++d) b2 = fma(diff[d], diff[d], b2);
+                    b2 *= 0.5 * f.b_gain / f.b_scale;
+                }
+                D2max = 1.01 * ((pm2 + r2) + 2.0 * ac * (pm1 + r1) + (2.0 * ac + ac * ac) * (pm0 + r0)
+                                + 2.0 * Ctot * (gmaxu * gmaxu + 2.0 * ac * (gmaxu + 1.0) + ac * ac) * Ah + b2);
+            }
+            const double tmax = fmax(fabs(L - 0.5), fabs(H - 0.5));
+            const double Amax = pt_taylor_cosh<Q>(cola, fac * caQ, tmax);
+            const double ptq1 = pt_powi(tmax, Q - 1);
+            // |F' - model'| anywhere in the bracket
+            const double Ed = 1.01 * (RQ * (double)Q * ptq1 + 2.0 * ac * tmax * RQ * ptq1 * tmax
+                                      + 1.5 * Ctot * (gmaxu + 2.0 * ac * tmax + 1.0) * Amax);
+            const double xm = 0.5 * (L + H);
+            double Bm = 0.0, B1m = 0.0, B2m = 0.0;
+            pt_taylor_model<Q>(col, c, xm - 0.5, &p, &dp, &ex);
+            if (f.has_barrier) pt_taylor_barrier(bp, geo, N, xm, &Bm, &B1m, &B2m);
+            double gv = fma(ex, p, f.bias) - Bm;
+            double gd = ex * fma(2.0 * c * (xm - 0.5), p, dp) - B1m;
+            const double EdB = Ed + 64.0 * PT_U64 * (fabs(gd) + bsum);
+            const double smin = fabs(gd) - EdB - 0.5 * w * D2max;
+            if (!(smin > 0.0)) continue;                                  // not provably monotone yet: next level
+            // Newton on the model inside (L, H), the barrier replaced by its quadratic expansion about the bracket
+            // midpoint (exact values come back in below)
+            double x = xm;
+#pragma unroll 1
+            for (int it = 0; it < 7; ++it) {
+                double xn = x - gv / gd;
+                if (!(xn > L && xn < H)) xn = 0.5 * (xn > x ? x + H : x + L);
+                const bool conv = fabs(xn - x) <= 1e-13;
+                x = xn;
+                const double sft = x - xm;
+                pt_taylor_model<Q>(col, c, x - 0.5, &p, &dp, &ex);
+                gv = fma(ex, p, f.bias) - fma(sft, fma(0.5 * B2m, sft, B1m), Bm);
+                gd = ex * fma(2.0 * c * (x - 0.5), p, dp) - fma(B2m, sft, B1m);
+                if (conv) break;
+            }
+            // exact barrier at the surrogate root, one corrected step, exact residual there
+            double Bx = 0.0, B1x = 0.0, B2x = 0.0;
+            if (f.has_barrier) {
+                pt_taylor_barrier(bp, geo, N, x, &Bx, &B1x, &B2x);
+                gv = fma(ex, p, f.bias) - Bx;
+                gd = ex * fma(2.0 * c * (x - 0.5), p, dp) - B1x;
+                double xn = x - gv / gd;
+                if (!(xn > L && xn < H)) xn = x;
+                const double moved = fabs(xn - x);
+                x = xn;
+                pt_taylor_model<Q>(col, c, x - 0.5, &p, &dp, &ex);
+                pt_taylor_barrier(bp, geo, N, x, &Bx, &B1x, &B2x);
+                gv = fma(ex, p, f.bias) - Bx;
+                gd = fmax(fabs(gd) - moved * D2max, 0.0);                  // |model'| at the new x, from below
+            }
+            const double agd = fabs(gd);
+            const double Eb = 64.0 * PT_U64 * (1.1 * (fabs(Bx) + w * bsum) + abias) + 1e-290;
+            const double tx = fabs(x - 0.5);
+            const double Ex = 1.001 * ex * (RQ * pt_powi(tx, Q) + Ctot * pt_taylor_cosh<Q>(cola, fac * caQ, tx)) + Eb;
+            const double eta = 1.001 * (Ctot * Amax) + Eb;                 // evaluation noise anywhere in the bracket
+            const double rho0 = (fabs(gv) + Ex) / smin;                    // |x - root| <= rho0
+            const double delta = rho0 + 2.0 * eta / smin;
+            double sloc = agd - EdB - delta * D2max;                       // |F'| on [x - delta, x + delta]
+            if (!(sloc > smin)) sloc = smin;
+            const double rho = 1.01 * (fabs(gv) + Ex) / sloc + 4e-16;
+            const double zeta = 1.01 * eta / sloc;
+            Jlo = x - rho - zeta; Jhi = x + rho + zeta;
+            bool open = false;
+            while (__dmul_rn(seg, __dsub_rn(H, L)) > eps) {
+                const double mr = __dmul_rn(0.5, __dadd_rn(L, H));
+                if (mr < Jlo) L = mr;
+                else if (mr > Jhi) H = mr;
+                else { open = true; break; }
+            }
+            flag = open ? 2 : 0;
+            break;
+        }
+    }
+    slow[ei] = (uint8_t)flag;
+    if (flag == 0) {
+        const double tf_ = __dmul_rn(0.5, __dadd_rn(L, H));
+#pragma unroll
+        for (int d = 0; d < N; ++d) out[ei * N + d] = __dadd_rn(a[d], __dmul_rn(tf_, diff[d]));
+    } else {
+        lo_io[ei] = L; hi_io[ei] = H;
+        jlo_out[ei] = flag == 2 ? Jlo : -1e300;
+        jhi_out[ei] = flag == 2 ? Jhi : 1e300;
+    }
+    if (flag) atomicAdd(&work[3], 1ull);                                  // rows left to the evaluation-based kernels
+    if (threadIdx.x == 0) {
+        const size_t first = (size_t)blockIdx.x * TH;
+        atomicAdd(&work[7], (unsigned long long)(m - first < (size_t)TH ? m - first : (size_t)TH));
+    }
+}

@@ -31,6 +31,7 @@ struct pt_ctx {
     // device-side work counters: [0] bisection field evaluations (rows x iterations), [1] points evaluated
     unsigned long long* work = nullptr;
     long long retry_evals = 0;           // snapshot taken by pt_ctx_work_counters
+    long long taylor_rows = 0;           // ditto: rows of the one-pass Taylor-model root solve (work[7])
     // where the sign evaluator counts ambiguous vertices (|F| < 1e-12*(sum|w|+|b|)); work + 6 unless a trace / refinement
     // points it at its own counter block for the duration of a call (PtAmbScope)
     unsigned long long* amb_sink = nullptr;

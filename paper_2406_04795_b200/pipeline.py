@@ -11,6 +11,8 @@ from __future__ import annotations
 
 import hashlib
 import json
+import os
+import sys
 import time
 import warnings
 from dataclasses import dataclass, field
@@ -426,7 +428,11 @@ def solve(problem: Problem, params: SolveParams | None = None):
         stats.seconds = time.perf_counter() - t0
         return value
 
+    live_log = os.environ.get("PERMATRACE_B200_SOLVE_LOG", "") not in ("", "0")
     for iteration in range(1, params.max_iters + 1):
+        if live_log and stats.iterations:      # the finished record of the previous iteration, as it happens
+            print(json.dumps({k: (round(v, 4) if isinstance(v, float) else v) for k, v in stats.iterations[-1].items()}),
+                  file=sys.stderr, flush=True)
         record: dict = {"iteration": iteration}
         stats.iterations.append(record)
         if time.perf_counter() > deadline:
@@ -485,6 +491,9 @@ def solve(problem: Problem, params: SolveParams | None = None):
         if refined.free_points.shape[0]:
             # the zero set still touches free space: feed those configurations back into the roadmap
             feedback = refined.free_points
+            if os.environ.get("PERMATRACE_B200_SOLVE_LOG", "") == "2":       # diagnostics only: where the free points are
+                record["free_lo"] = [round(float(v), 3) for v in feedback.min(axis=0)]
+                record["free_hi"] = [round(float(v), 3) for v in feedback.max(axis=0)]
             if params.feedback_cap is not None and feedback.shape[0] > params.feedback_cap:
                 feedback = feedback[np.linspace(0, feedback.shape[0] - 1, params.feedback_cap).astype(np.int64)]
             record["fed_back"] = insert_free_points(roadmap, feedback, dedup_tol=params.lam / 4.0)

@@ -16,6 +16,7 @@ from tests.conftest import (ANALYTIC_TRACES, LEARNED_TRACES, PRISM_ROBOT, PRISM_
                             robot_scene_dicts, trace_inputs)
 
 import os
+from paper_2406_04795_b200 import _cabi
 
 
 @pytest.fixture(autouse=True, params=["fp64", "fast"])
@@ -776,3 +777,74 @@ def test_ill_conditioned_field_root_solve(monkeypatch):
     resid = np.abs(m.values(out["1"][2]))
     from paper_2406_04795_b200.pipeline import _gradient_norms
     assert np.all(resid <= 4.0 * 1e-9 * (_gradient_norms(m, out["1"][2]) + 1e-12) + 1e-9 * np.abs(weights).sum() * 1e-3)
+
+
+# ---- one-pass Taylor-model root solve (pt_field_taylor.cuh) --------------------------------------------------
+def _crossing_segments(m, lo, hi, count, step, rng, max_axes):
+    """Random lattice-like segments (1..max_axes coordinates move by `step`) whose end points have different signs."""
+    n = lo.size
+    a_rows, b_rows, s_rows = [], [], []
+    have = 0
+    while have < count:
+        a = rng.uniform(lo, hi, size=(4 * count, n))
+        axes = rng.integers(1, max_axes + 1, size=a.shape[0])
+        order = np.argsort(rng.random(a.shape), axis=1)                       # a random subset of `axes[i]` coordinates
+        d = (order < axes[:, None]) * (step * rng.choice([-1.0, 1.0], size=(a.shape[0], 1)))
+        b = a + d
+        sa, sb = m.signs(a), m.signs(b)
+        keep = sa != sb
+        a_rows.append(a[keep]); b_rows.append(b[keep]); s_rows.append(sa[keep].astype(np.int8))
+        have += int(keep.sum())
+    return np.concatenate(a_rows)[:count], np.concatenate(b_rows)[:count], np.concatenate(s_rows)[:count]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,S,step,gamma,reg", [(6, 2048, 0.175, 2.0, 1e-3), (4, 1500, 0.15, 2.0, 1e-3), (3, 700, 0.3, 1.0, 1e-3),
+                                                (6, 4096, 0.175, 2.0, 1e-3), (5, 1024, 0.45, 2.0, 1e-5), (7, 512, 0.2, 1.5, 1e-3),
+                                                (2, 300, 0.1, 3.0, 1e-3)])
+def test_taylor_root_solve_equals_plain_bisection(monkeypatch, precision_mode, n, S, step, gamma, reg):
+    """Large batches take the one-pass Taylor-model kernel.  Its brackets are the reference's dyadic brackets, so the points
+    must be BIT-identical to plain fp64 bisection on the same device except where a midpoint value is below the evaluation
+    noise of either implementation (then the neighbouring cell, <= eps away): at most a handful of rows per million."""
+    if precision_mode != "fast":
+        pytest.skip("compares the two modes itself")
+    from paper_2406_04795_b200.scenes import synthetic_support
+    from bench import _train_numpy
+    pos, neg, rng = synthetic_support(n, S, 0.9 if n < 6 else 1.3, 1.5, seed=11 + n)
+    support, weights = _train_numpy(pos, neg, gamma, reg)
+    sigma = 1.0 / np.sqrt(2.0 * gamma)
+    lo, hi = -1.5 * np.ones(n), 1.5 * np.ones(n)
+    eps = 1e-9
+    pts = {}
+    left = [0]
+    for mode, taylor in (("1", "1"), ("0", "1"), ("1", "0")):
+        monkeypatch.setenv("PERMATRACE_B200_PRECISION", mode)
+        monkeypatch.setenv("PERMATRACE_B200_TAYLOR", taylor)
+        m = M.KernelClassifierManifold(support, weights, gamma, 0.3 * np.sqrt(2.0 * gamma),
+                                       barrier=M.BoxBarrier(lo, hi, sigma / 4.0, 2.0 / sigma))
+        if not pts:
+            a, b, sa = _crossing_segments(m, lo - 0.3, hi + 0.3, 160_000, step, np.random.default_rng(n), min(n, 6))
+        work = np.zeros(6, dtype=np.int64)
+        _cabi.check(_cabi.lib.pt_ctx_work_counters(_cabi.context().handle, work.ctypes.data, 1))
+        pts[(mode, taylor)] = M.intersection_points_batch(m, a, b, eps, signs_a=sa)
+        _cabi.check(_cabi.lib.pt_ctx_work_counters(_cabi.context().handle, work.ctypes.data, 1))
+        rows = int(_cabi.lib.pt_ctx_taylor_rows(_cabi.context().handle))
+        assert rows == (len(a) if (mode, taylor) == ("1", "1") else 0)
+        if rows:
+            left[0] = int(work[3])
+    new, plain, old = pts[("1", "1")], pts[("0", "1")], pts[("1", "0")]
+    diff, seg2 = b - a, np.einsum("ij,ij->i", b - a, b - a)
+    tol = 1e-12 * (np.abs(weights).sum() + abs(m.bias))        # the reference's own cross-backend tolerance on F
+    for name, got in (("taylor", new), ("screen+newton", old)):
+        assert np.max(np.abs(got - plain)) <= 2.5e-9
+        rows = np.flatnonzero(np.any(got != plain, axis=1))
+        assert len(rows) <= len(a) // 1000, f"{name}: {len(rows)} of {len(a)} rows differ from plain fp64 bisection"
+        if len(rows):
+            # the two bisections parted at the dyadic midpoint between their final cells: |F| there must be below the noise
+            t1 = np.einsum("ij,ij->i", got[rows] - a[rows], diff[rows]) / seg2[rows]
+            t0 = np.einsum("ij,ij->i", plain[rows] - a[rows], diff[rows]) / seg2[rows]
+            tm = np.round(0.5 * (t0 + t1) * 2.0 ** 40) / 2.0 ** 40
+            disputed = np.abs(m.values(a[rows] + tm[:, None] * diff[rows]))
+            assert np.all(disputed <= tol), f"{name}: a differing row is not ambiguous: |F| = {disputed.max():.3g} > {tol:.3g}"
+        print(f"{name} n={n} S={S}: {len(rows)} of {len(a)} rows differ from plain bisection (all ambiguous)")
+    print(f"taylor n={n} S={S}: {left[0]} of {len(a)} rows left to the evaluation kernels")
