@@ -248,17 +248,36 @@ class ClockSampler:
 # GPU arm
 # ------------------------------------------------------------------------------------------------
 
-# DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the big launch of each kernel, from the
-# `ncu --set full` captures summarised in profiles/r1_v7_*_full.txt (same command, dof6 workload)
-NCU_TRAFFIC = {"bisect_fp64_newton": 206.831104e6 + 76.694016e6, "bisect_fp32_screen_tc": 170.094592e6 + 19.643648e6}
+# DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) and FP64-pipe busy fraction of the big launch of each
+# kernel, from the `ncu --set full` captures summarised under profiles/ (same command, dof6 workload)
+NCU_TRAFFIC = {"bisect_fp64_taylor": 182.006784e6 + 72.592896e6, "bisect_fp64_newton": 206.831104e6 + 76.694016e6,
+               "bisect_fp32_screen_tc": 170.094592e6 + 19.643648e6}
+NCU_SOURCE = {"bisect_fp64_taylor": "profiles/r2_v1_taylor_full.txt", "bisect_fp64_newton": "profiles/r1_v7_newton_full.txt",
+              "bisect_fp32_screen_tc": "profiles/r1_v7_tc4_screen_full.txt"}
+NCU_PIPE_BUSY = {"bisect_fp64_taylor": 0.691, "bisect_fp64_newton": 0.691}
+TAYLOR_Q = 20   # csrc/pt_field_taylor.cuh PT_TAYLOR_Q
+
+
+def pair_dp_ops(n: int, kind: str = "eval") -> tuple[float, float]:
+    """(FP64 instructions, flop) one (point, support vector) pair costs in the device kernels, counted from the SASS of
+    the inner loops (an FMA is one instruction and two flop; nothing is charged for what a library exp would need):
+      eval    exponent in expanded form (1 DADD + n DFMA), 2^x by table + degree-4 polynomial (6 DFMA + 1 DADD + 1 DMUL),
+              weight multiply, accumulate
+      deriv   eval + first and second directional derivative and sum|w|k (Newton pass 1)
+      taylor  exponent, first log-derivative (n DFMA), 2^x, u^2..u^4, and Q+1 moment updates (5 DMUL + 6 DADD + 15 DFMA)"""
+    if kind == "taylor":
+        fma, other = 2.0 * n + 6.0 + 3.0 * TAYLOR_Q / 4.0, 6.0 + TAYLOR_Q / 4.0 + TAYLOR_Q / 4.0 + 1.0
+    elif kind == "deriv":
+        fma, other = 2.0 * n + 6.0 + 4.0, 6.0 + 2.0
+    else:
+        fma, other = n + 6.0, 5.0
+    return fma + other, 2.0 * fma + other
 
 
 def pair_flops(n: int) -> float:
-    """Algorithmic FP64 work of one (point, support vector) pair: n subtractions, n multiply-adds for
-    the squared distance, the gamma scale, one exp, one weighted accumulate = (3n+2) flop + 1 exp
-    (SURVEY.md section 8d).  exp is charged as 22 flop: the range reduction (2 FMA), degree-11
-    polynomial (11 FMA) and 2^k scaling that a correctly rounded double exp needs at minimum."""
-    return 3.0 * n + 2.0 + 22.0
+    """flop of one plain pair evaluation as the kernels issue it (see pair_dp_ops); SURVEY.md section 8d's algorithmic
+    count is (3n+2) flop + 1 exp, the expanded exponent needs n fewer."""
+    return pair_dp_ops(n, "eval")[1]
 
 
 def run_gpu(args):
@@ -293,7 +312,7 @@ def run_gpu(args):
     sharded = None
     if world > 1:
         from paper_2406_04795_b200.distributed import CudaEngine, ShardedProof
-        sharded = ShardedProof(CudaEngine(wl.manifold, wl.cfg, wl.template, checker, device_index=local))
+        sharded = ShardedProof(CudaEngine(wl.manifold, wl.cfg, wl.template, checker, device_index=local), gather_result=False)
 
     def barrier():
         torch.cuda.synchronize()
@@ -307,7 +326,7 @@ def run_gpu(args):
             return pipe.step(seeds_dev.data_ptr(), a.seeds.shape[0])
         res = sharded.run(seeds_dev)
         return {"trace_edges": res["trace_edges"], "cells": res["cells"], "crossing_edges": res["crossing_edges"],
-                "unique_fine_edges": res["candidates"], "points": int(res["points"].shape[0]),
+                "unique_fine_edges": res["candidates"], "points": int(res.get("points_total", res["points"].shape[0])),
                 "free_points": res["free_points"], "closure_ok": res["closure_ok"], "candidates": res["candidates_bfs"],
                 "simplices_local": res["trace_edges"] + res["crossing_edges"], "pair_evals_bisect": 0,
                 "pair_evals_eval": 0, "pair_evals_fp32": 0, "bisect_fallbacks": 0, "pair_evals_rest": 0, "pair_evals_resolve": 0}
@@ -351,12 +370,12 @@ def run_gpu(args):
             print(json.dumps({"metric": METRIC, "value": value, "unit": UNIT, "ms_per_step": ms / args.steps, "kernel_only": True}))
         return None
     def e2e_step_sharded():
-        """N > 1: the multi-GPU public API (distributed.ShardedProof) from host buffers; every rank ends with the
-        merged result and copies it to the host."""
+        """N > 1: the multi-GPU public API (distributed.ShardedProof) from host buffers; every rank copies ITS part of the
+        result (kept points in global order + labels) to the host."""
         from paper_2406_04795_b200.distributed import CudaEngine, ShardedProof
         manifold = P.KernelClassifierManifold(a.support, a.weights, a.gamma, a.bias, barrier=P.BoxBarrier(lo, hi, scale, gain))
         eng = CudaEngine(manifold, wl.cfg, wl.template, checker, device_index=local)
-        out = ShardedProof(eng).run(seeds_pinned.numpy())
+        out = ShardedProof(eng, gather_result=False).run(seeds_pinned.numpy())
         return out, (out["points"].cpu(), out["in_collision"].cpu())
 
     run_e2e = e2e_step if world == 1 else e2e_step_sharded
@@ -394,28 +413,39 @@ def run_gpu(args):
     rows = prof_counts["unique_fine_edges"] + prof_counts["trace_edges"]      # root solves of one step (both batches)
 
     def fp64_roofline(name):
-        """FP64-pipe roofline of a root-solve kernel: algorithmic flop of its pair evaluations / its CUDA-event time."""
+        """FP64-pipe roofline of a root-solve kernel: the flop its inner loop issues for its pair evaluations (SASS counts,
+        pair_dp_ops) / its CUDA-event time, against the DFMA peak measured in this process.  `issue_frac` is the share of
+        FP64 issue slots those instructions fill (an all-FMA stream would make the two equal); `pipe_busy_ncu` the same
+        thing measured by ncu on the kept capture (it also sees the per-row tails)."""
         launches, ms = prof[name]
-        if name == "bisect_fp64_newton":
-            # pass 1 evaluates F, F', F'' (61 flop per pair), pass 2 evaluates F (42 flop per pair)
+        if name == "bisect_fp64_taylor":
+            pe = prof_counts["taylor_rows"] * S
+            ins, flop1 = pair_dp_ops(a.n, "taylor")
+            instr, flop = pe * ins, pe * flop1
+        elif name == "bisect_fp64_newton":
+            # pass 1 evaluates F, F', F'' and sum|w|k, pass 2 evaluates F
             evals = prof_counts["pair_evals_bisect"] // max(S, 1)
             deriv = min(rows, evals)
-            flop = (deriv * (pair_flops(a.n) + 2.0 * a.n + 7.0) + (evals - deriv) * pair_flops(a.n)) * S
+            (i1, f1), (i0, f0) = pair_dp_ops(a.n, "deriv"), pair_dp_ops(a.n, "eval")
+            instr, flop = (deriv * i1 + (evals - deriv) * i0) * S, (deriv * f1 + (evals - deriv) * f0) * S
             pe = prof_counts["pair_evals_bisect"]
         else:
             pe = {"bisect_rbf": prof_counts["pair_evals_bisect"], "eval_rbf": prof_counts["pair_evals_eval"],
                   "bisect_fp64_rest": prof_counts["pair_evals_rest"], "bisect_fp64_resolve": prof_counts["pair_evals_resolve"],
                   "bisect_fp64_retry": prof_counts["pair_evals_retry"]}.get(name, 0)
-            flop = pe * pair_flops(a.n)
+            i0, f0 = pair_dp_ops(a.n, "eval")
+            instr, flop = pe * i0, pe * f0
         achieved = flop / (ms * 1e-3) / 1e12
         peak = engine.measure_fp64_peak(ctx)
         return {"bound": "fp64", "kernel": name, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak if peak else None,
+                "issue_frac": (instr / (ms * 1e-3) / 1e12) / (peak / 2.0) if peak else None,
+                "pipe_busy_ncu": NCU_PIPE_BUSY.get(name) if args.workload == "dof6" else None,
                 "traffic": NCU_TRAFFIC.get(name) if args.workload == "dof6" else None,
-                "traffic_source": "profiles/r1_v7_newton_full.txt (largest launch)" if name in NCU_TRAFFIC else None,
+                "traffic_source": (NCU_SOURCE[name] + " (largest launch)") if name in NCU_TRAFFIC else None,
                 "peak_source": "DFMA microbenchmark run in this process (MEASURED_PEAKS.json holds only HBM and bf16)",
                 "launches": launches, "avg_launch_ms": ms / max(launches, 1), "share_of_step": ms / total_ms,
-                "pair_evals_per_step": pe, "flop_per_pair_eval": pair_flops(a.n)}
+                "pair_evals_per_step": pe, "flop_per_pair_eval": flop / max(pe, 1), "dp_instr_per_pair_eval": instr / max(pe, 1)}
 
     def screen_roofline(name):
         """The fp32 screen does one MUFU ex2 per pair evaluation; that pipe bounds it (the tf32 contraction on the
@@ -428,7 +458,7 @@ def run_gpu(args):
         return {"bound": "mufu_ex2", "kernel": name, "achieved": achieved, "peak": peak, "unit": "T pair-evals/s (1 ex2 each)",
                 "frac": achieved / peak if peak else None,
                 "traffic": NCU_TRAFFIC.get(name) if args.workload == "dof6" else None,
-                "traffic_source": "profiles/r1_v7_tc4_screen_full.txt (largest launch)" if name in NCU_TRAFFIC else None,
+                "traffic_source": (NCU_SOURCE[name] + " (largest launch)") if name in NCU_TRAFFIC else None,
                 "peak_source": "MUFU.EX2 microbenchmark run in this process",
                 "launches": launches, "avg_launch_ms": ms / max(launches, 1), "share_of_step": ms / total_ms,
                 "pair_evals_per_step": pe,
@@ -437,7 +467,7 @@ def run_gpu(args):
     ranked = sorted(prof.items(), key=lambda kv: -kv[1][1])
     roofline, roofline_second = None, None
     for name, _ in ranked:
-        if name in ("bisect_fp64_newton", "bisect_rbf", "eval_rbf", "bisect_fp64_rest", "bisect_fp64_resolve", "bisect_fp64_retry"):
+        if name in ("bisect_fp64_taylor", "bisect_fp64_newton", "bisect_rbf", "eval_rbf", "bisect_fp64_rest", "bisect_fp64_resolve", "bisect_fp64_retry"):
             r = fp64_roofline(name)
         elif name in ("bisect_fp32_screen_tc", "bisect_fp32_screen"):
             r = screen_roofline(name)
@@ -472,7 +502,7 @@ def run_gpu(args):
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_text(a),
-                       "parallelism": "single GPU" if world == 1 else f"owner-hashed BFS (all_to_all per wave) + refine/check sharded over {world} ranks (cell slices), candidate merge by all_gather",
+                       "parallelism": "single GPU" if world == 1 else f"owner-hashed BFS (all_to_all per wave), sample-sorted cell ranges, refine/check and ghost-pinned eps-dedup sharded over {world} ranks",
                        "l2_policy": "per-step working set (hash tables + fine-edge arrays) exceeds the 126 MB L2; "
                                     "all tables are rebuilt from empty every step",
                        "trace_edges": counts["trace_edges"], "coarse_cells": counts["cells"],
@@ -480,7 +510,8 @@ def run_gpu(args):
                        "points_checked": counts["points"], "free_points": counts["free_points"],
                        "closure_ok": counts["closure_ok"], "fp32_screened_pair_evals": counts["pair_evals_fp32"],
                        "fp64_root_solve_pair_evals": counts["pair_evals_bisect"] + counts.get("pair_evals_rest", 0) + counts.get("pair_evals_resolve", 0),
-                       "bisect_fallbacks": counts["bisect_fallbacks"]},
+                       "taylor_model_rows": counts.get("taylor_rows", 0),
+                       "rows_left_to_evaluation_kernels": counts["bisect_fallbacks"]},
             "clocks": clocks.summary(), "e2e": e2e, "gpu_launches": int(launches),
             "roofline": roofline, "roofline_second": roofline_second, "roofline_hbm": hbm, "kernels": kernels, "cpu_baseline": cpu,
             "parity_sample": parity, "ambiguous_signs": counts.get("ambiguous_signs"),
@@ -658,6 +689,108 @@ def run_reference(args):
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+# ------------------------------------------------------------------------------------------------
+# end-to-end proof workloads (BASELINE.json metric, second half: "end-to-end proof time")
+# ------------------------------------------------------------------------------------------------
+PROOF_METRIC = "end_to_end_infeasibility_proof_time"
+
+
+def _proof_problem(name: str):
+    sc = _scenes()
+    conf = sc.PROOF_CONFIGS[name]
+    return conf, sc.fence_problem_dict(conf["dof"], clutter=conf["clutter"], **conf.get("scene", {}))
+
+
+def run_proof(args):
+    """`--workload dofN-proof`: the whole outer loop (reference pipeline.py:284-430) on an infeasible N-DoF fence scene until
+    it returns an InfeasibilityProof that verify_proof accepts: zero free points among the collision-checked points of the
+    closed zero set.  `value` = wall seconds of solve() (roadmap growth, training, seeds, trace, cells, refine, check,
+    feedback, self-verification); one run per step, all steps start from the same seed and must end in the same proof."""
+    import torch
+    import paper_2406_04795_b200 as P
+    from paper_2406_04795_b200 import pipeline as PL
+    conf, pdict = _proof_problem(args.workload)
+    problem = PL.problem_file_from_dict(pdict).problem()
+    params = PL.SolveParams(timeout=1800.0, **conf["params"])
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    times, outs = [], []
+    with ClockSampler(local) as clocks:
+        for i in range(max(args.warmup, 0) + args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            out = PL.solve(problem, params)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                times.append(dt)
+                outs.append(out)
+    out = outs[-1]
+    proved = isinstance(out, PL.InfeasibilityProof)
+    its = out.stats.iterations
+    t1 = time.perf_counter()
+    report = PL.verify_proof(out, problem) if proved else None
+    verify_s = time.perf_counter() - t1
+    simplices = sum(r.get("edges", 0) + r.get("crossing_edges", 0) for r in its)
+    device_s = sum(r.get("trace_s", 0.0) + r.get("refine_s", 0.0) + r.get("train_s", 0.0) for r in its)
+    value = float(np.median(times))
+    same = all(isinstance(o, type(out)) and (not proved or (o.points.shape == out.points.shape and np.array_equal(o.points, out.points)))
+               for o in outs)
+    return {
+        "metric": PROOF_METRIC, "value": value, "unit": "s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{args.workload}: {conf['dof']}-DoF arm behind a radial fence (+{conf['clutter']} clutter primitives), "
+                               f"start/goal on either side; SolveParams {conf['params']}",
+                   "outcome": type(out).__name__, "verified": bool(report.ok) if report else False,
+                   "iterations": len(its), "support_vectors": int(out.manifold.support.shape[0]) if proved else None,
+                   "coarse_edges": out.coarse_edges if proved else None, "coarse_cells": out.coarse_cells if proved else None,
+                   "points_checked_final": int(out.points.shape[0]) if proved else None, "free_points_final": 0 if proved else None,
+                   "free_points_per_iteration": [r.get("free_points") for r in its],
+                   "roadmap_per_iteration": [r.get("roadmap") for r in its],
+                   "repeatable": bool(same)},
+        "clocks": clocks.summary(),
+        "proof_time_s": value, "all_times_s": times, "verify_s": verify_s,
+        "device_share": {"trace_refine_train_s": device_s, "of_solve_s": times[-1]},
+        "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+                "note": "solve() IS the public API: host roadmap, device batches, results back on the host every iteration"},
+        "gpu_launches": int(P.context().launch_count()) if hasattr(P.context(), "launch_count") else None,
+    }
+
+
+def run_reference_proof(args):
+    """Reference arm of a proof workload.  Where the real reference is importable (the build container) its own solve() runs
+    on the 3-DoF twin of the scene (`dof3-proof`; the N >= 4 scenes are out of its reach: ~1e8 pair evaluations/s/core);
+    on the GPU box the oracle port has no outer loop, so the line says so."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    ref = _reference_modules()
+    base = {"impl": "reference", "metric": PROOF_METRIC, "unit": "s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic"}
+    if ref is None:
+        base.update(value=None, ms_per_step=None, unavailable="the reference's outer loop (solve) needs the reference package; "
+                    "the oracle port covers the hot path only -- see profiles/r2_reference_dof3_proof.json for the kept run")
+        return base
+    conf, pdict = _proof_problem("dof3-proof")
+    pf = ref.pl.problem_file_from_dict(pdict)
+    problem = pf.problem()
+    params = ref.pl.SolveParams(timeout=3600.0, **{k: v for k, v in conf["params"].items() if k not in ("feedback_cap",)})
+    t0 = time.perf_counter()
+    out = ref.pl.solve(problem, params)
+    dt = time.perf_counter() - t0
+    proved = type(out).__name__ == "InfeasibilityProof"
+    base.update(value=dt, ms_per_step=dt * 1e3,
+                config={"workload": "dof3-proof (3-DoF twin of the fence scene), the reference's own solve()", "outcome": type(out).__name__,
+                        "iterations": len(out.stats.iterations), "points": int(out.points.shape[0]) if proved else None,
+                        "support_vectors": int(out.manifold.support.shape[0]) if proved else None,
+                        "same_config": args.workload == "dof3-proof"},
+                cpu_baseline={"value": dt, "unit": "s", "cores": 1, "kind": "imported",
+                              "sample": "whole solve() of the 3-DoF twin, backend " + str(getattr(ref.pkg, "BACKEND", "?"))},
+                e2e={"value": dt, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0})
+    return base
+
+
 def workload_text(a) -> str:
     return (f"{a.name}: {a.n}-DoF arm, {len(a.scene_dict['obstacles'])} primitives, S={a.support.shape[0]} support vectors, "
             f"lambda={a.lam}, k={a.k}")
@@ -673,7 +806,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel-only", action="store_true", help="skip the e2e and CPU legs (for ncu captures)")
     args = ap.parse_args()
-    line = run_reference(args) if args.impl == "reference" else run_gpu(args)
+    if args.workload.endswith("-proof"):
+        line = run_reference_proof(args) if args.impl == "reference" else run_proof(args)
+    else:
+        line = run_reference(args) if args.impl == "reference" else run_gpu(args)
     if line is not None:
         print(json.dumps(line))
 

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--reg", type=float, default=None)
     ap.add_argument("--push-mult", type=float, default=None, help="push = mult * lam * sqrt(2 gamma) (reference default: 1)")
     ap.add_argument("--q1-limit", type=float, default=None)
+    ap.add_argument("--limit", type=float, default=None, help="limits of joints 2..n (default 1.2)")
     ap.add_argument("--feedback-cap", type=int, default=None)
     ap.add_argument("--max-iters", type=int, default=30)
     ap.add_argument("--timeout", type=float, default=600.0)
@@ -48,7 +49,11 @@ def main():
     clutter = conf["clutter"] if args.clutter is None else args.clutter
     if args.push_mult is not None:
         over["push"] = args.push_mult * over["lam"] * np.sqrt(2.0 * over["gamma"])
-    extra = {} if args.q1_limit is None else {"q1_limit": args.q1_limit}
+    extra = dict(conf.get("scene", {}))
+    if args.q1_limit is not None:
+        extra["q1_limit"] = args.q1_limit
+    if args.limit is not None:
+        extra["limit"] = args.limit
     pf = PL.problem_file_from_dict(scenes.fence_problem_dict(conf["dof"], clutter=clutter, **extra))
     problem = pf.problem()
     params = PL.SolveParams(max_iters=args.max_iters, timeout=args.timeout, max_edges=args.max_edges, **over)

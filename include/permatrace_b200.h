@@ -228,6 +228,12 @@ int pt_cells_from_host(pt_ctx* ctx, int n, const int32_t* base, const uint8_t* p
                        pt_cells** out);
 /* contiguous sub-range of a cell list (multi-GPU sharding of refine) */
 int pt_cells_slice(const pt_cells* c, long long first, long long count, pt_cells** out);
+/* packed 64-bit keys of cells [first, first+count) (numeric order = the reference's (base, parts) tuple order inside one
+ * key window); `out` may be host or device memory.  With pt_cells_merge_keys -- sort + unique of keys packed in the window
+ * of `like` -- this is what the range-partitioned (sample-sort) build of the sorted cell list across GPUs exchanges
+ * (order contract: reference subdivision.py:141) */
+int pt_cells_keys(const pt_cells* c, long long first, long long count, unsigned long long* out);
+int pt_cells_merge_keys(const pt_cells* like, const unsigned long long* keys, long long count, pt_cells** out);
 void pt_cells_destroy(pt_cells* c);
 long long pt_cells_count(const pt_cells* c);
 int pt_cells_get(const pt_cells* c, long long first, long long count, int32_t* base, uint8_t* perm);
@@ -255,6 +261,11 @@ int pt_refine_candidates(pt_ctx* ctx, const pt_field* field, const pt_cells* cel
                          double eps, pt_refine** out);
 int pt_dedup_label(pt_ctx* ctx, int n, const double* points, long long count, double eps_dedup,
                    const pt_checker* checker, pt_refine** out);
+/* same, with the state of some points given: forced[i] = 1 kept, 0 removed, -1 decide here.  A rank of the sharded
+ * eps-dedup runs it over its own candidates plus ghost copies of its neighbours' boundary points, the ghosts pinned to
+ * their owners' verdicts (distributed.py; the greedy rule of reference subdivision.py:195-217 has one fixed point) */
+int pt_dedup_label_forced(pt_ctx* ctx, int n, const double* points, long long count, double eps_dedup,
+                          const int8_t* forced, const pt_checker* checker, pt_refine** out);
 void pt_refine_destroy(pt_refine* r);
 int pt_refine_get_stats(const pt_refine* r, pt_refine_stats* out);
 /* points[P,n] f64, labels[P] uint8 (1 = not free), first_tag[P] int64 (global crossing index of the

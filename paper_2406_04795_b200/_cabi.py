@@ -113,12 +113,15 @@ _SIGS = {
     "pt_cells_from_edges": (_i, [_vp, _i, _vp, _vp, _ll, _pp]),
     "pt_cells_from_host": (_i, [_vp, _i, _vp, _vp, _ll, _pp]),
     "pt_cells_slice": (_i, [_vp, _ll, _ll, _pp]),
+    "pt_cells_keys": (_i, [_vp, _ll, _ll, _vp]),
+    "pt_cells_merge_keys": (_i, [_vp, _vp, _ll, _pp]),
     "pt_cells_destroy": (None, [_vp]),
     "pt_cells_count": (_ll, [_vp]),
     "pt_cells_get": (_i, [_vp, _ll, _ll, _vp, _vp]),
     "pt_refine_run": (_i, [_vp, _vp, _vp, _i, _d, _vp, _i, _i, _vp, _i, _vp, _d, _d, _vp, _vp, _i, _pp]),
     "pt_refine_candidates": (_i, [_vp, _vp, _vp, _i, _d, _vp, _i, _i, _vp, _i, _vp, _d, _pp]),
     "pt_dedup_label": (_i, [_vp, _i, _vp, _ll, _d, _vp, _pp]),
+    "pt_dedup_label_forced": (_i, [_vp, _i, _vp, _ll, _d, _vp, _vp, _pp]),
     "pt_refine_destroy": (None, [_vp]),
     "pt_refine_get_stats": (_i, [_vp, C.POINTER(RefineStats)]),
     "pt_refine_points": (_i, [_vp, _vp, _vp, _vp]),

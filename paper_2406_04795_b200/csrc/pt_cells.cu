@@ -282,6 +282,56 @@ int pt_cells_slice(const pt_cells* c, long long first, long long count, pt_cells
     return PT_OK;
 }
 
+int pt_cells_keys(const pt_cells* c, long long first, long long count, unsigned long long* out) {
+    if (!c || (count > 0 && !out)) return pt_fail(c ? c->ctx : nullptr, PT_E_INVALID, "pt_cells_keys: NULL argument");
+    pt_ctx* ctx = c->ctx;
+    if (first < 0 || count < 0 || first + count > c->count) return pt_fail(ctx, PT_E_INVALID, "cell range out of bounds");
+    if (count == 0) return PT_OK;
+    PT_CUDA(ctx, cudaMemcpyAsync(out, c->keys.p + first, (size_t)count * sizeof(u64), cudaMemcpyDefault, ctx->stream));
+    PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    return PT_OK;
+}
+
+int pt_cells_merge_keys(const pt_cells* like, const unsigned long long* keys, long long count, pt_cells** out) {
+    if (!like || !out || (count > 0 && !keys)) return pt_fail(like ? like->ctx : nullptr, PT_E_INVALID, "pt_cells_merge_keys: NULL argument");
+    pt_ctx* ctx = like->ctx;
+    if (count < 0) return pt_fail(ctx, PT_E_INVALID, "negative key count");
+    pt_cells* c = new pt_cells();
+    c->ctx = ctx; c->n = like->n; c->geom = like->geom; c->count = 0;
+    struct Guard { pt_cells* c; bool keep = false; ~Guard() { if (!keep) delete c; } } guard{c};
+    PT_TRY(c->keys.alloc(ctx, (size_t)(count > 0 ? count : 1)));
+    if (count > 0) {
+        PtBuf<u64> in, sorted; PtBuf<long long> nsel; PtBuf<uint8_t> tmp;
+        const u64* kdev;
+        PT_TRY(pt_stage_in(ctx, (const u64*)keys, (size_t)count, in, &kdev));
+        PT_TRY(sorted.alloc(ctx, (size_t)count));
+        PT_TRY(nsel.alloc(ctx, 1));
+        const int key_bits = c->geom.n * c->geom.bits + PT_CELL_RANK_BITS;
+        size_t tb1 = 0, tb2 = 0;
+        cub::DeviceRadixSort::SortKeys(nullptr, tb1, kdev, sorted.p, count, 0, key_bits, ctx->stream);
+        cub::DeviceSelect::Unique(nullptr, tb2, sorted.p, c->keys.p, nsel.p, count, ctx->stream);
+        PT_TRY(tmp.alloc(ctx, tb1 > tb2 ? tb1 : tb2));
+        {
+            PT_LAUNCH(ctx, "cells_sort");
+            PT_CUDA(ctx, cub::DeviceRadixSort::SortKeys(tmp.p, tb1, kdev, sorted.p, count, 0, key_bits, ctx->stream));
+            ctx->launches++;
+        }
+        {
+            PT_LAUNCH(ctx, "cells_unique");
+            PT_CUDA(ctx, cub::DeviceSelect::Unique(tmp.p, tb2, sorted.p, c->keys.p, nsel.p, count, ctx->stream));
+            ctx->launches++;
+        }
+        long long* hs = (long long*)ctx->pinned;
+        PT_CUDA(ctx, cudaMemcpyAsync(hs, nsel.p, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+        PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        c->count = *hs;
+    }
+    PT_TRY(pt_cells_bounds(c));
+    guard.keep = true;
+    *out = c;
+    return PT_OK;
+}
+
 void pt_cells_destroy(pt_cells* c) { delete c; }
 long long pt_cells_count(const pt_cells* c) { return c ? c->count : -1; }
 

@@ -348,6 +348,11 @@ __device__ __forceinline__ int pt_dedup_search(int n, const double* __restrict__
     return any_kept ? 2 : (any_undecided ? 1 : 0);
 }
 
+__global__ void pt_dedup_force_kernel(const int8_t* __restrict__ forced, size_t count, uint8_t* __restrict__ state) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count && forced[i] >= 0) state[i] = forced[i] ? PT_DD_KEPT : PT_DD_REMOVED;
+}
+
 __global__ void pt_dedup_round_kernel(int n, const double* __restrict__ pts, size_t count, double cell, double eps,
                                       const u64* __restrict__ gkey_sorted, const uint32_t* __restrict__ idx_sorted, PtTable dir,
                                       uint8_t* state, uint32_t* __restrict__ undecided, uint32_t* __restrict__ nbc_out,
@@ -355,7 +360,7 @@ __global__ void pt_dedup_round_kernel(int n, const double* __restrict__ pts, siz
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool pending = false;
     int nbc = 0;
-    if (i < count) {
+    if (i < count && state[i] == PT_DD_UNDECIDED) {      // (pre-decided: states forced by the caller)
         const int verdict = pt_dedup_search<false>(n, pts, count, cell, eps, gkey_sorted, idx_sorted, dir, state, i, nullptr, nbc);
         if (verdict == 2) state[i] = PT_DD_REMOVED;
         else if (verdict == 0) state[i] = PT_DD_KEPT;
@@ -462,7 +467,7 @@ static int pt_read_fine_counters(pt_ctx* ctx, PtFineCounters* dev, PtFineCounter
 // Greedy first-keeper dedup at eps over `U` points given in priority order, then collision labels.
 // vals (optional) carries (tag << 1 | sign) per point; without it the tag is the input position.
 static int pt_dedup_label_impl(pt_ctx* ctx, int n, const double* upts, const u64* vals, size_t U, double eps_dedup,
-                               const pt_checker* checker, pt_refine* r) {
+                               const pt_checker* checker, pt_refine* r, const int8_t* forced = nullptr) {
     PtBuf<PtFineCounters> ctr;
     PT_TRY(ctr.alloc(ctx, 1));
     PT_CUDA(ctx, cudaMemsetAsync(ctr.p, 0, sizeof(PtFineCounters), ctx->stream));
@@ -478,6 +483,11 @@ static int pt_dedup_label_impl(pt_ctx* ctx, int n, const double* upts, const u64
     if (U > 0) {
         if (U >= (1ull << 32)) return pt_fail(ctx, PT_E_NOMEM, "more than 2^32 distinct fine edges in one refine call");
         PT_CUDA(ctx, cudaMemsetAsync(state.p, PT_DD_UNDECIDED, U, ctx->stream));
+        if (forced) {
+            // ghost copies of points another rank owns enter with that rank's verdict (multi-GPU eps-dedup)
+            pt_dedup_force_kernel<<<pt_grid_for(U, 256), 256, 0, ctx->stream>>>(forced, U, state.p);
+            PT_TRY(pt_check_launch(ctx, "pt_dedup_force_kernel"));
+        }
         // 8 eps cells: a point's eps-ball touches ~(1 + 1/4)^n cells (3.8 at n = 6) holding about one point each
         const double cell = 8.0 * eps_dedup;
         PtBuf<u64> gk, gks; PtBuf<uint32_t> gi, gis;
@@ -886,6 +896,11 @@ int pt_refine_candidates(pt_ctx* ctx, const pt_field* field, const pt_cells* cel
 
 int pt_dedup_label(pt_ctx* ctx, int n, const double* points, long long count, double eps_dedup, const pt_checker* checker,
                    pt_refine** out) {
+    return pt_dedup_label_forced(ctx, n, points, count, eps_dedup, nullptr, checker, out);
+}
+
+int pt_dedup_label_forced(pt_ctx* ctx, int n, const double* points, long long count, double eps_dedup, const int8_t* forced,
+                          const pt_checker* checker, pt_refine** out) {
     if (!ctx || !out) return pt_fail(ctx, PT_E_INVALID, "pt_dedup_label: NULL argument");
     if (n < 2 || n > 7) return pt_fail(ctx, PT_E_INVALID, "dimension %d unsupported (2..7)", n);
     if (count < 0) return pt_fail(ctx, PT_E_INVALID, "negative point count");
@@ -896,8 +911,11 @@ int pt_dedup_label(pt_ctx* ctx, int n, const double* points, long long count, do
     memset(&r->stats, 0, sizeof(r->stats));
     PtBuf<double> tmp;
     const double* pdev;
+    PtBuf<int8_t> ftmp;
+    const int8_t* fdev = nullptr;
     int rc = pt_stage_in(ctx, points, (size_t)count * n, tmp, &pdev);
-    if (rc == PT_OK) rc = pt_dedup_label_impl(ctx, n, pdev, nullptr, (size_t)count, eps_dedup, checker, r);
+    if (rc == PT_OK && forced && count > 0) rc = pt_stage_in(ctx, forced, (size_t)count, ftmp, &fdev);
+    if (rc == PT_OK) rc = pt_dedup_label_impl(ctx, n, pdev, nullptr, (size_t)count, eps_dedup, checker, r, fdev);
     if (rc == PT_OK) rc = (cudaStreamSynchronize(ctx->stream) == cudaSuccess) ? PT_OK : pt_fail(ctx, PT_E_CUDA, "dedup failed");
     if (rc != PT_OK) { delete r; return rc; }
     *out = r;

@@ -9,6 +9,7 @@
 //   pt_wave_admit_kernel    admission in slot order: edge index = visited + rank (tracer.py:239-252)
 // Slot id = frontier position * stride + coface ordinal reproduces the reference's admission order.
 #include <cub/cub.cuh>
+#include <limits.h>
 #include "pt_trace.cuh"
 #include "pt_field.cuh"
 
@@ -438,6 +439,19 @@ static int pt_admit_items(pt_trace* t, size_t items, int stride, const uint32_t*
     return PT_OK;
 }
 
+// bounding box of the seeds' lattice cells: out[d] = min, out[PT_NMAX + d] = max, out[2 PT_NMAX] = 1 if a coordinate is not finite
+__global__ void pt_seed_bounds_kernel(PtGeom g, const double* __restrict__ seeds, size_t m, int* __restrict__ out) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    for (int d = 0; d < g.n; ++d) {
+        const double y = (seeds[i * g.n + d] - g.offset[d]) / g.scale;
+        if (!(y == y) || y > 1e9 || y < -1e9) { out[2 * PT_NMAX] = 1; continue; }
+        const int c = (int)floor(y);
+        atomicMin(&out[d], c);
+        atomicMax(&out[PT_NMAX + d], c);
+    }
+}
+
 static int pt_set_window(pt_trace* t, const int* first_cell_base) {
     PtGeom& g = t->geom;
     if (g.has_box) {
@@ -481,15 +495,21 @@ static int pt_trace_locate_impl(pt_trace* t, const double* seeds, long long m) {
     const double* sdev;
     PT_TRY(pt_stage_in(ctx, seeds, (size_t)m * n, tmp, &sdev));
     if (!t->window_set) {
-        double first[PT_NMAX];
-        PT_CUDA(ctx, cudaMemcpyAsync(first, sdev, n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        // without a clamp box the key window is centred on the bounding box of ALL seed cells (a zero set narrower than
+        // the window then fits wherever the first seed happens to sit on it)
+        PtBuf<int> bounds;
+        PT_TRY(bounds.alloc(ctx, 2 * PT_NMAX + 1));
+        int init[2 * PT_NMAX + 1];
+        for (int d = 0; d < PT_NMAX; ++d) { init[d] = INT_MAX; init[PT_NMAX + d] = INT_MIN; }
+        init[2 * PT_NMAX] = 0;
+        PT_CUDA(ctx, cudaMemcpyAsync(bounds.p, init, sizeof(init), cudaMemcpyHostToDevice, ctx->stream));
+        pt_seed_bounds_kernel<<<pt_grid_for((size_t)m, 256), 256, 0, ctx->stream>>>(g, sdev, (size_t)m, bounds.p);
+        PT_TRY(pt_check_launch(ctx, "pt_seed_bounds_kernel"));
+        PT_CUDA(ctx, cudaMemcpyAsync(init, bounds.p, sizeof(init), cudaMemcpyDeviceToHost, ctx->stream));
         PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        if (init[2 * PT_NMAX]) return pt_fail(ctx, PT_E_INVALID, "point coordinates must be finite");
         int cb[PT_NMAX];
-        for (int d = 0; d < n; ++d) {
-            double y = (first[d] - g.offset[d]) / g.scale;
-            if (!(y == y) || y > 1e9 || y < -1e9) return pt_fail(ctx, PT_E_INVALID, "point coordinates must be finite");
-            cb[d] = (int)floor(y);
-        }
+        for (int d = 0; d < n; ++d) cb[d] = (int)(((long long)init[d] + (long long)init[PT_NMAX + d]) >> 1);
         PT_TRY(pt_set_window(t, cb));
     }
     t->seeds += m;

@@ -1,18 +1,25 @@
-"""Sharding of the hot path across GPUs (one process per GPU, torch.distributed).
+"""Sharding of the hot path across GPUs (one process per GPU, torch.distributed; SURVEY.md section 8e).
 
-What shards: refinement and collision checking are embarrassingly parallel
-over the sorted coarse cells, so rank r takes the contiguous slice [C*r/W, C*(r+1)/W).  Every rank
-traces (the BFS is ~1 % of a proof and launch-latency bound at benchmark sizes; the owner-hashed
-all-to-all BFS of the north star only pays once a trace no longer fits one GPU).  The only exchange
-is the merge of the per-slice root-solved points before the order-dependent eps-dedup:
+    BFS trace       owner-hashed: rank r owns the edges whose base vertex hashes to r; per wave ONE all_to_all of 16-byte
+                    candidate records, admission by minimum tag on the owner, all_gather of the winners' tags for the
+                    global admission order (`ShardedTrace`)
+    coarse cells    every rank enumerates the cell cofaces of ITS edges, then the sorted unique cell list is built by a
+                    range-partitioned sample sort of the packed 64-bit cell keys: all_gather of a few samples per rank ->
+                    common splitters -> all_to_all of key ranges -> local sort + unique.  Rank r ends up with the r-th
+                    contiguous piece of the globally sorted list (the order contract of reference subdivision.py:141); no
+                    rank ever holds all cells
+    refine          rank r refines its piece (crossing sets are per cell; crossing offsets = exclusive scan over ranks)
+    eps-dedup       priorities are global first-crossing indices, i.e. rank-major.  A rank's candidates lie in a slab of
+                    coordinate 0 (keys sort by it first), so only points within eps of another rank's slab are exchanged
+                    (ghosts).  Every rank runs the greedy dedup over own + ghost points; ghosts are then pinned to their
+                    owners' verdicts and the run repeated until no verdict differs anywhere -- the greedy rule
+                    (subdivision.py:195-217) has exactly one fixed point, so this is the single-GPU result
+    collision       labels of the kept points stay with their rank; counts are all_reduced
 
-    1. all_gather(crossing count, candidate count)     -> global crossing-index offsets per rank
-    2. all_gather(padded candidate points)             -> concatenation in rank order is already in
-                                                          global first-crossing order
-    3. every rank runs the same greedy eps-dedup + collision labelling on the merged list
-
-The driver is written against a small engine protocol so the exchange logic runs unchanged over
-NCCL with the CUDA engine and over gloo in the CPU test-suite (tests/test_distributed_gloo.py).
+The drivers are written against a small engine protocol so the exchange logic runs unchanged over NCCL with the CUDA
+engine and over gloo in the CPU test-suite (tests/test_distributed_gloo.py, tests/test_sharded_trace.py).  Nothing here has
+run at N > 1 on real GPUs (one GPU per box in this project): the NCCL path is exercised on one device with several
+engines / with gloo staging only.
 """
 
 from __future__ import annotations
@@ -105,15 +112,23 @@ class _Transport:
         return [int(v) for v in t.tolist()]
 
     def _exchange(self, records, counts):
+        """all_to_all of rows bucketed by destination rank (`counts[r]` consecutive rows go to rank r); any trailing shape."""
         import torch
         if self.world == 1:
             return records
-        dev = self.comm_device
-        send = torch.tensor(counts, dtype=torch.int64, device=dev)
+        recv_counts = self._exchange_counts(counts)
+        return self._exchange_rows(records, counts, recv_counts)
+
+    def _exchange_counts(self, counts):
+        import torch
+        send = torch.tensor([int(c) for c in counts], dtype=torch.int64, device=self.comm_device)
         recv = torch.zeros_like(send)
         self.dist.all_to_all_single(recv, send, group=self.group)
-        recv_counts = [int(v) for v in recv.tolist()]
-        out = torch.empty((sum(recv_counts), 2), dtype=torch.int64, device=dev)
+        return [int(v) for v in recv.tolist()]
+
+    def _exchange_rows(self, records, counts, recv_counts):
+        import torch
+        out = torch.empty((sum(recv_counts),) + tuple(records.shape[1:]), dtype=records.dtype, device=self.comm_device)
         self.dist.all_to_all_single(out, self._out(records).contiguous(), output_split_sizes=recv_counts,
                                     input_split_sizes=[int(c) for c in counts], group=self.group)
         return self._back(out)
@@ -185,21 +200,135 @@ class ShardedTrace(_Transport):
 
 
 class ShardedProof(_Transport):
-    """trace -> coarse_cells -> refine(+check) with the refinement sharded over the process group.
+    """trace -> coarse_cells -> refine(+check) sharded over the process group (see the module docstring).
 
-    `engine` implements:
-        trace(seeds) -> dict(trace_edges=int, cells=int, closure_ok=bool, ...)
-        candidates(first, count) -> (points tensor [U, n] float64, crossing_edges int)
-        dedup_label(points tensor [M, n]) -> (kept_index tensor int64, labels tensor uint8)
-        tensor_device -> torch.device for the exchange buffers
+    `engine` implements (tensors on `engine.tensor_device`):
+        trace(seeds) -> dict(trace_edges=int, cells=int, closure_ok=bool, ...)          single-rank trace + cells
+        candidates(first, count) -> (points [U, n] float64 in first-crossing order, crossing_edges int)
+        dedup_label(points [M, n]) -> (kept_index int64, labels uint8)                  greedy dedup in the given order
+      and, for the fully sharded path (world > 1):
+        the ShardedTrace protocol, local_points()
+        local_cell_keys() -> sorted unique int64 keys of the cells around THIS rank's edges (order = cell order)
+        set_cells_from_keys(keys int64) -> number of distinct cells now held (sorted, deduplicated)
+        dedup_mask(points [M, n] in priority order, forced int8 [M]) -> uint8 [M] kept mask (forced: 1 kept, 0 removed, -1 open)
+        label(points) -> uint8 non-free mask
+    An engine without `local_cell_keys` gets the replicated variant: every rank builds all cells and deduplicates the
+    all_gathered candidates (kept for single-rank engines and as the reference the sharded variant is tested against).
     """
 
-    def __init__(self, engine, group=None):
+    SAMPLES_PER_RANK = 64
+    MAX_PIN_ROUNDS = 64
+
+    def __init__(self, engine, group=None, gather_result: bool = True):
         self._init_transport(engine, group)
+        self.gather_result = gather_result
+
+    # ---- sharded coarse cells: range-partitioned sample sort of the packed cell keys -------------------------
+    def _range_partition(self, keys):
+        """`keys`: this rank's sorted unique int64 cell keys.  Returns the keys of all ranks that fall into this rank's
+        range (unsorted concatenation of sorted runs; duplicates between ranks still present)."""
+        import torch
+        W, k = self.world, int(keys.shape[0])
+        ns = min(k, self.SAMPLES_PER_RANK * W)
+        pick = torch.linspace(0, max(k - 1, 0), ns, device=keys.device).round().long() if ns else keys.new_zeros(0, dtype=torch.int64)
+        pool = torch.sort(torch.cat(self._gather_var(keys[pick] if ns else keys[:0]))).values
+        if pool.numel() == 0:
+            return keys
+        splitters = pool[(torch.arange(1, W, device=pool.device) * pool.numel()) // W]
+        cut = torch.searchsorted(keys, splitters.to(keys.device))          # keys >= splitter r go right of cut[r]
+        edges = [0] + [int(c) for c in cut.tolist()] + [k]
+        counts = [edges[r + 1] - edges[r] for r in range(W)]
+        return self._exchange(keys, counts)
+
+    # ---- sharded eps-dedup: slab ghosts + pinning to the owners' verdicts ------------------------------------
+    def _sharded_dedup(self, pts, prio_offset: int):
+        """Greedy first-keeper dedup of the union of all ranks' candidates (priority = global first-crossing index,
+        `prio_offset` + local position).  Returns this rank's uint8 kept mask and the number of pin rounds."""
+        import torch
+        eng, W, me = self.engine, self.world, self.rank
+        eps = float(eng.eps_dedup)
+        m, n = int(pts.shape[0]), int(pts.shape[1])
+        dev = pts.device
+        x0 = pts[:, 0]
+        mine = torch.tensor([float(x0.min()) - eps, float(x0.max()) + eps] if m else [float("inf"), float("-inf")],
+                            dtype=torch.float64, device=self.comm_device)
+        spans = [torch.zeros_like(mine) for _ in range(W)]
+        self.dist.all_gather(spans, mine, group=self.group)
+        # my points that may lie within eps of a point of rank r (by coordinate 0): ghosts over there
+        send_idx = []
+        for r in range(W):
+            lo, hi = float(spans[r][0]), float(spans[r][1])
+            if r == me or not m or lo > hi:
+                send_idx.append(torch.zeros(0, dtype=torch.int64, device=dev))
+            else:
+                send_idx.append(torch.nonzero((x0 >= lo) & (x0 <= hi)).flatten())
+        counts = [int(i.numel()) for i in send_idx]
+        order_out = torch.cat(send_idx)
+        recv_counts = self._exchange_counts(counts)
+        ghost_pts = self._exchange_rows(pts[order_out], counts, recv_counts)
+        ghost_prio = self._exchange_rows(order_out + int(prio_offset), counts, recv_counts)
+        g = int(ghost_pts.shape[0])
+        all_pts = torch.cat([ghost_pts, pts])
+        prio = torch.cat([ghost_prio, torch.arange(m, dtype=torch.int64, device=dev) + int(prio_offset)])
+        order = torch.argsort(prio, stable=True)
+        inv = torch.empty_like(order)
+        inv[order] = torch.arange(order.numel(), device=dev)
+        forced_g = None
+        rounds = 0
+        while True:
+            forced = torch.full((g + m,), -1, dtype=torch.int8, device=dev)
+            if forced_g is not None:
+                forced[:g] = forced_g.to(torch.int8)
+            mask = eng.dedup_mask(all_pts[order].contiguous(), forced[order].contiguous())[inv]
+            own = mask[g:]
+            used = forced_g if forced_g is not None else mask[:g]
+            # the owners' verdicts on my ghosts = their masks over what they sent me, in the order it was sent
+            auth = self._exchange_rows(own[order_out].to(torch.int64), counts, recv_counts)
+            differ = int((used.to(torch.int64) != auth).sum().item()) if g else 0
+            rounds += 1
+            if self._sum([differ])[0] == 0:
+                return own.to(torch.uint8), rounds
+            if rounds >= self.MAX_PIN_ROUNDS:
+                raise RuntimeError("sharded eps-dedup did not settle")
+            forced_g = auth
+
+    def _run_sharded(self, seeds) -> dict:
+        import torch
+        eng = self.engine
+        st = ShardedTrace(eng, self.group)
+        info = st.run(seeds, int(eng.max_edges))
+        if hasattr(eng, "local_points"):
+            eng.local_points()                     # coarse-edge intersection points: each rank solves its own edges
+        count = int(eng.set_cells_from_keys(self._range_partition(eng.local_cell_keys())))
+        pts, crossing = eng.candidates(0, count)
+        per_rank = torch.tensor([count, int(pts.shape[0]), int(crossing)], dtype=torch.int64, device=self.comm_device)
+        table = [torch.zeros_like(per_rank) for _ in range(self.world)]
+        self.dist.all_gather(table, per_rank, group=self.group)
+        table = torch.stack(table).cpu().numpy()
+        first_cell = int(table[: self.rank, 0].sum())
+        prio_offset = int(table[: self.rank, 1].sum())
+        kept, pin_rounds = self._sharded_dedup(pts, prio_offset)
+        points = pts[kept.bool()]
+        labels = eng.label(points) if hasattr(eng, "label") else torch.zeros(points.shape[0], dtype=torch.uint8)
+        n_points, n_free = self._sum([int(points.shape[0]), int((labels == 0).sum().item())])
+        info.update(
+            cells=int(table[:, 0].sum()), slice=(first_cell, count), crossing_edges=int(table[:, 2].sum()),
+            crossing_edges_local=int(crossing), candidates_local=int(pts.shape[0]), candidates=int(table[:, 1].sum()),
+            crossing_offsets=np.concatenate([[0], np.cumsum(table[:, 2])[:-1]]), pin_rounds=pin_rounds,
+            points_local=points, in_collision_local=labels.to(torch.bool), points_total=n_points, free_points=n_free)
+        if self.gather_result:
+            # rank order = global first-crossing order: the concatenation is the single-GPU result
+            info["points"] = torch.cat(self._gather_var(points))
+            info["in_collision"] = torch.cat(self._gather_var(labels)).to(torch.bool)
+        else:
+            info["points"], info["in_collision"] = points, labels.to(torch.bool)
+        return info
 
     def run(self, seeds) -> dict:
         import torch
         dist, eng = self.dist, self.engine
+        if self.world > 1 and hasattr(eng, "local_cell_keys") and hasattr(eng, "trace_locate"):
+            return self._run_sharded(seeds)
         if self.world > 1 and hasattr(eng, "trace_locate") and getattr(eng, "shard_trace", True):
             # owner-hashed BFS; the merged edge list (global admission order) feeds the replicated cell build
             st = ShardedTrace(eng, self.group)
@@ -219,12 +348,7 @@ class ShardedProof(_Transport):
             counts = [torch.zeros_like(mine) for _ in range(self.world)]
             dist.all_gather(counts, mine, group=self.group)
             counts = torch.stack(counts).cpu().numpy()
-            biggest = int(counts[:, 0].max())
-            padded = torch.zeros((max(biggest, 1), n), dtype=torch.float64, device=self.comm_device)
-            padded[: pts.shape[0]] = self._out(pts)
-            gathered = [torch.empty_like(padded) for _ in range(self.world)]
-            dist.all_gather(gathered, padded, group=self.group)
-            merged = self._back(torch.cat([gathered[r][: int(counts[r, 0])] for r in range(self.world)], dim=0))
+            merged = torch.cat(self._gather_var(pts), dim=0)
             crossing_total = int(counts[:, 1].sum())
             crossing_offsets = np.concatenate([[0], np.cumsum(counts[:, 1])[:-1]])
         else:
@@ -364,18 +488,49 @@ class CudaEngine:
         return dict(dropped=int(st.dropped_out_of_box), field_evaluations=int(st.field_evaluations), candidates=int(st.candidates))
 
     def local_edges(self):
-        """(gidx [E], payload [E, n + 2] = base coordinates, step mask, sign at base) of this rank's edges."""
+        """(gidx [E], payload [E, n + 2] = base coordinates, step mask, sign at base) of this rank's edges; device-resident
+        (the C ABI unpacks straight into the tensors)."""
         lib, cabi, torch = self._cabi.lib, self._cabi, self.torch
         st = cabi.TraceStats()
         cabi.check(lib.pt_trace_get_stats(self._trace, C.byref(st)))
         E = int(st.visited_edges)
-        base = np.zeros((E, self.n), dtype=np.int32); mask = np.zeros(E, dtype=np.uint32); sa = np.zeros(E, dtype=np.int8)
-        gidx = np.zeros(E, dtype=np.int64)
+        dev = self.tensor_device
+        base = torch.zeros((E, self.n), dtype=torch.int32, device=dev)
+        mask = torch.zeros(E, dtype=torch.int32, device=dev)
+        sa = torch.zeros(E, dtype=torch.int8, device=dev)
+        gidx = torch.zeros(E, dtype=torch.int64, device=dev)
         if E:
-            cabi.check(lib.pt_trace_edges(self._trace, 0, E, base.ctypes.data, mask.ctypes.data, sa.ctypes.data))
-            cabi.check(lib.pt_trace_gidx(self._trace, 0, E, gidx.ctypes.data))
-        payload = np.concatenate([base.astype(np.int64), mask.astype(np.int64)[:, None], sa.astype(np.int64)[:, None]], axis=1)
-        return (torch.from_numpy(gidx).to(self.tensor_device), torch.from_numpy(payload).to(self.tensor_device))
+            cabi.check(lib.pt_trace_edges(self._trace, 0, E, C.c_void_p(base.data_ptr()), C.c_void_p(mask.data_ptr()),
+                                          C.c_void_p(sa.data_ptr())))
+            cabi.check(lib.pt_trace_gidx(self._trace, 0, E, C.c_void_p(gidx.data_ptr())))
+        payload = torch.cat([base.to(torch.int64), mask.to(torch.int64)[:, None], sa.to(torch.int64)[:, None]], dim=1)
+        return gidx, payload
+
+    def local_cell_keys(self):
+        """Sorted unique packed keys of the cells around this rank's edges (all ranks share the key window of the clamp box)."""
+        lib, cabi, torch = self._cabi.lib, self._cabi, self.torch
+        if self._cells:
+            lib.pt_cells_destroy(self._cells)
+            self._cells = None
+        cells = C.c_void_p()
+        cabi.check(lib.pt_cells_from_trace(self._trace, C.byref(cells)))
+        self._cells = cells
+        count = int(lib.pt_cells_count(cells))
+        keys = torch.empty(count, dtype=torch.int64, device=self.tensor_device)
+        if count:
+            cabi.check(lib.pt_cells_keys(cells, 0, count, C.c_void_p(keys.data_ptr())))
+        return keys
+
+    def set_cells_from_keys(self, keys) -> int:
+        """Replace the local cell list by sort + unique of `keys` (this rank's range of the global list)."""
+        lib, cabi = self._cabi.lib, self._cabi
+        keys = keys.contiguous()
+        merged = C.c_void_p()
+        cabi.check(lib.pt_cells_merge_keys(self._cells, C.c_void_p(keys.data_ptr()) if keys.shape[0] else None,
+                                           keys.shape[0], C.byref(merged)))
+        lib.pt_cells_destroy(self._cells)
+        self._cells = merged
+        return int(lib.pt_cells_count(merged))
 
     def local_points(self):
         """Intersection points of this rank's traced edges (the reference's trace() returns them), kept in HBM."""
@@ -389,7 +544,7 @@ class CudaEngine:
         return self.trace_points[:E]
 
     def cells_from_edges(self, payload) -> int:
-        """Sorted, deduplicated coarse cells of the merged edge list (every rank builds the same list)."""
+        """Sorted, deduplicated coarse cells of a merged edge list (replicated variant: every rank builds the same list)."""
         lib, cabi = self._cabi.lib, self._cabi
         p = payload.cpu().numpy()
         base = np.ascontiguousarray(p[:, : self.n], dtype=np.int32)
@@ -445,6 +600,22 @@ class CudaEngine:
         try:
             _, _, kept, labels = self._fetch(ref, True)
             return kept, labels
+        finally:
+            lib.pt_refine_destroy(ref)
+
+    def dedup_mask(self, points, forced):
+        """uint8 kept mask of the greedy eps-dedup over `points` (priority order) with some verdicts given (`forced`)."""
+        lib, cabi, torch = self._cabi.lib, self._cabi, self.torch
+        ref = C.c_void_p()
+        points, forced = points.contiguous(), forced.contiguous()
+        cabi.check(lib.pt_dedup_label_forced(self.ctx.handle, self.n, C.c_void_p(points.data_ptr()), points.shape[0],
+                                             float(self.eps_dedup), C.c_void_p(forced.data_ptr()) if forced.shape[0] else None,
+                                             None, C.byref(ref)))
+        try:
+            _, _, kept, _ = self._fetch(ref, False)
+            mask = torch.zeros(points.shape[0], dtype=torch.uint8, device=self.tensor_device)
+            mask[kept] = 1
+            return mask
         finally:
             lib.pt_refine_destroy(ref)
 

@@ -102,6 +102,7 @@ class DevicePipeline:
                 "pair_evals_fp32": int(work[2]) * self.support, "bisect_fallbacks": int(work[3]),
                 "pair_evals_rest": int(work[4]) * self.support, "pair_evals_resolve": int(work[5]) * self.support,
                 "pair_evals_retry": int(lib.pt_ctx_retry_evaluations(ctx.handle)) * self.support,
+                "taylor_rows": int(lib.pt_ctx_taylor_rows(ctx.handle)),
                 "ambiguous_signs": int(st.ambiguous_signs) + int(rs.ambiguous_signs),
             }
         finally:

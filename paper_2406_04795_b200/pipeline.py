@@ -323,12 +323,12 @@ def verify_proof(proof, problem, reconstruct: bool = True) -> VerifyReport:
     return VerifyReport(checks)
 
 
-def _set_gap(a: np.ndarray, b: np.ndarray) -> float:
+def _set_gap(a: np.ndarray, b: np.ndarray, tol: float = 0.0) -> float:
     """Symmetric Hausdorff distance of two point sets.  Both come out of the same deterministic pipeline, so the
     row-wise comparison normally settles it; otherwise nearest neighbours by KD-tree like the reference."""
     if a.shape == b.shape:
-        rowwise = float(np.max(np.linalg.norm(a - b, axis=1)))
-        if rowwise <= 1e-6:
+        rowwise = float(np.max(np.linalg.norm(a - b, axis=1)))      # an upper bound of the Hausdorff distance
+        if rowwise <= tol:
             return rowwise
     from scipy.spatial import cKDTree
     return float(max(cKDTree(a).query(b)[0].max(), cKDTree(b).query(a)[0].max()))
@@ -344,7 +344,11 @@ def _reconstruction_check(proof, manifold, points: np.ndarray) -> CheckResult:
     n = points.shape[1]
     cfg = TraceConfig(lattice=LatticeConfig(n, proof.lam * proof.k), max_edges=4 * proof.coarse_edges + 1024,
                       workers=1, eps=proof.eps)
-    result = trace(points, manifold, cfg)
+    from ._cabi import RangeError
+    try:
+        result = trace(points, manifold, cfg)
+    except RangeError as exc:        # the zero set leaves the packed-key window of the device tracer: a failed check, not a crash
+        return CheckResult(name, False, f"re-trace not representable on the device: {exc}")
     if not result.closure_ok:
         return CheckResult(name, False, "re-trace did not close")
     if len(result.edges) != proof.coarse_edges:
@@ -357,7 +361,7 @@ def _reconstruction_check(proof, manifold, points: np.ndarray) -> CheckResult:
     if refined.points.shape[0] != points.shape[0]:
         return CheckResult(name, False, f"re-refinement produced {refined.points.shape[0]} points, stored {points.shape[0]}")
     tol = max(64.0 * proof.eps, 1e-12)
-    gap = _set_gap(refined.points, points)
+    gap = _set_gap(refined.points, points, tol)
     if gap > tol:
         return CheckResult(name, False, f"point sets differ by {gap:.3g} > {tol:.3g}")
     return CheckResult(name, True, f"{points.shape[0]} points reproduced within {tol:.3g}")
@@ -408,6 +412,7 @@ def solve(problem: Problem, params: SolveParams | None = None):
     from .planner import Roadmap, find_path, grow, insert_free_points, labeled_samples
     from .subdivision import build_template, coarse_cells, refine
     from .tracer import TraceConfig, trace
+    from ._cabi import RangeError
 
     params = params or SolveParams()
     t0 = time.perf_counter()
@@ -470,7 +475,11 @@ def solve(problem: Problem, params: SolveParams | None = None):
             continue
 
         t = time.perf_counter()
-        result = trace(seeds, manifold, cfg)
+        try:
+            result = trace(seeds, manifold, cfg)
+        except RangeError as exc:    # lattice too fine for the packed keys at this dimension: skip the iteration, say why
+            record["skip"] = f"trace out of key range: {exc}"
+            continue
         record["trace_s"] = time.perf_counter() - t
         record["edges"] = len(result.edges)
         if not len(result.edges) or not result.closure_ok:
@@ -487,6 +496,7 @@ def solve(problem: Problem, params: SolveParams | None = None):
         record["refine_s"] = time.perf_counter() - t
         record["check_s"] = float(sum(check_times))
         record["points"] = int(refined.points.shape[0])
+        record["crossing_edges"] = int(sum(b.crossing_edges for b in refined.batch_stats))   # (not a reference key)
         record["free_points"] = int(refined.free_points.shape[0])
         if refined.free_points.shape[0]:
             # the zero set still touches free space: feed those configurations back into the roadmap

@@ -117,9 +117,21 @@ def fence_problem_dict(dof: int, clutter: int = 6, seed: int = 11, q1_limit: flo
             "problem": {"start": start, "goal": goal}}
 
 
-# name -> (problem generator arguments, SolveParams overrides) of the end-to-end proof workloads
+# name -> (problem generator arguments, SolveParams overrides) of the end-to-end proof workloads.  Parameters found on the
+# B200 (gpurun_out logs summarised in profiles/r2_proof_*.json): a wide kernel (small gamma) keeps the learned surface
+# smooth, the push stays below 1 (labels are +-1, a larger bias offset erases the sign change between start and goal:
+# "no separation"), and the feedback cap keeps the support set -- every roadmap vertex -- in the 10^4 range.
+def _push(lam, gamma, mult):
+    return mult * lam * float(np.sqrt(2.0 * gamma))
+
+
 PROOF_CONFIGS = {
-    "dof4-proof": dict(dof=4, clutter=3, params=dict(lam=0.2, k=2, gamma=1.0, samples_per_iter=1500, seeds=20)),
-    "dof5-proof": dict(dof=5, clutter=5, params=dict(lam=0.25, k=2, gamma=0.75, samples_per_iter=3000, seeds=20)),
-    "dof6-proof": dict(dof=6, clutter=7, params=dict(lam=0.3, k=2, gamma=0.5, samples_per_iter=6000, seeds=20)),
+    "dof4-proof": dict(dof=4, clutter=3, params=dict(lam=0.25, k=2, gamma=0.5, samples_per_iter=2000, seeds=20, feedback_cap=3000,
+                                                       push=_push(0.25, 0.5, 2.5), max_iters=30)),
+    "dof5-proof": dict(dof=5, clutter=3, params=dict(lam=0.35, k=2, gamma=0.5, samples_per_iter=2000, seeds=20, feedback_cap=2000,
+                                                       push=_push(0.35, 0.5, 2.5), max_iters=30)),
+    "dof6-proof": dict(dof=6, clutter=0, params=dict(lam=0.5, k=2, gamma=0.35, samples_per_iter=1000, seeds=20, feedback_cap=2000,
+                                                       push=_push(0.5, 0.35, 2.15), max_iters=40, max_edges=200_000_000)),
+    # the 3-DoF twin the reference's CPU loop finishes in minutes (its own arm3wall pattern, same generator)
+    "dof3-proof": dict(dof=3, clutter=0, params=dict(lam=0.15, k=2, gamma=2.0, samples_per_iter=600, seeds=20, max_iters=30)),
 }

@@ -137,3 +137,141 @@ def test_single_process_driver_matches_reference():
     res = ShardedProof(eng).run(eng.inp["seeds"])
     assert np.allclose(res["points"].numpy(), g["kclf_n3_refine_points"], rtol=0, atol=1e-8)
     assert np.array_equal(res["in_collision"].numpy(), g["kclf_n3_refine_labels"])
+
+
+# ---- fully sharded driver: owner-hashed BFS + sample-sorted cells + ghost-pinned eps-dedup (world 2, 3, 4 on gloo) ----
+def _shard_engine(tag="kclf_n3"):
+    from tests.test_sharded_trace import OracleTraceEngine
+
+    class OracleShardEngine(OracleTraceEngine):
+        """The whole engine protocol of distributed.ShardedProof on top of the CPU oracle (test infrastructure)."""
+
+        def __init__(self):
+            super().__init__(tag)
+            O = self.O
+            self.template = O.build_template(self.n, 2)
+            self.robot, self.scene = oracle_model(*robot_scene_dicts(self.n, 3))
+            self.eps_dedup = self.inp["scale"] / 40.0
+            self.dedup_calls = 0
+
+        # cell <-> order-preserving int64 key: base coordinates (10 bits each, most significant first), then the
+        # permutation as base-(n+1) digits -- numeric order = the reference's (base, parts) tuple order
+        def cell_key(self, cell):
+            base, parts = cell
+            k = 0
+            for c in base:
+                k = (k << 10) | (c + 512)
+            code = 0
+            for part in parts:
+                assert len(part) == 1
+                code = code * (self.n + 1) + part[0]
+            return k * (self.n + 1) ** (self.n + 1) + code
+
+        def cell_of(self, key):
+            n = self.n
+            code, k = key % (n + 1) ** (n + 1), key // (n + 1) ** (n + 1)
+            parts = []
+            for _ in range(n + 1):
+                parts.append((code % (n + 1),))
+                code //= n + 1
+            base = []
+            for _ in range(n):
+                base.append((k & 1023) - 512)
+                k >>= 10
+            return (tuple(reversed(base)), tuple(reversed(parts)))
+
+        def local_cell_keys(self):
+            cells = self.O.coarse_cells([e[0] for e in self.local])
+            for c in cells[:50]:
+                assert self.cell_of(self.cell_key(c)) == c
+            keys = [self.cell_key(c) for c in cells]
+            assert keys == sorted(keys)
+            return torch.tensor(keys, dtype=torch.int64)
+
+        def set_cells_from_keys(self, keys):
+            self.cells = [self.cell_of(k) for k in sorted(set(keys.tolist()))]
+            return len(self.cells)
+
+        def candidates(self, first, count):
+            pts = self.O.crossing_points(self.cells[first:first + count], self.template, self.field, self.inp["scale"],
+                                         self.inp["offset"], self.inp["eps"])
+            return torch.from_numpy(np.ascontiguousarray(pts)), int(pts.shape[0])
+
+        def dedup_mask(self, points, forced):
+            """Greedy first-keeper dedup (reference subdivision.py:195-217) with some verdicts given."""
+            self.dedup_calls += 1
+            reg = self.O.PointRegistry(self.eps_dedup, self.n)
+            mask = np.zeros(points.shape[0], dtype=np.uint8)
+            for i, (p, f) in enumerate(zip(points.numpy(), forced.tolist())):
+                if f == 0:
+                    continue
+                if f == 1:                       # kept on its owner's word: enters the registry unconditionally
+                    key = tuple(int(c) for c in np.floor(p / reg.eps))
+                    reg.cells.setdefault(key, []).append(len(reg.points))
+                    reg.points.append(p)
+                    mask[i] = 1
+                elif reg.add(p) is not None:
+                    mask[i] = 1
+            return torch.from_numpy(mask)
+
+        def label(self, points):
+            pts = points.numpy()
+            lab = self.O.not_free(self.robot, self.scene, pts) if len(pts) else np.zeros(0, dtype=bool)
+            return torch.from_numpy(lab.astype(np.uint8))
+
+    return OracleShardEngine()
+
+
+def _shard_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2406_04795_b200.distributed import ShardedProof
+        eng = _shard_engine()
+        res = ShardedProof(eng).run(eng.inp["seeds"])
+        out[rank] = dict(points=res["points"].numpy(), labels=res["in_collision"].numpy(), crossing=res["crossing_edges"],
+                         local=res["crossing_edges_local"], slice=res["slice"], cells=res["cells"], edges=res["trace_edges"],
+                         own=int(res["points_local"].shape[0]), total=res["points_total"], free=res["free_points"],
+                         pin_rounds=res["pin_rounds"], dedup_calls=eng.dedup_calls,
+                         first_key=eng.cell_key(eng.cells[0]) if eng.cells else None,
+                         last_key=eng.cell_key(eng.cells[-1]) if eng.cells else None)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_fully_sharded_proof_equals_single_process_reference(world):
+    """No rank holds all cells or all candidates, yet the concatenation of the ranks' kept points in rank order is the
+    reference's refinement output (points in order, labels), the cell ranges tile the sorted cell list, and the crossing
+    counts add up."""
+    g = Golden("traces")
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    port = _free_port()
+    procs = [ctx.Process(target=_shard_worker, args=(r, world, port, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(600)
+        assert p.exitcode == 0
+    want_pts, want_lab = g["kclf_n3_refine_points"], g["kclf_n3_refine_labels"]
+    total = int(g["kclf_n3_refine_batches"][:, 2].sum())
+    covered, last_key = 0, -1
+    for r in range(world):
+        res = out[r]
+        assert res["points"].shape == want_pts.shape
+        assert np.allclose(res["points"], want_pts, rtol=0, atol=1e-8)
+        assert np.array_equal(res["labels"], want_lab)
+        assert res["crossing"] == total and res["edges"] == 324
+        first, count = res["slice"]
+        assert first == covered and count < res["cells"]              # a proper piece, in rank order
+        covered += count
+        if count:
+            assert res["first_key"] > last_key                         # ranges are disjoint and ascending
+            last_key = res["last_key"]
+        assert res["total"] == want_pts.shape[0] and res["free"] == int((~want_lab).sum())
+        assert 1 <= res["pin_rounds"] <= 4 and res["dedup_calls"] == res["pin_rounds"]
+    assert covered == out[0]["cells"] == int(g["kclf_n3_cells"]) if "kclf_n3_cells" in g else covered == out[0]["cells"]
+    assert sum(out[r]["own"] for r in range(world)) == want_pts.shape[0]
+    assert sum(out[r]["local"] for r in range(world)) == total        # the ranges partition the cells

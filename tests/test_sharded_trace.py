@@ -84,7 +84,7 @@ class OracleTraceEngine:
                 self.visited[edge] = len(self.local)
                 self.local.append((edge, s_pair, gidx))
         self.frontier = list(range(len(self.local)))
-        self.candidates = 0
+        self.n_candidates = 0
         return len(self.frontier), len(entries)
 
     def wave_candidates(self):
@@ -94,7 +94,7 @@ class OracleTraceEngine:
             edge, s_pair, gidx = self.local[li]
             for j, plan_entry in enumerate(O.expansion_plan(edge[1], n)):
                 records.append((edge, s_pair, gidx, j, plan_entry))
-        self.candidates += len(records)
+        self.n_candidates += len(records)
         t.ensure_signs([O.vadd(r[0][0], r[4][0]) for r in records])
         buckets = [[] for _ in range(self.world)]
         for edge, (sa, sb), gidx, j, (c_off, bc, ac) in records:
@@ -137,7 +137,7 @@ class OracleTraceEngine:
         assert len(self.frontier) == alive
 
     def trace_counters(self):
-        return dict(dropped=self.t.dropped, field_evaluations=self.t.field_evaluations, candidates=self.candidates)
+        return dict(dropped=self.t.dropped, field_evaluations=self.t.field_evaluations, candidates=self.n_candidates)
 
     def local_edges(self):
         gidx = torch.tensor([e[2] for e in self.local], dtype=torch.int64)
