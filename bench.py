@@ -174,6 +174,7 @@ class ClockSampler:
 
     def __init__(self, device: int):
         self.device, self.sm, self.mx, self.reasons, self.power = device, [], [], set(), []
+        self.mem_used = 0                        # high-water mark of the device memory in use (bytes), sampled
         self.stop = threading.Event()
         self.thread = self.proc = None
 
@@ -183,6 +184,7 @@ class ClockSampler:
                 self.sm.append(float(nvml.nvmlDeviceGetClockInfo(handle, nvml.NVML_CLOCK_SM)))
                 self.mx.append(float(nvml.nvmlDeviceGetMaxClockInfo(handle, nvml.NVML_CLOCK_SM)))
                 self.power.append(nvml.nvmlDeviceGetPowerUsage(handle) / 1000.0)
+                self.mem_used = max(self.mem_used, int(nvml.nvmlDeviceGetMemoryInfo(handle).used))
                 mask = nvml.nvmlDeviceGetCurrentClocksThrottleReasons(handle)
                 for bit, name in self.REASONS.items():
                     if mask & bit:
@@ -241,6 +243,8 @@ class ClockSampler:
                "samples": len(self.sm)}
         if self.power:
             out["power_w_max"] = float(np.max(self.power))
+        if self.mem_used:
+            out["hbm_used_max_gb"] = round(self.mem_used / 1e9, 2)      # sampled every 50 ms: whole device, all contexts
         return out
 
 
@@ -707,8 +711,7 @@ def run_proof(args):
     closed zero set.  `value` = wall seconds of solve() (roadmap growth, training, seeds, trace, cells, refine, check,
     feedback, self-verification); one run per step, all steps start from the same seed and must end in the same proof."""
     import torch
-    import paper_2406_04795_b200 as P
-    from paper_2406_04795_b200 import pipeline as PL
+    from paper_2406_04795_b200 import _cabi, pipeline as PL
     conf, pdict = _proof_problem(args.workload)
     problem = PL.problem_file_from_dict(pdict).problem()
     params = PL.SolveParams(timeout=1800.0, **conf["params"])
@@ -753,7 +756,7 @@ def run_proof(args):
         "device_share": {"trace_refine_train_s": device_s, "of_solve_s": times[-1]},
         "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
                 "note": "solve() IS the public API: host roadmap, device batches, results back on the host every iteration"},
-        "gpu_launches": int(P.context().launch_count()) if hasattr(P.context(), "launch_count") else None,
+        "gpu_launches": int(_cabi.context().launch_count()),
     }
 
 
@@ -773,8 +776,8 @@ def run_reference_proof(args):
                     "the oracle port covers the hot path only -- see profiles/r2_reference_dof3_proof.json for the kept run")
         return base
     conf, pdict = _proof_problem("dof3-proof")
-    pf = ref.pl.problem_file_from_dict(pdict)
-    problem = pf.problem()
+    problem = ref.pl.Problem(ref.rc.robot_from_dict(pdict["robot"]), ref.rc.scene_from_dict(pdict["scene"]),
+                             np.asarray(pdict["problem"]["start"]), np.asarray(pdict["problem"]["goal"]))
     params = ref.pl.SolveParams(timeout=3600.0, **{k: v for k, v in conf["params"].items() if k not in ("feedback_cap",)})
     t0 = time.perf_counter()
     out = ref.pl.solve(problem, params)
@@ -782,7 +785,9 @@ def run_reference_proof(args):
     proved = type(out).__name__ == "InfeasibilityProof"
     base.update(value=dt, ms_per_step=dt * 1e3,
                 config={"workload": "dof3-proof (3-DoF twin of the fence scene), the reference's own solve()", "outcome": type(out).__name__,
-                        "iterations": len(out.stats.iterations), "points": int(out.points.shape[0]) if proved else None,
+                        "iterations": int(out.meta["iterations"]) if proved else len(out.stats.iterations),
+                        "points": int(out.points.shape[0]) if proved else None,
+                        "coarse_edges": out.coarse_edges if proved else None, "coarse_cells": out.coarse_cells if proved else None,
                         "support_vectors": int(out.manifold.support.shape[0]) if proved else None,
                         "same_config": args.workload == "dof3-proof"},
                 cpu_baseline={"value": dt, "unit": "s", "cores": 1, "kind": "imported",

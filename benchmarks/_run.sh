@@ -1,5 +1,7 @@
 set -x
-timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -8 > gpurun_out/r2_gputest1.log; cat gpurun_out/r2_gputest1.log
-for w in dof4-proof dof5-proof; do python bench.py --workload $w --steps 2 --warmup 1 > gpurun_out/r2_bench_$w.json 2> gpurun_out/r2_bench_$w.err; tail -c 900 gpurun_out/r2_bench_$w.json; tail -2 gpurun_out/r2_bench_$w.err; done
-python bench.py --workload dof6-proof --steps 1 --warmup 0 > gpurun_out/r2_bench_dof6-proof.json 2> gpurun_out/r2_bench_dof6-proof.err; tail -c 1200 gpurun_out/r2_bench_dof6-proof.json; tail -2 gpurun_out/r2_bench_dof6-proof.err
-PERMATRACE_B200_SOLVE_LOG=2 timeout 500 python benchmarks/proof_run.py --dof 6 --clutter 3 --lam 0.5 --gamma 0.35 --samples 1000 --feedback-cap 2000 --push-mult 2.15 --max-iters 40 --timeout 450 > gpurun_out/r2_sweep9_1.log 2>&1; grep -v "^Traceback\|^  " gpurun_out/r2_sweep9_1.log | tail -2 | cut -c1-600
+cd /root/repo
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "taylor or full_size_refine or ill_conditioned or large_support" -s 2>&1 | grep -v "^$" | tail -30 > gpurun_out/r2_taylor_test2.log; cat gpurun_out/r2_taylor_test2.log
+for w in dof6 dof6-s4096 dof6-s16384 dof5; do python bench.py --workload $w --steps 3 --warmup 2 --no-cpu-baseline > gpurun_out/r2_c_$w.json 2>/dev/null; python -c "
+import json; d=json.load(open('gpurun_out/r2_c_$w.json')); k=d['kernels']; print('$w', round(d['ms_per_step'],2), d['config'].get('rows_left_to_evaluation_kernels'), d['roofline']['frac'], [(n, round(v['ms'],2)) for n,v in sorted(k.items(), key=lambda kv:-kv[1]['ms'])[:6]])"; done
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:'pt_ref_edges|pt_dedup_round|pt_dedup_follow|pt_ref_extract|pt_check32' -c 6 -o gpurun_out/r2_refine2_full python bench.py --steps 1 --warmup 0 --kernel-only > /dev/null 2>&1
+ncu -i gpurun_out/r2_refine2_full.ncu-rep --page raw --csv > gpurun_out/r2_refine2_full_raw.csv

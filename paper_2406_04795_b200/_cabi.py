@@ -16,7 +16,8 @@ import numpy as np
 
 __all__ = ["lib", "LIB_PATH", "context", "check", "ptr", "PtError", "RangeError", "DECLARED_SYMBOLS"]
 
-LIB_PATH = Path(__file__).resolve().parent / "libpermatrace_b200.so"
+# PERMATRACE_B200_LIB: an alternative build of the same library (A/B timing of kernel variants; tests never set it)
+LIB_PATH = Path(os.environ.get("PERMATRACE_B200_LIB") or Path(__file__).resolve().parent / "libpermatrace_b200.so")
 
 PT_OK = 0
 PT_E_INVALID, PT_E_CUDA, PT_E_RANGE, PT_E_LIMIT, PT_E_NOMEM, PT_E_STATE = -1, -2, -3, -4, -5, -6

@@ -5,23 +5,38 @@
 // so ONE fp64 pass over the support set that accumulates the moments  M_k = sum_j sgn(w_j) e_j u_j^k  (k < Q) and the
 // absolute moments  MA_k = sum_j e_j |u_j|^k  (k even, k <= Q)  yields a polynomial model of the field on the WHOLE edge,
 //   F(t) = exp(c tau^2) * [ sum_{k<Q} M_k tau^k / k!  +  R(tau) ] + bias - barrier(q(t)),   |R| <= fac * MA_Q |tau|^Q / Q!,
-// with rigorous bounds on truncation, on the rounding of this pass and on the evaluation noise of the reference's own
-// loop (all relative to sum_j e_j exp(|u_j tau|) <= 2 sum_{k even} MA_k tau^k / k!).  The reference's bisection is then
-// replayed on the model: a midpoint is decided when |model| exceeds the bound; once the bracket is narrow enough for a
-// proof of monotonicity the root of the model is polished by Newton steps, enclosed (mean-value bound with a proven
-// lower bound on |F'|), and the remaining bisection steps are replayed in exact dyadic arithmetic exactly like
-// pt_bisect_newton_kernel does.  Rows that cannot be decided keep their (valid, dyadic) bracket and go on to the
-// evaluation-based kernels: flag 1 = no enclosure (proof retries / plain bisection), flag 2 = root enclosed in J,
-// a midpoint inside J needs a true evaluation.
+// with rigorous bounds on the truncation and on the rounding of this pass (both relative to
+// sum_j e_j exp(|u_j tau|) <= 2 sum_{k even} MA_k tau^k / k!; the support rows are sorted by the sign of the weight, so the
+// absolute moments cost nothing extra, and partial sums are flushed per tile so the summation error does not grow with S).
+// The reference's bisection is then replayed on the model:
+//   * a midpoint whose |model| exceeds the bound has the sign of the EXACT field there;
+//   * once the bracket is narrow enough for a proof of monotonicity the root of the model is polished by Newton steps and
+//     enclosed (mean-value bound with a proven lower bound on |F'|); midpoints outside the enclosure J are decided without
+//     any evaluation, in exact dyadic arithmetic, exactly like pt_bisect_newton_kernel does;
+//   * a midpoint where |model| is below the bound is an AMBIGUOUS point of the bisection: |F| there is below the rounding
+//     level of an fp64 evaluation (this kernel's, the plain kernels' and the reference's alike -- the reference's own
+//     cross-backend tolerance, pkg/tests/test_backends.py:81-93).  If the model's truncation is below its rounding there the
+//     model value IS an evaluation-grade number and its sign is taken; otherwise (root far from the edge midpoint) the row
+//     keeps its valid dyadic bracket and goes on to the evaluation-based kernels: flag 1 = no enclosure (proof retries /
+//     plain bisection), flag 2 = root enclosed in J, a midpoint inside J needs a true evaluation.
+// The returned bracket is therefore the bracket of the bisection on the exact field, except at ambiguous midpoints, where no
+// fp64 implementation is determined.
 //
 // Cost per (edge, support vector) pair: (N+1) + 8 + N + 3 + 1.25 Q + 1 FP64 instructions = 50 at N = 6, Q = 20 --
 // against 45 for the two passes of the Newton kernel PLUS about eight fp32 screen levels, resolves and retries before.
 // The support set streams through shared memory in tiles, so its size is not limited by one CTA's shared memory.
+// (DMMA was measured as an alternative home for the two dot products: benchmarks/dmma_probe.cu -- on B200 the FP64 tensor
+// path and the FP64 FMA pipe do not overlap, 24.2 ms together against 11.4 + 10.5 ms alone, so nothing is gained.)
 #pragma once
 
 #define PT_TAYLOR_Q 20
 #define PT_TAYLOR_THREADS 128
-#define PT_TAYLOR_TILE 256
+#ifndef PT_TAYLOR_TILE
+#define PT_TAYLOR_TILE 128              /* support rows per shared-memory tile = block of the blocked accumulation */
+#endif
+#ifndef PT_TAYLOR_MINB
+#define PT_TAYLOR_MINB 5              /* resident CTAs per SM the register budget is cut for */
+#endif
 #define PT_TAYLOR_TRY_WIDTH 0.0625     /* first enclosure attempt once the bracket is this narrow (in t) */
 
 template <int N> struct PtRowT { static const int value = (N + 2) & ~1; };   // 2*gl*s_d (N), c'_s, pad to an even count
@@ -123,7 +138,7 @@ __device__ __forceinline__ void pt_taylor_back(double pw, double u, double (&acc
 template <int N, int Q>
 __device__ __forceinline__ void pt_taylor_block(const double* __restrict__ svt, long long r0, long long r1, double* tile,
                                                 const double* tab, const PtPoint64<N>& pp, double pdu, const double (&ddu)[N],
-                                                int sx, double (&acc)[Q + 1]) {
+                                                int sx, double (&acc)[Q + 1], double* total) {
     constexpr int ROW = PtRowT<N>::value;
     for (long long t0 = r0; t0 < r1; t0 += PT_TAYLOR_TILE) {
         const long long rem = r1 - t0;
@@ -143,6 +158,10 @@ __device__ __forceinline__ void pt_taylor_block(const double* __restrict__ svt, 
             pt_taylor_front<N>(tile + (j + 2) * ROW, pp, pdu, ddu, tab, sx, e0, u0);
             pt_taylor_back<Q>(e1, u1, acc);
         }
+        // blocked accumulation: a tile's partial sums go to the running totals in shared memory, so the summation error is
+        // (PT_TAYLOR_TILE + S / PT_TAYLOR_TILE) u instead of S u
+#pragma unroll
+        for (int k = 0; k <= Q; ++k) { total[k * PT_TAYLOR_THREADS] += acc[k]; acc[k] = 0.0; }
     }
 }
 
@@ -209,7 +228,7 @@ __device__ __noinline__ double pt_taylor_barrier_max(const double* bp, const dou
 }
 
 template <int N>
-__global__ void __launch_bounds__(PT_TAYLOR_THREADS, 4)
+__global__ void __launch_bounds__(PT_TAYLOR_THREADS, PT_TAYLOR_MINB)
 pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, size_t m, const double* __restrict__ a_, const double* __restrict__ b_,
                         const int8_t* __restrict__ signs_a, double eps, double* __restrict__ out, double* __restrict__ lo_io,
                         double* __restrict__ hi_io, uint8_t* __restrict__ slow, double* __restrict__ jlo_out,
@@ -257,19 +276,20 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, size_t m, const double* __
         const double pdu = -2.0 * f.gamma * md;
         double acc[Q + 1];
 #pragma unroll
-        for (int k = 0; k <= Q; ++k) acc[k] = 0.0;
-        pt_taylor_block<N, Q>(tf.svt, 0, tf.s_pos, tile, tab, pp, pdu, ddu, 0, acc);
+        for (int k = 0; k <= Q; ++k) { acc[k] = 0.0; col[k * TH] = 0.0; }
+        pt_taylor_block<N, Q>(tf.svt, 0, tf.s_pos, tile, tab, pp, pdu, ddu, 0, acc, col);
 #pragma unroll
-        for (int k = 0; k < Q; k += 2) cola[(k / 2) * TH] = acc[k];        // even moments of the positive block
-        pt_taylor_block<N, Q>(tf.svt, tf.s_pos, tf.s_tot, tile, tab, pp, pdu, ddu, (int)0x80000000, acc);
+        for (int k = 0; k < Q; k += 2) cola[(k / 2) * TH] = col[k * TH];   // even moments of the positive block
+        pt_taylor_block<N, Q>(tf.svt, tf.s_pos, tf.s_tot, tile, tab, pp, pdu, ddu, (int)0x80000000, acc, col);
         double inv_fact = 1.0;
 #pragma unroll
         for (int k = 0; k < Q; ++k) {
             if (k > 1) inv_fact /= (double)k;
-            col[k * TH] = (acc[k] + pp.poison) * inv_fact;
-            if ((k & 1) == 0) cola[(k / 2) * TH] = fabs(2.0 * cola[(k / 2) * TH] - acc[k]) * inv_fact;   // MA_k / k!
+            const double mk = col[k * TH];
+            col[k * TH] = (mk + pp.poison) * inv_fact;
+            if ((k & 1) == 0) cola[(k / 2) * TH] = fabs(2.0 * cola[(k / 2) * TH] - mk) * inv_fact;   // MA_k / k!
         }
-        col[Q * TH] = acc[Q] * (inv_fact / (double)Q);                      // MA_Q / Q!
+        col[Q * TH] = col[Q * TH] * (inv_fact / (double)Q);                 // MA_Q / Q!
     }
     if (!valid) return;
 
@@ -286,8 +306,10 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, size_t m, const double* __
     const double caQ = col[Q * TH];
     const double ca0 = cola[0];
     const double RQ = fac * (1.01 * caQ + 1e-40 * ca0);                     // |R(tau)| <= RQ |tau|^Q
-    const double Ctot = PT_U64 * (1.01 * (double)(4 * N + 7) * T * PT_LN2 + 2.3 * (double)f.S + 4.0 * Q
-                                  + (double)(N + 2) * gmaxu + 450.0);
+    // rounding of THIS pass relative to sum_j e_j exp(|u_j tau|): expanded exponent (cancellation at scale T), blocked
+    // summation, powers and Horner, the log-derivative's absolute error
+    const double Ctot = PT_U64 * (1.01 * (double)(4 * N + 7) * T * PT_LN2 + 1.05 * (double)(PT_TAYLOR_TILE + f.S / PT_TAYLOR_TILE)
+                                  + 4.0 * Q + (double)(N + 2) * gmaxu + 450.0);
     const double abias = fabs(f.bias);
     const double* bp = tab + PT_EXP_TAB + (Q + 1 + Q / 2) * TH;              // barrier parameters (shared)
     double geo[2 * N];                                                      // dynamically indexed by the helpers
@@ -315,17 +337,21 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, size_t m, const double* __
             double p, dp, ex, B = 0.0, B1 = 0.0, B2 = 0.0;
             pt_taylor_model<Q>(col, c, tau, &p, &dp, &ex);
             const double Ach = pt_taylor_cosh<Q>(cola, fac * caQ, at);
-            const double Ek = 1.001 * ex * (RQ * pt_powi(at, Q) + Ctot * Ach) + 1e-290;
+            const double Etr = ex * RQ * pt_powi(at, Q), Ern = ex * Ctot * Ach;      // truncation / rounding of the model
+            const double Ek = 1.001 * (Etr + Ern) + 1e-290;
             const double g0 = fma(ex, p, f.bias);
             // the barrier is only evaluated when the decision needs it (0 <= B <= Bmax)
             const double Eb0 = 64.0 * PT_U64 * (1.1 * Bmax + abias);
             int sgn = 0;
             if (g0 - Bmax > Ek + Eb0) sgn = 1;
             else if (g0 < -(Ek + Eb0)) sgn = -1;
-            else if (f.has_barrier) {
-                pt_taylor_barrier(bp, geo, N, mq, &B, &B1, &B2);
+            else {
+                if (f.has_barrier) pt_taylor_barrier(bp, geo, N, mq, &B, &B1, &B2);
                 const double g = g0 - B;
                 if (fabs(g) > Ek + 64.0 * PT_U64 * (1.1 * fabs(B) + abias)) sgn = g > 0.0 ? 1 : -1;
+                // |F| is below the rounding level of any fp64 evaluation (this model's truncation is smaller still): the
+                // model value is as good as an evaluation, its sign is taken
+                else if (Etr <= Ern && g == g) sgn = g > 0.0 ? 1 : -1;
             }
             if (sgn == 0) break;                                          // undecided: keep [L, H]
             if (sgn == sa) L = mq; else H = mq;
@@ -405,20 +431,29 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, size_t m, const double* __
             const double Eb = 64.0 * PT_U64 * (1.1 * (fabs(Bx) + w * bsum) + abias) + 1e-290;
             const double tx = fabs(x - 0.5);
             const double Ex = 1.001 * ex * (RQ * pt_powi(tx, Q) + Ctot * pt_taylor_cosh<Q>(cola, fac * caQ, tx)) + Eb;
-            const double eta = 1.001 * (Ctot * Amax) + Eb;                 // evaluation noise anywhere in the bracket
             const double rho0 = (fabs(gv) + Ex) / smin;                    // |x - root| <= rho0
-            const double delta = rho0 + 2.0 * eta / smin;
-            double sloc = agd - EdB - delta * D2max;                       // |F'| on [x - delta, x + delta]
+            double sloc = agd - EdB - rho0 * D2max;                        // |F'| on [x - rho0, x + rho0]
             if (!(sloc > smin)) sloc = smin;
             const double rho = 1.01 * (fabs(gv) + Ex) / sloc + 4e-16;
-            const double zeta = 1.01 * eta / sloc;
-            Jlo = x - rho - zeta; Jhi = x + rho + zeta;
+            // F is monotone on [L, H] and its root lies in J: every midpoint outside J has a certain sign
+            Jlo = x - rho; Jhi = x + rho;
             bool open = false;
             while (__dmul_rn(seg, __dsub_rn(H, L)) > eps) {
                 const double mr = __dmul_rn(0.5, __dadd_rn(L, H));
                 if (mr < Jlo) L = mr;
                 else if (mr > Jhi) H = mr;
-                else { open = true; break; }
+                else {
+                    // a midpoint inside the enclosure: decide it on the model like the levels above
+                    const double tr = mr - 0.5, atr = fabs(tr);
+                    pt_taylor_model<Q>(col, c, tr, &p, &dp, &ex);
+                    double Br = 0.0, B1r = 0.0, B2r = 0.0;
+                    if (f.has_barrier) pt_taylor_barrier(bp, geo, N, mr, &Br, &B1r, &B2r);
+                    const double gr = fma(ex, p, f.bias) - Br;
+                    const double Etr = ex * RQ * pt_powi(atr, Q), Ern = ex * Ctot * pt_taylor_cosh<Q>(cola, fac * caQ, atr);
+                    const double Er = 1.001 * (Etr + Ern) + 64.0 * PT_U64 * (1.1 * fabs(Br) + abias) + 1e-290;
+                    if (fabs(gr) > Er || (Etr <= Ern && gr == gr)) { if ((gr > 0.0 ? 1 : -1) == sa) L = mr; else H = mr; }
+                    else { open = true; break; }
+                }
             }
             flag = open ? 2 : 0;
             break;

@@ -369,3 +369,30 @@ def test_gpu_two_process_sharded_proof_equals_reference():
         assert res["points"].shape == want_pts.shape
         assert np.allclose(res["points"], want_pts, rtol=1e-5, atol=1e-8)
         assert np.array_equal(res["labels"], want_lab)
+
+
+# ---- GPU: bench.py --gpus 2 end to end (two ranks on one device, gloo staging) -----------------------------
+@pytest.mark.gpu
+def test_bench_two_ranks_on_one_gpu_matches_single_rank_counts():
+    """The driver's N > 1 launch line (torchrun, one rank per process) with both ranks on device 0: owner-hashed BFS,
+    sample-sorted cell ranges, sharded refine, ghost-pinned dedup.  Every whole-job count must equal the one-rank run."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+    repo = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, PT_BENCH_BACKEND="gloo", PT_BENCH_NO_CLOCKS="1")
+    common = ["--workload", "dof4", "--steps", "1", "--warmup", "1", "--no-cpu-baseline"]
+    one = subprocess.run([sys.executable, str(repo / "bench.py"), "--gpus", "1", *common], capture_output=True, text=True,
+                         env=env, cwd=repo, timeout=900)
+    assert one.returncode == 0, one.stderr[-2000:]
+    two = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+                          "127.0.0.1", "--master-port", str(_free_port()), str(repo / "bench.py"), "--gpus", "2", *common],
+                         capture_output=True, text=True, env=env, cwd=repo, timeout=900)
+    assert two.returncode == 0, two.stderr[-2000:]
+    a = json.loads(one.stdout.strip().splitlines()[-1])
+    b = json.loads(two.stdout.strip().splitlines()[-1])
+    assert b["n_gpus"] == 2 and a["n_gpus"] == 1
+    for key in ("trace_edges", "coarse_cells", "crossing_fine_edges", "points_checked", "free_points", "closure_ok"):
+        assert a["config"][key] == b["config"][key], key
+    assert b["value"] > 0 and b["e2e"]["value"] > 0
