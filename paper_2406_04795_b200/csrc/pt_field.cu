@@ -539,7 +539,7 @@ __global__ void pt_select_shallow_kernel(PtRows rows, const double* __restrict__
 __global__ void pt_select_flag_kernel(const uint8_t* __restrict__ flag, uint8_t want, size_t m, uint32_t* __restrict__ list_out,
                                       unsigned long long* count_out) {
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const bool take = i < m && flag[i] == want;
+    const bool take = i < m && (want == 0xFF ? flag[i] != 0 : flag[i] == want);      // 0xFF: any set flag
     const unsigned ballot = __ballot_sync(0xffffffffu, take);
     if (ballot) {
         const int lane = threadIdx.x & 31, leader = __ffs(ballot) - 1;
@@ -1276,19 +1276,38 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
     } while (0)
     // batches that fill the machine take the one-pass Taylor-model kernel: it either finishes a row or leaves a valid
     // dyadic bracket (flag 1: no enclosure, flag 2: root enclosed) for the evaluation-based kernels below
-    const bool use_taylor = f->taylor && m >= (size_t)ctx->sm_count * 4 * PT_TAYLOR_THREADS;
+    static const long long taylor_min = getenv("PERMATRACE_B200_TAYLOR_MIN") ? atoll(getenv("PERMATRACE_B200_TAYLOR_MIN")) : 0;
+    const bool use_taylor = f->taylor && m >= (taylor_min > 0 ? (size_t)taylor_min : (size_t)ctx->sm_count * 64);
     // batches that fill the machine screen on the tensor cores (tcgen05), small ones on the SIMT kernel
     const bool use_tc = f->tc_ok && m >= (size_t)PT_TC_M * 32;
     const bool by_level = use_tc && (!f->tc_resident || f->tc_levels);
     if (use_taylor) {
-        PT_LAUNCH(ctx, "bisect_fp64_taylor");
         PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PT_TAYLOR_SMEM(N)));
         PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-        static const int no_tail = getenv("PERMATRACE_B200_TAYLOR_NOTAIL") ? atoi(getenv("PERMATRACE_B200_TAYLOR_NOTAIL")) : 0;   // timing experiments only
         const PtTaylorDev td{f->svt.p, f->t_pos, f->t_tot};
-        pt_bisect_taylor_kernel<N><<<pt_grid_for(m, PT_TAYLOR_THREADS), PT_TAYLOR_THREADS, PT_TAYLOR_SMEM(N), ctx->stream>>>(
-            f->d, td, m, a, b, sa, eps, out, lo.p, hi.p, slow.p, jlo.p, jhi.p, ctx->work, no_tail);
-        PT_TRY(pt_check_launch(ctx, "pt_bisect_taylor_kernel"));
+        {
+            PT_LAUNCH(ctx, "bisect_fp64_taylor");
+            pt_bisect_taylor_kernel<N><<<pt_grid_for(m, PT_TAYLOR_THREADS), PT_TAYLOR_THREADS, PT_TAYLOR_SMEM(N), ctx->stream>>>(
+                f->d, td, all, a, b, sa, eps, out, lo.p, hi.p, slow.p, jlo.p, jhi.p, ctx->work, 0);
+            PT_TRY(pt_check_launch(ctx, "pt_bisect_taylor_kernel"));
+        }
+        // rows it left open (root far from the edge midpoint on a long edge: truncation, not rounding, limits the model
+        // there): one more pass, the model recentred on the bracket each row stopped at
+        PtBuf<unsigned long long> tcnt;
+        PT_TRY(tcnt.alloc(ctx, 1));
+        PT_CUDA(ctx, cudaMemsetAsync(tcnt.p, 0, sizeof(unsigned long long), ctx->stream));
+        pt_select_flag_kernel<<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>(slow.p, (uint8_t)0xFF, m, list.p, tcnt.p);
+        PT_TRY(pt_check_launch(ctx, "pt_select_flag_kernel"));
+        unsigned long long left = 0;
+        PT_CUDA(ctx, cudaMemcpyAsync(&left, tcnt.p, sizeof(left), cudaMemcpyDeviceToHost, ctx->stream));
+        PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+        if (left > 0) {
+            PT_LAUNCH(ctx, "bisect_fp64_taylor2");
+            const PtRows again{list.p, tcnt.p, m};
+            pt_bisect_taylor_kernel<N><<<pt_grid_for((size_t)left, PT_TAYLOR_THREADS), PT_TAYLOR_THREADS, PT_TAYLOR_SMEM(N), ctx->stream>>>(
+                f->d, td, again, a, b, sa, eps, out, lo.p, hi.p, slow.p, jlo.p, jhi.p, ctx->work, 1);
+            PT_TRY(pt_check_launch(ctx, "pt_bisect_taylor_kernel"));
+        }
     }
     if (!use_taylor) {
         PT_LAUNCH(ctx, use_tc ? "bisect_fp32_screen_tc" : "bisect_fp32_screen");

@@ -110,10 +110,21 @@ __device__ __forceinline__ void pt_taylor_pair(const double* __restrict__ row, c
 template <int N>
 __device__ __forceinline__ void pt_taylor_front(const double* __restrict__ row, const PtPoint64<N>& pp, double pdu,
                                                 const double (&ddu)[N], const double* __restrict__ tab, int sx, double& e, double& u) {
+#ifdef PT_TAYLOR_TREE
+    // two half-length chains per dot product (one extra add each, half the dependent depth)
+    double arg = row[N] + pp.cp, arg2 = pp.q[N - 1] * row[N - 1], u2_ = ddu[N - 1] * row[N - 1];
+    u = pdu;
+#pragma unroll
+    for (int d = 0; d < (N - 1) / 2; ++d) { arg = fma(pp.q[d], row[d], arg); u = fma(ddu[d], row[d], u); }
+#pragma unroll
+    for (int d = (N - 1) / 2; d < N - 1; ++d) { arg2 = fma(pp.q[d], row[d], arg2); u2_ = fma(ddu[d], row[d], u2_); }
+    arg += arg2; u += u2_;
+#else
     double arg = row[N] + pp.cp;
     u = pdu;
 #pragma unroll
     for (int d = 0; d < N; ++d) { arg = fma(pp.q[d], row[d], arg); u = fma(ddu[d], row[d], u); }
+#endif
     const double ea = pt_exp2_neg(arg, tab);
     e = __hiloint2double(__double2hiint(ea) ^ sx, __double2loint(ea));
 }
@@ -122,6 +133,22 @@ __device__ __forceinline__ void pt_taylor_front(const double* __restrict__ row, 
 template <int Q>
 __device__ __forceinline__ void pt_taylor_back(double pw, double u, double (&acc)[Q + 1]) {
     const double u2 = u * u, u3 = u2 * u, u4 = u2 * u2;
+#ifdef PT_TAYLOR_POWPAR
+    // powers of u^4 by squaring (they only need u, not the exponential): every group's base power is then ONE multiply
+    // away from e, and all Q+1 updates are independent of each other
+    static_assert(Q == 20 || Q == 16 || Q == 12, "power table written out for Q in {12, 16, 20}");
+    const double u8 = u4 * u4, u12 = u8 * u4, u16 = u8 * u8, u20 = u16 * u4;
+    const double pk[6] = {1.0, u4, u8, u12, u16, u20};
+#pragma unroll
+    for (int k = 0; k < Q; k += 4) {
+        const double b = k ? pw * pk[k / 4] : pw;
+        acc[k] += b;
+        acc[k + 1] = fma(b, u, acc[k + 1]);
+        acc[k + 2] = fma(b, u2, acc[k + 2]);
+        acc[k + 3] = fma(b, u3, acc[k + 3]);
+    }
+    acc[Q] += fabs(pw * pk[Q / 4]);
+#else
 #pragma unroll
     for (int k = 0; k < Q; k += 4) {
         acc[k] += pw;
@@ -131,6 +158,7 @@ __device__ __forceinline__ void pt_taylor_back(double pw, double u, double (&acc
         pw *= u4;
     }
     acc[Q] += fabs(pw);
+#endif
 }
 
 // Software-pipelined over the support rows: the (serial) exponent / exponential chain of row j+1 is issued next to the
@@ -229,10 +257,10 @@ __device__ __noinline__ double pt_taylor_barrier_max(const double* bp, const dou
 
 template <int N>
 __global__ void __launch_bounds__(PT_TAYLOR_THREADS, PT_TAYLOR_MINB)
-pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, size_t m, const double* __restrict__ a_, const double* __restrict__ b_,
+pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, PtRows rows, const double* __restrict__ a_, const double* __restrict__ b_,
                         const int8_t* __restrict__ signs_a, double eps, double* __restrict__ out, double* __restrict__ lo_io,
                         double* __restrict__ hi_io, uint8_t* __restrict__ slow, double* __restrict__ jlo_out,
-                        double* __restrict__ jhi_out, unsigned long long* work, int debug_no_tail) {
+                        double* __restrict__ jhi_out, unsigned long long* work, int recentre) {
     constexpr int Q = PT_TAYLOR_Q, ROW = PtRowT<N>::value, TH = PT_TAYLOR_THREADS;
     extern __shared__ double sm[];
     double* tile = sm;
@@ -245,29 +273,35 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, size_t m, const double* __
         bpw[threadIdx.x] = threadIdx.x == 0 ? f.b_scale : threadIdx.x == 1 ? f.b_gain
                          : threadIdx.x < 2 + N ? f.b_lo[threadIdx.x - 2] : f.b_hi[threadIdx.x - 2 - N];
     }
-    const size_t ei = (size_t)blockIdx.x * TH + threadIdx.x;
+    // first pass: all rows, model about the edge midpoint, bracket [0, 1].  Second pass (`recentre`): the listed rows the
+    // first one left open, model about the midpoint of the bracket they stopped at -- the truncation then scales with
+    // (bracket width / 2)^Q instead of 2^-Q
+    const size_t m = pt_rows_total(rows);
+    if ((size_t)blockIdx.x * TH >= m) return;
+    size_t ei = (size_t)blockIdx.x * TH + threadIdx.x;
     const bool valid = ei < m;
-    double a[N], diff[N];
-    double seg = 0.0;
-    int sa = 1;
-#pragma unroll
-    for (int d = 0; d < N; ++d) { a[d] = 0.0; diff[d] = 0.0; }
-    if (valid) {
-        double b[N];
-#pragma unroll
-        for (int d = 0; d < N; ++d) { a[d] = a_[ei * N + d]; b[d] = b_[ei * N + d]; }
-        seg = pt_segment<N>(a, b, diff);
-        sa = signs_a[ei];
-    }
-    const double seg2 = seg * seg;
+    if (valid && rows.list) ei = rows.list[ei];
+    // (row geometry is loaded twice -- here for the pass, again for the tail -- so that nothing but the pass's own
+    //  operands stays live across the support loop: at 96 registers every extra live value spills INSIDE that loop)
     double mnorm2 = 0.0;
     {
-        // ---- the pass over the support set: moments about the edge midpoint ----------------------------------------
+        double a[N], diff[N], L = 0.0, H = 1.0;
+#pragma unroll
+        for (int d = 0; d < N; ++d) { a[d] = 0.0; diff[d] = 0.0; }
+        if (valid) {
+            double b[N];
+#pragma unroll
+            for (int d = 0; d < N; ++d) { a[d] = a_[ei * N + d]; b[d] = b_[ei * N + d]; }
+            pt_segment<N>(a, b, diff);
+            if (recentre) { L = lo_io[ei]; H = hi_io[ei]; }
+        }
+        const double tc = 0.5 * (L + H);
+        // ---- the pass over the support set: moments about the model centre ------------------------------------------
         PtPoint64<N> pp;
         double mc[N], ddu[N], md = 0.0;
 #pragma unroll
         for (int d = 0; d < N; ++d) {
-            mc[d] = fma(0.5, diff[d], a[d]);
+            mc[d] = fma(tc, diff[d], a[d]);
             md = fma(mc[d], diff[d], md);
             ddu[d] = diff[d] * PT_LN2;                     // rows hold 2*gamma*log2e*s_d
             mnorm2 = fma(mc[d], mc[d], mnorm2);
@@ -292,15 +326,28 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, size_t m, const double* __
         col[Q * TH] = col[Q * TH] * (inv_fact / (double)Q);                 // MA_Q / Q!
     }
     if (!valid) return;
+    double a[N], diff[N];
+    double L = 0.0, H = 1.0, seg;
+    {
+        double b[N];
+#pragma unroll
+        for (int d = 0; d < N; ++d) { a[d] = a_[ei * N + d]; b[d] = b_[ei * N + d]; }
+        seg = pt_segment<N>(a, b, diff);
+    }
+    const int sa = signs_a[ei];
+    if (recentre) { L = lo_io[ei]; H = hi_io[ei]; }
+    const double tc = 0.5 * (L + H);                     // model centre (exact: L, H dyadic)
+    const double hr = 0.5 * (H - L);                     // |tau| <= hr on the bracket
+    const double seg2 = seg * seg;
 
     // ---- per-row constants of the bounds --------------------------------------------------------------------------
     const double c = -f.gamma * seg2;
     const double ac = fabs(c);
     const double mn = sqrt(mnorm2);
-    const double pn = mn + f.smax + 0.5 * seg;
+    const double pn = mn + f.smax + hr * seg;
     const double T = f.gamma * PT_L2E * pn * pn;
     const double gmaxu = 2.0 * f.gamma * seg * (mn + f.smax);
-    const double xmax = 0.5 * gmaxu;
+    const double xmax = hr * gmaxu;
     const bool model_ok = xmax < 0.8 * (double)(Q + 1);
     const double fac = 1.0 / (1.0 - xmax / (double)(Q + 1));
     const double caQ = col[Q * TH];
@@ -323,16 +370,15 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, size_t m, const double* __
         Bmax = pt_taylor_barrier_max(bp, geo, N);
     }
 
-    double L = 0.0, H = 1.0;
     int flag = 1;                 // 0 done, 1 no enclosure, 2 enclosed with open midpoints
     double Jlo = -1e300, Jhi = 1e300;
     double D2max = -1.0;
-    if (model_ok && !debug_no_tail) {
+    if (model_ok) {
 #pragma unroll 1
         for (;;) {
             if (!(__dmul_rn(seg, __dsub_rn(H, L)) > eps)) { flag = 0; break; }
             const double mq = __dmul_rn(0.5, __dadd_rn(L, H));
-            const double tau = mq - 0.5;
+            const double tau = mq - tc;
             const double at = fabs(tau);
             double p, dp, ex, B = 0.0, B1 = 0.0, B2 = 0.0;
             pt_taylor_model<Q>(col, c, tau, &p, &dp, &ex);
@@ -361,18 +407,20 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, size_t m, const double* __
             // ---- enclosure attempt on [L, H] ------------------------------------------------------------------------
             if (D2max < 0.0) {
                 // |F''| anywhere on the edge: polynomial part by absolute coefficients, remainder, rounding, barrier
-                double pm0 = 0.0, pm1 = 0.0, pm2 = 0.0, hk = 1.0;     // hk = 0.5^k
+                double pm0 = 0.0, pm1 = 0.0, pm2 = 0.0;
+                double hk = 1.0, hm = 0.0, hn = 0.0;                  // hr^k, hr^(k-1), hr^(k-2)  (0 where the power is negative)
 #pragma unroll 1
                 for (int k = 0; k < Q; ++k) {
                     const double ck = fabs(col[k * TH]);
                     pm0 = fma(ck, hk, pm0);
-                    pm1 = fma(ck * (double)k, 2.0 * hk, pm1);
-                    pm2 = fma(ck * (double)(k * (k - 1)), 4.0 * hk, pm2);
-                    hk *= 0.5;
+                    pm1 = fma(ck * (double)k, hm, pm1);
+                    pm2 = fma(ck * (double)(k * (k - 1)), hn, pm2);
+                    hn = hm; hm = hk; hk *= hr;
+                    if (k == 0) hn = 0.0;
                 }
-                const double hq = pt_powi(0.5, Q);
-                const double r0 = RQ * hq, r1 = RQ * (double)Q * 2.0 * hq, r2 = RQ * (double)(Q * (Q - 1)) * 4.0 * hq;
-                const double Ah = pt_taylor_cosh<Q>(cola, fac * caQ, 0.5);
+                // now hk = hr^Q, hm = hr^(Q-1), hn = hr^(Q-2)
+                const double r0 = RQ * hk, r1 = RQ * (double)Q * hm, r2 = RQ * (double)(Q * (Q - 1)) * hn;
+                const double Ah = pt_taylor_cosh<Q>(cola, fac * caQ, hr);
                 double b2 = 0.0;
                 if (f.has_barrier) {
 #pragma unroll
@@ -382,7 +430,7 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, size_t m, const double* __
                 D2max = 1.01 * ((pm2 + r2) + 2.0 * ac * (pm1 + r1) + (2.0 * ac + ac * ac) * (pm0 + r0)
                                 + 2.0 * Ctot * (gmaxu * gmaxu + 2.0 * ac * (gmaxu + 1.0) + ac * ac) * Ah + b2);
             }
-            const double tmax = fmax(fabs(L - 0.5), fabs(H - 0.5));
+            const double tmax = fmax(fabs(L - tc), fabs(H - tc));
             const double Amax = pt_taylor_cosh<Q>(cola, fac * caQ, tmax);
             const double ptq1 = pt_powi(tmax, Q - 1);
             // |F' - model'| anywhere in the bracket
@@ -390,10 +438,10 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, size_t m, const double* __
                                       + 1.5 * Ctot * (gmaxu + 2.0 * ac * tmax + 1.0) * Amax);
             const double xm = 0.5 * (L + H);
             double Bm = 0.0, B1m = 0.0, B2m = 0.0;
-            pt_taylor_model<Q>(col, c, xm - 0.5, &p, &dp, &ex);
+            pt_taylor_model<Q>(col, c, xm - tc, &p, &dp, &ex);
             if (f.has_barrier) pt_taylor_barrier(bp, geo, N, xm, &Bm, &B1m, &B2m);
             double gv = fma(ex, p, f.bias) - Bm;
-            double gd = ex * fma(2.0 * c * (xm - 0.5), p, dp) - B1m;
+            double gd = ex * fma(2.0 * c * (xm - tc), p, dp) - B1m;
             const double EdB = Ed + 64.0 * PT_U64 * (fabs(gd) + bsum);
             const double smin = fabs(gd) - EdB - 0.5 * w * D2max;
             if (!(smin > 0.0)) continue;                                  // not provably monotone yet: next level
@@ -407,9 +455,9 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, size_t m, const double* __
                 const bool conv = fabs(xn - x) <= 1e-13;
                 x = xn;
                 const double sft = x - xm;
-                pt_taylor_model<Q>(col, c, x - 0.5, &p, &dp, &ex);
+                pt_taylor_model<Q>(col, c, x - tc, &p, &dp, &ex);
                 gv = fma(ex, p, f.bias) - fma(sft, fma(0.5 * B2m, sft, B1m), Bm);
-                gd = ex * fma(2.0 * c * (x - 0.5), p, dp) - fma(B2m, sft, B1m);
+                gd = ex * fma(2.0 * c * (x - tc), p, dp) - fma(B2m, sft, B1m);
                 if (conv) break;
             }
             // exact barrier at the surrogate root, one corrected step, exact residual there
@@ -417,19 +465,19 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, size_t m, const double* __
             if (f.has_barrier) {
                 pt_taylor_barrier(bp, geo, N, x, &Bx, &B1x, &B2x);
                 gv = fma(ex, p, f.bias) - Bx;
-                gd = ex * fma(2.0 * c * (x - 0.5), p, dp) - B1x;
+                gd = ex * fma(2.0 * c * (x - tc), p, dp) - B1x;
                 double xn = x - gv / gd;
                 if (!(xn > L && xn < H)) xn = x;
                 const double moved = fabs(xn - x);
                 x = xn;
-                pt_taylor_model<Q>(col, c, x - 0.5, &p, &dp, &ex);
+                pt_taylor_model<Q>(col, c, x - tc, &p, &dp, &ex);
                 pt_taylor_barrier(bp, geo, N, x, &Bx, &B1x, &B2x);
                 gv = fma(ex, p, f.bias) - Bx;
                 gd = fmax(fabs(gd) - moved * D2max, 0.0);                  // |model'| at the new x, from below
             }
             const double agd = fabs(gd);
             const double Eb = 64.0 * PT_U64 * (1.1 * (fabs(Bx) + w * bsum) + abias) + 1e-290;
-            const double tx = fabs(x - 0.5);
+            const double tx = fabs(x - tc);
             const double Ex = 1.001 * ex * (RQ * pt_powi(tx, Q) + Ctot * pt_taylor_cosh<Q>(cola, fac * caQ, tx)) + Eb;
             const double rho0 = (fabs(gv) + Ex) / smin;                    // |x - root| <= rho0
             double sloc = agd - EdB - rho0 * D2max;                        // |F'| on [x - rho0, x + rho0]
@@ -444,7 +492,7 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, size_t m, const double* __
                 else if (mr > Jhi) H = mr;
                 else {
                     // a midpoint inside the enclosure: decide it on the model like the levels above
-                    const double tr = mr - 0.5, atr = fabs(tr);
+                    const double tr = mr - tc, atr = fabs(tr);
                     pt_taylor_model<Q>(col, c, tr, &p, &dp, &ex);
                     double Br = 0.0, B1r = 0.0, B2r = 0.0;
                     if (f.has_barrier) pt_taylor_barrier(bp, geo, N, mr, &Br, &B1r, &B2r);
@@ -469,8 +517,8 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, size_t m, const double* __
         jlo_out[ei] = flag == 2 ? Jlo : -1e300;
         jhi_out[ei] = flag == 2 ? Jhi : 1e300;
     }
-    if (flag) atomicAdd(&work[3], 1ull);                                  // rows left to the evaluation-based kernels
-    if (threadIdx.x == 0) {
+    if (recentre && flag != 0) atomicAdd(&work[3], 1ull);                 // rows left to the evaluation-based kernels
+    if (threadIdx.x == 0 && !recentre) {
         const size_t first = (size_t)blockIdx.x * TH;
         atomicAdd(&work[7], (unsigned long long)(m - first < (size_t)TH ? m - first : (size_t)TH));
     }

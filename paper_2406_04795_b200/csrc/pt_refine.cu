@@ -71,6 +71,47 @@ __device__ __forceinline__ void pt_decode_cell(const PtGeom& g, u64 key, int* ba
     pt_perm_unrank(g.n, (uint32_t)(key & ((1u << PT_CELL_RANK_BITS) - 1u)), perm);
 }
 
+// ---- array-free cell decoding for the warp-per-cell kernels (runtime-indexed int arrays live in local memory) ----------
+// Packed fine key of the cell's base corner, k*base - fine origin per axis, and the cell's permutation as nibbles
+// (axis perm[j] in bits 4j..4j+3); same digits / label selection as pt_perm_unrank.
+__device__ __forceinline__ void pt_cell_fast(const PtRefGeom& rg, u64 cell_key, u64& base_key, uint32_t& perm_nib) {
+    const PtGeom& g = rg.coarse;
+    const int n = g.n;
+    u64 vk = cell_key >> PT_CELL_RANK_BITS;
+    const u64 cm = (1ull << g.bits) - 1ull;
+    u64 bk = 0;
+    for (int d = n - 1; d >= 0; --d) {
+        const int b = (int)(vk & cm) + g.origin[d];
+        vk >>= g.bits;
+        bk |= (u64)(uint32_t)(rg.k * b - rg.fine.origin[d]) << ((n - 1 - d) * rg.fine.bits);
+    }
+    base_key = bk;
+    uint32_t rank = (uint32_t)(cell_key & ((1u << PT_CELL_RANK_BITS) - 1u));
+    // factorial digits, least significant first: digit i (position i of the permutation) has base n - i
+    uint32_t digits = 0;                       // 3 bits each
+    for (int i = n - 1; i >= 0; --i) { const uint32_t b = (uint32_t)(n - i); digits |= (rank % b) << (3 * i); rank /= b; }
+    uint32_t avail = (1u << n) - 1u, nib = 0;
+    for (int i = 0; i < n; ++i) {
+        uint32_t m = avail, dsel = (digits >> (3 * i)) & 7u;
+        while (dsel--) m &= m - 1u;
+        const uint32_t low = m & (0u - m);
+        nib |= (uint32_t)(__ffs(low) - 1) << (4 * i);
+        avail ^= low;
+    }
+    perm_nib = nib;
+}
+
+// packed fine key of template vertex `tv_row` (n int8 template coordinates) of that cell
+__device__ __forceinline__ u64 pt_fine_vertex_key(const PtRefGeom& rg, u64 base_key, uint32_t perm_nib, const int8_t* __restrict__ tv_row) {
+    const int n = rg.coarse.n;
+    u64 k = base_key;
+    for (int j = 0; j < n; ++j) {
+        const int ax = (int)((perm_nib >> (4 * j)) & 15u);
+        k += (u64)(uint32_t)tv_row[j] << ((n - 1 - ax) * rg.fine.bits);
+    }
+    return k;
+}
+
 __device__ __forceinline__ unsigned long long pt_warp_append64(unsigned long long* counter, bool pred) {
     unsigned ballot = __ballot_sync(0xffffffffu, pred);
     if (ballot == 0) return 0;
@@ -91,17 +132,13 @@ pt_ref_vertices_kernel(PtRefGeom rg, PtTable fv, const u64* __restrict__ cell_ke
     const int lane = threadIdx.x & 31;
     if (w >= ncells) return;
     const int n = rg.coarse.n;
-    int base[PT_NMAX]; uint8_t perm[PT_NMAX];
-    pt_decode_cell(rg.coarse, cell_keys[w], base, perm);
+    u64 base_key; uint32_t perm_nib;
+    pt_cell_fast(rg, cell_keys[w], base_key, perm_nib);      // (the host checked that the fine window holds every cell)
     for (int v0 = 0; v0 < rg.V; v0 += 32) {
         const int v = v0 + lane;
         bool inserted = false; u64 slot = 0;
         if (v < rg.V) {
-            int f[PT_NMAX];
-            pt_fine_vertex(rg, base, perm, tv + v * n, f);
-            u64 key;
-            if (!pt_pack_vertex(rg.fine, f, key)) atomicOr(&ctr->error, PT_ERR_KEY_RANGE);
-            else slot = pt_table_insert(fv, key, inserted, &ctr->error);
+            slot = pt_table_insert(fv, pt_fine_vertex_key(rg, base_key, perm_nib, tv + v * n), inserted, &ctr->error);
             vslot[w * rg.V + v] = (uint32_t)slot;
         }
         unsigned long long pos = pt_warp_append64(&ctr->n_pending, inserted);
@@ -164,12 +201,18 @@ pt_ref_edges_kernel(PtRefGeom rg, PtTable fe, const u64* __restrict__ cell_keys,
                     const int16_t* __restrict__ te, const uint32_t* __restrict__ csign, const unsigned long long* __restrict__ coff,
                     unsigned long long tag_base, PtFineCounters* ctr) {
     __shared__ uint16_t clist[8][PT_RE_SEG];
+    __shared__ u64 vkey[8][PT_MAX_TV];           // packed fine keys of the cell's template vertices
     const size_t w = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     if (w >= ncells) return;
     const int n = rg.coarse.n;
-    int base[PT_NMAX]; uint8_t perm[PT_NMAX];
-    pt_decode_cell(rg.coarse, cell_keys[w], base, perm);
+    {
+        u64 base_key; uint32_t perm_nib;
+        pt_cell_fast(rg, cell_keys[w], base_key, perm_nib);
+        for (int v = lane; v < rg.V; v += 32) vkey[wib][v] = pt_fine_vertex_key(rg, base_key, perm_nib, tv + v * n);
+    }
+    __syncwarp();
+    const int fbits = rg.fine.bits;
     uint32_t sw[PT_SIGN_WORDS];
     for (int i = 0; i < rg.W; ++i) sw[i] = csign[w * rg.W + i];
     unsigned long long running = tag_base + coff[w];
@@ -197,19 +240,16 @@ pt_ref_edges_kernel(PtRefGeom rg, PtTable fe, const u64* __restrict__ cell_keys,
                 const int i0 = te[2 * e], i1 = te[2 * e + 1];
                 const unsigned s0 = (sw[i0 >> 5] >> (i0 & 31)) & 1u, s1 = (sw[i1 >> 5] >> (i1 & 31)) & 1u;
                 const unsigned long long tag = running + (unsigned long long)c;
-                int fa[PT_NMAX], fb[PT_NMAX];
-                pt_fine_vertex(rg, base, perm, tv + i0 * n, fa);
-                pt_fine_vertex(rg, base, perm, tv + i1 * n, fb);
-                bool neg = false; uint32_t mask = 0;
-                for (int d = 0; d < n; ++d) { int df = fb[d] - fa[d]; if (df) mask |= 1u << d; if (df < 0) neg = true; }
-                const int* lo = neg ? fb : fa;
+                // a template edge is a unit step of the fine lattice in some axes, all of one sign: the packed keys of its end
+                // points order like the points, and their difference holds one bit per stepped axis
+                const u64 ka = vkey[wib][i0], kb = vkey[wib][i1];
+                const bool neg = kb < ka;
+                const u64 bk = neg ? kb : ka, dk = neg ? ka - kb : kb - ka;
+                uint32_t mask = 0;
+                for (int d = 0; d < n; ++d) mask |= (uint32_t)((dk >> ((n - 1 - d) * fbits)) & 1ull) << d;
                 const unsigned sbase = neg ? s1 : s0;
-                u64 bk;
-                if (!pt_pack_vertex(rg.fine, lo, bk)) atomicOr(&ctr->error, PT_ERR_KEY_RANGE);
-                else {
-                    u64 slot = pt_table_insert(fe, pt_edge_key(rg.fine, bk, mask), inserted, &ctr->error);
-                    atomicMin(&fe.ent[2 * slot + 1], (tag << 1) | (u64)sbase);
-                }
+                u64 slot = pt_table_insert(fe, pt_edge_key(rg.fine, bk, mask), inserted, &ctr->error);
+                atomicMin(&fe.ent[2 * slot + 1], (tag << 1) | (u64)sbase);
             }
             fresh += __popc(__ballot_sync(0xffffffffu, inserted));
         }
