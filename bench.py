@@ -254,11 +254,11 @@ class ClockSampler:
 
 # DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) and FP64-pipe busy fraction of the big launch of each
 # kernel, from the `ncu --set full` captures summarised under profiles/ (same command, dof6 workload)
-NCU_TRAFFIC = {"bisect_fp64_taylor": 182.006784e6 + 72.592896e6, "bisect_fp64_newton": 206.831104e6 + 76.694016e6,
+NCU_TRAFFIC = {"bisect_fp64_taylor": 171.227392e6 + 82.568192e6, "bisect_fp64_newton": 206.831104e6 + 76.694016e6,
                "bisect_fp32_screen_tc": 170.094592e6 + 19.643648e6}
-NCU_SOURCE = {"bisect_fp64_taylor": "profiles/r2_v1_taylor_full.txt", "bisect_fp64_newton": "profiles/r1_v7_newton_full.txt",
+NCU_SOURCE = {"bisect_fp64_taylor": "profiles/r2_v2_taylor_full.txt", "bisect_fp64_newton": "profiles/r1_v7_newton_full.txt",
               "bisect_fp32_screen_tc": "profiles/r1_v7_tc4_screen_full.txt"}
-NCU_PIPE_BUSY = {"bisect_fp64_taylor": 0.691, "bisect_fp64_newton": 0.691}
+NCU_PIPE_BUSY = {"bisect_fp64_taylor": 0.734, "bisect_fp64_newton": 0.691}
 TAYLOR_Q = 20   # csrc/pt_field_taylor.cuh PT_TAYLOR_Q
 
 
@@ -522,6 +522,9 @@ def run_gpu(args):
             # ONE trace -> cells -> refine(+check) attempt on this synthetic manifold (it is unrelated to the obstacles, so
             # free points remain); a real proof (zero free points, verified certificate) is `--workload dofN-proof`
             "attempt_time_s": ms / args.steps * 1e-3,
+            # every (cell, template edge) crossing is a counted simplex, but the device root-solves each DISTINCT fine edge once
+            "unique_fine_edges_per_s": counts["unique_fine_edges"] * args.steps / (ms * 1e-3),
+            "points_checked_per_s": counts["points"] * args.steps / (ms * 1e-3),
         }
     if world > 1:
         dist.destroy_process_group()

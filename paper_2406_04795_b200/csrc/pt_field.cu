@@ -1492,6 +1492,8 @@ int pt_field_bisect_dev(pt_ctx* ctx, const pt_field* f, const double* a_dev, con
 #undef CALL
 }
 
+extern "C" int pt_debug_tc_arg_error(pt_ctx* ctx, const pt_field* f, const double* a, const double* b, long long m, double* out);
+
 static int pt_field_build_rbf(pt_ctx* ctx, int n, long long S, const double* support, const double* weights,
                               double gamma, double bias, const double* barrier_host, pt_field** out) {
     if (n < 2 || n > 7) return pt_fail(ctx, PT_E_INVALID, "dimension %d unsupported (2..7)", n);
@@ -1588,6 +1590,22 @@ static int pt_field_build_rbf(pt_ctx* ctx, int n, long long S, const double* sup
             const size_t smem4 = (size_t)5 * spad * 16 + 4 * (size_t)6 * PT_TC_M * 16 + (size_t)spad * 4 + 64;
             f->tc4 = n == 6 && smem4 <= PT_TC_SMEM_LIMIT && !(g4_env && g4_env[0] == '0');
             cudaStreamSynchronize(ctx->stream);   // sdev/wdev may be staging buffers released on return
+            // The tensor-core accumulation error is not specified by PTX; PT_TC_ARG_ULPS is calibrated.  Spot-check it on
+            // THIS field (exponents of up to 4096 support vectors against all of them, in fp64): a field whose measured
+            // error passes half the bound does not get the tensor-core paths at all.
+            if (f->tc_resident && S >= 64) {
+                const long long ms = S < 4096 ? S : 4096;
+                std::vector<double> errs((size_t)ms);
+                f->d.sv = f->sv.p;
+                const int src = pt_debug_tc_arg_error(ctx, f, sdev, sdev, ms, errs.data());
+                double worst = 0.0;
+                for (double e : errs) worst = (e == e && e > worst) ? e : (e == e ? worst : 1e300);
+                if (src != PT_OK || !(worst < 0.5 * PT_TC_ARG_ULPS)) {
+                    fprintf(stderr, "[permatrace_b200] tensor-core exponent error %.3g u32*T on this field (bound %.1f): "
+                                    "tensor-core paths disabled for it\n", worst, (double)PT_TC_ARG_ULPS);
+                    f->tc_ok = false; f->tc_resident = false; f->tc4 = false;
+                }
+            }
         }
     }
     f->d.sv = f->sv.p;

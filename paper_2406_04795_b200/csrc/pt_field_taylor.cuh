@@ -224,12 +224,16 @@ __device__ __noinline__ double pt_powi(double x, int k) {
 // barrier(q(t)) and its first two t-derivatives along q(t) = a + t*diff; bp = {scale, gain, lo[n], hi[n]} in shared
 // memory, geo = per-thread {a[n], diff[n]}.  One exp + log1p + division per term; a few ulps from the reference's
 // logaddexp, far inside the 64 u |B| the bounds allow for it.
-__device__ __noinline__ void pt_taylor_barrier(const double* bp, const double* geo, int n, double t, double* B, double* B1, double* B2) {
+// `moving` = bit mask of the coordinates that change along the edge; `acc0` = the (t-independent) sum of the softplus
+// terms of the others (pt_taylor_barrier_const).
+__device__ __noinline__ void pt_taylor_barrier(const double* bp, const double* geo, int n, unsigned moving, double acc0, double t,
+                                               double* B, double* B1, double* B2) {
     const double sc = bp[0], gain = bp[1];
-    double acc = 0.0, b1 = 0.0, b2 = 0.0;
+    double acc = acc0, b1 = 0.0, b2 = 0.0;
 #pragma unroll 1
     for (int i = 0; i < 2 * n; ++i) {
         const int d = i >> 1;
+        if (!((moving >> d) & 1u)) continue;
         const double q = __dadd_rn(geo[d], __dmul_rn(t, geo[n + d]));
         const double x = (i & 1) ? (q - bp[2 + n + d]) / sc : (bp[2 + d] - q) / sc;      // hi side / lo side
         const double e = exp(-fabs(x));
@@ -240,6 +244,20 @@ __device__ __noinline__ void pt_taylor_barrier(const double* bp, const double* g
         b2 = fma(dq * dq, sg * (1.0 - sg), b2);
     }
     *B = gain * sc * acc; *B1 = gain * b1; *B2 = gain / sc * b2;
+}
+
+// softplus terms of the coordinates that do NOT move along the edge (evaluated once per row)
+__device__ __noinline__ double pt_taylor_barrier_const(const double* bp, const double* geo, int n, unsigned moving) {
+    const double sc = bp[0];
+    double acc = 0.0;
+#pragma unroll 1
+    for (int i = 0; i < 2 * n; ++i) {
+        const int d = i >> 1;
+        if ((moving >> d) & 1u) continue;
+        const double x = (i & 1) ? (geo[d] - bp[2 + n + d]) / sc : (bp[2 + d] - geo[d]) / sc;
+        acc += fmax(x, 0.0) + log1p(exp(-fabs(x)));
+    }
+    return acc;
 }
 
 // upper bound of the barrier anywhere on the edge: softplus(x) <= exp(x), each coordinate at its worst end
@@ -362,6 +380,11 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, PtRows rows, const double*
     double geo[2 * N];                                                      // dynamically indexed by the helpers
 #pragma unroll
     for (int d = 0; d < N; ++d) { geo[d] = a[d]; geo[N + d] = diff[d]; }
+    unsigned moving = 0;
+#pragma unroll
+    for (int d = 0; d < N; ++d) moving |= (diff[d] != 0.0 ? 1u : 0u) << d;
+    double bconst_v = -1.0;                                                 // lazily: the barrier terms of the resting coordinates
+    auto bconst = [&]() { if (bconst_v < 0.0) bconst_v = pt_taylor_barrier_const(bp, geo, N, moving); return bconst_v; };
     double bsum = 0.0, Bmax = 0.0;                                          // |B'| <= bsum, 0 <= B <= Bmax on the edge
     if (f.has_barrier) {
 #pragma unroll
@@ -392,7 +415,7 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, PtRows rows, const double*
             if (g0 - Bmax > Ek + Eb0) sgn = 1;
             else if (g0 < -(Ek + Eb0)) sgn = -1;
             else {
-                if (f.has_barrier) pt_taylor_barrier(bp, geo, N, mq, &B, &B1, &B2);
+                if (f.has_barrier) pt_taylor_barrier(bp, geo, N, moving, bconst(), mq, &B, &B1, &B2);
                 const double g = g0 - B;
                 if (fabs(g) > Ek + 64.0 * PT_U64 * (1.1 * fabs(B) + abias)) sgn = g > 0.0 ? 1 : -1;
                 // |F| is below the rounding level of any fp64 evaluation (this model's truncation is smaller still): the
@@ -439,7 +462,7 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, PtRows rows, const double*
             const double xm = 0.5 * (L + H);
             double Bm = 0.0, B1m = 0.0, B2m = 0.0;
             pt_taylor_model<Q>(col, c, xm - tc, &p, &dp, &ex);
-            if (f.has_barrier) pt_taylor_barrier(bp, geo, N, xm, &Bm, &B1m, &B2m);
+            if (f.has_barrier) pt_taylor_barrier(bp, geo, N, moving, bconst(), xm, &Bm, &B1m, &B2m);
             double gv = fma(ex, p, f.bias) - Bm;
             double gd = ex * fma(2.0 * c * (xm - tc), p, dp) - B1m;
             const double EdB = Ed + 64.0 * PT_U64 * (fabs(gd) + bsum);
@@ -460,20 +483,19 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, PtRows rows, const double*
                 gd = ex * fma(2.0 * c * (x - tc), p, dp) - fma(B2m, sft, B1m);
                 if (conv) break;
             }
-            // exact barrier at the surrogate root, one corrected step, exact residual there
+            // exact barrier at the surrogate root and one corrected Newton step; the residual after that step is bounded, not
+            // evaluated: |G(x - G/G')| <= |G''|/2 (G/G')^2
             double Bx = 0.0, B1x = 0.0, B2x = 0.0;
             if (f.has_barrier) {
-                pt_taylor_barrier(bp, geo, N, x, &Bx, &B1x, &B2x);
+                pt_taylor_barrier(bp, geo, N, moving, bconst(), x, &Bx, &B1x, &B2x);
                 gv = fma(ex, p, f.bias) - Bx;
                 gd = ex * fma(2.0 * c * (x - tc), p, dp) - B1x;
-                double xn = x - gv / gd;
-                if (!(xn > L && xn < H)) xn = x;
-                const double moved = fabs(xn - x);
-                x = xn;
-                pt_taylor_model<Q>(col, c, x - tc, &p, &dp, &ex);
-                pt_taylor_barrier(bp, geo, N, x, &Bx, &B1x, &B2x);
-                gv = fma(ex, p, f.bias) - Bx;
-                gd = fmax(fabs(gd) - moved * D2max, 0.0);                  // |model'| at the new x, from below
+                const double step = gv / gd, xn = x - step;
+                if (xn > L && xn < H) {
+                    x = xn;
+                    gv = 0.505 * D2max * step * step;
+                    gd = fmax(fabs(gd) - fabs(step) * D2max, 0.0);         // |model'| at the new x, from below
+                }
             }
             const double agd = fabs(gd);
             const double Eb = 64.0 * PT_U64 * (1.1 * (fabs(Bx) + w * bsum) + abias) + 1e-290;
@@ -495,7 +517,7 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, PtRows rows, const double*
                     const double tr = mr - tc, atr = fabs(tr);
                     pt_taylor_model<Q>(col, c, tr, &p, &dp, &ex);
                     double Br = 0.0, B1r = 0.0, B2r = 0.0;
-                    if (f.has_barrier) pt_taylor_barrier(bp, geo, N, mr, &Br, &B1r, &B2r);
+                    if (f.has_barrier) pt_taylor_barrier(bp, geo, N, moving, bconst(), mr, &Br, &B1r, &B2r);
                     const double gr = fma(ex, p, f.bias) - Br;
                     const double Etr = ex * RQ * pt_powi(atr, Q), Ern = ex * Ctot * pt_taylor_cosh<Q>(cola, fac * caQ, atr);
                     const double Er = 1.001 * (Etr + Ern) + 64.0 * PT_U64 * (1.1 * fabs(Br) + abias) + 1e-290;

@@ -69,7 +69,7 @@ BENCH_CONFIGS = {
     "dof6": dict(n=6, support=2048, lam=0.35, r_split=1.3, obstacles=8),
     "dof6-stress": dict(n=6, support=2048, lam=0.2, r_split=1.3, obstacles=48),
     # BASELINE.json config 5 at its stated size: ~10^9 simplices (crossings grow like lambda^-5)
-    "dof6-stress1g": dict(n=6, support=2048, lam=0.178, r_split=1.3, obstacles=48),
+    "dof6-stress1g": dict(n=6, support=2048, lam=0.175, r_split=1.3, obstacles=48),
     # support set of the size the reference's own solve loop ends with (arm3wall: 4 199 roadmap samples)
     "dof6-s4096": dict(n=6, support=4096, lam=0.35, r_split=1.3, obstacles=8),
     # the support-set size the SURVEY expects for real 6-DoF proofs (10^3..10^4 roadmap samples): 8 support chunks

@@ -23,7 +23,14 @@ def pytest_configure(config):
 @pytest.fixture(scope="session", autouse=True)
 def _built():
     """Make sure the oracle's C kernels and the CUDA library exist (compiles only, no GPU needed)."""
+    import shutil
+    import subprocess
     import __graft_entry__ as entry
+    lib = REPO / "paper_2406_04795_b200" / "libpermatrace_b200.so"
+    if shutil.which("nvcc") is None and lib.exists():
+        # no CUDA toolkit on this machine but a built library travelled with the tree: only the oracle needs compiling
+        subprocess.run(["make", "-s", "-C", str(REPO / "oracle")], check=True)
+        return
     entry.build()
 
 
