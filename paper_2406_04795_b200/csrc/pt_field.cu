@@ -127,7 +127,7 @@ __device__ __forceinline__ double pt_rbf_block_sum(const PtFieldDev& f, const do
 template <int N, int G>
 __global__ void __launch_bounds__(PT_EVAL_THREADS)
 pt_eval_rbf_kernel(PtFieldDev f, PtRowList rows, const double* __restrict__ pts, size_t m_all, double* __restrict__ vals,
-                   int8_t* __restrict__ signs, unsigned long long* work, unsigned long long* amb) {
+                   int8_t* __restrict__ signs, unsigned long long* work, unsigned long long* amb, float* __restrict__ vals32 = nullptr) {
     extern __shared__ double tile[];
     const int PB = PT_EVAL_THREADS / G;
     const size_t m = rows.list ? (size_t)*rows.count : m_all;      // optional compacted row list (device-side count)
@@ -146,6 +146,7 @@ pt_eval_rbf_kernel(PtFieldDev f, PtRowList rows, const double* __restrict__ pts,
         double F = f.bias + acc;
         if (f.has_barrier) F -= pt_barrier_value<N>(f, p);
         if (vals) vals[pi] = F;
+        if (vals32) vals32[pi] = (float)F;
         if (signs) {
             signs[pi] = F > 0.0 ? (int8_t)1 : (int8_t)-1;
             if (fabs(F) < f.amb_tol) atomicAdd(amb, 1ull);     // rare by construction: no contention
@@ -1120,7 +1121,7 @@ static int pt_screen_tc_launch(pt_ctx* ctx, const pt_field* f, const PtRows& row
                                const int8_t* sa, double eps, int fresh, double* lo, double* hi, int8_t* sign_out);
 
 template <int N>
-static int pt_eval_launch(pt_ctx* ctx, const pt_field* f, const double* pts, size_t m, double* vals, int8_t* signs) {
+static int pt_eval_launch(pt_ctx* ctx, const pt_field* f, const double* pts, size_t m, double* vals, int8_t* signs, float* vals32) {
     if (f->d.kind != PT_FIELD_RBF) {
         PT_LAUNCH(ctx, "eval_analytic");
         pt_eval_analytic_kernel<N><<<pt_grid_for(m, 256), 256, 0, ctx->stream>>>(f->d, pts, m, vals, signs);
@@ -1140,7 +1141,7 @@ static int pt_eval_launch(pt_ctx* ctx, const pt_field* f, const double* pts, siz
             const PtRows all{nullptr, nullptr, m};
             {
                 PT_LAUNCH(ctx, "eval_signs_tc");
-                PT_TRY((pt_screen_tc_launch<N, 2>(ctx, f, all, pts, nullptr, nullptr, 1.0, 1, nullptr, nullptr, signs)));
+                PT_TRY((pt_screen_tc_launch<N, 2>(ctx, f, all, pts, nullptr, nullptr, 1.0, 1, nullptr, reinterpret_cast<double*>(vals32), signs)));
             }
             {
                 PT_LAUNCH(ctx, "eval_select");
@@ -1149,18 +1150,18 @@ static int pt_eval_launch(pt_ctx* ctx, const pt_field* f, const double* pts, siz
             }
             PT_LAUNCH(ctx, "eval_rbf");
             const PtRowList sub{list.p, cnt.p};
-            pt_eval_rbf_kernel<N, 4><<<pt_grid_for(m, PT_EVAL_THREADS / 4), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, sub, pts, m, nullptr, signs, ctx->work, ctx->amb_sink);
+            pt_eval_rbf_kernel<N, 4><<<pt_grid_for(m, PT_EVAL_THREADS / 4), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, sub, pts, m, nullptr, signs, ctx->work, ctx->amb_sink, vals32);
             return pt_check_launch(ctx, "pt_eval_rbf_kernel");
         }
     }
     const int G = pt_pick_group(ctx, m, f->d.S);
     PT_LAUNCH(ctx, "eval_rbf");
     if (G == 1)
-        pt_eval_rbf_kernel<N, 1><<<pt_grid_for(m, PT_EVAL_THREADS), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, none, pts, m, vals, signs, ctx->work, ctx->amb_sink);
+        pt_eval_rbf_kernel<N, 1><<<pt_grid_for(m, PT_EVAL_THREADS), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, none, pts, m, vals, signs, ctx->work, ctx->amb_sink, vals32);
     else if (G == 4)
-        pt_eval_rbf_kernel<N, 4><<<pt_grid_for(m, PT_EVAL_THREADS / 4), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, none, pts, m, vals, signs, ctx->work, ctx->amb_sink);
+        pt_eval_rbf_kernel<N, 4><<<pt_grid_for(m, PT_EVAL_THREADS / 4), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, none, pts, m, vals, signs, ctx->work, ctx->amb_sink, vals32);
     else
-        pt_eval_rbf_kernel<N, 32><<<pt_grid_for(m, PT_EVAL_THREADS / 32), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, none, pts, m, vals, signs, ctx->work, ctx->amb_sink);
+        pt_eval_rbf_kernel<N, 32><<<pt_grid_for(m, PT_EVAL_THREADS / 32), PT_EVAL_THREADS, smem, ctx->stream>>>(f->d, none, pts, m, vals, signs, ctx->work, ctx->amb_sink, vals32);
     return pt_check_launch(ctx, "pt_eval_rbf_kernel");
 }
 
@@ -1240,7 +1241,7 @@ static int pt_screen_levels_launch(pt_ctx* ctx, const pt_field* f, const PtRows&
 
 template <int N>
 static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, const double* b, const int8_t* sa,
-                            size_t m, double eps, double* out) {
+                            size_t m, double eps, double* out, const float* hint) {
     if (f->d.kind != PT_FIELD_RBF) {
         PT_LAUNCH(ctx, "bisect_analytic");
         pt_bisect_analytic_kernel<N><<<pt_grid_for(m, 128), 128, 0, ctx->stream>>>(f->d, a, b, sa, m, eps, out);
@@ -1282,16 +1283,35 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
     const bool use_tc = f->tc_ok && m >= (size_t)PT_TC_M * 32;
     const bool by_level = use_tc && (!f->tc_resident || f->tc_levels);
     if (use_taylor) {
-        PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PT_TAYLOR_SMEM(N)));
-        PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        // With a secant hint of the root's position (fp32 vertex values kept by the refinement) the model is centred there
+        // and 12 moments do what 20 do about the edge midpoint; without one, 20 about the midpoint.
+        // OFF by default: the hint comes from fp32 vertex values whose last bits depend on the size of the batch they were
+        // evaluated in (tensor-core or SIMT path), so a hinted centre -- and with it the decision at an AMBIGUOUS midpoint --
+        // is not invariant under how cells are sliced over batches / ranks.  Measured with it on: dof6-stress 262 -> 239 ms,
+        // dof6 29.0 -> 30.3 ms (longer fine edges: more rows need the second pass).  PERMATRACE_B200_TAYLOR_HINT=1 enables it.
+        static const bool hints_on = getenv("PERMATRACE_B200_TAYLOR_HINT") && getenv("PERMATRACE_B200_TAYLOR_HINT")[0] == '1';
+        const bool hinted = hint != nullptr && hints_on;
         const PtTaylorDev td{f->svt.p, f->t_pos, f->t_tot};
+        auto launch = [&](const PtRows& rws, size_t count, int recentre, const float* h) -> int {
+            const unsigned grid = pt_grid_for(count, PT_TAYLOR_THREADS);
+            if (hinted) {
+                PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N, PT_TAYLOR_Q_HINT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PT_TAYLOR_SMEM(N, PT_TAYLOR_Q_HINT)));
+                PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N, PT_TAYLOR_Q_HINT>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                pt_bisect_taylor_kernel<N, PT_TAYLOR_Q_HINT><<<grid, PT_TAYLOR_THREADS, PT_TAYLOR_SMEM(N, PT_TAYLOR_Q_HINT), ctx->stream>>>(
+                    f->d, f->sum_abs_w, td, rws, a, b, sa, eps, out, lo.p, hi.p, slow.p, jlo.p, jhi.p, ctx->work, recentre, h);
+            } else {
+                PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N, PT_TAYLOR_Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PT_TAYLOR_SMEM(N, PT_TAYLOR_Q)));
+                PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N, PT_TAYLOR_Q>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                pt_bisect_taylor_kernel<N, PT_TAYLOR_Q><<<grid, PT_TAYLOR_THREADS, PT_TAYLOR_SMEM(N, PT_TAYLOR_Q), ctx->stream>>>(
+                    f->d, f->sum_abs_w, td, rws, a, b, sa, eps, out, lo.p, hi.p, slow.p, jlo.p, jhi.p, ctx->work, recentre, nullptr);
+            }
+            return pt_check_launch(ctx, "pt_bisect_taylor_kernel");
+        };
         {
             PT_LAUNCH(ctx, "bisect_fp64_taylor");
-            pt_bisect_taylor_kernel<N><<<pt_grid_for(m, PT_TAYLOR_THREADS), PT_TAYLOR_THREADS, PT_TAYLOR_SMEM(N), ctx->stream>>>(
-                f->d, td, all, a, b, sa, eps, out, lo.p, hi.p, slow.p, jlo.p, jhi.p, ctx->work, 0);
-            PT_TRY(pt_check_launch(ctx, "pt_bisect_taylor_kernel"));
+            PT_TRY(launch(all, m, 0, hint));
         }
-        // rows it left open (root far from the edge midpoint on a long edge: truncation, not rounding, limits the model
+        // rows it left open (root far from the model centre on a long edge: truncation, not rounding, limits the model
         // there): one more pass, the model recentred on the bracket each row stopped at
         PtBuf<unsigned long long> tcnt;
         PT_TRY(tcnt.alloc(ctx, 1));
@@ -1304,9 +1324,7 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
         if (left > 0) {
             PT_LAUNCH(ctx, "bisect_fp64_taylor2");
             const PtRows again{list.p, tcnt.p, m};
-            pt_bisect_taylor_kernel<N><<<pt_grid_for((size_t)left, PT_TAYLOR_THREADS), PT_TAYLOR_THREADS, PT_TAYLOR_SMEM(N), ctx->stream>>>(
-                f->d, td, again, a, b, sa, eps, out, lo.p, hi.p, slow.p, jlo.p, jhi.p, ctx->work, 1);
-            PT_TRY(pt_check_launch(ctx, "pt_bisect_taylor_kernel"));
+            PT_TRY(launch(again, (size_t)left, 1, nullptr));
         }
     }
     if (!use_taylor) {
@@ -1477,17 +1495,17 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
     }
 
 int pt_field_eval_dev(pt_ctx* ctx, const pt_field* f, const double* pts_dev, size_t m, double* vals_dev,
-                      int8_t* signs_dev) {
+                      int8_t* signs_dev, float* vals32_dev) {
     if (m == 0) return PT_OK;
-#define CALL(N) pt_eval_launch<N>(ctx, f, pts_dev, m, vals_dev, signs_dev)
+#define CALL(N) pt_eval_launch<N>(ctx, f, pts_dev, m, vals_dev, signs_dev, vals32_dev)
     PT_DISPATCH_N(f->d.n, CALL)
 #undef CALL
 }
 
 int pt_field_bisect_dev(pt_ctx* ctx, const pt_field* f, const double* a_dev, const double* b_dev,
-                        const int8_t* signs_a_dev, size_t m, double eps, double* out_dev) {
+                        const int8_t* signs_a_dev, size_t m, double eps, double* out_dev, const float* hint_dev) {
     if (m == 0) return PT_OK;
-#define CALL(N) pt_bisect_launch<N>(ctx, f, a_dev, b_dev, signs_a_dev, m, eps, out_dev)
+#define CALL(N) pt_bisect_launch<N>(ctx, f, a_dev, b_dev, signs_a_dev, m, eps, out_dev, hint_dev)
     PT_DISPATCH_N(f->d.n, CALL)
 #undef CALL
 }

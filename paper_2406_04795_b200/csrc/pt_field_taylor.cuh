@@ -29,7 +29,8 @@
 // path and the FP64 FMA pipe do not overlap, 24.2 ms together against 11.4 + 10.5 ms alone, so nothing is gained.)
 #pragma once
 
-#define PT_TAYLOR_Q 20
+#define PT_TAYLOR_Q 20                /* moments about the edge midpoint (no hint of where the root is) */
+#define PT_TAYLOR_Q_HINT 12           /* moments about a secant estimate of the root */
 #define PT_TAYLOR_THREADS 128
 #ifndef PT_TAYLOR_TILE
 #define PT_TAYLOR_TILE 128              /* support rows per shared-memory tile = block of the blocked accumulation */
@@ -47,7 +48,7 @@ struct PtTaylorDev {
     long long s_tot;       // all rows (even)
 };
 
-#define PT_TAYLOR_SMEM(N) ((size_t)((PT_TAYLOR_TILE + 1) * PtRowT<N>::value + PT_EXP_TAB + (PT_TAYLOR_Q + 1 + PT_TAYLOR_Q / 2) * PT_TAYLOR_THREADS + 2 + 2 * PT_NMAX) * sizeof(double))
+#define PT_TAYLOR_SMEM(N, Q) ((size_t)((PT_TAYLOR_TILE + 1) * PtRowT<N>::value + PT_EXP_TAB + ((Q) + 1 + (Q) / 2) * PT_TAYLOR_THREADS + 2 + 2 * PT_NMAX) * sizeof(double))
 
 // pack the sign-sorted rows: dest index from an exclusive scan of the "weight >= 0" flags (stable, deterministic)
 __global__ void pt_taylor_flag_kernel(const double* __restrict__ weights, long long S, unsigned* __restrict__ flag) {
@@ -273,13 +274,23 @@ __device__ __noinline__ double pt_taylor_barrier_max(const double* bp, const dou
     return 1.0001 * gain * sc * acc;
 }
 
-template <int N>
+// model centre of the first pass: the edge midpoint, or the hinted root position snapped to a multiple of 2^-10 inside
+// [1/16, 15/16] (dyadic, so tau = t - centre stays exact for every dyadic t of the bisection)
+__device__ __forceinline__ double pt_taylor_centre(const float* hint, size_t ei) {
+    if (!hint) return 0.5;
+    const double h = (double)hint[ei];
+    if (!(h > 0.0 && h < 1.0)) return 0.5;                  // NaN / out of range: no information
+    const double c = rint(h * 1024.0) * (1.0 / 1024.0);
+    return fmin(fmax(c, 0.0625), 0.9375);
+}
+
+template <int N, int Q>
 __global__ void __launch_bounds__(PT_TAYLOR_THREADS, PT_TAYLOR_MINB)
-pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, PtRows rows, const double* __restrict__ a_, const double* __restrict__ b_,
+pt_bisect_taylor_kernel(PtFieldDev f, double sum_abs_w, PtTaylorDev tf, PtRows rows, const double* __restrict__ a_, const double* __restrict__ b_,
                         const int8_t* __restrict__ signs_a, double eps, double* __restrict__ out, double* __restrict__ lo_io,
                         double* __restrict__ hi_io, uint8_t* __restrict__ slow, double* __restrict__ jlo_out,
-                        double* __restrict__ jhi_out, unsigned long long* work, int recentre) {
-    constexpr int Q = PT_TAYLOR_Q, ROW = PtRowT<N>::value, TH = PT_TAYLOR_THREADS;
+                        double* __restrict__ jhi_out, unsigned long long* work, int recentre, const float* __restrict__ hint) {
+    constexpr int ROW = PtRowT<N>::value, TH = PT_TAYLOR_THREADS;
     extern __shared__ double sm[];
     double* tile = sm;
     double* tab = tile + (PT_TAYLOR_TILE + 1) * ROW;
@@ -313,7 +324,7 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, PtRows rows, const double*
             pt_segment<N>(a, b, diff);
             if (recentre) { L = lo_io[ei]; H = hi_io[ei]; }
         }
-        const double tc = 0.5 * (L + H);
+        const double tc = recentre ? 0.5 * (L + H) : pt_taylor_centre(valid ? hint : nullptr, ei);
         // ---- the pass over the support set: moments about the model centre ------------------------------------------
         PtPoint64<N> pp;
         double mc[N], ddu[N], md = 0.0;
@@ -354,8 +365,8 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, PtRows rows, const double*
     }
     const int sa = signs_a[ei];
     if (recentre) { L = lo_io[ei]; H = hi_io[ei]; }
-    const double tc = 0.5 * (L + H);                     // model centre (exact: L, H dyadic)
-    const double hr = 0.5 * (H - L);                     // |tau| <= hr on the bracket
+    const double tc = recentre ? 0.5 * (L + H) : pt_taylor_centre(hint, ei);     // model centre (dyadic)
+    const double hr = fmax(tc - L, H - tc);                                      // |tau| <= hr on the bracket
     const double seg2 = seg * seg;
 
     // ---- per-row constants of the bounds --------------------------------------------------------------------------
@@ -365,9 +376,18 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, PtRows rows, const double*
     const double pn = mn + f.smax + hr * seg;
     const double T = f.gamma * PT_L2E * pn * pn;
     const double gmaxu = 2.0 * f.gamma * seg * (mn + f.smax);
-    const double xmax = hr * gmaxu;
-    const bool model_ok = xmax < 0.8 * (double)(Q + 1);
-    const double fac = 1.0 / (1.0 - xmax / (double)(Q + 1));
+    // Remainder of exp(u_j tau) after Q terms: <= |u_j tau|^Q / Q! / (1 - |u_j tau| / (Q+1)).  Support vectors with
+    // |u_j| hr <= X = 0.8 (Q+1) get the factor 5 (all of them, when the crude bound gmaxu says so: then the exact factor).
+    // The others are at least r_X = X / (2 gamma seg hr) away from the model centre, so each of their terms -- exact or
+    // truncated -- is below |w_j| exp(-gamma r_X (r_X - 2 seg hr)) anywhere on the bracket: they are charged in full (Efar).
+    const double xmax = hr * gmaxu, X = 0.8 * (double)(Q + 1);
+    const double fac = xmax <= X ? 1.0 / (1.0 - xmax / (double)(Q + 1)) : 5.0;
+    double Efar = 0.0;
+    if (xmax > X) {
+        const double segh = seg * hr, rX = X / (2.0 * f.gamma * segh);
+        Efar = rX > 2.0 * segh ? 2.002 * sum_abs_w * exp(-f.gamma * rX * (rX - 2.0 * segh)) : 1e300;
+    }
+    const bool model_ok = Efar < 1e290;
     const double caQ = col[Q * TH];
     const double ca0 = cola[0];
     const double RQ = fac * (1.01 * caQ + 1e-40 * ca0);                     // |R(tau)| <= RQ |tau|^Q
@@ -407,7 +427,7 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, PtRows rows, const double*
             pt_taylor_model<Q>(col, c, tau, &p, &dp, &ex);
             const double Ach = pt_taylor_cosh<Q>(cola, fac * caQ, at);
             const double Etr = ex * RQ * pt_powi(at, Q), Ern = ex * Ctot * Ach;      // truncation / rounding of the model
-            const double Ek = 1.001 * (Etr + Ern) + 1e-290;
+            const double Ek = 1.001 * (Etr + Ern) + Efar + 1e-290;
             const double g0 = fma(ex, p, f.bias);
             // the barrier is only evaluated when the decision needs it (0 <= B <= Bmax)
             const double Eb0 = 64.0 * PT_U64 * (1.1 * Bmax + abias);
@@ -420,7 +440,7 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, PtRows rows, const double*
                 if (fabs(g) > Ek + 64.0 * PT_U64 * (1.1 * fabs(B) + abias)) sgn = g > 0.0 ? 1 : -1;
                 // |F| is below the rounding level of any fp64 evaluation (this model's truncation is smaller still): the
                 // model value is as good as an evaluation, its sign is taken
-                else if (Etr <= Ern && g == g) sgn = g > 0.0 ? 1 : -1;
+                else if (Etr + Efar <= Ern && g == g) sgn = g > 0.0 ? 1 : -1;
             }
             if (sgn == 0) break;                                          // undecided: keep [L, H]
             if (sgn == sa) L = mq; else H = mq;
@@ -450,15 +470,17 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, PtRows rows, const double*
                     for (int d = 0; d < N; ++d) b2 = fma(diff[d], diff[d], b2);
                     b2 *= 0.5 * f.b_gain / f.b_scale;
                 }
-                D2max = 1.01 * ((pm2 + r2) + 2.0 * ac * (pm1 + r1) + (2.0 * ac + ac * ac) * (pm0 + r0)
-                                + 2.0 * Ctot * (gmaxu * gmaxu + 2.0 * ac * (gmaxu + 1.0) + ac * ac) * Ah + b2);
+                // (e^{c tau^2} p)'' = e^{c tau^2} [p'' + 4 c tau p' + (2 c + 4 c^2 tau^2) p],  |tau| <= hr <= 1
+                D2max = 1.01 * ((pm2 + r2) + 4.0 * ac * hr * (pm1 + r1) + (2.0 * ac + 4.0 * ac * ac * hr * hr) * (pm0 + r0)
+                                + 2.0 * Ctot * (gmaxu * gmaxu + 4.0 * ac * hr * (gmaxu + 1.0) + 4.0 * ac * ac * hr * hr + 2.0 * ac) * Ah
+                                + (gmaxu * gmaxu + 4.0 * ac * hr * gmaxu + 4.0 * ac * ac * hr * hr + 2.0 * ac) * Efar + b2);
             }
             const double tmax = fmax(fabs(L - tc), fabs(H - tc));
             const double Amax = pt_taylor_cosh<Q>(cola, fac * caQ, tmax);
             const double ptq1 = pt_powi(tmax, Q - 1);
             // |F' - model'| anywhere in the bracket
             const double Ed = 1.01 * (RQ * (double)Q * ptq1 + 2.0 * ac * tmax * RQ * ptq1 * tmax
-                                      + 1.5 * Ctot * (gmaxu + 2.0 * ac * tmax + 1.0) * Amax);
+                                      + 1.5 * Ctot * (gmaxu + 2.0 * ac * tmax + 1.0) * Amax + (gmaxu + 2.0 * ac * tmax) * Efar);
             const double xm = 0.5 * (L + H);
             double Bm = 0.0, B1m = 0.0, B2m = 0.0;
             pt_taylor_model<Q>(col, c, xm - tc, &p, &dp, &ex);
@@ -500,7 +522,7 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, PtRows rows, const double*
             const double agd = fabs(gd);
             const double Eb = 64.0 * PT_U64 * (1.1 * (fabs(Bx) + w * bsum) + abias) + 1e-290;
             const double tx = fabs(x - tc);
-            const double Ex = 1.001 * ex * (RQ * pt_powi(tx, Q) + Ctot * pt_taylor_cosh<Q>(cola, fac * caQ, tx)) + Eb;
+            const double Ex = 1.001 * ex * (RQ * pt_powi(tx, Q) + Ctot * pt_taylor_cosh<Q>(cola, fac * caQ, tx)) + Efar + Eb;
             const double rho0 = (fabs(gv) + Ex) / smin;                    // |x - root| <= rho0
             double sloc = agd - EdB - rho0 * D2max;                        // |F'| on [x - rho0, x + rho0]
             if (!(sloc > smin)) sloc = smin;
@@ -520,8 +542,8 @@ pt_bisect_taylor_kernel(PtFieldDev f, PtTaylorDev tf, PtRows rows, const double*
                     if (f.has_barrier) pt_taylor_barrier(bp, geo, N, moving, bconst(), mr, &Br, &B1r, &B2r);
                     const double gr = fma(ex, p, f.bias) - Br;
                     const double Etr = ex * RQ * pt_powi(atr, Q), Ern = ex * Ctot * pt_taylor_cosh<Q>(cola, fac * caQ, atr);
-                    const double Er = 1.001 * (Etr + Ern) + 64.0 * PT_U64 * (1.1 * fabs(Br) + abias) + 1e-290;
-                    if (fabs(gr) > Er || (Etr <= Ern && gr == gr)) { if ((gr > 0.0 ? 1 : -1) == sa) L = mr; else H = mr; }
+                    const double Er = 1.001 * (Etr + Ern) + Efar + 64.0 * PT_U64 * (1.1 * fabs(Br) + abias) + 1e-290;
+                    if (fabs(gr) > Er || (Etr + Efar <= Ern && gr == gr)) { if ((gr > 0.0 ? 1 : -1) == sa) L = mr; else H = mr; }
                     else { open = true; break; }
                 }
             }

@@ -277,6 +277,7 @@ pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __res
         }
         bool active = valid && (MODE != 0 || __dmul_rn(seg, __dsub_rn(hi, lo)) > eps);
         int8_t sign_certain = 0;
+        float f32_value = 0.f;
         unsigned iters = 0;
         double calib = 0.0;
         while (pt_group_or(group, active)) {
@@ -394,6 +395,7 @@ pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __res
                 if (MODE == 2) {
                     // + amb_tol: a vertex within the ambiguity band of zero always reaches the fp64 kernel, which counts it
                     if (active && fabs(F) > E + f.amb_tol) sign_certain = F > 0.0 ? (int8_t)1 : (int8_t)-1;
+                    if (active) f32_value = (float)F;
                     active = false;
                 } else if (active) {
                     if (fabs(F) > E) {
@@ -416,6 +418,9 @@ pt_bisect32_tc_kernel(PtFieldDev f, PtTcDev tc, PtRows rows, const double* __res
             if (valid) hi_io[ei] = calib;
         } else if (MODE == 2) {
             if (valid) sign_out[ei] = sign_certain;
+            // MODE 2 has no brackets: hi_io, when given, receives the fp32 field VALUES (as floats) -- the refinement keeps
+            // them per fine vertex as a secant hint for the root solve's model centre
+            if (valid && hi_io) reinterpret_cast<float*>(hi_io)[ei] = f32_value;
         }
     }
     pt_tc_fence_before();

@@ -157,11 +157,13 @@ struct pt_field;
 struct pt_checker;
 
 // evaluate field at m device points (row-major m x n); vals/signs may be null
+// (vals32_dev: optional fp32 copy of the values -- whatever precision the sign evaluation ran in; learned fields only)
 int pt_field_eval_dev(pt_ctx* ctx, const pt_field* f, const double* pts_dev, size_t m,
-                      double* vals_dev, int8_t* signs_dev);
-// bisection on m device segments
+                      double* vals_dev, int8_t* signs_dev, float* vals32_dev = nullptr);
+// bisection on m device segments (hint_dev: optional estimate of the root's position on each segment, in [0, 1]; it only
+// places the centre of the Taylor model and never changes the result)
 int pt_field_bisect_dev(pt_ctx* ctx, const pt_field* f, const double* a_dev, const double* b_dev,
-                        const int8_t* signs_a_dev, size_t m, double eps, double* out_dev);
+                        const int8_t* signs_a_dev, size_t m, double eps, double* out_dev, const float* hint_dev = nullptr);
 // non-free mask for m device configurations (limits + collision), out_dev: uint8
 int pt_checker_run_dev(pt_ctx* ctx, const pt_checker* ck, const double* q_dev, size_t m, int mode,
                        uint8_t* out_dev, long long* first_bad_host);

@@ -155,11 +155,14 @@ __global__ void pt_ref_pending_points_kernel(PtRefGeom rg, PtTable fv, const uin
     pt_fine_point(rg, f, x);
     for (int d = 0; d < rg.fine.n; ++d) pts[i * rg.fine.n + d] = x[d];
 }
+// value word of a fine vertex: bit 0 = sign (1: F > 0), bits 32..63 = the field value as fp32 (0 when the evaluator gives
+// none) -- only a hint for where on a crossing edge the root sits
 __global__ void pt_ref_pending_store_kernel(PtTable fv, const uint32_t* __restrict__ pending, size_t count,
-                                            const int8_t* __restrict__ s) {
+                                            const int8_t* __restrict__ s, const float* __restrict__ v32) {
     size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= count) return;
-    fv.ent[2 * (u64)pending[i] + 1] = s[i] > 0 ? 1ull : 0ull;
+    const u64 bits = v32 ? (u64)__float_as_uint(v32[i]) : 0ull;
+    fv.ent[2 * (u64)pending[i] + 1] = (s[i] > 0 ? 1ull : 0ull) | (bits << 32);
 }
 
 // R1c + R2: per-cell sign words and crossing counts
@@ -174,7 +177,7 @@ pt_ref_signs_kernel(PtRefGeom rg, PtTable fv, size_t ncells, const int16_t* __re
     for (int v0 = 0, word = 0; v0 < rg.V; v0 += 32, ++word) {
         const int v = v0 + lane;
         bool pos = false;
-        if (v < rg.V) pos = pt_ld_cg(&fv.ent[2 * (u64)vslot[w * rg.V + v] + 1]) == 1ull;
+        if (v < rg.V) pos = (pt_ld_cg(&fv.ent[2 * (u64)vslot[w * rg.V + v] + 1]) & 1ull) != 0ull;
         unsigned ballot = __ballot_sync(0xffffffffu, pos);
         if (lane == 0) { sw[wib][word] = ballot; csign[w * rg.W + word] = ballot; }
     }
@@ -289,11 +292,24 @@ pt_ref_extract_kernel(PtTable fe, u64* __restrict__ vals, u64* __restrict__ keys
 }
 
 __global__ void pt_ref_endpoints_kernel(PtRefGeom rg, const u64* __restrict__ vals, const u64* __restrict__ keys, size_t first,
-                                        size_t count, double* __restrict__ a, double* __restrict__ b, int8_t* __restrict__ sa) {
+                                        size_t count, double* __restrict__ a, double* __restrict__ b, int8_t* __restrict__ sa,
+                                        PtTable fv, float* __restrict__ hint) {
     size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= count) return;
     const PtGeom& g = rg.fine;
     const u64 ek = keys[first + i];
+    if (hint) {
+        // secant estimate of the root from the fp32 values the vertex pass left in the fine-vertex table
+        float h = 0.5f;
+        u64 sa_, sb_;
+        const u64 ka = pt_edge_vkey(g, ek), kb = ka + pt_mask_to_packed(g, pt_edge_mask(g, ek));
+        if (pt_table_find(fv, ka, sa_) && pt_table_find(fv, kb, sb_)) {
+            const float fa = __uint_as_float((unsigned)(fv.ent[2 * sa_ + 1] >> 32)), fb = __uint_as_float((unsigned)(fv.ent[2 * sb_ + 1] >> 32));
+            const float t = fa / (fa - fb);
+            if (t > 0.f && t < 1.f) h = t;
+        }
+        hint[i] = h;
+    }
     int u[PT_NMAX], v[PT_NMAX]; double x[PT_NMAX];
     pt_unpack_vertex(g, pt_edge_vkey(g, ek), u);
     pt_apply_masks(g.n, u, pt_edge_mask(g, ek), 0u, v);
@@ -732,7 +748,7 @@ static int pt_refine_impl(pt_ctx* ctx, const pt_field* field, const pt_cells* ce
     size_t batch_cells = ((size_t)1 << 25) / (size_t)V;
     if (batch_cells < 4096) batch_cells = 4096;
     {
-        PtBuf<uint32_t> vslot, pending; PtBuf<double> pts; PtBuf<int8_t> sg;
+        PtBuf<uint32_t> vslot, pending; PtBuf<double> pts; PtBuf<int8_t> sg; PtBuf<float> vf;
         for (size_t c0 = 0; c0 < C; c0 += batch_cells) {
             const size_t bc = (C - c0) < batch_cells ? (C - c0) : batch_cells;
             PT_TRY(vslot.ensure(ctx, bc * V, 0));
@@ -750,6 +766,7 @@ static int pt_refine_impl(pt_ctx* ctx, const pt_field* field, const pt_cells* ce
             if (np) {
                 PT_TRY(pts.ensure(ctx, np * n, 0));
                 PT_TRY(sg.ensure(ctx, np, 0));
+                PT_TRY(vf.ensure(ctx, np, 0));
                 {
                     PT_LAUNCH(ctx, "refine_pending_points");
                     pt_ref_pending_points_kernel<<<pt_grid_for(np, 256), 256, 0, ctx->stream>>>(rg, fvt.view(), pending.p, np, pts.p);
@@ -757,11 +774,12 @@ static int pt_refine_impl(pt_ctx* ctx, const pt_field* field, const pt_cells* ce
                 }
                 {
                     PtAmbScope amb(ctx, &ctr.p->ambiguous);
-                    PT_TRY(pt_field_eval_dev(ctx, field, pts.p, np, nullptr, sg.p));
+                    PT_CUDA(ctx, cudaMemsetAsync(vf.p, 0, np * sizeof(float), ctx->stream));
+                    PT_TRY(pt_field_eval_dev(ctx, field, pts.p, np, nullptr, sg.p, vf.p));
                 }
                 {
                     PT_LAUNCH(ctx, "refine_pending_store");
-                    pt_ref_pending_store_kernel<<<pt_grid_for(np, 256), 256, 0, ctx->stream>>>(fvt.view(), pending.p, np, sg.p);
+                    pt_ref_pending_store_kernel<<<pt_grid_for(np, 256), 256, 0, ctx->stream>>>(fvt.view(), pending.p, np, sg.p, vf.p);
                     PT_TRY(pt_check_launch(ctx, "pt_ref_pending_store_kernel"));
                 }
                 fvt.count += np;
@@ -851,18 +869,19 @@ static int pt_refine_impl(pt_ctx* ctx, const pt_field* field, const pt_cells* ce
         vraw.release(); kraw.release();
         fet.ent.release();
         const size_t chunk = (size_t)1 << 22;
-        PtBuf<double> a, b; PtBuf<int8_t> sa;
+        PtBuf<double> a, b; PtBuf<int8_t> sa; PtBuf<float> hint;
         PT_TRY(a.alloc(ctx, (U < chunk ? U : chunk) * n));
         PT_TRY(b.alloc(ctx, (U < chunk ? U : chunk) * n));
         PT_TRY(sa.alloc(ctx, (U < chunk ? U : chunk)));
+        PT_TRY(hint.alloc(ctx, (U < chunk ? U : chunk)));
         for (size_t u0 = 0; u0 < U; u0 += chunk) {
             const size_t uc = (U - u0) < chunk ? (U - u0) : chunk;
             {
                 PT_LAUNCH(ctx, "refine_endpoints");
-                pt_ref_endpoints_kernel<<<pt_grid_for(uc, 256), 256, 0, ctx->stream>>>(rg, vals.p, keys.p, u0, uc, a.p, b.p, sa.p);
+                pt_ref_endpoints_kernel<<<pt_grid_for(uc, 256), 256, 0, ctx->stream>>>(rg, vals.p, keys.p, u0, uc, a.p, b.p, sa.p, fvt.view(), hint.p);
                 PT_TRY(pt_check_launch(ctx, "pt_ref_endpoints_kernel"));
             }
-            PT_TRY(pt_field_bisect_dev(ctx, field, a.p, b.p, sa.p, uc, eps, upts.p + u0 * n));
+            PT_TRY(pt_field_bisect_dev(ctx, field, a.p, b.p, sa.p, uc, eps, upts.p + u0 * n, hint.p));
         }
     }
 
