@@ -194,17 +194,54 @@ __global__ void pt_pending_store_kernel(PtTable sgn, const uint32_t* __restrict_
 }
 
 // ---- wave kernels ----------------------------------------------------------------------------
+// Packed-key arithmetic for the wave kernels.  Every vertex a frontier edge (u, s) touches is u + 1_P - 1_M with disjoint
+// coordinate sets P, M (its cofaces' third vertices and partner-edge end points), so with
+//   * the packed key of u,
+//   * a per-block table `pk[mask]` = packed image of a 0/1 coordinate mask (shared memory, 2^n entries),
+//   * two per-edge bit sets: the coordinates where u sits on the upper / lower face of the clamp box,
+// a candidate costs a few adds and bit tests instead of unpacking into runtime-indexed int arrays (local memory):
+//   key(u + 1_P - 1_M) = key(u) + pk[P] - pk[M]     (no carry crosses a field while every coordinate stays in the window)
+//   in box  <=>  P misses the upper-face set and M misses the lower-face set.
+// `safe` (all coordinates of u at least one unit inside the key window) guards the arithmetic; the few edges on the window
+// border take the array path below.
+struct PtEdgeFast { u64 vk; uint32_t at_hi, at_lo; bool safe; };
+
+__device__ __forceinline__ void pt_fill_packmask(const PtGeom& g, u64* pk) {
+    for (uint32_t m = threadIdx.x; m < (1u << g.n); m += blockDim.x) pk[m] = pt_mask_to_packed(g, m);
+}
+
+__device__ __forceinline__ PtEdgeFast pt_edge_fast(const PtGeom& g, u64 ek) {
+    PtEdgeFast e;
+    e.vk = pt_edge_vkey(g, ek);
+    e.at_hi = 0; e.at_lo = 0; e.safe = true;
+    const u64 fm = (1ull << g.bits) - 1ull;
+    u64 k = e.vk;
+    for (int d = g.n - 1; d >= 0; --d) {
+        const int r = (int)(k & fm);
+        k >>= g.bits;
+        e.safe = e.safe && r >= 1 && r <= (int)fm - 1;
+        if (g.has_box) {
+            const int v = r + g.origin[d];
+            if (v >= g.box_hi[d]) e.at_hi |= 1u << d;
+            if (v <= g.box_lo[d]) e.at_lo |= 1u << d;
+        }
+    }
+    return e;
+}
+
 __global__ void __launch_bounds__(256)
 pt_wave_probe_kernel(PtGeom g, PtTable sgn, const u64* __restrict__ edge_key, const uint32_t* __restrict__ frontier,
                      size_t fcount, int stride, uint32_t* __restrict__ sgn_slot, uint32_t* __restrict__ pending,
                      PtCounters* ctr) {
+    __shared__ u64 pk[1 << PT_NMAX];
+    pt_fill_packmask(g, pk);
+    __syncthreads();
     const size_t w = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= fcount) return;
     const u64 ek = edge_key[frontier[w]];
     const uint32_t s = pt_edge_mask(g, ek);
-    int u[PT_NMAX];
-    pt_unpack_vertex(g, pt_edge_vkey(g, ek), u);
+    const PtEdgeFast ef = pt_edge_fast(g, ek);
     const int nc = pt_ncofaces(g.n, s);
     if (lane == 0) atomicAdd(&ctr->candidates, (unsigned long long)nc);
     for (int j0 = 0; j0 < nc; j0 += 32) {
@@ -212,11 +249,16 @@ pt_wave_probe_kernel(PtGeom g, PtTable sgn, const u64* __restrict__ edge_key, co
         bool inserted = false; u64 slot = 0;
         if (j < nc) {
             PtCoface f = pt_coface(g.n, s, j);
-            int c[PT_NMAX];
-            pt_apply_masks(g.n, u, f.c_plus, f.c_minus, c);
-            u64 ck;
-            if (!pt_pack_vertex(g, c, ck)) atomicOr(&ctr->error, PT_ERR_KEY_RANGE);
-            else slot = pt_table_insert(sgn, ck, inserted, &ctr->error);
+            if (ef.safe) {
+                slot = pt_table_insert(sgn, ef.vk + pk[f.c_plus] - pk[f.c_minus], inserted, &ctr->error);
+            } else {
+                int u[PT_NMAX], c[PT_NMAX];
+                pt_unpack_vertex(g, ef.vk, u);
+                pt_apply_masks(g.n, u, f.c_plus, f.c_minus, c);
+                u64 ck;
+                if (!pt_pack_vertex(g, c, ck)) atomicOr(&ctr->error, PT_ERR_KEY_RANGE);
+                else slot = pt_table_insert(sgn, ck, inserted, &ctr->error);
+            }
             sgn_slot[w * stride + j] = (uint32_t)slot;
         }
         unsigned long long pos = pt_warp_append(&ctr->n_pending, inserted);
@@ -246,6 +288,9 @@ pt_wave_partner_kernel(PtGeom g, PtTable sgn, PtTable vis, const u64* __restrict
                        const int8_t* __restrict__ edge_sa, const uint32_t* __restrict__ frontier, size_t fcount,
                        int stride, const uint32_t* __restrict__ sgn_slot, uint32_t* __restrict__ vis_slot,
                        PtCounters* ctr) {
+    __shared__ u64 pk[1 << PT_NMAX];
+    pt_fill_packmask(g, pk);
+    __syncthreads();
     const size_t w = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (w >= fcount) return;
@@ -253,8 +298,7 @@ pt_wave_partner_kernel(PtGeom g, PtTable sgn, PtTable vis, const u64* __restrict
     const u64 ek = edge_key[e];
     const int sa = edge_sa[e];
     const uint32_t s = pt_edge_mask(g, ek);
-    int u[PT_NMAX];
-    pt_unpack_vertex(g, pt_edge_vkey(g, ek), u);
+    const PtEdgeFast ef = pt_edge_fast(g, ek);
     const int nc = pt_ncofaces(g.n, s);
     for (int j0 = 0; j0 < stride; j0 += 32) {
         const int j = j0 + lane;
@@ -262,23 +306,35 @@ pt_wave_partner_kernel(PtGeom g, PtTable sgn, PtTable vis, const u64* __restrict
         bool dropped = false;
         if (j < nc) {
             const int sc = pt_ld_cg(&sgn.ent[2 * (u64)sgn_slot[w * stride + j] + 1]) ? 1 : -1;
-            PtPartner p = pt_partner(g.n, u, s, sa, j, sc);
-            int other[PT_NMAX];
-            pt_apply_masks(g.n, p.base, p.mask, 0u, other);
-            if (!(pt_in_box(g, p.base) && pt_in_box(g, other))) {
-                dropped = true;
+            u64 bk = 0; uint32_t pmask = 0; int sign_base = 0; bool ok = true;
+            if (ef.safe) {
+                // partner edge (tracer.py:340-350): base = u + 1_bplus - 1_bminus, other end = base + 1_mask; both are
+                // u plus / minus disjoint coordinate sets, so the box test is two bit tests
+                const PtCoface f = pt_coface(g.n, s, j);
+                uint32_t bplus, bminus;
+                if (sc == sa) { bplus = f.bc_bplus; bminus = f.bc_bminus; pmask = f.bc_mask; sign_base = f.bc_shared ? -sa : sc; }
+                else { bplus = f.ac_bplus; bminus = f.ac_bminus; pmask = f.ac_mask; sign_base = f.ac_shared ? sa : sc; }
+                const uint32_t up = bplus | (pmask & ~bminus), down = bminus & ~pmask;      // all vertices: u + 1_up' - 1_down', up' <= up
+                if (((bplus | up) & ef.at_hi) || ((bminus | down) & ef.at_lo)) dropped = true;
+                else bk = ef.vk + pk[bplus] - pk[bminus];
             } else {
-                u64 bk;
-                if (!pt_pack_vertex(g, p.base, bk)) atomicOr(&ctr->error, PT_ERR_KEY_RANGE);
-                else {
-                    bool ins;
-                    u64 slot = pt_table_insert(vis, pt_edge_key(g, bk, p.mask), ins, &ctr->error);
-                    const u64 mine = PT_VAL_PENDING_BASE + (u64)(w * stride + j);
-                    const u64 old = atomicMin(&vis.ent[2 * slot + 1], mine);
-                    // an already admitted edge or a smaller pending slot beats this candidate for good:
-                    // only candidates that lowered the value stay in the winner scan
-                    if (old > mine) marker = (uint32_t)slot | (p.sign_base > 0 ? 0x80000000u : 0u);
-                }
+                int u[PT_NMAX];
+                pt_unpack_vertex(g, ef.vk, u);
+                PtPartner p = pt_partner(g.n, u, s, sa, j, sc);
+                int other[PT_NMAX];
+                pt_apply_masks(g.n, p.base, p.mask, 0u, other);
+                pmask = p.mask; sign_base = p.sign_base;
+                if (!(pt_in_box(g, p.base) && pt_in_box(g, other))) dropped = true;
+                else if (!pt_pack_vertex(g, p.base, bk)) { atomicOr(&ctr->error, PT_ERR_KEY_RANGE); ok = false; }
+            }
+            if (!dropped && ok) {
+                bool ins;
+                u64 slot = pt_table_insert(vis, pt_edge_key(g, bk, pmask), ins, &ctr->error);
+                const u64 mine = PT_VAL_PENDING_BASE + (u64)(w * stride + j);
+                const u64 old = atomicMin(&vis.ent[2 * slot + 1], mine);
+                // an already admitted edge or a smaller pending slot beats this candidate for good:
+                // only candidates that lowered the value stay in the winner scan
+                if (old > mine) marker = (uint32_t)slot | (sign_base > 0 ? 0x80000000u : 0u);
             }
         }
         unsigned db = __ballot_sync(0xffffffffu, dropped);
