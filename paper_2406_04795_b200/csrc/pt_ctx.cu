@@ -1,5 +1,6 @@
 // Context, error reporting, stream-ordered allocation and the CUDA-event kernel profiler.
 #include <stdarg.h>
+#include <stdlib.h>
 #include "pt_internal.cuh"
 
 // FP64 peak microbenchmark: 8 independent DFMA chains per thread, enough blocks to fill the chip
@@ -98,6 +99,16 @@ void pt_dev_free(pt_ctx* ctx, void* p) {
     if (size > PT_CACHE_MAX_BLOCK) { cudaFreeAsync(p, ctx->stream); return; }
     ctx->free_blocks.emplace(size, p);
     ctx->cached_bytes += size;
+    // the cache is a working-set optimisation, not a reservation: a loop whose batch sizes keep growing (solve() at 6 DoF)
+    // leaves ever larger free blocks behind; past the cap everything cached goes back to the driver's pool
+    static const size_t cap = (size_t)(getenv("PERMATRACE_B200_CACHE_GB") ? atof(getenv("PERMATRACE_B200_CACHE_GB")) : 48.0) << 30;
+    if (ctx->cached_bytes > cap) {
+        pt_cache_release(ctx);
+        // cudaFreeAsync only hands the blocks to the stream-ordered pool; trimming the pool is what gives the memory back
+        cudaStreamSynchronize(ctx->stream);
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, ctx->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+    }
 }
 
 extern "C" void* pt_host_alloc(pt_ctx* ctx, long long bytes) {

@@ -1,8 +1,9 @@
 """Sharding of the hot path across GPUs (one process per GPU, torch.distributed).
 
-    BFS trace       owner-hashed: rank r owns the edges whose base vertex hashes to r; per wave ONE all_to_all of 16-byte
-                    candidate records, admission by minimum tag on the owner, all_gather of the winners' tags for the
-                    global admission order (`ShardedTrace`)
+    BFS trace       owner-hashed: rank r owns the edges whose base vertex hashes to r; per wave three collectives --
+                    all_gather of the W x W count matrix, ONE all_to_all of 16-byte candidate records, all_gather of the
+                    winners' tags (padded to a bound the count matrix already gives) -- admission by minimum tag on the
+                    owner, global admission order from the tags (`ShardedTrace`)
     coarse cells    every rank enumerates the cell cofaces of ITS edges, then the sorted unique cell list is built by a
                     range-partitioned sample sort of the packed 64-bit cell keys: all_gather of a few samples per rank ->
                     common splitters -> all_to_all of key ranges -> local sort + unique.  Rank r ends up with the r-th
@@ -170,16 +171,47 @@ class ShardedTrace(_Transport):
     def __init__(self, engine, group=None):
         self._init_transport(engine, group)
 
+    def _wave_exchange(self, records, counts):
+        """Candidates to their owners.  ONE all_gather of the per-destination counts gives every rank the whole W x W count
+        matrix (its own receive sizes AND an upper bound for every rank's winner list), then one all_to_all of the records."""
+        import torch
+        if self.world == 1:
+            return records, [int(records.shape[0])]
+        mine = torch.tensor([int(c) for c in counts], dtype=torch.int64, device=self.comm_device)
+        rows = [torch.zeros_like(mine) for _ in range(self.world)]
+        self.dist.all_gather(rows, mine, group=self.group)
+        matrix = torch.stack(rows).tolist()                        # matrix[src][dst]
+        recv_counts = [int(matrix[src][self.rank]) for src in range(self.world)]
+        received = self._exchange_rows(records, counts, recv_counts)
+        return received, [sum(int(matrix[src][dst]) for src in range(self.world)) for dst in range(self.world)]
+
+    def _wave_winners(self, tags, bounds):
+        """All ranks' ascending winner tags.  A rank wins at most what it received (`bounds`, known from the count matrix),
+        so the lists are gathered padded to the largest bound with a sentinel -- no separate size exchange."""
+        import torch
+        if self.world == 1:
+            return [tags]
+        cap = max(max(bounds), 1)
+        sentinel = torch.iinfo(torch.int64).max
+        padded = torch.full((cap,), sentinel, dtype=torch.int64, device=self.comm_device)
+        padded[: tags.shape[0]] = self._out(tags)
+        parts = [torch.empty_like(padded) for _ in range(self.world)]
+        self.dist.all_gather(parts, padded, group=self.group)
+        stacked = torch.stack(parts)
+        sizes = (stacked != sentinel).sum(dim=1).tolist()
+        return [self._back(stacked[r, : int(sizes[r])]) for r in range(self.world)]
+
     def run(self, seeds, max_edges: int) -> dict:
         eng = self.engine
         local_frontier, total = eng.trace_locate(seeds, self.rank, self.world)
         frontier = self._sum([local_frontier])[0]
         levels, complete = 0, total <= max_edges
         while frontier > 0 and complete:
+            # per wave: all_gather(counts) + all_to_all(records) + all_gather(winner tags)
             records, counts = eng.wave_candidates()
-            received = self._exchange(records, counts)
+            received, bounds = self._wave_exchange(records, counts)
             tags = eng.wave_admit(received)
-            gidx, alive, new_total, complete = rank_winners(self._gather_var(tags), self.rank, total, max_edges)
+            gidx, alive, new_total, complete = rank_winners(self._wave_winners(tags, bounds), self.rank, total, max_edges)
             eng.wave_commit(gidx, alive, new_total)
             frontier, total = new_total - total, new_total
             levels += 1
