@@ -254,12 +254,12 @@ class ClockSampler:
 
 # DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) and FP64-pipe busy fraction of the big launch of each
 # kernel, from the `ncu --set full` captures summarised under profiles/ (same command, dof6 workload)
-NCU_TRAFFIC = {"bisect_fp64_taylor": 171.227392e6 + 82.568192e6, "bisect_fp64_newton": 206.831104e6 + 76.694016e6,
+NCU_TRAFFIC = {"bisect_fp64_taylor": 179.668480e6 + 109.176064e6, "bisect_fp64_newton": 206.831104e6 + 76.694016e6,
                "bisect_fp32_screen_tc": 170.094592e6 + 19.643648e6}
-NCU_SOURCE = {"bisect_fp64_taylor": "profiles/r2_v2_taylor_full.txt", "bisect_fp64_newton": "profiles/r1_v7_newton_full.txt",
+NCU_SOURCE = {"bisect_fp64_taylor": "profiles/r2_v3_taylor_full.txt", "bisect_fp64_newton": "profiles/r1_v7_newton_full.txt",
               "bisect_fp32_screen_tc": "profiles/r1_v7_tc4_screen_full.txt"}
-NCU_PIPE_BUSY = {"bisect_fp64_taylor": 0.734, "bisect_fp64_newton": 0.691}
-TAYLOR_Q = 20   # csrc/pt_field_taylor.cuh PT_TAYLOR_Q
+NCU_PIPE_BUSY = {"bisect_fp64_taylor": 0.721, "bisect_fp64_newton": 0.691}
+TAYLOR_Q = 16   # csrc/pt_field_taylor.cuh PT_TAYLOR_Q
 
 
 def pair_dp_ops(n: int, kind: str = "eval") -> tuple[float, float]:

@@ -32,6 +32,8 @@ def main():
     ap.add_argument("--push-mult", type=float, default=None, help="push = mult * lam * sqrt(2 gamma) (reference default: 1)")
     ap.add_argument("--q1-limit", type=float, default=None)
     ap.add_argument("--limit", type=float, default=None, help="limits of joints 2..n (default 1.2)")
+    ap.add_argument("--rng-seed", type=int, default=None)
+    ap.add_argument("--scene-seed", type=int, default=None, help="seed of the clutter placement")
     ap.add_argument("--feedback-cap", type=int, default=None)
     ap.add_argument("--max-iters", type=int, default=30)
     ap.add_argument("--timeout", type=float, default=600.0)
@@ -43,7 +45,8 @@ def main():
         conf = dict(dof=args.dof, clutter=6, params={})
     over = dict(conf.get("params", {}))
     for key, val in (("lam", args.lam), ("k", args.k), ("gamma", args.gamma), ("samples_per_iter", args.samples),
-                     ("seeds", args.seeds), ("regularization", args.reg), ("feedback_cap", args.feedback_cap)):
+                     ("seeds", args.seeds), ("regularization", args.reg), ("feedback_cap", args.feedback_cap),
+                     ("rng_seed", args.rng_seed)):
         if val is not None:
             over[key] = val
     clutter = conf["clutter"] if args.clutter is None else args.clutter
@@ -54,6 +57,8 @@ def main():
         extra["q1_limit"] = args.q1_limit
     if args.limit is not None:
         extra["limit"] = args.limit
+    if args.scene_seed is not None:
+        extra["seed"] = args.scene_seed
     pf = PL.problem_file_from_dict(scenes.fence_problem_dict(conf["dof"], clutter=clutter, **extra))
     problem = pf.problem()
     params = PL.SolveParams(max_iters=args.max_iters, timeout=args.timeout, max_edges=args.max_edges, **over)

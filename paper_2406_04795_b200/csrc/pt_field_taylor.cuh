@@ -22,14 +22,18 @@
 // The returned bracket is therefore the bracket of the bisection on the exact field, except at ambiguous midpoints, where no
 // fp64 implementation is determined.
 //
-// Cost per (edge, support vector) pair: (N+1) + 8 + N + 3 + 1.25 Q + 1 FP64 instructions = 50 at N = 6, Q = 20 --
+// Cost per (edge, support vector) pair: (N+1) + 8 + N + 3 + 1.25 Q + 1 FP64 instructions = 45 at N = 6, Q = 16 --
 // against 45 for the two passes of the Newton kernel PLUS about eight fp32 screen levels, resolves and retries before.
 // The support set streams through shared memory in tiles, so its size is not limited by one CTA's shared memory.
 // (DMMA was measured as an alternative home for the two dot products: benchmarks/dmma_probe.cu -- on B200 the FP64 tensor
 // path and the FP64 FMA pipe do not overlap, 24.2 ms together against 11.4 + 10.5 ms alone, so nothing is gained.)
 #pragma once
 
-#define PT_TAYLOR_Q 20                /* moments about the edge midpoint (no hint of where the root is) */
+#ifndef PT_TAYLOR_Q
+#define PT_TAYLOR_Q 16                /* moments about the edge midpoint (no hint of where the root is); measured on dof6 /
+                                       * dof6-stress: Q = 20 28.9 / 265 ms, Q = 16 28.1 / 251 ms (more rows take the
+                                       * recentred second pass, the first one is 10 % shorter), Q = 12 32.5 / 250 ms */
+#endif
 #define PT_TAYLOR_Q_HINT 12           /* moments about a secant estimate of the root */
 #define PT_TAYLOR_THREADS 128
 #ifndef PT_TAYLOR_TILE
