@@ -134,6 +134,11 @@ PROOF_CONFIGS = {
                                                        push=_push(0.35, 0.5, 2.5), max_iters=30)),
     "dof6-proof": dict(dof=6, clutter=0, params=dict(lam=0.5, k=2, gamma=0.35, samples_per_iter=1000, seeds=20, feedback_cap=2000,
                                                        push=_push(0.5, 0.35, 2.15), max_iters=40, max_edges=200_000_000)),
+    # the same arm with three clutter primitives in reach of the distal links (clutter seed 5; seeds 11 and 3 leave the loop
+    # with 2-4 free points in a joint-limit corner after 40 iterations)
+    "dof6-clutter-proof": dict(dof=6, clutter=3, scene=dict(seed=5),
+                               params=dict(lam=0.5, k=2, gamma=0.35, samples_per_iter=1000, seeds=20, feedback_cap=2000,
+                                           push=_push(0.5, 0.35, 2.15), max_iters=40, max_edges=200_000_000)),
     # the 3-DoF twin the reference's CPU loop finishes in minutes (its own arm3wall pattern, same generator)
     "dof3-proof": dict(dof=3, clutter=0, params=dict(lam=0.15, k=2, gamma=2.0, samples_per_iter=600, seeds=20, max_iters=30)),
 }
