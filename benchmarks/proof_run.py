@@ -61,7 +61,7 @@ def main():
         extra["seed"] = args.scene_seed
     pf = PL.problem_file_from_dict(scenes.fence_problem_dict(conf["dof"], clutter=clutter, **extra))
     problem = pf.problem()
-    params = PL.SolveParams(max_iters=args.max_iters, timeout=args.timeout, max_edges=args.max_edges, **over)
+    params = PL.SolveParams(**{**dict(max_iters=args.max_iters, timeout=args.timeout, max_edges=args.max_edges), **over})
     t0 = time.perf_counter()
     out = PL.solve(problem, params)
     dt = time.perf_counter() - t0
