@@ -307,8 +307,10 @@ __global__ void pt_bisect_analytic_kernel(PtFieldDev f, const double* __restrict
 }
 
 
-// ==== fast root solve ===================================================================================
-// The reference bisects every crossing edge ~30 times in fp64.  The fast path returns the SAME dyadic
+// ==== evaluation-based root solve =======================================================================
+// Batches of 9.5 k rows and more are solved by ONE pass of the Taylor-model kernel (pt_field_taylor.cuh, included below);
+// what follows serves smaller batches and the rows that kernel leaves open (none on the benchmark workloads).
+// The reference bisects every crossing edge ~30 times in fp64.  This path returns the SAME dyadic
 // bracket midpoint with ~6 fp64 evaluations per edge:
 //   K1 pt_bisect32_kernel     replays the bisection with the field evaluated in fp32; a step is taken only
 //                             when |F32| exceeds a rigorous bound on |F32 - F| (the decision then equals the

@@ -261,3 +261,23 @@ def test_collision_schema_roundtrip_and_validation():
         CO.batch_check(np.zeros((1, 4)), robot, scene, on_limit="maybe")
     lo, hi = CO.joint_limits(robot)
     assert np.all(lo == -1.5) and np.all(hi == 1.5)
+
+
+def test_proof_workloads_are_well_formed_problem_files():
+    """Every end-to-end proof workload (scenes.PROOF_CONFIGS) is a problem file in the reference's schema: robot and scene
+    parse, start / goal have the robot's dimension and respect its limits, the SolveParams overrides are accepted, and the
+    bias push stays below 1 (labels are +-1: a larger push cannot separate start from goal)."""
+    from paper_2406_04795_b200 import collision as CO, pipeline as PL, scenes
+    for name, conf in scenes.PROOF_CONFIGS.items():
+        pdict = scenes.fence_problem_dict(conf["dof"], clutter=conf["clutter"], **conf.get("scene", {}))
+        robot, scene = CO.robot_from_dict(pdict["robot"]), CO.scene_from_dict(pdict["scene"])
+        assert robot.dof == conf["dof"] and len(scene.obstacles) == 1 + conf["clutter"], name
+        lo, hi = CO.joint_limits(robot)
+        for key in ("start", "goal"):
+            q = np.asarray(pdict["problem"][key], dtype=np.float64)
+            assert q.shape == (conf["dof"],) and np.all(q >= lo) and np.all(q <= hi), (name, key)
+        params = PL.SolveParams(**conf["params"])
+        push = params.push if params.push is not None else params.lam * np.sqrt(2.0 * params.gamma)
+        assert 0.0 < push < 1.0, name
+        # the same dict is what the reference's loader takes (round trip through its YAML-level schema)
+        assert set(pdict) == {"robot", "scene", "problem"}

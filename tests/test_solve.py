@@ -271,3 +271,44 @@ def test_problem_rejects_bad_endpoints(golden):
     robot2, scene2, _ = _problem(g, "gap2d")
     b = PL.Problem(robot2, scene2, g["gap2d/start"], g["gap2d/goal"])
     assert PL.fingerprint(a) != PL.fingerprint(b) and len(PL.fingerprint(a)) == 64
+
+
+# ---- the proof workloads of bench.py (scenes.PROOF_CONFIGS) ---------------------------------------------------
+def _solve_proof_workload(name):
+    from paper_2406_04795_b200 import pipeline as PL, scenes
+    conf = scenes.PROOF_CONFIGS[name]
+    pdict = scenes.fence_problem_dict(conf["dof"], clutter=conf["clutter"], **conf.get("scene", {}))
+    problem = PL.problem_file_from_dict(pdict).problem()
+    out = PL.solve(problem, PL.SolveParams(timeout=600.0, **conf["params"]))
+    return problem, out
+
+
+@pytest.mark.gpu
+def test_fence_twin_matches_the_reference_solve():
+    """`dof3-proof`, the 3-DoF twin of the fence scenes: the reference's own solve() on the same problem file and parameters
+    (profiles/r2_reference_dof3_proof.json, 52 s on the CPU) ends after 3 iterations with 1984 coarse edges, 3002 cells,
+    7877 certificate points and 2305 support vectors -- so must this one, and the certificate must verify."""
+    from paper_2406_04795_b200 import pipeline as PL
+    problem, out = _solve_proof_workload("dof3-proof")
+    assert isinstance(out, PL.InfeasibilityProof)
+    assert int(out.meta["iterations"]) == 3
+    assert (out.coarse_edges, out.coarse_cells, out.points.shape[0], out.manifold.support.shape[0]) == (1984, 3002, 7877, 2305)
+    assert [r.get("roadmap") for r in out.stats.iterations] == [602, 1643, 2305]
+    assert PL.verify_proof(out, problem).ok
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["dof4-proof", "dof5-proof"])
+def test_high_dof_infeasibility_proofs(name):
+    """BASELINE configs 2-3: the whole outer loop on a 4- / 5-DoF arm behind a fence, with clutter: it must end in an
+    InfeasibilityProof with no free point among its collision-checked points, accepted by verify_proof incl. the
+    reconstruction check (re-trace + re-refinement from the certificate alone)."""
+    from paper_2406_04795_b200 import pipeline as PL
+    problem, out = _solve_proof_workload(name)
+    assert isinstance(out, PL.InfeasibilityProof), getattr(out, "reason", out)
+    assert out.closure_ok and out.points.shape[0] > 100_000 and out.points.shape[1] == problem.dof
+    last = out.stats.iterations[-1]
+    assert last["free_points"] == 0 and last["points"] == out.points.shape[0]
+    report = PL.verify_proof(out, problem)
+    assert report.ok, report.first_failure()
+    assert [c.name for c in report.checks][-1] == "reconstruction"
