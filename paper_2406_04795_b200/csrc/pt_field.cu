@@ -28,6 +28,8 @@ struct pt_field {
     PtBuf<double> svt;
     long long t_pos = 0, t_tot = 0;
     bool taylor = false;
+    PtBuf<double> dirtab;        // direction sums of the sorted rows (rows grouped by direction take one FMA for u_j)
+    bool taylor_dir = false;
 };
 
 int pt_field_dim(const pt_field* f) { return f->d.n; }
@@ -1293,23 +1295,87 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
         // dof6 29.0 -> 30.3 ms (longer fine edges: more rows need the second pass).  PERMATRACE_B200_TAYLOR_HINT=1 enables it.
         static const bool hints_on = getenv("PERMATRACE_B200_TAYLOR_HINT") && getenv("PERMATRACE_B200_TAYLOR_HINT")[0] == '1';
         const bool hinted = hint != nullptr && hints_on;
-        const PtTaylorDev td{f->svt.p, f->t_pos, f->t_tot};
+        const PtTaylorDev td{f->svt.p, f->t_pos, f->t_tot, f->taylor_dir ? f->dirtab.p : nullptr};
+        const PtTaylorGroup nogrp{nullptr, nullptr};
         auto launch = [&](const PtRows& rws, size_t count, int recentre, const float* h) -> int {
             const unsigned grid = pt_grid_for(count, PT_TAYLOR_THREADS);
             if (hinted) {
-                PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N, PT_TAYLOR_Q_HINT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PT_TAYLOR_SMEM(N, PT_TAYLOR_Q_HINT)));
-                PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N, PT_TAYLOR_Q_HINT>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-                pt_bisect_taylor_kernel<N, PT_TAYLOR_Q_HINT><<<grid, PT_TAYLOR_THREADS, PT_TAYLOR_SMEM(N, PT_TAYLOR_Q_HINT), ctx->stream>>>(
-                    f->d, f->sum_abs_w, td, rws, a, b, sa, eps, out, lo.p, hi.p, slow.p, jlo.p, jhi.p, ctx->work, recentre, h);
+                PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N, PT_TAYLOR_Q_HINT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PT_TAYLOR_SMEM(N, PT_TAYLOR_Q_HINT)));
+                PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N, PT_TAYLOR_Q_HINT, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                pt_bisect_taylor_kernel<N, PT_TAYLOR_Q_HINT, false><<<grid, PT_TAYLOR_THREADS, PT_TAYLOR_SMEM(N, PT_TAYLOR_Q_HINT), ctx->stream>>>(
+                    f->d, f->sum_abs_w, td, rws, nogrp, a, b, sa, eps, out, lo.p, hi.p, slow.p, jlo.p, jhi.p, ctx->work, recentre, h);
             } else {
-                PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N, PT_TAYLOR_Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PT_TAYLOR_SMEM(N, PT_TAYLOR_Q)));
-                PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N, PT_TAYLOR_Q>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-                pt_bisect_taylor_kernel<N, PT_TAYLOR_Q><<<grid, PT_TAYLOR_THREADS, PT_TAYLOR_SMEM(N, PT_TAYLOR_Q), ctx->stream>>>(
-                    f->d, f->sum_abs_w, td, rws, a, b, sa, eps, out, lo.p, hi.p, slow.p, jlo.p, jhi.p, ctx->work, recentre, nullptr);
+                PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N, PT_TAYLOR_Q, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PT_TAYLOR_SMEM(N, PT_TAYLOR_Q)));
+                PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N, PT_TAYLOR_Q, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                pt_bisect_taylor_kernel<N, PT_TAYLOR_Q, false><<<grid, PT_TAYLOR_THREADS, PT_TAYLOR_SMEM(N, PT_TAYLOR_Q), ctx->stream>>>(
+                    f->d, f->sum_abs_w, td, rws, nogrp, a, b, sa, eps, out, lo.p, hi.p, slow.p, jlo.p, jhi.p, ctx->work, recentre, nullptr);
             }
             return pt_check_launch(ctx, "pt_bisect_taylor_kernel");
         };
-        {
+        // Rows grouped by direction (lattice edges move along h * 1_mask): blocks whose rows share the mask get the first
+        // log-derivative from the direction table with one FMA per pair.  Rows that are not lattice edges (class 0) and
+        // hinted batches keep the generic kernel.
+        bool grouped = false;
+        if (f->taylor_dir && !hinted && m < 0xFFFFFFFFull - (size_t)(PT_TAYLOR_THREADS << N)) {
+            constexpr int NC = 1 << N;
+            PtBuf<uint8_t> cls, bmask; PtBuf<unsigned> hist; PtBuf<uint32_t> glist;
+            PT_TRY(cls.alloc(ctx, m));
+            PT_TRY(hist.alloc(ctx, 2 * NC + 2));
+            PT_CUDA(ctx, cudaMemsetAsync(hist.p, 0, (2 * NC + 2) * sizeof(unsigned), ctx->stream));
+            {
+                PT_LAUNCH(ctx, "bisect_taylor_group");
+                pt_taylor_classify_kernel<N><<<pt_grid_for(m, PT_TAYLOR_CLS_THREADS), PT_TAYLOR_CLS_THREADS, 0, ctx->stream>>>(a, b, m, cls.p, hist.p);
+                PT_TRY(pt_check_launch(ctx, "pt_taylor_classify_kernel"));
+            }
+            unsigned* hh = (unsigned*)ctx->pinned;
+            PT_CUDA(ctx, cudaMemcpyAsync(hh, hist.p, NC * sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+            PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+            PtTaylorOffsets offs;
+            memset(&offs, 0, sizeof(offs));
+            // class 0 first (unpadded: it is walked as a plain row list), then the masks, each padded to whole blocks
+            size_t slot = ((size_t)hh[0] + PT_TAYLOR_THREADS - 1) / PT_TAYLOR_THREADS * PT_TAYLOR_THREADS;
+            const size_t n0 = hh[0];
+            for (int c = 1; c < NC; ++c) {
+                offs.off[c] = (unsigned)slot;
+                slot += ((size_t)hh[c] + PT_TAYLOR_THREADS - 1) / PT_TAYLOR_THREADS * PT_TAYLOR_THREADS;
+            }
+            const size_t first_slot = offs.off[1], total_slots = slot;
+            const size_t nblocks = (total_slots - first_slot) / PT_TAYLOR_THREADS;
+            PT_TRY(glist.alloc(ctx, total_slots > 0 ? total_slots : 1));
+            PT_TRY(bmask.alloc(ctx, nblocks > 0 ? nblocks : 1));
+            PT_CUDA(ctx, cudaMemsetAsync(glist.p, 0xFF, (total_slots > 0 ? total_slots : 1) * sizeof(uint32_t), ctx->stream));
+            {
+                PT_LAUNCH(ctx, "bisect_taylor_group");
+                pt_taylor_scatter_kernel<N><<<pt_grid_for(m, PT_TAYLOR_CLS_THREADS), PT_TAYLOR_CLS_THREADS, 0, ctx->stream>>>(cls.p, m, offs, hist.p + NC, glist.p);
+                PT_TRY(pt_check_launch(ctx, "pt_taylor_scatter_kernel"));
+                if (nblocks > 0) {
+                    pt_taylor_bmask_kernel<<<pt_grid_for(nblocks, 256), 256, 0, ctx->stream>>>(offs, NC, (unsigned)first_slot, nblocks, bmask.p);
+                    PT_TRY(pt_check_launch(ctx, "pt_taylor_bmask_kernel"));
+                }
+            }
+            {
+                PT_LAUNCH(ctx, "bisect_fp64_taylor");
+                if (nblocks > 0) {
+                    const PtTaylorGroup grp{glist.p + first_slot, bmask.p};
+                    PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N, PT_TAYLOR_Q, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PT_TAYLOR_SMEM_DIR(N, PT_TAYLOR_Q)));
+                    PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N, PT_TAYLOR_Q, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+                    pt_bisect_taylor_kernel<N, PT_TAYLOR_Q, true><<<(unsigned)nblocks, PT_TAYLOR_THREADS, PT_TAYLOR_SMEM_DIR(N, PT_TAYLOR_Q), ctx->stream>>>(
+                        f->d, f->sum_abs_w, td, all, grp, a, b, sa, eps, out, lo.p, hi.p, slow.p, jlo.p, jhi.p, ctx->work, 0, nullptr);
+                    PT_TRY(pt_check_launch(ctx, "pt_bisect_taylor_kernel"));
+                }
+                if (n0 > 0) {
+                    PtBuf<unsigned long long> c0;
+                    PT_TRY(c0.alloc(ctx, 1));
+                    const unsigned long long n0v = n0;
+                    PT_CUDA(ctx, cudaMemcpyAsync(c0.p, &n0v, sizeof(n0v), cudaMemcpyHostToDevice, ctx->stream));
+                    const PtRows rest_l{glist.p, c0.p, m};
+                    PT_TRY(launch(rest_l, n0, 0, nullptr));
+                    PT_CUDA(ctx, cudaStreamSynchronize(ctx->stream));      // c0 leaves scope
+                }
+            }
+            grouped = true;
+        }
+        if (!grouped) {
             PT_LAUNCH(ctx, "bisect_fp64_taylor");
             PT_TRY(launch(all, m, 0, hint));
         }
@@ -1588,6 +1654,18 @@ static int pt_field_build_rbf(pt_ctx* ctx, int n, long long S, const double* sup
                 if (rc != PT_OK) { delete f; return rc; }
                 cudaStreamSynchronize(ctx->stream);
                 f->taylor = true;
+                // direction sums for the grouped variant (2^n x t_tot doubles: 1 MB at n = 6, S = 2048)
+                const char* dir_env = getenv("PERMATRACE_B200_TAYLOR_DIR");
+                if (!(dir_env && dir_env[0] == '0') && n <= 7 && ((size_t)f->t_tot << n) * sizeof(double) <= ((size_t)1 << 30)) {
+                    rc = f->dirtab.alloc(ctx, (size_t)f->t_tot << n);
+                    if (rc != PT_OK) { delete f; return rc; }
+                    const dim3 dgrid(pt_grid_for((size_t)f->t_tot, 256), 1u << n);
+                    pt_taylor_dirtab_kernel<<<dgrid, 256, 0, ctx->stream>>>(f->svt.p, rowt, n, f->t_tot, f->dirtab.p);
+                    rc = pt_check_launch(ctx, "pt_taylor_dirtab_kernel");
+                    if (rc != PT_OK) { delete f; return rc; }
+                    cudaStreamSynchronize(ctx->stream);
+                    f->taylor_dir = true;
+                }
             }
         }
         // tensor-core screen operand, when the whole packed support set fits one CTA's shared memory

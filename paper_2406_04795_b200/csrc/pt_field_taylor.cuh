@@ -42,17 +42,38 @@
 #ifndef PT_TAYLOR_MINB
 #define PT_TAYLOR_MINB 5              /* resident CTAs per SM the register budget is cut for */
 #endif
+#ifndef PT_TAYLOR_MINB_DIR
+#define PT_TAYLOR_MINB_DIR 6          /* ditto, direction-table variant (its loop keeps N-1 fewer values live) */
+#endif
 #define PT_TAYLOR_TRY_WIDTH 0.0625     /* first enclosure attempt once the bracket is this narrow (in t) */
 
 template <int N> struct PtRowT { static const int value = (N + 2) & ~1; };   // 2*gl*s_d (N), c'_s, pad to an even count
+
+// shared-memory row of the direction-table variant: the packed row plus T_j = sum_{d in mask} 2*gl*s_jd in slot N+1
+template <int N> struct PtRowX { static const int value = (N + 3) & ~1; };
 
 struct PtTaylorDev {
     const double* svt;     // [s_tot][ROWT] rows sorted by the sign of the weight: positive block (padded to even), negative block
     long long s_pos;       // rows of the positive block (even)
     long long s_tot;       // all rows (even)
+    const double* dirtab;  // [2^N][s_tot] direction sums T_j(mask) of the sorted rows (null: no direction-table variant)
 };
 
-#define PT_TAYLOR_SMEM(N, Q) ((size_t)((PT_TAYLOR_TILE + 1) * PtRowT<N>::value + PT_EXP_TAB + ((Q) + 1 + (Q) / 2) * PT_TAYLOR_THREADS + 2 + 2 * PT_NMAX) * sizeof(double))
+// Rows grouped by direction (pt_taylor_classify / scatter kernels): lattice edges move along diff = h * 1_mask, so the
+// first log-derivative of a term is u_j = pdu + h * T_j(mask) -- ONE FMA per pair instead of N once a block's rows share
+// the mask (T_j comes in with the tile).  glist holds the row indices class by class, every class padded to a whole block
+// with 0xFFFFFFFF; bmask[b] is block b's mask.
+struct PtTaylorGroup {
+    const uint32_t* glist;
+    const uint8_t* bmask;
+};
+
+// tile (+ look-ahead row) | 2^x table | running totals of the Q+1 moments | fp32 stash of the positive block's even moments |
+// barrier parameters.  (The absolute moments MA_k / k! of the tail live in the tile's space once the pass is over.)
+#define PT_TAYLOR_TILE_D(ROWS, Q) ((PT_TAYLOR_TILE + 1) * (ROWS) > ((Q) / 2) * PT_TAYLOR_THREADS ? (PT_TAYLOR_TILE + 1) * (ROWS) : ((Q) / 2) * PT_TAYLOR_THREADS)
+#define PT_TAYLOR_SMEM_ROWS(ROWS, Q) ((size_t)(PT_TAYLOR_TILE_D(ROWS, Q) + PT_EXP_TAB + ((Q) + 1 + (Q) / 4) * PT_TAYLOR_THREADS + 2 + 2 * PT_NMAX) * sizeof(double))
+#define PT_TAYLOR_SMEM(N, Q) PT_TAYLOR_SMEM_ROWS(PtRowT<N>::value, Q)
+#define PT_TAYLOR_SMEM_DIR(N, Q) PT_TAYLOR_SMEM_ROWS(PtRowX<N>::value, Q)
 
 // pack the sign-sorted rows: dest index from an exclusive scan of the "weight >= 0" flags (stable, deterministic)
 __global__ void pt_taylor_flag_kernel(const double* __restrict__ weights, long long S, unsigned* __restrict__ flag) {
@@ -112,9 +133,19 @@ __device__ __forceinline__ void pt_taylor_pair(const double* __restrict__ row, c
 }
 
 // front half of a pair: the term e = |w| k(q(1/2), s) (sign applied) and its first log-derivative u
-template <int N>
+template <int N, bool DIR>
 __device__ __forceinline__ void pt_taylor_front(const double* __restrict__ row, const PtPoint64<N>& pp, double pdu,
                                                 const double (&ddu)[N], const double* __restrict__ tab, int sx, double& e, double& u) {
+    if (DIR) {
+        // ddu[0] = h*ln2: the common step of the moving coordinates; row[N + 1] = T_j(mask)
+        double arg = row[N] + pp.cp;
+        u = fma(ddu[0], row[N + 1], pdu);
+#pragma unroll
+        for (int d = 0; d < N; ++d) arg = fma(pp.q[d], row[d], arg);
+        const double ea = pt_exp2_neg(arg, tab);
+        e = __hiloint2double(__double2hiint(ea) ^ sx, __double2loint(ea));
+        return;
+    }
 #ifdef PT_TAYLOR_TREE
     // two half-length chains per dot product (one extra add each, half the dependent depth)
     double arg = row[N] + pp.cp, arg2 = pp.q[N - 1] * row[N - 1], u2_ = ddu[N - 1] * row[N - 1];
@@ -168,27 +199,39 @@ __device__ __forceinline__ void pt_taylor_back(double pw, double u, double (&acc
 
 // Software-pipelined over the support rows: the (serial) exponent / exponential chain of row j+1 is issued next to the
 // (parallel) moment updates of row j.  The tile carries one zero pad row behind the last one for the final look-ahead.
-template <int N, int Q>
-__device__ __forceinline__ void pt_taylor_block(const double* __restrict__ svt, long long r0, long long r1, double* tile,
-                                                const double* tab, const PtPoint64<N>& pp, double pdu, const double (&ddu)[N],
-                                                int sx, double (&acc)[Q + 1], double* total) {
-    constexpr int ROW = PtRowT<N>::value;
+template <int N, int Q, bool DIR>
+__device__ __forceinline__ void pt_taylor_block(const double* __restrict__ svt, const double* __restrict__ dir, long long r0, long long r1,
+                                                double* tile, const double* tab, const PtPoint64<N>& pp, double pdu,
+                                                const double (&ddu)[N], int sx, double (&acc)[Q + 1], double* total) {
+    constexpr int ROWG = PtRowT<N>::value;                               // row in global memory
+    constexpr int ROW = DIR ? PtRowX<N>::value : PtRowT<N>::value;       // row in the tile
     for (long long t0 = r0; t0 < r1; t0 += PT_TAYLOR_TILE) {
         const long long rem = r1 - t0;
         const int cnt = rem < PT_TAYLOR_TILE ? (int)rem : PT_TAYLOR_TILE;     // even by construction
         __syncthreads();
-        const double2* src = reinterpret_cast<const double2*>(svt + t0 * ROW);
+        const double2* src = reinterpret_cast<const double2*>(svt + t0 * ROWG);
         double2* dst = reinterpret_cast<double2*>(tile);
-        for (int i = threadIdx.x; i < cnt * ROW / 2; i += PT_TAYLOR_THREADS) dst[i] = src[i];
+        if (!DIR) {
+            for (int i = threadIdx.x; i < cnt * ROWG / 2; i += PT_TAYLOR_THREADS) dst[i] = src[i];
+        } else {
+            for (int i = threadIdx.x; i < cnt * ROWG / 2; i += PT_TAYLOR_THREADS) {
+                const int r = i / (ROWG / 2), c = i - r * (ROWG / 2);
+                double2 v = src[i];
+                if ((N & 1) == 0 && c == ROWG / 2 - 1) v.y = dir[t0 + r];      // even N: T_j takes the packed row's pad slot
+                dst[r * (ROW / 2) + c] = v;
+            }
+            if (N & 1)                                                          // odd N: slot N+1 lies behind the packed row
+                for (int r = threadIdx.x; r < cnt; r += PT_TAYLOR_THREADS) tile[r * ROW + N + 1] = dir[t0 + r];
+        }
         if (threadIdx.x < ROW) tile[cnt * ROW + threadIdx.x] = 0.0;
         __syncthreads();
         double e0, u0, e1, u1;
-        pt_taylor_front<N>(tile, pp, pdu, ddu, tab, sx, e0, u0);
+        pt_taylor_front<N, DIR>(tile, pp, pdu, ddu, tab, sx, e0, u0);
 #pragma unroll 1
         for (int j = 0; j < cnt; j += 2) {
-            pt_taylor_front<N>(tile + (j + 1) * ROW, pp, pdu, ddu, tab, sx, e1, u1);
+            pt_taylor_front<N, DIR>(tile + (j + 1) * ROW, pp, pdu, ddu, tab, sx, e1, u1);
             pt_taylor_back<Q>(e0, u0, acc);
-            pt_taylor_front<N>(tile + (j + 2) * ROW, pp, pdu, ddu, tab, sx, e0, u0);
+            pt_taylor_front<N, DIR>(tile + (j + 2) * ROW, pp, pdu, ddu, tab, sx, e0, u0);
             pt_taylor_back<Q>(e1, u1, acc);
         }
         // blocked accumulation: a tile's partial sums go to the running totals in shared memory, so the summation error is
@@ -288,32 +331,119 @@ __device__ __forceinline__ double pt_taylor_centre(const float* hint, size_t ei)
     return fmin(fmax(c, 0.0625), 0.9375);
 }
 
-template <int N, int Q>
-__global__ void __launch_bounds__(PT_TAYLOR_THREADS, PT_TAYLOR_MINB)
-pt_bisect_taylor_kernel(PtFieldDev f, double sum_abs_w, PtTaylorDev tf, PtRows rows, const double* __restrict__ a_, const double* __restrict__ b_,
-                        const int8_t* __restrict__ signs_a, double eps, double* __restrict__ out, double* __restrict__ lo_io,
-                        double* __restrict__ hi_io, uint8_t* __restrict__ slow, double* __restrict__ jlo_out,
+// common step of the moving coordinates (the first one's) and the largest deviation of any coordinate's step from the
+// direction model diff = h * 1_mask; the deviation (roundings of the two end points, ~1e-16) enters the error bound
+template <int N>
+__device__ __forceinline__ double pt_taylor_step(const double (&diff)[N], unsigned mask, double& dev) {
+    double h = 0.0;
+#pragma unroll
+    for (int d = N - 1; d >= 0; --d) if ((mask >> d) & 1u) h = diff[d];
+    dev = 0.0;
+#pragma unroll
+    for (int d = 0; d < N; ++d) dev = fmax(dev, fabs(diff[d] - (((mask >> d) & 1u) ? h : 0.0)));
+    return h;
+}
+
+// direction sums of the sorted rows: dirtab[mask][j] = sum_{d in mask} svt[j][d]   (2^n x s_tot doubles, L2-resident)
+__global__ void pt_taylor_dirtab_kernel(const double* __restrict__ svt, int row, int n, long long s_tot, double* __restrict__ dirtab) {
+    const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const unsigned mask = blockIdx.y;
+    if (j >= s_tot) return;
+    double t = 0.0;
+    for (int d = 0; d < n; ++d) if ((mask >> d) & 1u) t += svt[j * row + d];
+    dirtab[(size_t)mask * (size_t)s_tot + j] = t;
+}
+
+// ---- grouping of a batch's rows by direction ------------------------------------------------------------------------
+// class of a row = the mask of its moving coordinates when all of them move by the same step (to 1e-12 relative: lattice
+// edges, whose end points are rounded separately), 0 otherwise (arbitrary segments keep the N-term dot product).
+#define PT_TAYLOR_CLS_THREADS 256
+template <int N>
+__global__ void __launch_bounds__(PT_TAYLOR_CLS_THREADS)
+pt_taylor_classify_kernel(const double* __restrict__ a_, const double* __restrict__ b_, size_t m, uint8_t* __restrict__ cls,
+                          unsigned* __restrict__ hist) {
+    __shared__ unsigned sh[1 << N];
+    for (int i = threadIdx.x; i < (1 << N); i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < m) {
+        double diff[N];
+        unsigned mask = 0;
+#pragma unroll
+        for (int d = 0; d < N; ++d) { diff[d] = __dsub_rn(b_[i * N + d], a_[i * N + d]); mask |= (diff[d] != 0.0 ? 1u : 0u) << d; }
+        double dev;
+        const double h = pt_taylor_step<N>(diff, mask, dev);
+        if (!(dev <= 1e-12 * fabs(h))) mask = 0;            // (NaN steps land here too)
+        cls[i] = (uint8_t)mask;
+        atomicAdd(&sh[mask], 1u);
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < (1 << N); c += blockDim.x) if (sh[c]) atomicAdd(&hist[c], sh[c]);
+}
+
+struct PtTaylorOffsets { unsigned off[1 << PT_NMAX]; };     // first slot of every class in glist (block-aligned for mask != 0)
+
+// rows to their class's run of glist; the order inside a class does not matter (every row is solved on its own)
+template <int N>
+__global__ void __launch_bounds__(PT_TAYLOR_CLS_THREADS)
+pt_taylor_scatter_kernel(const uint8_t* __restrict__ cls, size_t m, PtTaylorOffsets offs, unsigned* __restrict__ cursor,
+                         uint32_t* __restrict__ glist) {
+    __shared__ unsigned cnt[1 << N], base[1 << N];
+    for (int i = threadIdx.x; i < (1 << N); i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    unsigned c = 0, local = 0;
+    if (i < m) { c = cls[i]; local = atomicAdd(&cnt[c], 1u); }
+    __syncthreads();
+    for (int k = threadIdx.x; k < (1 << N); k += blockDim.x) if (cnt[k]) base[k] = atomicAdd(&cursor[k], cnt[k]);
+    __syncthreads();
+    if (i < m) glist[(size_t)offs.off[c] + base[c] + local] = (uint32_t)i;
+}
+
+// block -> mask of the grouped launch: blocks [off[c]/TH, off[c+1]/TH) belong to class c (classes in ascending order from 1)
+__global__ void pt_taylor_bmask_kernel(PtTaylorOffsets offs, int ncls, unsigned first_slot, size_t nblocks, uint8_t* __restrict__ bmask) {
+    const size_t b = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nblocks) return;
+    const unsigned slot = first_slot + (unsigned)b * PT_TAYLOR_THREADS;
+    int c = 1;
+    while (c + 1 < ncls && offs.off[c + 1] <= slot) ++c;
+    bmask[b] = (uint8_t)c;
+}
+
+template <int N, int Q, bool DIR>
+__global__ void __launch_bounds__(PT_TAYLOR_THREADS, DIR ? PT_TAYLOR_MINB_DIR : PT_TAYLOR_MINB)
+pt_bisect_taylor_kernel(PtFieldDev f, double sum_abs_w, PtTaylorDev tf, PtRows rows, PtTaylorGroup grp, const double* __restrict__ a_,
+                        const double* __restrict__ b_, const int8_t* __restrict__ signs_a, double eps, double* __restrict__ out,
+                        double* __restrict__ lo_io, double* __restrict__ hi_io, uint8_t* __restrict__ slow, double* __restrict__ jlo_out,
                         double* __restrict__ jhi_out, unsigned long long* work, int recentre, const float* __restrict__ hint) {
-    constexpr int ROW = PtRowT<N>::value, TH = PT_TAYLOR_THREADS;
+    constexpr int ROW = DIR ? PtRowX<N>::value : PtRowT<N>::value, TH = PT_TAYLOR_THREADS;
     extern __shared__ double sm[];
     double* tile = sm;
-    double* tab = tile + (PT_TAYLOR_TILE + 1) * ROW;
+    double* tab = tile + PT_TAYLOR_TILE_D(ROW, Q);
     double* col = tab + PT_EXP_TAB + threadIdx.x;          // c_k at col[k*TH], k < Q;  RQ-independent
-    double* cola = col + (Q + 1) * TH;                     // ca_k (k even < Q) at cola[(k/2)*TH]
+    float* stash = reinterpret_cast<float*>(tab + PT_EXP_TAB + (Q + 1) * TH) + threadIdx.x;   // even moments of the positive block
+    double* cola = tile + threadIdx.x;                     // ca_k (k even < Q) at cola[(k/2)*TH]: the tile's space, after the pass
     pt_exp_table_init(tab);
     if (threadIdx.x < 2 + 2 * N) {
-        double* bpw = tab + PT_EXP_TAB + (Q + 1 + Q / 2) * TH;
+        double* bpw = tab + PT_EXP_TAB + (Q + 1 + Q / 4) * TH;
         bpw[threadIdx.x] = threadIdx.x == 0 ? f.b_scale : threadIdx.x == 1 ? f.b_gain
                          : threadIdx.x < 2 + N ? f.b_lo[threadIdx.x - 2] : f.b_hi[threadIdx.x - 2 - N];
     }
     // first pass: all rows, model about the edge midpoint, bracket [0, 1].  Second pass (`recentre`): the listed rows the
     // first one left open, model about the midpoint of the bracket they stopped at -- the truncation then scales with
     // (bracket width / 2)^Q instead of 2^-Q
-    const size_t m = pt_rows_total(rows);
+    const size_t m = DIR ? (size_t)gridDim.x * TH : pt_rows_total(rows);
     if ((size_t)blockIdx.x * TH >= m) return;
     size_t ei = (size_t)blockIdx.x * TH + threadIdx.x;
-    const bool valid = ei < m;
-    if (valid && rows.list) ei = rows.list[ei];
+    bool valid = ei < m;
+    unsigned mask = 0;
+    if (DIR) {
+        // grouped rows: the block's rows share the direction mask; 0xFFFFFFFF pads a class to a whole block
+        ei = grp.glist[ei];
+        valid = ei != 0xFFFFFFFFull;
+        mask = grp.bmask[blockIdx.x];
+    } else if (valid && rows.list) ei = rows.list[ei];
+    const double* dir = DIR ? tf.dirtab + (size_t)mask * (size_t)tf.s_tot : nullptr;
     // (row geometry is loaded twice -- here for the pass, again for the tail -- so that nothing but the pass's own
     //  operands stays live across the support loop: at 96 registers every extra live value spills INSIDE that loop)
     double mnorm2 = 0.0;
@@ -339,24 +469,32 @@ pt_bisect_taylor_kernel(PtFieldDev f, double sum_abs_w, PtTaylorDev tf, PtRows r
             ddu[d] = diff[d] * PT_LN2;                     // rows hold 2*gamma*log2e*s_d
             mnorm2 = fma(mc[d], mc[d], mnorm2);
         }
+        if (DIR) { double dev; ddu[0] = pt_taylor_step<N>(diff, mask, dev) * PT_LN2; }
         pp.set(mc, f.gamma * PT_L2E);
         const double pdu = -2.0 * f.gamma * md;
         double acc[Q + 1];
 #pragma unroll
         for (int k = 0; k <= Q; ++k) { acc[k] = 0.0; col[k * TH] = 0.0; }
-        pt_taylor_block<N, Q>(tf.svt, 0, tf.s_pos, tile, tab, pp, pdu, ddu, 0, acc, col);
+        pt_taylor_block<N, Q, DIR>(tf.svt, dir, 0, tf.s_pos, tile, tab, pp, pdu, ddu, 0, acc, col);
+        // even moments of the positive block, rounded up to fp32: they only enter error bounds (MA_k = 2 M_k^+ - M_k)
 #pragma unroll
-        for (int k = 0; k < Q; k += 2) cola[(k / 2) * TH] = col[k * TH];   // even moments of the positive block
-        pt_taylor_block<N, Q>(tf.svt, tf.s_pos, tf.s_tot, tile, tab, pp, pdu, ddu, (int)0x80000000, acc, col);
+        for (int k = 0; k < Q; k += 2) stash[(k / 2) * TH] = __double2float_ru(col[k * TH]);
+        pt_taylor_block<N, Q, DIR>(tf.svt, dir, tf.s_pos, tf.s_tot, tile, tab, pp, pdu, ddu, (int)0x80000000, acc, col);
+        __syncthreads();                                   // the last tile is dead: its space takes the absolute moments
         double inv_fact = 1.0;
 #pragma unroll
         for (int k = 0; k < Q; ++k) {
             if (k > 1) inv_fact /= (double)k;
             const double mk = col[k * TH];
             col[k * TH] = (mk + pp.poison) * inv_fact;
-            if ((k & 1) == 0) cola[(k / 2) * TH] = fabs(2.0 * cola[(k / 2) * TH] - mk) * inv_fact;   // MA_k / k!
+            // MA_k / k! (fp32 stash: relative 1.2e-7, inside the 2.002 of pt_taylor_cosh; the max keeps MA_k >= |M_k|)
+            if ((k & 1) == 0) cola[(k / 2) * TH] = fmax(fabs(2.0 * (double)stash[(k / 2) * TH] - mk), fabs(mk)) * inv_fact;
         }
         col[Q * TH] = col[Q * TH] * (inv_fact / (double)Q);                 // MA_Q / Q!
+    }
+    if (DIR && !recentre) {
+        const int nvalid = __syncthreads_count(valid ? 1 : 0);
+        if (threadIdx.x == 0) atomicAdd(&work[7], (unsigned long long)nvalid);
     }
     if (!valid) return;
     double a[N], diff[N];
@@ -397,10 +535,18 @@ pt_bisect_taylor_kernel(PtFieldDev f, double sum_abs_w, PtTaylorDev tf, PtRows r
     const double RQ = fac * (1.01 * caQ + 1e-40 * ca0);                     // |R(tau)| <= RQ |tau|^Q
     // rounding of THIS pass relative to sum_j e_j exp(|u_j tau|): expanded exponent (cancellation at scale T), blocked
     // summation, powers and Horner, the log-derivative's absolute error
+    // (direction-table variant: u_j = pdu + h T_j instead of the N-term dot product -- T_j's own rounding, and the
+    //  deviation of the true steps from h * 1_mask times 2 gamma |s_j| sqrt(N), an absolute error of the log-derivative)
+    double Cdir = 0.0;
+    if (DIR) {
+        double dev;
+        pt_taylor_step<N>(diff, mask, dev);
+        Cdir = 1.01 * 2.0 * f.gamma * f.smax * sqrt((double)N) * dev;
+    }
     const double Ctot = PT_U64 * (1.01 * (double)(4 * N + 7) * T * PT_LN2 + 1.05 * (double)(PT_TAYLOR_TILE + f.S / PT_TAYLOR_TILE)
-                                  + 4.0 * Q + (double)(N + 2) * gmaxu + 450.0);
+                                  + 4.0 * Q + (double)(DIR ? 4 * N + 2 : N + 2) * gmaxu + 450.0) + Cdir;
     const double abias = fabs(f.bias);
-    const double* bp = tab + PT_EXP_TAB + (Q + 1 + Q / 2) * TH;              // barrier parameters (shared)
+    const double* bp = tab + PT_EXP_TAB + (Q + 1 + Q / 4) * TH;              // barrier parameters (shared)
     double geo[2 * N];                                                      // dynamically indexed by the helpers
 #pragma unroll
     for (int d = 0; d < N; ++d) { geo[d] = a[d]; geo[N + d] = diff[d]; }
@@ -566,7 +712,7 @@ pt_bisect_taylor_kernel(PtFieldDev f, double sum_abs_w, PtTaylorDev tf, PtRows r
         jhi_out[ei] = flag == 2 ? Jhi : 1e300;
     }
     if (recentre && flag != 0) atomicAdd(&work[3], 1ull);                 // rows left to the evaluation-based kernels
-    if (threadIdx.x == 0 && !recentre) {
+    if (!DIR && threadIdx.x == 0 && !recentre) {
         const size_t first = (size_t)blockIdx.x * TH;
         atomicAdd(&work[7], (unsigned long long)(m - first < (size_t)TH ? m - first : (size_t)TH));
     }
