@@ -71,7 +71,7 @@ struct PtTaylorGroup {
 // tile (+ look-ahead row) | 2^x table | running totals of the Q+1 moments | fp32 stash of the positive block's even moments |
 // barrier parameters.  (The absolute moments MA_k / k! of the tail live in the tile's space once the pass is over.)
 #define PT_TAYLOR_TILE_D(ROWS, Q) ((PT_TAYLOR_TILE + 1) * (ROWS) > ((Q) / 2) * PT_TAYLOR_THREADS ? (PT_TAYLOR_TILE + 1) * (ROWS) : ((Q) / 2) * PT_TAYLOR_THREADS)
-#define PT_TAYLOR_SMEM_ROWS(ROWS, Q) ((size_t)(PT_TAYLOR_TILE_D(ROWS, Q) + PT_EXP_TAB + ((Q) + 1 + (Q) / 4) * PT_TAYLOR_THREADS + 2 + 2 * PT_NMAX) * sizeof(double))
+#define PT_TAYLOR_SMEM_ROWS(ROWS, Q) ((size_t)(PT_TAYLOR_TILE_D(ROWS, Q) + PT_EXP_TAB + ((Q) + 1 + ((Q) + 3) / 4) * PT_TAYLOR_THREADS + 2 + 2 * PT_NMAX) * sizeof(double))
 #define PT_TAYLOR_SMEM(N, Q) PT_TAYLOR_SMEM_ROWS(PtRowT<N>::value, Q)
 #define PT_TAYLOR_SMEM_DIR(N, Q) PT_TAYLOR_SMEM_ROWS(PtRowX<N>::value, Q)
 
@@ -185,13 +185,19 @@ __device__ __forceinline__ void pt_taylor_back(double pw, double u, double (&acc
     }
     acc[Q] += fabs(pw * pk[Q / 4]);
 #else
+    static_assert((Q & 1) == 0, "an even number of moments");
 #pragma unroll
-    for (int k = 0; k < Q; k += 4) {
+    for (int k = 0; k + 4 <= Q; k += 4) {
         acc[k] += pw;
         acc[k + 1] = fma(pw, u, acc[k + 1]);
         acc[k + 2] = fma(pw, u2, acc[k + 2]);
         acc[k + 3] = fma(pw, u3, acc[k + 3]);
         pw *= u4;
+    }
+    if (Q % 4 == 2) {
+        acc[Q - 2] += pw;
+        acc[Q - 1] = fma(pw, u, acc[Q - 1]);
+        pw *= u2;
     }
     acc[Q] += fabs(pw);
 #endif
@@ -269,13 +275,22 @@ __device__ __noinline__ double pt_powi(double x, int k) {
     return r;
 }
 
-// barrier(q(t)) and its first two t-derivatives along q(t) = a + t*diff; bp = {scale, gain, lo[n], hi[n]} in shared
-// memory, geo = per-thread {a[n], diff[n]}.  One exp + log1p + division per term; a few ulps from the reference's
-// logaddexp, far inside the 64 u |B| the bounds allow for it.
+// log1p(e) for e in (0, 1]: seven terms of the series below 2^-8 (truncation 2^-59 relative), the library above
+__device__ __forceinline__ double pt_log1p_unit(double e) {
+    if (e < 0.00390625)
+        return e * fma(e, fma(e, fma(e, fma(e, fma(e, fma(e, 1.0 / 7.0, -1.0 / 6.0), 0.2), -0.25), 1.0 / 3.0), -0.5), 1.0);
+    return log1p(e);
+}
+
+// barrier(q(t)) and (deriv != 0) its first two t-derivatives along q(t) = a + t*diff; bp = {scale, gain, lo[n], hi[n]} in
+// shared memory, geo = per-thread {a[n], diff[n]}, tab = the 2^x table of the pass.  Per term one table-based exponential
+// (relative error <= (2 + |x|) u: the argument is rescaled to base 2), a short series or log1p, and a division only when the
+// derivatives are wanted -- a few ulps of every term plus |x| u of the (then tiny) far ones, inside the `bulp` u |B| the
+// bounds allow for it (bulp >= 64 grows with the largest |x| on the edge, pt_taylor_barrier_max).
 // `moving` = bit mask of the coordinates that change along the edge; `acc0` = the (t-independent) sum of the softplus
 // terms of the others (pt_taylor_barrier_const).
-__device__ __noinline__ void pt_taylor_barrier(const double* bp, const double* geo, int n, unsigned moving, double acc0, double t,
-                                               double* B, double* B1, double* B2) {
+__device__ __noinline__ void pt_taylor_barrier(const double* bp, const double* tab, const double* geo, int n, unsigned moving,
+                                               double acc0, double t, int deriv, double* B, double* B1, double* B2) {
     const double sc = bp[0], gain = bp[1];
     double acc = acc0, b1 = 0.0, b2 = 0.0;
 #pragma unroll 1
@@ -284,18 +299,20 @@ __device__ __noinline__ void pt_taylor_barrier(const double* bp, const double* g
         if (!((moving >> d) & 1u)) continue;
         const double q = __dadd_rn(geo[d], __dmul_rn(t, geo[n + d]));
         const double x = (i & 1) ? (q - bp[2 + n + d]) / sc : (bp[2 + d] - q) / sc;      // hi side / lo side
-        const double e = exp(-fabs(x));
-        acc += fmax(x, 0.0) + log1p(e);
-        const double sg = (x > 0.0 ? 1.0 : e) / (1.0 + e);                                // sigmoid(x)
-        const double dq = (i & 1) ? geo[n + d] : -geo[n + d];                             // d x / d t * scale
-        b1 = fma(dq, sg, b1);
-        b2 = fma(dq * dq, sg * (1.0 - sg), b2);
+        const double e = pt_exp2_neg(-fabs(x) * PT_L2E, tab);
+        acc += fmax(x, 0.0) + pt_log1p_unit(e);
+        if (deriv) {
+            const double sg = (x > 0.0 ? 1.0 : e) / (1.0 + e);                            // sigmoid(x)
+            const double dq = (i & 1) ? geo[n + d] : -geo[n + d];                         // d x / d t * scale
+            b1 = fma(dq, sg, b1);
+            b2 = fma(dq * dq, sg * (1.0 - sg), b2);
+        }
     }
     *B = gain * sc * acc; *B1 = gain * b1; *B2 = gain / sc * b2;
 }
 
 // softplus terms of the coordinates that do NOT move along the edge (evaluated once per row)
-__device__ __noinline__ double pt_taylor_barrier_const(const double* bp, const double* geo, int n, unsigned moving) {
+__device__ __noinline__ double pt_taylor_barrier_const(const double* bp, const double* tab, const double* geo, int n, unsigned moving) {
     const double sc = bp[0];
     double acc = 0.0;
 #pragma unroll 1
@@ -303,21 +320,24 @@ __device__ __noinline__ double pt_taylor_barrier_const(const double* bp, const d
         const int d = i >> 1;
         if ((moving >> d) & 1u) continue;
         const double x = (i & 1) ? (geo[d] - bp[2 + n + d]) / sc : (bp[2 + d] - geo[d]) / sc;
-        acc += fmax(x, 0.0) + log1p(exp(-fabs(x)));
+        acc += fmax(x, 0.0) + pt_log1p_unit(pt_exp2_neg(-fabs(x) * PT_L2E, tab));
     }
     return acc;
 }
 
-// upper bound of the barrier anywhere on the edge: softplus(x) <= exp(x), each coordinate at its worst end
-__device__ __noinline__ double pt_taylor_barrier_max(const double* bp, const double* geo, int n) {
+// upper bound of the barrier anywhere on the edge: softplus(x) <= exp(x), each coordinate at its worst end; *xabs = the
+// largest |x| of any term anywhere on the edge
+__device__ __noinline__ double pt_taylor_barrier_max(const double* bp, const double* geo, int n, double* xabs) {
     const double sc = bp[0], gain = bp[1];
-    double acc = 0.0;
+    double acc = 0.0, xa = 0.0;
 #pragma unroll 1
     for (int d = 0; d < n; ++d) {
         const double q0 = geo[d], q1 = geo[d] + geo[n + d];
         const double xl = (bp[2 + d] - fmin(q0, q1)) / sc, xh = (fmax(q0, q1) - bp[2 + n + d]) / sc;
         acc += (xl > 0.0 ? xl + 0.6931471805599453 : exp(xl)) + (xh > 0.0 ? xh + 0.6931471805599453 : exp(xh));
+        xa = fmax(xa, fmax(fmax(fabs(xl), fabs(xh)), fmax(fabs((bp[2 + d] - fmax(q0, q1)) / sc), fabs((fmin(q0, q1) - bp[2 + n + d]) / sc))));
     }
+    *xabs = xa;
     return 1.0001 * gain * sc * acc;
 }
 
@@ -425,7 +445,7 @@ pt_bisect_taylor_kernel(PtFieldDev f, double sum_abs_w, PtTaylorDev tf, PtRows r
     double* cola = tile + threadIdx.x;                     // ca_k (k even < Q) at cola[(k/2)*TH]: the tile's space, after the pass
     pt_exp_table_init(tab);
     if (threadIdx.x < 2 + 2 * N) {
-        double* bpw = tab + PT_EXP_TAB + (Q + 1 + Q / 4) * TH;
+        double* bpw = tab + PT_EXP_TAB + (Q + 1 + (Q + 3) / 4) * TH;
         bpw[threadIdx.x] = threadIdx.x == 0 ? f.b_scale : threadIdx.x == 1 ? f.b_gain
                          : threadIdx.x < 2 + N ? f.b_lo[threadIdx.x - 2] : f.b_hi[threadIdx.x - 2 - N];
     }
@@ -546,21 +566,25 @@ pt_bisect_taylor_kernel(PtFieldDev f, double sum_abs_w, PtTaylorDev tf, PtRows r
     const double Ctot = PT_U64 * (1.01 * (double)(4 * N + 7) * T * PT_LN2 + 1.05 * (double)(PT_TAYLOR_TILE + f.S / PT_TAYLOR_TILE)
                                   + 4.0 * Q + (double)(DIR ? 4 * N + 2 : N + 2) * gmaxu + 450.0) + Cdir;
     const double abias = fabs(f.bias);
-    const double* bp = tab + PT_EXP_TAB + (Q + 1 + Q / 4) * TH;              // barrier parameters (shared)
+    const double* bp = tab + PT_EXP_TAB + (Q + 1 + (Q + 3) / 4) * TH;              // barrier parameters (shared)
     double geo[2 * N];                                                      // dynamically indexed by the helpers
 #pragma unroll
     for (int d = 0; d < N; ++d) { geo[d] = a[d]; geo[N + d] = diff[d]; }
     unsigned moving = 0;
 #pragma unroll
     for (int d = 0; d < N; ++d) moving |= (diff[d] != 0.0 ? 1u : 0u) << d;
-    double bconst_v = -1.0;                                                 // lazily: the barrier terms of the resting coordinates
-    auto bconst = [&]() { if (bconst_v < 0.0) bconst_v = pt_taylor_barrier_const(bp, geo, N, moving); return bconst_v; };
+    // the barrier terms of the resting coordinates: once per row, by all lanes together (every enclosure attempt needs them)
+    const double bconst_v = f.has_barrier ? pt_taylor_barrier_const(bp, tab, geo, N, moving) : 0.0;
+    auto bconst = [&]() { return bconst_v; };
+    double bulp = 64.0;                                                     // allowance, in ulps of |B|, for the barrier's evaluation
     double bsum = 0.0, Bmax = 0.0;                                          // |B'| <= bsum, 0 <= B <= Bmax on the edge
     if (f.has_barrier) {
 #pragma unroll
         for (int d = 0; d < N; ++d) bsum += fabs(diff[d]);
         bsum *= f.b_gain;
-        Bmax = pt_taylor_barrier_max(bp, geo, N);
+        double xabs;
+        Bmax = pt_taylor_barrier_max(bp, geo, N, &xabs);
+        bulp = fmax(64.0, 16.0 + 2.0 * xabs);
     }
 
     int flag = 1;                 // 0 done, 1 no enclosure, 2 enclosed with open midpoints
@@ -580,14 +604,14 @@ pt_bisect_taylor_kernel(PtFieldDev f, double sum_abs_w, PtTaylorDev tf, PtRows r
             const double Ek = 1.001 * (Etr + Ern) + Efar + 1e-290;
             const double g0 = fma(ex, p, f.bias);
             // the barrier is only evaluated when the decision needs it (0 <= B <= Bmax)
-            const double Eb0 = 64.0 * PT_U64 * (1.1 * Bmax + abias);
+            const double Eb0 = bulp * PT_U64 * (1.1 * Bmax + abias);
             int sgn = 0;
             if (g0 - Bmax > Ek + Eb0) sgn = 1;
             else if (g0 < -(Ek + Eb0)) sgn = -1;
             else {
-                if (f.has_barrier) pt_taylor_barrier(bp, geo, N, moving, bconst(), mq, &B, &B1, &B2);
+                if (f.has_barrier) pt_taylor_barrier(bp, tab, geo, N, moving, bconst(), mq, 0, &B, &B1, &B2);
                 const double g = g0 - B;
-                if (fabs(g) > Ek + 64.0 * PT_U64 * (1.1 * fabs(B) + abias)) sgn = g > 0.0 ? 1 : -1;
+                if (fabs(g) > Ek + bulp * PT_U64 * (1.1 * fabs(B) + abias)) sgn = g > 0.0 ? 1 : -1;
                 // |F| is below the rounding level of any fp64 evaluation (this model's truncation is smaller still): the
                 // model value is as good as an evaluation, its sign is taken
                 else if (Etr + Efar <= Ern && g == g) sgn = g > 0.0 ? 1 : -1;
@@ -634,10 +658,10 @@ pt_bisect_taylor_kernel(PtFieldDev f, double sum_abs_w, PtTaylorDev tf, PtRows r
             const double xm = 0.5 * (L + H);
             double Bm = 0.0, B1m = 0.0, B2m = 0.0;
             pt_taylor_model<Q>(col, c, xm - tc, &p, &dp, &ex);
-            if (f.has_barrier) pt_taylor_barrier(bp, geo, N, moving, bconst(), xm, &Bm, &B1m, &B2m);
+            if (f.has_barrier) pt_taylor_barrier(bp, tab, geo, N, moving, bconst(), xm, 1, &Bm, &B1m, &B2m);
             double gv = fma(ex, p, f.bias) - Bm;
             double gd = ex * fma(2.0 * c * (xm - tc), p, dp) - B1m;
-            const double EdB = Ed + 64.0 * PT_U64 * (fabs(gd) + bsum);
+            const double EdB = Ed + bulp * PT_U64 * (fabs(gd) + bsum);
             const double smin = fabs(gd) - EdB - 0.5 * w * D2max;
             if (!(smin > 0.0)) continue;                                  // not provably monotone yet: next level
             // Newton on the model inside (L, H), the barrier replaced by its quadratic expansion about the bracket
@@ -659,7 +683,7 @@ pt_bisect_taylor_kernel(PtFieldDev f, double sum_abs_w, PtTaylorDev tf, PtRows r
             // evaluated: |G(x - G/G')| <= |G''|/2 (G/G')^2
             double Bx = 0.0, B1x = 0.0, B2x = 0.0;
             if (f.has_barrier) {
-                pt_taylor_barrier(bp, geo, N, moving, bconst(), x, &Bx, &B1x, &B2x);
+                pt_taylor_barrier(bp, tab, geo, N, moving, bconst(), x, 1, &Bx, &B1x, &B2x);
                 gv = fma(ex, p, f.bias) - Bx;
                 gd = ex * fma(2.0 * c * (x - tc), p, dp) - B1x;
                 const double step = gv / gd, xn = x - step;
@@ -670,7 +694,7 @@ pt_bisect_taylor_kernel(PtFieldDev f, double sum_abs_w, PtTaylorDev tf, PtRows r
                 }
             }
             const double agd = fabs(gd);
-            const double Eb = 64.0 * PT_U64 * (1.1 * (fabs(Bx) + w * bsum) + abias) + 1e-290;
+            const double Eb = bulp * PT_U64 * (1.1 * (fabs(Bx) + w * bsum) + abias) + 1e-290;
             const double tx = fabs(x - tc);
             const double Ex = 1.001 * ex * (RQ * pt_powi(tx, Q) + Ctot * pt_taylor_cosh<Q>(cola, fac * caQ, tx)) + Efar + Eb;
             const double rho0 = (fabs(gv) + Ex) / smin;                    // |x - root| <= rho0
@@ -689,10 +713,10 @@ pt_bisect_taylor_kernel(PtFieldDev f, double sum_abs_w, PtTaylorDev tf, PtRows r
                     const double tr = mr - tc, atr = fabs(tr);
                     pt_taylor_model<Q>(col, c, tr, &p, &dp, &ex);
                     double Br = 0.0, B1r = 0.0, B2r = 0.0;
-                    if (f.has_barrier) pt_taylor_barrier(bp, geo, N, moving, bconst(), mr, &Br, &B1r, &B2r);
+                    if (f.has_barrier) pt_taylor_barrier(bp, tab, geo, N, moving, bconst(), mr, 0, &Br, &B1r, &B2r);
                     const double gr = fma(ex, p, f.bias) - Br;
                     const double Etr = ex * RQ * pt_powi(atr, Q), Ern = ex * Ctot * pt_taylor_cosh<Q>(cola, fac * caQ, atr);
-                    const double Er = 1.001 * (Etr + Ern) + Efar + 64.0 * PT_U64 * (1.1 * fabs(Br) + abias) + 1e-290;
+                    const double Er = 1.001 * (Etr + Ern) + Efar + bulp * PT_U64 * (1.1 * fabs(Br) + abias) + 1e-290;
                     if (fabs(gr) > Er || (Etr + Efar <= Ern && gr == gr)) { if ((gr > 0.0 ? 1 : -1) == sa) L = mr; else H = mr; }
                     else { open = true; break; }
                 }
