@@ -780,8 +780,10 @@ def test_ill_conditioned_field_root_solve(monkeypatch):
 
 
 # ---- one-pass Taylor-model root solve (pt_field_taylor.cuh) --------------------------------------------------
-def _crossing_segments(m, lo, hi, count, step, rng, max_axes):
-    """Random lattice-like segments (1..max_axes coordinates move by `step`) whose end points have different signs."""
+def _crossing_segments(m, lo, hi, count, step, rng, max_axes, generic_frac=0.0):
+    """Random lattice-like segments (1..max_axes coordinates move by `step`, all by the same signed amount -- the rows the
+    Taylor kernel groups by direction) whose end points have different signs; a fraction `generic_frac` of them gets an
+    arbitrary direction of that length instead (rows that keep the N-term dot product)."""
     n = lo.size
     a_rows, b_rows, s_rows = [], [], []
     have = 0
@@ -790,6 +792,10 @@ def _crossing_segments(m, lo, hi, count, step, rng, max_axes):
         axes = rng.integers(1, max_axes + 1, size=a.shape[0])
         order = np.argsort(rng.random(a.shape), axis=1)                       # a random subset of `axes[i]` coordinates
         d = (order < axes[:, None]) * (step * rng.choice([-1.0, 1.0], size=(a.shape[0], 1)))
+        if generic_frac > 0.0:
+            g = rng.normal(size=a.shape)
+            g *= (np.linalg.norm(d, axis=1) / np.linalg.norm(g, axis=1))[:, None]
+            d = np.where(rng.random(a.shape[0])[:, None] < generic_frac, g, d)
         b = a + d
         sa, sb = m.signs(a), m.signs(b)
         keep = sa != sb
@@ -825,7 +831,8 @@ def test_taylor_root_solve_equals_plain_bisection(monkeypatch, precision_mode, n
         m = M.KernelClassifierManifold(support, weights, gamma, 0.3 * np.sqrt(2.0 * gamma),
                                        barrier=M.BoxBarrier(lo, hi, sigma / 4.0, 2.0 / sigma))
         if not pts:
-            a, b, sa = _crossing_segments(m, lo - 0.3, hi + 0.3, 160_000, step, np.random.default_rng(n), min(n, 6))
+            # four fifths lattice edges (grouped by direction: direction-table kernel), one fifth arbitrary segments
+            a, b, sa = _crossing_segments(m, lo - 0.3, hi + 0.3, 160_000, step, np.random.default_rng(n), min(n, 6), generic_frac=0.2)
         work = np.zeros(6, dtype=np.int64)
         _cabi.check(_cabi.lib.pt_ctx_work_counters(_cabi.context().handle, work.ctypes.data, 1))
         pts[(mode, taylor)] = M.intersection_points_batch(m, a, b, eps, signs_a=sa)
