@@ -321,11 +321,18 @@ __global__ void pt_ref_endpoints_kernel(PtRefGeom rg, const u64* __restrict__ va
 }
 
 // ---- R5: greedy eps-dedup ----------------------------------------------------------------------
-__device__ __forceinline__ u64 pt_grid_hash(int n, const long long* c) {
-    u64 h = 0x9e3779b97f4a7c15ULL;
-    for (int d = 0; d < n; ++d) h = pt_mix(h ^ (u64)c[d]);
-    return h & 0x7fffffffffffffffULL;
+// hash of a grid cell: a linear form of the coordinates (odd 64-bit multipliers) through one mixing round -- the search
+// gets a neighbouring cell's form by adding one multiplier per stepped axis
+__device__ __constant__ u64 pt_grid_mult[PT_NMAX] = {
+    0x9e3779b97f4a7c15ULL, 0xc2b2ae3d27d4eb4fULL, 0x165667b19e3779f9ULL, 0xd6e8feb86659fd93ULL,
+    0xff51afd7ed558ccdULL, 0xc4ceb9fe1a85ec53ULL, 0x2545f4914f6cdd1dULL, 0x94d049bb133111ebULL};
+__device__ __forceinline__ u64 pt_grid_form(int n, const long long* c) {
+    u64 h = 0;
+    for (int d = 0; d < n; ++d) h += (u64)c[d] * pt_grid_mult[d];
+    return h;
 }
+__device__ __forceinline__ u64 pt_grid_finish(u64 form) { return pt_mix(form) & 0x7fffffffffffffffULL; }
+__device__ __forceinline__ u64 pt_grid_hash(int n, const long long* c) { return pt_grid_finish(pt_grid_form(n, c)); }
 
 __global__ void pt_dedup_hash_kernel(int n, const double* __restrict__ pts, size_t count, double cell, u64* __restrict__ gkey,
                                      uint32_t* __restrict__ idx) {
@@ -338,15 +345,18 @@ __global__ void pt_dedup_hash_kernel(int n, const double* __restrict__ pts, size
     idx[i] = (uint32_t)i;
 }
 
-// directory of the sorted grid keys: hash(cell) -> first position of the cell's run
-__global__ void pt_dedup_directory_kernel(const u64* __restrict__ gkey_sorted, size_t count, PtTable dir, unsigned* err) {
+// directory of the sorted grid keys: hash(cell) -> (first position of the cell's run) << 32 | the run's smallest point index
+// (the sort is stable, so that is the run's first entry): a probe from a point that precedes everything in the cell -- the
+// usual case, the cell holds the point itself or nothing earlier -- ends at the directory entry
+__global__ void pt_dedup_directory_kernel(const u64* __restrict__ gkey_sorted, const uint32_t* __restrict__ idx_sorted, size_t count,
+                                          PtTable dir, unsigned* err) {
     const size_t a = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (a >= count) return;
     const u64 gk = gkey_sorted[a];
     if (a > 0 && gkey_sorted[a - 1] == gk) return;
     bool ins;
     const u64 slot = pt_table_insert(dir, gk, ins, err);
-    dir.ent[2 * slot + 1] = (u64)a;
+    dir.ent[2 * slot + 1] = ((u64)a << 32) | (u64)idx_sorted[a];
 }
 
 #define PT_DD_UNDECIDED 0
@@ -376,16 +386,17 @@ __device__ __forceinline__ int pt_dedup_search(int n, const double* __restrict__
     }
     bool any_kept = false, any_undecided = false;
     nbc = 0;
+    const u64 form_lo = pt_grid_form(n, lo);
     for (int comb = 0; comb < ncomb && !any_kept; ++comb) {
-        long long c[PT_NMAX]; int bit = 0;
-        for (int d = 0; d < n; ++d) {
-            if (hi[d] != lo[d]) { c[d] = ((comb >> bit) & 1) ? hi[d] : lo[d]; ++bit; }
-            else c[d] = lo[d];
-        }
-        const u64 gk = pt_grid_hash(n, c);
+        u64 form = form_lo; int bit = 0;
+        for (int d = 0; d < n; ++d)
+            if (hi[d] != lo[d]) { if ((comb >> bit) & 1) form += (u64)(hi[d] - lo[d]) * pt_grid_mult[d]; ++bit; }
+        const u64 gk = pt_grid_finish(form);
         u64 slot;
         if (!pt_table_find(dir, gk, slot)) continue;          // no point in that cell
-        size_t a = (size_t)dir.ent[2 * slot + 1];
+        const u64 entry = dir.ent[2 * slot + 1];
+        if ((size_t)(uint32_t)entry >= i) continue;           // nothing earlier than i in that cell
+        size_t a = (size_t)(entry >> 32);
         for (; a < count && gkey_sorted[a] == gk; ++a) {
             const size_t j = idx_sorted[a];
             if (j >= i) break;           // the sort is stable: a cell's run is in ascending point order
@@ -566,7 +577,7 @@ static int pt_dedup_label_impl(pt_ctx* ctx, int n, const double* upts, const u64
         PT_TRY(pt_table_init(ctx, dir, 2 * (u64)U));
         {
             PT_LAUNCH(ctx, "dedup_directory");
-            pt_dedup_directory_kernel<<<pt_grid_for(U, 256), 256, 0, ctx->stream>>>(gks.p, U, dir.view(), &ctr.p->error);
+            pt_dedup_directory_kernel<<<pt_grid_for(U, 256), 256, 0, ctx->stream>>>(gks.p, gis.p, U, dir.view(), &ctr.p->error);
             PT_TRY(pt_check_launch(ctx, "pt_dedup_directory_kernel"));
         }
         PtBuf<uint32_t> point_of, nbc, off, csr, list_a, list_b;
