@@ -254,11 +254,11 @@ class ClockSampler:
 
 # DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) and FP64-pipe busy fraction of the big launch of each
 # kernel, from the `ncu --set full` captures summarised under profiles/ (same command, dof6 workload)
-NCU_TRAFFIC = {"bisect_fp64_taylor": 179.668480e6 + 109.176064e6, "bisect_fp64_newton": 206.831104e6 + 76.694016e6,
+NCU_TRAFFIC = {"bisect_fp64_taylor": 636.986624e6 + 538.354688e6, "bisect_fp64_newton": 206.831104e6 + 76.694016e6,
                "bisect_fp32_screen_tc": 170.094592e6 + 19.643648e6}
-NCU_SOURCE = {"bisect_fp64_taylor": "profiles/r2_v3_taylor_full.txt", "bisect_fp64_newton": "profiles/r1_v7_newton_full.txt",
+NCU_SOURCE = {"bisect_fp64_taylor": "profiles/r2_v5_taylor_traffic.txt", "bisect_fp64_newton": "profiles/r1_v7_newton_full.txt",
               "bisect_fp32_screen_tc": "profiles/r1_v7_tc4_screen_full.txt"}
-NCU_PIPE_BUSY = {"bisect_fp64_taylor": 0.721, "bisect_fp64_newton": 0.691}
+NCU_PIPE_BUSY = {"bisect_fp64_taylor": 0.697, "bisect_fp64_newton": 0.691}
 TAYLOR_Q = 16   # csrc/pt_field_taylor.cuh PT_TAYLOR_Q
 
 
@@ -268,9 +268,11 @@ def pair_dp_ops(n: int, kind: str = "eval") -> tuple[float, float]:
       eval    exponent in expanded form (1 DADD + n DFMA), 2^x by table + degree-4 polynomial (6 DFMA + 1 DADD + 1 DMUL),
               weight multiply, accumulate
       deriv   eval + first and second directional derivative and sum|w|k (Newton pass 1)
-      taylor  exponent, first log-derivative (n DFMA), 2^x, u^2..u^4, and Q+1 moment updates (5 DMUL + 6 DADD + 15 DFMA)"""
+      taylor  exponent (n DFMA), first log-derivative from the direction table (1 DFMA: every row of the benchmark is a
+              lattice edge), 2^x, u^2..u^4, and Q+1 moment updates (5 DMUL + 6 DADD + 15 DFMA at Q = 16): 40 at n = 6
+              (arbitrary segments take the generic kernel: n DFMA for the log-derivative, 45 at n = 6)"""
     if kind == "taylor":
-        fma, other = 2.0 * n + 6.0 + 3.0 * TAYLOR_Q / 4.0, 6.0 + TAYLOR_Q / 4.0 + TAYLOR_Q / 4.0 + 1.0
+        fma, other = n + 1.0 + 6.0 + 3.0 * TAYLOR_Q / 4.0, 6.0 + TAYLOR_Q / 4.0 + TAYLOR_Q / 4.0 + 1.0
     elif kind == "deriv":
         fma, other = 2.0 * n + 6.0 + 4.0, 6.0 + 2.0
     else:

@@ -45,6 +45,13 @@
 #ifndef PT_TAYLOR_MINB_DIR
 #define PT_TAYLOR_MINB_DIR 6          /* ditto, direction-table variant (its loop keeps N-1 fewer values live) */
 #endif
+#ifdef PT_TAYLOR_NO_CS
+#define PT_TAYLOR_LDCS(p) (*(p))
+#define PT_TAYLOR_STCS(p, v) (*(p) = (v))
+#else
+#define PT_TAYLOR_LDCS(p) __ldcs(p)
+#define PT_TAYLOR_STCS(p, v) __stcs((p), (v))
+#endif
 #define PT_TAYLOR_TRY_WIDTH 0.0625     /* first enclosure attempt once the bracket is this narrow (in t) */
 
 template <int N> struct PtRowT { static const int value = (N + 2) & ~1; };   // 2*gl*s_d (N), c'_s, pad to an even count
@@ -522,7 +529,7 @@ pt_bisect_taylor_kernel(PtFieldDev f, double sum_abs_w, PtTaylorDev tf, PtRows r
     {
         double b[N];
 #pragma unroll
-        for (int d = 0; d < N; ++d) { a[d] = a_[ei * N + d]; b[d] = b_[ei * N + d]; }
+        for (int d = 0; d < N; ++d) { a[d] = PT_TAYLOR_LDCS(&a_[ei * N + d]); b[d] = PT_TAYLOR_LDCS(&b_[ei * N + d]); }   // last use
         seg = pt_segment<N>(a, b, diff);
     }
     const int sa = signs_a[ei];
@@ -725,11 +732,13 @@ pt_bisect_taylor_kernel(PtFieldDev f, double sum_abs_w, PtTaylorDev tf, PtRows r
             break;
         }
     }
+    // (results are written once and read by later kernels: streaming stores, so they do not push the resident tiles, the
+    //  direction table and the threads' local memory out of L2)
     slow[ei] = (uint8_t)flag;
     if (flag == 0) {
         const double tf_ = __dmul_rn(0.5, __dadd_rn(L, H));
 #pragma unroll
-        for (int d = 0; d < N; ++d) out[ei * N + d] = __dadd_rn(a[d], __dmul_rn(tf_, diff[d]));
+        for (int d = 0; d < N; ++d) PT_TAYLOR_STCS(&out[ei * N + d], __dadd_rn(a[d], __dmul_rn(tf_, diff[d])));
     } else {
         lo_io[ei] = L; hi_io[ei] = H;
         jlo_out[ei] = flag == 2 ? Jlo : -1e300;
