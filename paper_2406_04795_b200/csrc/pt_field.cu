@@ -1305,10 +1305,27 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
                 pt_bisect_taylor_kernel<N, PT_TAYLOR_Q_HINT, false><<<grid, PT_TAYLOR_THREADS, PT_TAYLOR_SMEM(N, PT_TAYLOR_Q_HINT), ctx->stream>>>(
                     f->d, f->sum_abs_w, td, rws, nogrp, a, b, sa, eps, out, lo.p, hi.p, slow.p, jlo.p, jhi.p, ctx->work, recentre, h);
             } else {
-                PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N, PT_TAYLOR_Q, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PT_TAYLOR_SMEM(N, PT_TAYLOR_Q)));
-                PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N, PT_TAYLOR_Q, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-                pt_bisect_taylor_kernel<N, PT_TAYLOR_Q, false><<<grid, PT_TAYLOR_THREADS, PT_TAYLOR_SMEM(N, PT_TAYLOR_Q), ctx->stream>>>(
-                    f->d, f->sum_abs_w, td, rws, nogrp, a, b, sa, eps, out, lo.p, hi.p, slow.p, jlo.p, jhi.p, ctx->work, recentre, nullptr);
+                // tiny batches (at most one block per SM: recentred passes of a few thousand rows, late waves of a trace): the
+                // per-edge loop over the support set is the launch's latency, so G lanes share an edge.  Measured on B200: a
+                // 111-row pass 0.16 -> 0.09 ms with G = 4; from ~50 k rows on the launch is throughput-sized and sharing LOSES
+                // (4x the blocks, each staging the whole support set: 47.6 k rows 0.73 -> 1.24 ms, 95 k rows 1.4 -> 2.5 ms)
+                int G = 1;
+                for (int g = 2; g <= 4; g *= 2)
+                    if ((double)count * g / PT_TAYLOR_THREADS <= (double)ctx->sm_count) G = g;
+                const char* g_env = getenv("PERMATRACE_B200_TAYLOR_SHARE");          // tests / A-B timing: force 1, 2 or 4
+                if (g_env) G = atoi(g_env) == 4 ? 4 : atoi(g_env) == 2 ? 2 : 1;
+#define PT_TAYLOR_GEN_LAUNCH(GG)                                                                                                          \
+                do {                                                                                                                  \
+                    const unsigned gridg = pt_grid_for(count, PT_TAYLOR_THREADS / GG);                                                \
+                    PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N, PT_TAYLOR_Q, false, GG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PT_TAYLOR_SMEM(N, PT_TAYLOR_Q)));   \
+                    PT_CUDA(ctx, cudaFuncSetAttribute(pt_bisect_taylor_kernel<N, PT_TAYLOR_Q, false, GG>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));                            \
+                    pt_bisect_taylor_kernel<N, PT_TAYLOR_Q, false, GG><<<gridg, PT_TAYLOR_THREADS, PT_TAYLOR_SMEM(N, PT_TAYLOR_Q), ctx->stream>>>(                                          \
+                        f->d, f->sum_abs_w, td, rws, nogrp, a, b, sa, eps, out, lo.p, hi.p, slow.p, jlo.p, jhi.p, ctx->work, recentre, nullptr);                                          \
+                } while (0)
+                if (G == 4) PT_TAYLOR_GEN_LAUNCH(4);
+                else if (G == 2) PT_TAYLOR_GEN_LAUNCH(2);
+                else PT_TAYLOR_GEN_LAUNCH(1);
+#undef PT_TAYLOR_GEN_LAUNCH
             }
             return pt_check_launch(ctx, "pt_bisect_taylor_kernel");
         };
@@ -1316,7 +1333,10 @@ static int pt_bisect_launch(pt_ctx* ctx, const pt_field* f, const double* a, con
         // log-derivative from the direction table with one FMA per pair.  Rows that are not lattice edges (class 0) and
         // hinted batches keep the generic kernel.
         bool grouped = false;
-        if (f->taylor_dir && !hinted && m < 0xFFFFFFFFull - (size_t)(PT_TAYLOR_THREADS << N)) {
+        // (batches of up to two waves of blocks skip the grouping: they are latency-sized and take the shared-row generic kernel)
+        if (f->taylor_dir && !hinted && m < 0xFFFFFFFFull - (size_t)(PT_TAYLOR_THREADS << N) &&
+            m > (getenv("PERMATRACE_B200_TAYLOR_GROUP_MIN") ? (size_t)atoll(getenv("PERMATRACE_B200_TAYLOR_GROUP_MIN"))
+                                                            : (size_t)2 * ctx->sm_count * PT_TAYLOR_MINB_DIR * PT_TAYLOR_THREADS)) {
             constexpr int NC = 1 << N;
             PtBuf<uint8_t> cls, bmask; PtBuf<unsigned> hist; PtBuf<uint32_t> glist;
             PT_TRY(cls.alloc(ctx, m));

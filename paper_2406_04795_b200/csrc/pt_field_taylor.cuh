@@ -212,7 +212,7 @@ __device__ __forceinline__ void pt_taylor_back(double pw, double u, double (&acc
 
 // Software-pipelined over the support rows: the (serial) exponent / exponential chain of row j+1 is issued next to the
 // (parallel) moment updates of row j.  The tile carries one zero pad row behind the last one for the final look-ahead.
-template <int N, int Q, bool DIR>
+template <int N, int Q, bool DIR, int G>
 __device__ __forceinline__ void pt_taylor_block(const double* __restrict__ svt, const double* __restrict__ dir, long long r0, long long r1,
                                                 double* tile, const double* tab, const PtPoint64<N>& pp, double pdu,
                                                 const double (&ddu)[N], int sx, double (&acc)[Q + 1], double* total) {
@@ -238,10 +238,18 @@ __device__ __forceinline__ void pt_taylor_block(const double* __restrict__ svt, 
         }
         if (threadIdx.x < ROW) tile[cnt * ROW + threadIdx.x] = 0.0;
         __syncthreads();
+        // G lanes share an edge (small batches: the per-edge loop over the support set is the launch's latency): lane g of
+        // the group takes an even-sized share [j0, j1) of every tile
+        int j0 = 0, j1 = cnt;
+        if (G > 1) {
+            const int per = ((cnt + G - 1) / G + 1) & ~1;
+            j0 = (int)(threadIdx.x % G) * per; if (j0 > cnt) j0 = cnt;
+            j1 = j0 + per < cnt ? j0 + per : cnt;
+        }
         double e0, u0, e1, u1;
-        pt_taylor_front<N, DIR>(tile, pp, pdu, ddu, tab, sx, e0, u0);
+        pt_taylor_front<N, DIR>(tile + j0 * ROW, pp, pdu, ddu, tab, sx, e0, u0);
 #pragma unroll 1
-        for (int j = 0; j < cnt; j += 2) {
+        for (int j = j0; j < j1; j += 2) {
             pt_taylor_front<N, DIR>(tile + (j + 1) * ROW, pp, pdu, ddu, tab, sx, e1, u1);
             pt_taylor_back<Q>(e0, u0, acc);
             pt_taylor_front<N, DIR>(tile + (j + 2) * ROW, pp, pdu, ddu, tab, sx, e0, u0);
@@ -437,7 +445,7 @@ __global__ void pt_taylor_bmask_kernel(PtTaylorOffsets offs, int ncls, unsigned 
     bmask[b] = (uint8_t)c;
 }
 
-template <int N, int Q, bool DIR>
+template <int N, int Q, bool DIR, int G = 1>
 __global__ void __launch_bounds__(PT_TAYLOR_THREADS, DIR ? PT_TAYLOR_MINB_DIR : PT_TAYLOR_MINB)
 pt_bisect_taylor_kernel(PtFieldDev f, double sum_abs_w, PtTaylorDev tf, PtRows rows, PtTaylorGroup grp, const double* __restrict__ a_,
                         const double* __restrict__ b_, const int8_t* __restrict__ signs_a, double eps, double* __restrict__ out,
@@ -459,9 +467,11 @@ pt_bisect_taylor_kernel(PtFieldDev f, double sum_abs_w, PtTaylorDev tf, PtRows r
     // first pass: all rows, model about the edge midpoint, bracket [0, 1].  Second pass (`recentre`): the listed rows the
     // first one left open, model about the midpoint of the bracket they stopped at -- the truncation then scales with
     // (bracket width / 2)^Q instead of 2^-Q
+    static_assert(G == 1 || !DIR, "shared rows only in the generic kernel");
+    constexpr int RPB = TH / G;                                // rows per block: G adjacent lanes share one
     const size_t m = DIR ? (size_t)gridDim.x * TH : pt_rows_total(rows);
-    if ((size_t)blockIdx.x * TH >= m) return;
-    size_t ei = (size_t)blockIdx.x * TH + threadIdx.x;
+    if ((size_t)blockIdx.x * RPB >= m) return;
+    size_t ei = (size_t)blockIdx.x * RPB + threadIdx.x / G;
     bool valid = ei < m;
     unsigned mask = 0;
     if (DIR) {
@@ -502,11 +512,23 @@ pt_bisect_taylor_kernel(PtFieldDev f, double sum_abs_w, PtTaylorDev tf, PtRows r
         double acc[Q + 1];
 #pragma unroll
         for (int k = 0; k <= Q; ++k) { acc[k] = 0.0; col[k * TH] = 0.0; }
-        pt_taylor_block<N, Q, DIR>(tf.svt, dir, 0, tf.s_pos, tile, tab, pp, pdu, ddu, 0, acc, col);
+        pt_taylor_block<N, Q, DIR, G>(tf.svt, dir, 0, tf.s_pos, tile, tab, pp, pdu, ddu, 0, acc, col);
         // even moments of the positive block, rounded up to fp32: they only enter error bounds (MA_k = 2 M_k^+ - M_k)
 #pragma unroll
-        for (int k = 0; k < Q; k += 2) stash[(k / 2) * TH] = __double2float_ru(col[k * TH]);
-        pt_taylor_block<N, Q, DIR>(tf.svt, dir, tf.s_pos, tf.s_tot, tile, tab, pp, pdu, ddu, (int)0x80000000, acc, col);
+        for (int k = 0; k < Q; k += 2) {
+            double v = col[k * TH];
+            if (G > 1) for (int o = 1; o < G; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);     // the group's lanes' shares
+            stash[(k / 2) * TH] = __double2float_ru(v * (G > 1 ? 1.0 + 1e-15 : 1.0));
+        }
+        pt_taylor_block<N, Q, DIR, G>(tf.svt, dir, tf.s_pos, tf.s_tot, tile, tab, pp, pdu, ddu, (int)0x80000000, acc, col);
+        if (G > 1) {
+#pragma unroll
+            for (int k = 0; k <= Q; ++k) {
+                double v = col[k * TH];
+                for (int o = 1; o < G; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                col[k * TH] = v;
+            }
+        }
         __syncthreads();                                   // the last tile is dead: its space takes the absolute moments
         double inv_fact = 1.0;
 #pragma unroll
@@ -523,6 +545,17 @@ pt_bisect_taylor_kernel(PtFieldDev f, double sum_abs_w, PtTaylorDev tf, PtRows r
         const int nvalid = __syncthreads_count(valid ? 1 : 0);
         if (threadIdx.x == 0) atomicAdd(&work[7], (unsigned long long)nvalid);
     }
+    if (G > 1) {
+        // shared rows: the tails of the block's RPB rows go to its first RPB threads (whole warps, not every G-th lane); thread
+        // r reads the coefficient columns the group of row r left behind (all G lanes of a group hold the same totals)
+        __syncthreads();
+        if (threadIdx.x >= RPB) return;
+        ei = (size_t)blockIdx.x * RPB + threadIdx.x;
+        valid = ei < m;
+        if (valid && rows.list) ei = rows.list[ei];
+        col = tab + PT_EXP_TAB + threadIdx.x * G;
+        cola = tile + threadIdx.x * G;
+    }
     if (!valid) return;
     double a[N], diff[N];
     double L = 0.0, H = 1.0, seg;
@@ -535,6 +568,11 @@ pt_bisect_taylor_kernel(PtFieldDev f, double sum_abs_w, PtTaylorDev tf, PtRows r
     const int sa = signs_a[ei];
     if (recentre) { L = lo_io[ei]; H = hi_io[ei]; }
     const double tc = recentre ? 0.5 * (L + H) : pt_taylor_centre(hint, ei);     // model centre (dyadic)
+    if (G > 1) {
+        mnorm2 = 0.0;                                                            // (the pass computed it for another row)
+#pragma unroll
+        for (int d = 0; d < N; ++d) { const double mcd = fma(tc, diff[d], a[d]); mnorm2 = fma(mcd, mcd, mnorm2); }
+    }
     const double hr = fmax(tc - L, H - tc);                                      // |tau| <= hr on the bracket
     const double seg2 = seg * seg;
 
@@ -746,7 +784,7 @@ pt_bisect_taylor_kernel(PtFieldDev f, double sum_abs_w, PtTaylorDev tf, PtRows r
     }
     if (recentre && flag != 0) atomicAdd(&work[3], 1ull);                 // rows left to the evaluation-based kernels
     if (!DIR && threadIdx.x == 0 && !recentre) {
-        const size_t first = (size_t)blockIdx.x * TH;
-        atomicAdd(&work[7], (unsigned long long)(m - first < (size_t)TH ? m - first : (size_t)TH));
+        const size_t first = (size_t)blockIdx.x * RPB;
+        atomicAdd(&work[7], (unsigned long long)(m - first < (size_t)RPB ? m - first : (size_t)RPB));
     }
 }

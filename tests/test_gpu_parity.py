@@ -825,9 +825,18 @@ def test_taylor_root_solve_equals_plain_bisection(monkeypatch, precision_mode, n
     eps = 1e-9
     pts = {}
     left = [0]
-    for mode, taylor in (("1", "1"), ("0", "1"), ("1", "0")):
+    # ("1", "1"): the library's own choice at this batch size (generic kernel, one lane per edge); "grouped": the
+    # direction-table kernel the big refinement batches take (grouping forced); "shared": generic kernel with four lanes per
+    # edge (what tiny batches take)
+    for mode, taylor in (("1", "1"), ("1", "grouped"), ("1", "shared"), ("0", "1"), ("1", "0")):
         monkeypatch.setenv("PERMATRACE_B200_PRECISION", mode)
-        monkeypatch.setenv("PERMATRACE_B200_TAYLOR", taylor)
+        monkeypatch.setenv("PERMATRACE_B200_TAYLOR", "0" if taylor == "0" else "1")
+        monkeypatch.delenv("PERMATRACE_B200_TAYLOR_GROUP_MIN", raising=False)
+        monkeypatch.delenv("PERMATRACE_B200_TAYLOR_SHARE", raising=False)
+        if taylor == "grouped":
+            monkeypatch.setenv("PERMATRACE_B200_TAYLOR_GROUP_MIN", "1")
+        if taylor == "shared":
+            monkeypatch.setenv("PERMATRACE_B200_TAYLOR_SHARE", "4")
         m = M.KernelClassifierManifold(support, weights, gamma, 0.3 * np.sqrt(2.0 * gamma),
                                        barrier=M.BoxBarrier(lo, hi, sigma / 4.0, 2.0 / sigma))
         if not pts:
@@ -838,13 +847,14 @@ def test_taylor_root_solve_equals_plain_bisection(monkeypatch, precision_mode, n
         pts[(mode, taylor)] = M.intersection_points_batch(m, a, b, eps, signs_a=sa)
         _cabi.check(_cabi.lib.pt_ctx_work_counters(_cabi.context().handle, work.ctypes.data, 1))
         rows = int(_cabi.lib.pt_ctx_taylor_rows(_cabi.context().handle))
-        assert rows == (len(a) if (mode, taylor) == ("1", "1") else 0)
+        assert rows == (len(a) if mode == "1" and taylor != "0" else 0)
         if rows:
             left[0] = int(work[3])
     new, plain, old = pts[("1", "1")], pts[("0", "1")], pts[("1", "0")]
+    grouped, shared = pts[("1", "grouped")], pts[("1", "shared")]
     diff, seg2 = b - a, np.einsum("ij,ij->i", b - a, b - a)
     tol = 1e-12 * (np.abs(weights).sum() + abs(m.bias))        # the reference's own cross-backend tolerance on F
-    for name, got in (("taylor", new), ("screen+newton", old)):
+    for name, got in (("taylor", new), ("taylor grouped", grouped), ("taylor 4 lanes / edge", shared), ("screen+newton", old)):
         assert np.max(np.abs(got - plain)) <= 2.5e-9
         rows = np.flatnonzero(np.any(got != plain, axis=1))
         assert len(rows) <= len(a) // 200, f"{name}: {len(rows)} of {len(a)} rows differ from plain fp64 bisection"
