@@ -1,5 +1,5 @@
 """Overhead of the multi-GPU driver itself: ShardedProof with a process group of ONE rank (no data crosses any link)
-against the single-GPU device pipeline on the same workload.  What differs is the orchestration: per-wave candidate
+against the single-GPU device pipeline on the same workload, over the NCCL backend.  What differs is the orchestration: per-wave candidate
 records and winner ranking through torch tensors, candidates merged by all_gather, dedup + labels as separate calls.
 
     python benchmarks/sharded_overhead.py [workload]
@@ -38,10 +38,20 @@ def main():
     single = timed(lambda: pipe.step(seeds.data_ptr(), seeds.shape[0]))
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29541")
-    dist.init_process_group("gloo", rank=0, world_size=1)
-    proof = ShardedProof(CudaEngine(wl.manifold, wl.cfg, wl.template, checker))
+    # the real transport: a one-rank NCCL group (NCCL refuses two ranks on one device)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    proof = ShardedProof(CudaEngine(wl.manifold, wl.cfg, wl.template, checker), gather_result=False)
     sharded = timed(lambda: proof.run(seeds))
-    print(f"device pipeline {single:.2f} ms | ShardedProof(world=1) {sharded:.2f} ms")
+    # ... and the same with every collective of the fully sharded path actually issued to NCCL (count matrix, record
+    # all_to_all and winner all_gather per wave, sample sort, ghost exchange, pin rounds): their launch + host-sync cost
+    os.environ["PERMATRACE_B200_FORCE_COLLECTIVES"] = "1"
+    forced_proof = ShardedProof(CudaEngine(wl.manifold, wl.cfg, wl.template, checker), gather_result=False)
+    res = forced_proof.run(seeds)
+    forced = timed(lambda: forced_proof.run(seeds))
+    print(f"device pipeline {single:.2f} ms | ShardedProof(world=1, replicated path) {sharded:.2f} ms | "
+          f"fully sharded path, all collectives through NCCL on one rank {forced:.2f} ms "
+          f"(levels {res['levels']}, pin rounds {res.get('pin_rounds')}, points {res['points_total']})")
     dist.destroy_process_group()
 
 

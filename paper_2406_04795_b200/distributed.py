@@ -26,6 +26,7 @@ engines / with gloo staging only.
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 
@@ -93,6 +94,9 @@ class _Transport:
         self.on = dist.is_available() and dist.is_initialized()
         self.rank = dist.get_rank(group) if self.on else 0
         self.world = dist.get_world_size(group) if self.on else 1
+        # collectives run when there is somebody to talk to -- or, with PERMATRACE_B200_FORCE_COLLECTIVES=1, on a one-rank
+        # group as well: the only way to drive the sharded code through the real NCCL backend on a one-GPU box
+        self.collective = self.world > 1 or (self.on and os.environ.get("PERMATRACE_B200_FORCE_COLLECTIVES") == "1")
         dev = engine.tensor_device
         staged = self.on and dist.get_backend(group) == "gloo" and torch.device(dev).type == "cuda"
         self.comm_device = torch.device("cpu") if staged else dev
@@ -108,14 +112,23 @@ class _Transport:
     def _sum(self, values):
         import torch
         t = torch.tensor(list(values), dtype=torch.int64, device=self.comm_device)
-        if self.world > 1:
+        if self.collective:
             self.dist.all_reduce(t, group=self.group)
         return [int(v) for v in t.tolist()]
+
+    def _gather_rows(self, vec):
+        """all_gather of equal-length 1-D tensors on the transport device into ONE [world, len] tensor (flat output buffer:
+        no per-rank output list, no stack)."""
+        import torch
+        vec = vec.contiguous()
+        out = torch.empty(self.world * vec.numel(), dtype=vec.dtype, device=vec.device)
+        self.dist.all_gather_into_tensor(out, vec, group=self.group)
+        return out.view(self.world, vec.numel())
 
     def _exchange(self, records, counts):
         """all_to_all of rows bucketed by destination rank (`counts[r]` consecutive rows go to rank r); any trailing shape."""
         import torch
-        if self.world == 1:
+        if not self.collective:
             return records
         recv_counts = self._exchange_counts(counts)
         return self._exchange_rows(records, counts, recv_counts)
@@ -137,7 +150,7 @@ class _Transport:
     def _gather_var(self, tensor):
         """all_gather of per-rank tensors with different leading sizes -> list of tensors."""
         import torch
-        if self.world == 1:
+        if not self.collective:
             return [tensor]
         dev = self.comm_device
         size = torch.tensor([tensor.shape[0]], dtype=torch.int64, device=dev)
@@ -175,31 +188,40 @@ class ShardedTrace(_Transport):
         """Candidates to their owners.  ONE all_gather of the per-destination counts gives every rank the whole W x W count
         matrix (its own receive sizes AND an upper bound for every rank's winner list), then one all_to_all of the records."""
         import torch
-        if self.world == 1:
+        if not self.collective:
             return records, [int(records.shape[0])]
         mine = torch.tensor([int(c) for c in counts], dtype=torch.int64, device=self.comm_device)
-        rows = [torch.zeros_like(mine) for _ in range(self.world)]
-        self.dist.all_gather(rows, mine, group=self.group)
-        matrix = torch.stack(rows).tolist()                        # matrix[src][dst]
+        matrix = self._gather_rows(mine).tolist()                   # matrix[src][dst]
         recv_counts = [int(matrix[src][self.rank]) for src in range(self.world)]
         received = self._exchange_rows(records, counts, recv_counts)
         return received, [sum(int(matrix[src][dst]) for src in range(self.world)) for dst in range(self.world)]
 
-    def _wave_winners(self, tags, bounds):
-        """All ranks' ascending winner tags.  A rank wins at most what it received (`bounds`, known from the count matrix),
-        so the lists are gathered padded to the largest bound with a sentinel -- no separate size exchange."""
+    def _wave_rank(self, tags, bounds, total_before: int, max_edges: int):
+        """`rank_winners` over all ranks' winner tags without unpacking them: the lists travel padded to the largest bound
+        with a sentinel that sorts behind every tag (so a padded row can be searched as it is), every rank's winner count
+        rides in slot 0, and the ONE host read of the wave brings back those counts and this rank's number of live winners.
+        Returns (gidx, alive, new_total, complete) like rank_winners."""
         import torch
-        if self.world == 1:
-            return [tags]
+        if not self.collective:
+            return rank_winners([tags], self.rank, total_before, max_edges)
+        W, k = self.world, int(tags.shape[0])
         cap = max(max(bounds), 1)
         sentinel = torch.iinfo(torch.int64).max
-        padded = torch.full((cap,), sentinel, dtype=torch.int64, device=self.comm_device)
-        padded[: tags.shape[0]] = self._out(tags)
-        parts = [torch.empty_like(padded) for _ in range(self.world)]
-        self.dist.all_gather(parts, padded, group=self.group)
-        stacked = torch.stack(parts)
-        sizes = (stacked != sentinel).sum(dim=1).tolist()
-        return [self._back(stacked[r, : int(sizes[r])]) for r in range(self.world)]
+        padded = torch.full((cap + 1,), sentinel, dtype=torch.int64, device=self.comm_device)
+        padded[0] = k
+        padded[1:1 + k] = self._out(tags)
+        stacked = self._back(self._gather_rows(padded))
+        if k:
+            below = torch.searchsorted(stacked[:, 1:].contiguous(), tags.unsqueeze(0).expand(W, k).contiguous()).sum(dim=0)
+        else:
+            below = torch.zeros(0, dtype=torch.int64, device=tags.device)
+        gidx = below + int(total_before)
+        dead = gidx >= int(max_edges)
+        gidx = torch.where(dead, torch.full_like(gidx, -1), gidx)
+        host = torch.cat([stacked[:, 0], (~dead).sum().reshape(1)]).tolist()
+        wave_total, alive = sum(int(v) for v in host[:W]), int(host[W])
+        new_total = min(int(total_before) + wave_total, int(max_edges))
+        return gidx, alive, new_total, int(total_before) + wave_total <= int(max_edges)
 
     def run(self, seeds, max_edges: int) -> dict:
         eng = self.engine
@@ -207,11 +229,11 @@ class ShardedTrace(_Transport):
         frontier = self._sum([local_frontier])[0]
         levels, complete = 0, total <= max_edges
         while frontier > 0 and complete:
-            # per wave: all_gather(counts) + all_to_all(records) + all_gather(winner tags)
+            # per wave: all_gather(counts) + all_to_all(records) + all_gather(padded winner tags, ranked in place)
             records, counts = eng.wave_candidates()
             received, bounds = self._wave_exchange(records, counts)
             tags = eng.wave_admit(received)
-            gidx, alive, new_total, complete = rank_winners(self._wave_winners(tags, bounds), self.rank, total, max_edges)
+            gidx, alive, new_total, complete = self._wave_rank(tags, bounds, total, max_edges)
             eng.wave_commit(gidx, alive, new_total)
             frontier, total = new_total - total, new_total
             levels += 1
@@ -282,10 +304,11 @@ class ShardedProof(_Transport):
         m, n = int(pts.shape[0]), int(pts.shape[1])
         dev = pts.device
         x0 = pts[:, 0]
-        mine = torch.tensor([float(x0.min()) - eps, float(x0.max()) + eps] if m else [float("inf"), float("-inf")],
-                            dtype=torch.float64, device=self.comm_device)
-        spans = [torch.zeros_like(mine) for _ in range(W)]
-        self.dist.all_gather(spans, mine, group=self.group)
+        if m:
+            mine = self._out(torch.stack([x0.min() - eps, x0.max() + eps]))
+        else:
+            mine = torch.tensor([float("inf"), float("-inf")], dtype=torch.float64, device=self.comm_device)
+        spans = self._gather_rows(mine).tolist()
         # my points that may lie within eps of a point of rank r (by coordinate 0): ghosts over there
         send_idx = []
         for r in range(W):
@@ -298,22 +321,21 @@ class ShardedProof(_Transport):
         order_out = torch.cat(send_idx)
         recv_counts = self._exchange_counts(counts)
         ghost_pts = self._exchange_rows(pts[order_out], counts, recv_counts)
-        ghost_prio = self._exchange_rows(order_out + int(prio_offset), counts, recv_counts)
         g = int(ghost_pts.shape[0])
-        all_pts = torch.cat([ghost_pts, pts])
-        prio = torch.cat([ghost_prio, torch.arange(m, dtype=torch.int64, device=dev) + int(prio_offset)])
-        order = torch.argsort(prio, stable=True)
-        inv = torch.empty_like(order)
-        inv[order] = torch.arange(order.numel(), device=dev)
+        # priorities are rank-major and the ghosts arrive bucketed by source rank, each bucket in ascending index order:
+        # [ghosts of lower ranks | own points | ghosts of higher ranks] IS the priority order -- nothing to sort
+        g_lo = int(sum(recv_counts[:me]))
+        all_pts = torch.cat([ghost_pts[:g_lo], pts, ghost_pts[g_lo:]]) if g else pts
         forced_g = None
         rounds = 0
         while True:
             forced = torch.full((g + m,), -1, dtype=torch.int8, device=dev)
             if forced_g is not None:
-                forced[:g] = forced_g.to(torch.int8)
-            mask = eng.dedup_mask(all_pts[order].contiguous(), forced[order].contiguous())[inv]
-            own = mask[g:]
-            used = forced_g if forced_g is not None else mask[:g]
+                forced[:g_lo] = forced_g[:g_lo].to(torch.int8)
+                forced[g_lo + m:] = forced_g[g_lo:].to(torch.int8)
+            mask = eng.dedup_mask(all_pts, forced)
+            own = mask[g_lo:g_lo + m]
+            used = forced_g if forced_g is not None else torch.cat([mask[:g_lo], mask[g_lo + m:]])
             # the owners' verdicts on my ghosts = their masks over what they sent me, in the order it was sent
             auth = self._exchange_rows(own[order_out].to(torch.int64), counts, recv_counts)
             differ = int((used.to(torch.int64) != auth).sum().item()) if g else 0
@@ -327,11 +349,25 @@ class ShardedProof(_Transport):
     def _run_sharded(self, seeds) -> dict:
         import torch
         eng = self.engine
-        st = ShardedTrace(eng, self.group)
-        info = st.run(seeds, int(eng.max_edges))
-        if hasattr(eng, "local_points"):
-            eng.local_points()                     # coarse-edge intersection points: each rank solves its own edges
-        count = int(eng.set_cells_from_keys(self._range_partition(eng.local_cell_keys())))
+        info = None
+        small = int(getattr(eng, "replicate_trace_below", 0))
+        if small > 0 and hasattr(eng, "cell_slice_keep"):
+            # Latency regime: a trace of up to `small` edges is a few dozen waves of sub-millisecond kernels, and sharding it
+            # buys three collectives + five host reads per wave for nothing.  Every rank runs the same (deterministic)
+            # single-device trace and cell build, capped at `small` edges, and keeps ITS contiguous range of the sorted
+            # cell list; a trace that hits the cap is discarded and done again by the owner-hashed BFS below.
+            cap = int(eng.max_edges)
+            whole = eng.trace(seeds, max_edges=small if small < cap else None)
+            if small >= cap or whole["complete"]:
+                first, count = cell_slice(whole["cells"], self.rank, self.world)
+                eng.cell_slice_keep(first, count)
+                info = dict(whole, replicated_trace=True)
+        if info is None:
+            st = ShardedTrace(eng, self.group)
+            info = st.run(seeds, int(eng.max_edges))
+            if hasattr(eng, "local_points"):
+                eng.local_points()                 # coarse-edge intersection points: each rank solves its own edges
+            count = int(eng.set_cells_from_keys(self._range_partition(eng.local_cell_keys())))
         pts, crossing = eng.candidates(0, count)
         per_rank = torch.tensor([count, int(pts.shape[0]), int(crossing)], dtype=torch.int64, device=self.comm_device)
         table = [torch.zeros_like(per_rank) for _ in range(self.world)]
@@ -359,9 +395,9 @@ class ShardedProof(_Transport):
     def run(self, seeds) -> dict:
         import torch
         dist, eng = self.dist, self.engine
-        if self.world > 1 and hasattr(eng, "local_cell_keys") and hasattr(eng, "trace_locate"):
+        if self.collective and hasattr(eng, "local_cell_keys") and hasattr(eng, "trace_locate"):
             return self._run_sharded(seeds)
-        if self.world > 1 and hasattr(eng, "trace_locate") and getattr(eng, "shard_trace", True):
+        if self.collective and hasattr(eng, "trace_locate") and getattr(eng, "shard_trace", True):
             # owner-hashed BFS; the merged edge list (global admission order) feeds the replicated cell build
             st = ShardedTrace(eng, self.group)
             info = st.run(seeds, int(eng.max_edges))
@@ -376,7 +412,7 @@ class ShardedProof(_Transport):
         dev = eng.tensor_device
         n = pts.shape[1]
         mine = torch.tensor([pts.shape[0], crossing], dtype=torch.int64, device=self.comm_device)
-        if self.world > 1:
+        if self.collective:
             counts = [torch.zeros_like(mine) for _ in range(self.world)]
             dist.all_gather(counts, mine, group=self.group)
             counts = torch.stack(counts).cpu().numpy()
@@ -385,7 +421,7 @@ class ShardedProof(_Transport):
             crossing_offsets = np.concatenate([[0], np.cumsum(counts[:, 1])[:-1]])
         else:
             merged, crossing_total, crossing_offsets = pts, int(crossing), np.zeros(1, dtype=np.int64)
-        if self.world > 1 and hasattr(eng, "label"):
+        if self.collective and hasattr(eng, "label"):
             # every rank runs the same deterministic dedup; the collision check of the kept points shards trivially
             kept, _ = eng.dedup_label(merged, label=False)
             points = merged[kept]
@@ -422,6 +458,8 @@ class CudaEngine:
         self.eps_dedup = cfg.lattice.scale / (10.0 * template.k * template.k)
         self.field = manifold.device_field()
         self._trace = self._cells = None
+        # traces up to this many edges are run whole on every rank instead of owner-hashed (ShardedProof._run_sharded)
+        self.replicate_trace_below = int(os.environ.get("PERMATRACE_B200_REPLICATE_TRACE_BELOW", 1 << 21))
 
     def _drop(self):
         lib = self._cabi.lib
@@ -433,7 +471,9 @@ class CudaEngine:
 
     __del__ = _drop
 
-    def trace(self, seeds) -> dict:
+    def trace(self, seeds, max_edges: int | None = None) -> dict:
+        """Whole trace + coarse cells on THIS device; `max_edges` caps it below the configured limit (`complete` False
+        when the cap was hit: the hybrid driver then switches to the owner-hashed BFS)."""
         lib, cabi = self._cabi.lib, self._cabi
         self._drop()
         torch = self.torch
@@ -446,12 +486,14 @@ class CudaEngine:
         cabi.check(lib.pt_trace_create(
             self.ctx.handle, self.field, self.n, self.cfg.lattice.scale, self.offset.ctypes.data,
             self.lo.ctypes.data if self.lo is not None else None, self.hi.ctypes.data if self.hi is not None else None,
-            min(int(self.cfg.max_edges), (1 << 31) - 2), float(self.cfg.eps), C.byref(trace)))
+            min(int(self.cfg.max_edges if max_edges is None else max_edges), (1 << 31) - 2), float(self.cfg.eps), C.byref(trace)))
         self._trace = trace
         cabi.check(lib.pt_trace_run(trace, C.c_void_p(ptr), m))
         st = cabi.TraceStats()
         cabi.check(lib.pt_trace_get_stats(trace, C.byref(st)))
         edges = int(st.visited_edges)
+        if max_edges is not None and not st.complete:
+            return dict(trace_edges=edges, complete=False)
         self.trace_points = torch.empty((max(edges, 1), self.n), dtype=torch.float64, device=self.tensor_device)
         if edges:
             cabi.check(lib.pt_trace_points(trace, C.c_void_p(self.trace_points.data_ptr())))
@@ -459,8 +501,8 @@ class CudaEngine:
         cabi.check(lib.pt_cells_from_trace(trace, C.byref(cells)))
         self._cells = cells
         return dict(trace_edges=edges, levels=int(st.levels), candidates_bfs=int(st.candidates),
-                    vertex_evaluations=int(st.field_evaluations), closure_ok=bool(st.closure_ok),
-                    cells=int(lib.pt_cells_count(cells)))
+                    vertex_evaluations=int(st.field_evaluations), closure_ok=bool(st.closure_ok), complete=bool(st.complete),
+                    dropped_out_of_box=int(st.dropped_out_of_box), cells=int(lib.pt_cells_count(cells)))
 
     # ---- ShardedTrace protocol ------------------------------------------------------------------------
     @property
@@ -563,6 +605,14 @@ class CudaEngine:
         lib.pt_cells_destroy(self._cells)
         self._cells = merged
         return int(lib.pt_cells_count(merged))
+
+    def cell_slice_keep(self, first: int, count: int) -> None:
+        """Keep cells [first, first + count) of the (replicated) sorted cell list as this rank's range."""
+        lib, cabi = self._cabi.lib, self._cabi
+        sub = C.c_void_p()
+        cabi.check(lib.pt_cells_slice(self._cells, first, count, C.byref(sub)))
+        lib.pt_cells_destroy(self._cells)
+        self._cells = sub
 
     def local_points(self):
         """Intersection points of this rank's traced edges (the reference's trace() returns them), kept in HBM."""

@@ -317,11 +317,17 @@ def test_gpu_shard_kernels_lockstep_equals_reference(tag, world):
 
 # ---- GPU: two real processes (gloo process group, both CUDA engines on device 0) -----------------------
 
-def _gpu_worker(rank, world, port, tag, out):
+def _gpu_worker(rank, world, port, tag, out, backend="gloo", replicate_below=0):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     os.environ["LOCAL_RANK"] = "0"
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if backend == "nccl":
+        import torch
+        torch.cuda.set_device(0)
+        os.environ["PERMATRACE_B200_FORCE_COLLECTIVES"] = "1"      # a one-rank group still runs every collective
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2406_04795_b200 as P
         from paper_2406_04795_b200.distributed import CudaEngine, ShardedProof
@@ -338,7 +344,9 @@ def _gpu_worker(rank, world, port, tag, out):
         problem.robot, problem.scene = CO.robot_from_dict(rd), CO.scene_from_dict(sd)
         checker = P.not_free_checker(problem)
         eng = CudaEngine(manifold, cfg, P.build_template(inp["n"], 2), checker, device_index=0)
+        eng.replicate_trace_below = replicate_below      # 0: owner-hashed BFS; > edges of the trace: whole trace on every rank
         res = ShardedProof(eng).run(inp["seeds"])
+        assert bool(res.get("replicated_trace", False)) == (replicate_below > res["trace_edges"])
         out[rank] = dict(points=res["points"].cpu().numpy(), labels=res["in_collision"].cpu().numpy(), edges=res["trace_edges"],
                          cells=res["cells"], crossing=res["crossing_edges"], closure=res["closure_ok"], levels=res["levels"])
     finally:
@@ -346,15 +354,17 @@ def _gpu_worker(rank, world, port, tag, out):
 
 
 @pytest.mark.gpu
-def test_gpu_two_process_sharded_proof_equals_reference():
-    """trace (owner-hashed BFS with a real all_to_all per wave) -> cells -> sharded refine -> merged dedup + labels,
+@pytest.mark.parametrize("replicate_below", [0, 1 << 21, 100])
+def test_gpu_two_process_sharded_proof_equals_reference(replicate_below):
+    """trace (owner-hashed BFS with a real all_to_all per wave; or, for small traces, the whole trace on every rank; or a
+    capped whole trace that is discarded for the owner-hashed one) -> cells -> sharded refine -> ghost-pinned dedup + labels,
     two processes, against the reference's golden refinement of the same manifold."""
     tag = "kclf_n3"
     g = Golden("traces")
     ctx = mp.get_context("spawn")
     out = ctx.Manager().dict()
     port = _free_port()
-    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, tag, out)) for r in range(2)]
+    procs = [ctx.Process(target=_gpu_worker, args=(r, 2, port, tag, out, "gloo", replicate_below)) for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:
@@ -369,6 +379,30 @@ def test_gpu_two_process_sharded_proof_equals_reference():
         assert res["points"].shape == want_pts.shape
         assert np.allclose(res["points"], want_pts, rtol=1e-5, atol=1e-8)
         assert np.array_equal(res["labels"], want_lab)
+
+
+# ---- GPU: the real NCCL backend (one rank: NCCL refuses two ranks on one device), every collective forced ----------
+@pytest.mark.gpu
+def test_gpu_nccl_one_rank_forced_collectives_equals_reference():
+    """The fully sharded driver with CUDA tensors handed to NCCL itself (all_gather, all_to_all_single with split sizes,
+    all_reduce -- no host staging): a one-rank NCCL group with PERMATRACE_B200_FORCE_COLLECTIVES=1, against the
+    reference's golden refinement.  What it cannot show is a second rank; the gloo tests above cover that logic."""
+    tag = "kclf_n3"
+    g = Golden("traces")
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    p = ctx.Process(target=_gpu_worker, args=(0, 1, _free_port(), tag, out, "nccl", 0))
+    p.start()
+    p.join(600)
+    assert p.exitcode == 0
+    res = out[0]
+    want_pts, want_lab = g[f"{tag}_refine_points"], g[f"{tag}_refine_labels"]
+    assert res["edges"] == int(g[f"{tag}_stats"][2]) and res["closure"] and res["levels"] == int(g[f"{tag}_stats"][0])
+    assert res["cells"] == g[f"{tag}_cells_base"].shape[0]
+    assert res["crossing"] == int(g[f"{tag}_refine_batches"][:, 2].sum())
+    assert res["points"].shape == want_pts.shape
+    assert np.allclose(res["points"], want_pts, rtol=1e-5, atol=1e-8)
+    assert np.array_equal(res["labels"], want_lab)
 
 
 # ---- GPU: bench.py --gpus 2 end to end (two ranks on one device, gloo staging) -----------------------------
