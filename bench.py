@@ -508,7 +508,7 @@ def run_gpu(args):
             "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_text(a),
-                       "parallelism": "single GPU" if world == 1 else f"owner-hashed BFS (all_to_all per wave), sample-sorted cell ranges, refine/check and ghost-pinned eps-dedup sharded over {world} ranks",
+                       "parallelism": "single GPU" if world == 1 else f"trace whole on every rank up to 2 M edges (owner-hashed BFS with an all_to_all per wave above), contiguous / sample-sorted cell ranges, refine/check and ghost-pinned eps-dedup sharded over {world} ranks",
                        "l2_policy": "per-step working set (hash tables + fine-edge arrays) exceeds the 126 MB L2; "
                                     "all tables are rebuilt from empty every step",
                        "trace_edges": counts["trace_edges"], "coarse_cells": counts["cells"],
