@@ -1,6 +1,9 @@
 """Sharding of the hot path across GPUs (one process per GPU, torch.distributed).
 
-    BFS trace       owner-hashed: rank r owns the edges whose base vertex hashes to r; per wave three collectives --
+    BFS trace       small traces (up to `replicate_trace_below` edges, default 2 M): run whole on every rank, no collective
+                    -- a wave of the owner-hashed BFS costs about a millisecond of host-synchronised launches and collectives
+                    whatever its size (measured over NCCL, benchmarks/sharded_phases.py).  Larger ones:
+                    owner-hashed: rank r owns the edges whose base vertex hashes to r; per wave three collectives --
                     all_gather of the W x W count matrix, ONE all_to_all of 16-byte candidate records, all_gather of the
                     winners' tags (padded to a bound the count matrix already gives) -- admission by minimum tag on the
                     owner, global admission order from the tags (`ShardedTrace`)
@@ -19,8 +22,8 @@
 
 The drivers are written against a small engine protocol so the exchange logic runs unchanged over NCCL with the CUDA
 engine and over gloo in the CPU test-suite (tests/test_distributed_gloo.py, tests/test_sharded_trace.py).  Nothing here has
-run at N > 1 on real GPUs (one GPU per box in this project): the NCCL path is exercised on one device with several
-engines / with gloo staging only.
+run at N > 1 on real GPUs (one GPU per box in this project): several engines on one device, gloo staging, and the real NCCL
+backend on a one-rank group with every collective issued anyway (PERMATRACE_B200_FORCE_COLLECTIVES=1).
 """
 
 from __future__ import annotations
